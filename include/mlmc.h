@@ -1,0 +1,225 @@
+/*
+ * mlmc.h -- C-ABI of the B200-native MPML hot path (arXiv 2503.05533).
+ *
+ * The library (paper_2503_05533_b200/libmlmc.so, sm_100a) computes, for one
+ * level l of the multilevel hierarchy and a batch of samples, the coupled
+ * differences Y_l = Q~_l(omega) - Q~_{l-1}(omega) of the paper's MLMC estimator
+ * (Eq. (3)), each Q~ obtained by solving the P1 FE system
+ * A(omega) x = b of -div(a grad u) = 1 on (0,1)^2 (Eq. (19)) only to
+ * the relative residual the adaptive algorithm permits (Eq. (2), P:70-73;
+ * Eq. (16)), and returns the per-level sums Algorithm 2 needs
+ * (P:357-379).  Citation keys: P:n = PAPER.md line n; Rk = reading k of
+ * DESIGN.md section 3.
+ *
+ * Conventions for every entry point
+ *  - Return value: MLMC_OK (0) or one of the MLMC_E* codes below.  A failing
+ *    call leaves outputs unspecified; mlmc_last_error() gives a message.
+ *  - Pointers are plain host or device pointers; no framework types.  "dev"
+ *    means CUDA device memory on the ctx's device, "host" means ordinary (or
+ *    pinned) host memory.  The caller owns every buffer it passes; the
+ *    library never frees or retains caller memory beyond the call, except the
+ *    workspace bound with mlmc_bind_workspace (borrowed until rebound or
+ *    mlmc_destroy).
+ *  - A ctx is bound to one device and one CUDA stream; it is not thread-safe.
+ *  - Sample identity: (seed, level, global index) fully determines the random
+ *    input xi (Philox4x32-10, R12), so results do not depend on batching,
+ *    rank count or call order.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns MLMC_ECUDA.
+ */
+#ifndef MLMC_H
+#define MLMC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes (mirroring the SPEC exit codes 0/2/3/4) ---------- */
+#define MLMC_OK      0
+#define MLMC_EINVAL  2   /* invalid argument / configuration */
+#define MLMC_ESOLVER 3   /* a solve failed (no convergence, breakdown, overflow) */
+#define MLMC_ELMAX   4   /* Algorithm 2 reached L_max with the bias test failing (R2) */
+#define MLMC_ECUDA   5   /* CUDA error, no device, or kernel image missing */
+#define MLMC_ENOMEM  6   /* workspace too small / allocation failed */
+
+#define MLMC_MAX_LEVELS 16
+#define MLMC_SUMS_LEN   12   /* doubles per mlmc_level_sums */
+#define MLMC_SAMPLE_LEN 8    /* doubles per per-sample record */
+
+/* ---- problem definition ----------------------------------------------------
+ * field = MLMC_FIELD_EXPCOV_KL: log a is a centred Gaussian field with
+ *   covariance sigma2 * exp(-|x1-y1|/corr_len - |x2-y2|/corr_len), truncated
+ *   to its m largest Karhunen-Loeve modes (BASELINE configs; R11).
+ * field = MLMC_FIELD_PAPER_EQ20: Eq. (20): log a = sum_{j<=m}
+ *   omega_j j^-q_decay sin(2 pi j x1) cos(2 pi j x2), omega_j ~ N(0, sigma2)
+ *   (the paper's s is m here).
+ * Mesh level l has h_l = 1/(h0_inv * refine^l), refine must be 2,
+ * levels 0..L_max; h0_inv * 2^L_max <= 512.                                  */
+typedef enum { MLMC_FIELD_EXPCOV_KL = 0, MLMC_FIELD_PAPER_EQ20 = 1 } mlmc_field;
+
+typedef struct {
+    int32_t field;
+    int32_t m;          /* KL terms (1..1024) */
+    double  sigma2;     /* variance of log a (EXPCOV) / of omega_j (EQ20) */
+    double  corr_len;   /* EXPCOV correlation length, > 0 */
+    double  q_decay;    /* EQ20 decay exponent */
+    int32_t h0_inv;     /* 1/h0 (>= 2) */
+    int32_t refine;     /* m of P:308; only 2 is supported */
+    int32_t L_max;      /* finest level the plan supports */
+    int32_t device;     /* CUDA device ordinal */
+} mlmc_problem;
+
+/* ---- solver and precision (Algorithm 1's quadruple) -------------
+ * solver = MLMC_SOLVER_MINRES: unpreconditioned MINRES from x0 = 0, all
+ *   arithmetic binary64, stop at the first k with phibar_k/||b|| <=
+ *   tol (Eq. (2) with C = 1, R9).  u_* fields ignored.
+ * solver = MLMC_SOLVER_CHOL_IR: Algorithm 1: banded Cholesky in
+ *   u_f (MLMC_FMT_F16 / F32 / F64), initial and correction substitutions in
+ *   u_s (F32 or F64, R24), residual in u_r and x in u (both F64), stop when
+ *   ||r||/||b|| < tol, at most max_iter refinement steps.
+ * max_iter = 0 selects the default (MINRES: 4n+100, IR: 50).                 */
+typedef enum { MLMC_FMT_E4M3 = 0, MLMC_FMT_F16 = 1, MLMC_FMT_F32 = 2, MLMC_FMT_F64 = 3 } mlmc_fmt;
+typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1 } mlmc_solver;
+
+typedef struct {
+    int32_t solver;
+    int32_t u_f, u_s, u, u_r;   /* mlmc_fmt codes */
+    int32_t max_iter;
+} mlmc_precision;
+
+/* ---- per-level accumulators (Algorithm 2 steps 5-6) -------------
+ * Layout: MLMC_SUMS_LEN doubles, so a rank-sum is a plain double all-reduce
+ * (the two *_max fields need a MAX reduction).
+ * cost = deterministic work model (R5): MINRES iters * n per solve; IR
+ * n*bw^2*bits(u_f)/64 + steps*4*n*bw per solve; summed over fine + coarse.  */
+typedef struct {
+    double sum_y, sum_y2;        /* sum_k Y^(k), sum_k (Y^(k))^2 */
+    double sum_qf, sum_qc;       /* sum of fine / coarse QoIs */
+    double sum_cost;
+    double n;                    /* samples accumulated */
+    double n_fail;               /* samples with a non-converged / failed solve */
+    double iters_f, iters_c;     /* summed MINRES iterations or IR steps */
+    double iters_f_max, iters_c_max;
+    double reserved;
+} mlmc_level_sums;
+
+/* per-sample record (MLMC_SAMPLE_LEN doubles, sample-major):
+ *   [0] Q_f   [1] Q_c (0 at level 0)   [2] iters_f   [3] iters_c
+ *   [4] true relative residual ||b-Ax||/||b|| of the fine solve  [5] coarse
+ *   [6] status_f  [7] status_c   (0 ok, 1 max_iter, 2 breakdown, 3 non-finite) */
+
+typedef struct mlmc_ctx mlmc_ctx;   /* opaque */
+
+/* ---- plan ------------------------------------------------------------------
+ * mlmc_plan_levels: validate `problem`, compute the KL eigenpairs on the host
+ * (1D transcendental equations, R11), and upload the per-level synthesis
+ * matrices Phi_l[p][k] (2 N_l^2 triangle centroids x m, binary64) to the
+ * device lazily on first use of a level.  Creates its own stream unless one
+ * is bound later.  Errors: EINVAL (bad problem), ECUDA (no device).
+ * The ctx owns its plan data; free with mlmc_destroy.                        */
+int  mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out);
+void mlmc_destroy(mlmc_ctx* ctx);
+const char* mlmc_strerror(int code);
+const char* mlmc_last_error(const mlmc_ctx* ctx);
+
+/* Geometry of mesh level l: N = 1/h, n = (N-1)^2 unknowns, P = 2N^2 triangles,
+ * band width bw = N-1.  Errors: EINVAL if l is outside 0..L_max.            */
+typedef struct { int32_t N, n, P, bw; double h; } mlmc_level_info;
+int mlmc_level_info_get(const mlmc_ctx* ctx, int level, mlmc_level_info* out);
+
+/* Device workspace needed to process `batch` coupled samples of `level` per
+ * kernel pass (larger n are processed in passes).  Host-only.               */
+int mlmc_workspace_bytes(const mlmc_ctx* ctx, int level, uint64_t batch, size_t* out);
+
+/* Lend the library a device buffer (>= 256-byte aligned) and a cudaStream_t
+ * (NULL = the ctx's own stream).  The buffer stays borrowed until rebound or
+ * mlmc_destroy.  Errors: EINVAL (NULL buffer / misaligned).                  */
+int mlmc_bind_workspace(mlmc_ctx* ctx, void* dev_ptr, size_t bytes, void* cuda_stream);
+
+/* ---- the hot path -----------------------------------------------------------
+ * mlmc_sample_level: for global sample indices first_index .. first_index+n-1
+ * of `level`: xi = Philox(seed, level, index) (R12); the KL field on the
+ * level-l and level-(l-1) meshes from the SAME xi; P1 assembly
+ * (centroid rule, R10); fine solve to tol_fine with prec_fine and
+ * coarse solve to tol_coarse with prec_coarse (R8; ignored at level 0); Q =
+ * int_D u_h; Y = Q_f - Q_c (Y = Q_f at level 0).
+ *   out_sums   host, required: the level's sums over these n samples.
+ *   per_sample optional (NULL to skip), host or dev, n * MLMC_SAMPLE_LEN doubles.
+ * Synchronises the bound stream before returning.  n = 0 is valid (zero sums).
+ * Errors: EINVAL (level, tolerances <= 0 or >= 1 for MINRES, formats),
+ * ENOMEM (no / too small workspace for one sample), ECUDA.  A solve failure
+ * is NOT an error here: it is counted in n_fail and flagged per sample.      */
+int mlmc_sample_level(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint64_t first_index,
+                      const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse,
+                      double tol_fine, double tol_coarse,
+                      mlmc_level_sums* out_sums, double* per_sample);
+
+/* Same computation, fully asynchronous on the bound stream: sums_dev (dev,
+ * MLMC_SUMS_LEN doubles) is overwritten with this call's sums; per_sample_dev
+ * optional (dev).  No host synchronisation.                                 */
+int mlmc_sample_level_async(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint64_t first_index,
+                            const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse,
+                            double tol_fine, double tol_coarse,
+                            double* sums_dev, double* per_sample_dev);
+
+/* ---- Algorithm 2 -------------------------------------------------
+ * Cross-rank reduction callback: reduce `count` doubles in place across all
+ * ranks (op 0 = SUM, 1 = MAX); return 0 on success.  Called once per round
+ * with the per-level sums; with world = 1 it may be NULL.                    */
+typedef int (*mlmc_allreduce_fn)(double* buf, int count, int op, void* user);
+
+typedef struct {
+    double  k_p;         /* Eq. (16) safety constant (0.05); <= 0 = standard MLMC */
+    double  fixed_tol;   /* standard-MLMC solver tolerance (used when k_p <= 0) */
+    double  r_bias;      /* the "r" of the bias test, R1: default 1 */
+    int32_t N_init;      /* R6: default 100 */
+    int32_t policy;      /* 0 = MINRES everywhere (paper-minres), 1 = Table 1 IR quads (paper-ir) */
+    int32_t rank, world; /* this process's slice of every level's new indices */
+    int32_t max_rounds;  /* safety cap (default 100) */
+    uint64_t seed;
+} mlmc_adaptive_opts;
+
+typedef struct {
+    double   estimate;                   /* Eq. (3): sum_l hat Y_l */
+    int32_t  L, rounds, code;            /* code: MLMC_OK or MLMC_ELMAX */
+    int32_t  reserved;
+    uint64_t N[MLMC_MAX_LEVELS];         /* samples drawn per level (all ranks) */
+    double   eps[MLMC_MAX_LEVELS];       /* eps_l of the last round */
+    double   mean[MLMC_MAX_LEVELS];      /* hat Y_l */
+    double   var[MLMC_MAX_LEVELS];       /* s_l^2 (Eq. (4), 1/N_l) */
+    double   cost[MLMC_MAX_LEVELS];      /* C_l (R5) */
+    double   solve_seconds;              /* wall time inside mlmc_sample_level calls */
+} mlmc_result;
+
+/* Run Algorithm 2 to RMSE eps (R16: TOL = eps).  Every rank calls this with
+ * identical arguments except opts->rank; all ranks return identical results.
+ * Errors: EINVAL, ECUDA, ESOLVER (a failed solve under the abort policy),
+ * ELMAX (result still filled).                                              */
+int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
+                      mlmc_allreduce_fn allreduce, void* user, mlmc_result* out);
+
+/* ---- host-only helpers (no device needed; used by the controller) ---------- */
+/* Eq. (16): eps[l] = sqrt(k_p) h_l^2 for l < L, eps[L] = k_p h_L^2. */
+int mlmc_eps_schedule(int L, double h0, double k_p, double* eps_out);
+/* Algorithm 2 step 7, real-valued N_l; C[l] must be > 0.             */
+int mlmc_optimal_samples(int nlev, const double* V, const double* C, double tol, double* N_out);
+/* The m retained KL modes (R11): 1-based 1D indices ik, jk, eigenvalues lam
+ * (descending), and the first `nroots` 1D roots w (w[i-1] for 1D mode i).    */
+int mlmc_kl_modes(double sigma2, double corr_len, int m, int32_t* ik, int32_t* jk, double* lam,
+                  double* w, int nroots);
+
+/* ---- diagnostics (device) ---------------------------------------------------
+ * Run only the field stages for samples first_index.. of `level` on the mesh
+ * of level `mesh_level` (level or level-1): xi_dev gets n*m normals, a_dev
+ * gets n*2N^2 triangle coefficients a_T (tri 2*(j*N+i) = lower, +1 = upper
+ * triangle of cell (i,j)).  Either output may be NULL.  Synchronous.        */
+int mlmc_debug_field(mlmc_ctx* ctx, int level, int mesh_level, uint64_t n, uint64_t seed,
+                     uint64_t first_index, double* xi_dev, double* a_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLMC_H */

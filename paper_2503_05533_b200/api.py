@@ -1,0 +1,223 @@
+"""Thin Python binding of the MPML C-ABI (include/mlmc.h).
+
+Argument marshalling only: every step of the hot path runs in libmlmc.so's
+sm_100a kernels.  PyTorch supplies device memory (the workspace), the CUDA
+stream and, for multi-rank runs, the torch.distributed process group that
+carries the per-round all-reduce of the level sums.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _capi as K
+
+__all__ = ["Context", "precision", "mlmc_plan_levels", "mlmc_sample_level", "mlmc_sample_level_async",
+           "mlmc_adaptive_run", "mlmc_eps_schedule", "mlmc_optimal_samples", "mlmc_kl_modes",
+           "mlmc_debug_field", "mlmc_workspace_bytes", "SUM_FIELDS"]
+
+SUM_FIELDS = ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail", "iters_f", "iters_c",
+              "iters_f_max", "iters_c_max", "reserved")
+
+
+def precision(solver: str = "minres", u_f: str = "s", u_s: str = "s", u: str = "d", u_r: str = "d",
+              max_iter: int = 0) -> K.Precision:
+    """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad."""
+    s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR}[solver]
+    return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter)
+
+
+def _as_prec(p) -> K.Precision:
+    if p is None:
+        return precision("minres")
+    if isinstance(p, K.Precision):
+        return p
+    if isinstance(p, str):
+        if p == "minres":
+            return precision("minres")
+        # quad string like "hsdd": Cholesky-IR (u_f, u_s, u, u_r)
+        return precision("chol_ir", p[0], p[1], p[2], p[3])
+    raise TypeError(p)
+
+
+@dataclass
+class LevelResult:
+    sums: dict
+    per_sample: Optional[np.ndarray]
+
+
+class Context:
+    """One mlmc_ctx on one device: plan + borrowed torch workspace + stream."""
+
+    def __init__(self, field: str = "expcov", m: int = 16, sigma2: float = 1.0, corr_len: float = 0.3,
+                 q_decay: float = 2.0, h0_inv: int = 8, L_max: int = 1, device: int = 0,
+                 workspace_bytes: int = 1 << 30, stream=None):
+        import torch
+        self._torch = torch
+        L = K.lib()
+        f = {"expcov": K.FIELD_EXPCOV_KL, "eq20": K.FIELD_PAPER_EQ20}[field]
+        self.problem = K.Problem(f, m, sigma2, corr_len, q_decay, h0_inv, 2, L_max, device)
+        ctx = C.c_void_p()
+        K.check(L.mlmc_plan_levels(C.byref(self.problem), C.byref(ctx)))
+        self.ctx = ctx
+        self.device = torch.device("cuda", device)
+        self.m = m
+        self.L_max = L_max
+        self.h0_inv = h0_inv
+        self.ws = torch.empty(int(workspace_bytes), dtype=torch.uint8, device=self.device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        K.check(L.mlmc_bind_workspace(ctx, C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws.numel()),
+                                      C.c_void_p(self.stream.cuda_stream)), ctx)
+        self._sums_dev = torch.zeros(K.MLMC_SUMS_LEN, dtype=torch.float64, device=self.device)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            K.lib().mlmc_destroy(self.ctx)
+            self.ctx = None
+
+    __del__ = close
+
+    def level_info(self, level: int) -> dict:
+        li = K.LevelInfo()
+        K.check(K.lib().mlmc_level_info_get(self.ctx, level, C.byref(li)), self.ctx)
+        return {"N": li.N, "n": li.n, "P": li.P, "bw": li.bw, "h": li.h}
+
+    def workspace_bytes(self, level: int, batch: int) -> int:
+        out = C.c_size_t()
+        K.check(K.lib().mlmc_workspace_bytes(self.ctx, level, batch, C.byref(out)), self.ctx)
+        return out.value
+
+    # ------------------------------------------------------------------ hot path
+    def sample_level(self, level: int, n: int, seed: int, first_index: int = 0, prec_fine="minres",
+                     prec_coarse=None, tol_fine: float = 1e-8, tol_coarse: Optional[float] = None,
+                     per_sample=False) -> LevelResult:
+        """mlmc_sample_level: host sums (+ optional per-sample records, host numpy or device tensor)."""
+        pf = _as_prec(prec_fine)
+        pc = _as_prec(prec_coarse if prec_coarse is not None else prec_fine)
+        tc = tol_coarse if tol_coarse is not None else tol_fine
+        sums = K.LevelSums()
+        ps = None
+        ptr = None
+        if per_sample is True or per_sample == "host":
+            ps = np.zeros((n, K.MLMC_SAMPLE_LEN), np.float64)
+            ptr = C.c_void_p(ps.ctypes.data) if n else None
+        elif per_sample == "device":
+            ps = self._torch.zeros((n, K.MLMC_SAMPLE_LEN), dtype=self._torch.float64, device=self.device)
+            ptr = C.c_void_p(ps.data_ptr()) if n else None
+        rc = K.lib().mlmc_sample_level(self.ctx, level, n, seed, first_index, C.byref(pf), C.byref(pc), tol_fine, tc,
+                                       C.byref(sums), ptr)
+        K.check(rc, self.ctx)
+        return LevelResult({f: getattr(sums, f) for f in SUM_FIELDS}, ps)
+
+    def sample_level_async(self, level: int, n: int, seed: int, first_index: int = 0, prec_fine="minres",
+                           prec_coarse=None, tol_fine: float = 1e-8, tol_coarse: Optional[float] = None,
+                           sums_out=None, per_sample_out=None):
+        """mlmc_sample_level_async: enqueue on the bound stream; sums land in a device tensor."""
+        pf = _as_prec(prec_fine)
+        pc = _as_prec(prec_coarse if prec_coarse is not None else prec_fine)
+        tc = tol_coarse if tol_coarse is not None else tol_fine
+        out = sums_out if sums_out is not None else self._sums_dev
+        rc = K.lib().mlmc_sample_level_async(self.ctx, level, n, seed, first_index, C.byref(pf), C.byref(pc),
+                                             tol_fine, tc, C.c_void_p(out.data_ptr()),
+                                             C.c_void_p(per_sample_out.data_ptr()) if per_sample_out is not None
+                                             else None)
+        K.check(rc, self.ctx)
+        return out
+
+    def debug_field(self, level: int, mesh_level: int, n: int, seed: int, first_index: int = 0):
+        """mlmc_debug_field: (xi [n, m], a [n, 2N^2]) device tensors."""
+        t = self._torch
+        N = self.h0_inv << mesh_level
+        xi = t.zeros((max(n, 1), self.m), dtype=t.float64, device=self.device)
+        a = t.zeros((max(n, 1), 2 * N * N), dtype=t.float64, device=self.device)
+        K.check(K.lib().mlmc_debug_field(self.ctx, level, mesh_level, n, seed, first_index,
+                                         C.c_void_p(xi.data_ptr()), C.c_void_p(a.data_ptr())), self.ctx)
+        return xi[:n], a[:n]
+
+    def adaptive_run(self, eps: float, k_p: float = 0.05, N_init: int = 100, policy: int = 0, seed: int = 0,
+                     fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None) -> dict:
+        """mlmc_adaptive_run (Algorithm 2).  With a torch.distributed group the per-round level sums are
+        all-reduced through it (NCCL on GPU tensors, gloo on CPU tensors)."""
+        t = self._torch
+        rank, world = 0, 1
+        cb = K.ALLREDUCE_FN(0)
+        keep = None
+        if group is not None or (t.distributed.is_available() and t.distributed.is_initialized()):
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            backend = dist.get_backend(group)
+            dev = self.device if backend == "nccl" else t.device("cpu")
+
+            def _allreduce(buf, count, op, user):
+                try:
+                    arr = np.ctypeslib.as_array(buf, shape=(count,))
+                    ten = t.from_numpy(arr.copy()).to(dev)
+                    dist.all_reduce(ten, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+                    arr[:] = ten.cpu().numpy()
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported to the C side as a failure
+                    return 1
+
+            keep = cb = K.ALLREDUCE_FN(_allreduce)
+        opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed)
+        res = K.Result()
+        rc = K.lib().mlmc_adaptive_run(self.ctx, eps, C.byref(opts), cb, None, C.byref(res))
+        del keep
+        if rc not in (K.MLMC_OK, K.MLMC_ELMAX):
+            K.check(rc, self.ctx)
+        L = res.L
+        return {"estimate": res.estimate, "L": L, "rounds": res.rounds, "code": res.code,
+                "N": list(res.N[:L + 1]), "eps": list(res.eps[:L + 1]), "mean": list(res.mean[:L + 1]),
+                "var": list(res.var[:L + 1]), "cost": list(res.cost[:L + 1]), "solve_seconds": res.solve_seconds}
+
+
+# ---------------------------------------------------------------------- C-ABI names
+def mlmc_plan_levels(**problem) -> Context:
+    return Context(**problem)
+
+
+def mlmc_sample_level(ctx: Context, *a, **k) -> LevelResult:
+    return ctx.sample_level(*a, **k)
+
+
+def mlmc_sample_level_async(ctx: Context, *a, **k):
+    return ctx.sample_level_async(*a, **k)
+
+
+def mlmc_adaptive_run(ctx: Context, eps: float, **k) -> dict:
+    return ctx.adaptive_run(eps, **k)
+
+
+def mlmc_debug_field(ctx: Context, *a, **k):
+    return ctx.debug_field(*a, **k)
+
+
+def mlmc_workspace_bytes(ctx: Context, level: int, batch: int) -> int:
+    return ctx.workspace_bytes(level, batch)
+
+
+def mlmc_eps_schedule(L: int, h0: float, k_p: float) -> list:
+    out = (C.c_double * (L + 1))()
+    K.check(K.lib().mlmc_eps_schedule(L, h0, k_p, out))
+    return list(out)
+
+
+def mlmc_optimal_samples(V, Cst, tol: float) -> list:
+    n = len(V)
+    v = (C.c_double * n)(*V)
+    c = (C.c_double * n)(*Cst)
+    out = (C.c_double * n)()
+    K.check(K.lib().mlmc_optimal_samples(n, v, c, tol, out))
+    return list(out)
+
+
+def mlmc_kl_modes(sigma2: float, corr_len: float, m: int, nroots: int = 0):
+    ik = (C.c_int32 * m)()
+    jk = (C.c_int32 * m)()
+    lam = (C.c_double * m)()
+    w = (C.c_double * max(nroots, 1))()
+    K.check(K.lib().mlmc_kl_modes(sigma2, corr_len, m, ik, jk, lam, w, nroots))
+    return np.array(ik), np.array(jk), np.array(lam), np.array(w[:nroots])

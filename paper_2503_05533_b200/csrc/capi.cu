@@ -1,0 +1,341 @@
+// capi.cu -- the C-ABI of include/mlmc.h: plan, workspace, per-level sampling and Algorithm 2.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mlmc;
+
+struct mlmc_ctx {
+    mlmc_problem pr{};
+    KLModes kl;
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::vector<double*> phi_dev;        // per level, lazily built
+    unsigned char* ws = nullptr;         // borrowed workspace
+    size_t ws_bytes = 0;
+    double* sums_dev = nullptr;          // owned: MLMC_MAX_LEVELS * kSumsLen
+    std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(mlmc_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess) return fail(ctx, MLMC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int level_N(const mlmc_ctx* c, int level) { return c->pr.h0_inv << level; }
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Workspace layout for one pass of `batch` samples of `level`.
+struct WsLayout {
+    size_t xi, a_f, a_c, rec, chunks, ctr, total;
+};
+WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch) {
+    WsLayout L{};
+    int Nf = level_N(c, level), Nc = level > 0 ? level_N(c, level - 1) : 0;
+    size_t off = 0;
+    L.xi = off;     off += align256(sizeof(double) * batch * c->pr.m);
+    L.a_f = off;    off += align256(sizeof(double) * batch * 2 * (size_t)Nf * Nf);
+    L.a_c = off;    off += align256(sizeof(double) * batch * 2 * (size_t)Nc * Nc);
+    L.rec = off;    off += align256(sizeof(double) * batch * kRecLen);
+    L.chunks = off; off += align256(sizeof(double) * kSumsLen * ((batch + kChunk - 1) / kChunk + 1));
+    L.ctr = off;    off += align256(sizeof(unsigned) * 16);
+    L.total = off;
+    return L;
+}
+
+uint64_t max_batch(const mlmc_ctx* c, int level) {
+    if (!c->ws) return 0;
+    uint64_t lo = 0, hi = 1;
+    while (ws_layout(c, level, hi).total <= c->ws_bytes && hi < (1ull << 40)) { lo = hi; hi *= 2; }
+    while (hi - lo > 1) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (ws_layout(c, level, mid).total <= c->ws_bytes) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+int ensure_phi(mlmc_ctx* ctx, int level) {
+    if (ctx->phi_dev[level]) return MLMC_OK;
+    int N = level_N(ctx, level);
+    std::vector<double> phi;
+    build_phi(ctx->pr, ctx->kl, N, phi);
+    double* d = nullptr;
+    CU(cudaMalloc(&d, phi.size() * sizeof(double)));
+    CU(cudaMemcpy(d, phi.data(), phi.size() * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->phi_dev[level] = d;
+    return MLMC_OK;
+}
+
+int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
+    if (!p) return fail(ctx, MLMC_EINVAL, "precision is NULL");
+    if (!(tol > 0.0) || !std::isfinite(tol)) return fail(ctx, MLMC_EINVAL, "tolerance must be > 0");
+    if (p->solver == MLMC_SOLVER_MINRES) {
+        if (!minres_supported(N)) return fail(ctx, MLMC_EINVAL, "MINRES kernel not built for N=" + std::to_string(N));
+        return MLMC_OK;
+    }
+    if (p->solver == MLMC_SOLVER_CHOL_IR) {
+        if (p->u != MLMC_FMT_F64 || p->u_r != MLMC_FMT_F64)
+            return fail(ctx, MLMC_EINVAL, "IR supports u = u_r = binary64 only");
+        if (!chol_supported(N, p->u_f, p->u_s))
+            return fail(ctx, MLMC_EINVAL, "Cholesky-IR (u_f, u_s) not supported for N=" + std::to_string(N));
+        return MLMC_OK;
+    }
+    return fail(ctx, MLMC_EINVAL, "unknown solver");
+}
+
+double fmt_bits(int f) { return f == MLMC_FMT_F16 ? 16 : f == MLMC_FMT_F32 ? 32 : f == MLMC_FMT_E4M3 ? 8 : 64; }
+
+// cost model R5: fixed + per-iteration work of one solve on mesh N
+void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
+    double n = (double)(N - 1) * (N - 1), bw = N - 1;
+    if (p->solver == MLMC_SOLVER_MINRES) { fixed = 0.0; step = n; }
+    else { fixed = n * bw * bw * fmt_bits(p->u_f) / 64.0; step = 4.0 * n * bw; }
+}
+
+int solve_mesh(mlmc_ctx* ctx, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb, double* rec,
+               int slot, unsigned* ctr) {
+    int n = (N - 1) * (N - 1);
+    if (p->solver == MLMC_SOLVER_MINRES) {
+        int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
+        CU(launch_minres(N, a, nb, tol, mi, rec, slot, ctr, ctx->stream));
+    } else {
+        int mi = p->max_iter > 0 ? p->max_iter : 50;
+        CU(launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ctx->stream));
+    }
+    return MLMC_OK;
+}
+
+int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint64_t first_index,
+                      const mlmc_precision* pf, const mlmc_precision* pc, double tol_f, double tol_c, double* sums_dev,
+                      double* per_sample, bool per_sample_is_dev) {
+    if (!ctx) return MLMC_EINVAL;
+    if (level < 0 || level > ctx->pr.L_max) return fail(ctx, MLMC_EINVAL, "level out of range");
+    const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
+    int rc = check_prec(ctx, pf, Nf, tol_f);
+    if (rc) return rc;
+    if (level > 0 && (rc = check_prec(ctx, pc, Nc, tol_c))) return rc;
+    if (!ctx->ws) return fail(ctx, MLMC_ENOMEM, "no workspace bound");
+    const uint64_t B = max_batch(ctx, level);
+    if (B == 0 && n > 0) return fail(ctx, MLMC_ENOMEM, "workspace too small for one sample");
+    if ((rc = ensure_phi(ctx, level))) return rc;
+    if (level > 0 && (rc = ensure_phi(ctx, level - 1))) return rc;
+    const WsLayout L = ws_layout(ctx, level, std::max<uint64_t>(B, 1));
+    double* xi = reinterpret_cast<double*>(ctx->ws + L.xi);
+    double* af = reinterpret_cast<double*>(ctx->ws + L.a_f);
+    double* ac = reinterpret_cast<double*>(ctx->ws + L.a_c);
+    double* rec = reinterpret_cast<double*>(ctx->ws + L.rec);
+    double* chunks = reinterpret_cast<double*>(ctx->ws + L.chunks);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ctx->ws + L.ctr);
+    double cff, cfs, ccf = 0, ccs = 0;
+    cost_model(pf, Nf, cff, cfs);
+    if (level > 0) cost_model(pc, Nc, ccf, ccs);
+    const int m = ctx->pr.m;
+    CU(cudaMemsetAsync(sums_dev, 0, sizeof(double) * kSumsLen, ctx->stream));
+    for (uint64_t done = 0; done < n;) {
+        const uint64_t nb = std::min<uint64_t>(B, n - done);
+        CU(launch_rng(xi, m, nb, seed, level, first_index + done, ctx->stream));
+        CU(launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, ctx->stream));
+        if (level > 0) CU(launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, ctx->stream));
+        if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, ctx->stream));
+        if ((rc = solve_mesh(ctx, Nf, pf, tol_f, af, nb, rec, 0, ctr))) return rc;
+        if (level > 0 && (rc = solve_mesh(ctx, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4))) return rc;
+        CU(launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, ctx->stream));
+        if (per_sample) {
+            double* dst = per_sample + done * kRecLen;
+            CU(cudaMemcpyAsync(dst, rec, sizeof(double) * kRecLen * nb,
+                               per_sample_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        done += nb;
+    }
+    return MLMC_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mlmc_strerror(int code) {
+    switch (code) {
+        case MLMC_OK: return "ok";
+        case MLMC_EINVAL: return "invalid argument";
+        case MLMC_ESOLVER: return "solver failure";
+        case MLMC_ELMAX: return "L_max reached with the bias test failing";
+        case MLMC_ECUDA: return "CUDA error";
+        case MLMC_ENOMEM: return "insufficient workspace / memory";
+        default: return "unknown error";
+    }
+}
+
+const char* mlmc_last_error(const mlmc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
+    mlmc_ctx* ctx = nullptr;
+    if (!problem || !out) return fail(nullptr, MLMC_EINVAL, "NULL argument");
+    const mlmc_problem& p = *problem;
+    if (p.field != MLMC_FIELD_EXPCOV_KL && p.field != MLMC_FIELD_PAPER_EQ20) return fail(nullptr, MLMC_EINVAL, "bad field");
+    if (p.m < 1 || p.m > 1024) return fail(nullptr, MLMC_EINVAL, "m out of range");
+    if (p.refine != 2) return fail(nullptr, MLMC_EINVAL, "only refine = 2 is supported");
+    if (p.h0_inv < 2 || p.L_max < 0 || p.L_max >= MLMC_MAX_LEVELS || ((long)p.h0_inv << p.L_max) > 512)
+        return fail(nullptr, MLMC_EINVAL, "mesh hierarchy out of range (h0_inv * 2^L_max <= 512)");
+    if (!(p.sigma2 > 0.0)) return fail(nullptr, MLMC_EINVAL, "sigma2 must be > 0");
+    if (p.field == MLMC_FIELD_EXPCOV_KL && !(p.corr_len > 0.0)) return fail(nullptr, MLMC_EINVAL, "corr_len must be > 0");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, MLMC_ECUDA, "no CUDA device");
+    }
+    if (p.device < 0 || p.device >= ndev) return fail(nullptr, MLMC_EINVAL, "bad device ordinal");
+    ctx = new mlmc_ctx();
+    ctx->pr = p;
+    ctx->device = p.device;
+    if (p.field == MLMC_FIELD_EXPCOV_KL) {
+        int rc = kl_modes(p.sigma2, p.corr_len, p.m, ctx->kl);
+        if (rc) { delete ctx; return fail(nullptr, rc, "KL eigenpairs failed"); }
+    }
+    ctx->phi_dev.assign(p.L_max + 1, nullptr);
+    cudaError_t e = cudaSetDevice(p.device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->sums_dev, sizeof(double) * kSumsLen * MLMC_MAX_LEVELS);
+    if (e != cudaSuccess) {
+        std::string msg = cudaGetErrorString(e);
+        mlmc_destroy(ctx);
+        return fail(nullptr, MLMC_ECUDA, msg);
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return MLMC_OK;
+}
+
+void mlmc_destroy(mlmc_ctx* ctx) {
+    if (!ctx) return;
+    for (double* d : ctx->phi_dev) if (d) cudaFree(d);
+    if (ctx->sums_dev) cudaFree(ctx->sums_dev);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+int mlmc_level_info_get(const mlmc_ctx* ctx, int level, mlmc_level_info* out) {
+    if (!ctx || !out || level < 0 || level > ctx->pr.L_max) return MLMC_EINVAL;
+    int N = level_N(ctx, level);
+    out->N = N; out->n = (N - 1) * (N - 1); out->P = 2 * N * N; out->bw = N - 1; out->h = 1.0 / N;
+    return MLMC_OK;
+}
+
+int mlmc_workspace_bytes(const mlmc_ctx* ctx, int level, uint64_t batch, size_t* out) {
+    if (!ctx || !out || level < 0 || level > ctx->pr.L_max) return MLMC_EINVAL;
+    *out = ws_layout(ctx, level, std::max<uint64_t>(batch, 1)).total;
+    return MLMC_OK;
+}
+
+int mlmc_bind_workspace(mlmc_ctx* ctx, void* dev_ptr, size_t bytes, void* cuda_stream) {
+    if (!ctx) return MLMC_EINVAL;
+    if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 255)) return fail(ctx, MLMC_EINVAL, "workspace NULL or not 256-byte aligned");
+    ctx->ws = static_cast<unsigned char*>(dev_ptr);
+    ctx->ws_bytes = bytes;
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    return MLMC_OK;
+}
+
+int mlmc_sample_level_async(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint64_t first_index,
+                            const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse, double tol_fine,
+                            double tol_coarse, double* sums_dev, double* per_sample_dev) {
+    if (!ctx || !sums_dev) return fail(ctx, MLMC_EINVAL, "NULL argument");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    return sample_level_impl(ctx, level, n, seed, first_index, prec_fine, prec_coarse, tol_fine, tol_coarse, sums_dev,
+                             per_sample_dev, true);
+}
+
+int mlmc_sample_level(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint64_t first_index,
+                      const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse, double tol_fine,
+                      double tol_coarse, mlmc_level_sums* out_sums, double* per_sample) {
+    if (!ctx || !out_sums) return fail(ctx, MLMC_EINVAL, "NULL argument");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    bool dev = per_sample ? is_device_ptr(per_sample) : false;
+    int rc = sample_level_impl(ctx, level, n, seed, first_index, prec_fine, prec_coarse, tol_fine, tol_coarse,
+                               ctx->sums_dev, per_sample, dev);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(out_sums, ctx->sums_dev, sizeof(double) * kSumsLen, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MLMC_OK;
+}
+
+int mlmc_debug_field(mlmc_ctx* ctx, int level, int mesh_level, uint64_t n, uint64_t seed, uint64_t first_index,
+                     double* xi_dev, double* a_dev) {
+    if (!ctx) return MLMC_EINVAL;
+    if (level < 0 || level > ctx->pr.L_max || mesh_level < 0 || mesh_level > level || mesh_level < level - 1)
+        return fail(ctx, MLMC_EINVAL, "bad level / mesh_level");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    int rc = ensure_phi(ctx, mesh_level);
+    if (rc) return rc;
+    double* xi = xi_dev;
+    if (!xi) CU(cudaMalloc(&xi, sizeof(double) * std::max<uint64_t>(n, 1) * ctx->pr.m));
+    CU(launch_rng(xi, ctx->pr.m, n, seed, level, first_index, ctx->stream));
+    int N = level_N(ctx, mesh_level);
+    if (a_dev) CU(launch_field(ctx->phi_dev[mesh_level], xi, a_dev, 2 * N * N, ctx->pr.m, n, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (!xi_dev) cudaFree(xi);
+    return MLMC_OK;
+}
+
+// ---------------------------------------------------------------- host helpers
+int mlmc_eps_schedule(int L, double h0, double k_p, double* eps_out) {
+    if (L < 0 || !(h0 > 0) || !(k_p > 0) || !eps_out) return MLMC_EINVAL;
+    for (int l = 0; l <= L; ++l) {
+        double hl = h0 / std::ldexp(1.0, l);
+        eps_out[l] = (l < L) ? std::sqrt(k_p) * hl * hl : k_p * hl * hl;   // Eq. (16)
+    }
+    return MLMC_OK;
+}
+
+int mlmc_optimal_samples(int nlev, const double* V, const double* C, double tol, double* N_out) {
+    if (nlev < 1 || !V || !C || !N_out || !(tol > 0)) return MLMC_EINVAL;
+    double S = 0.0;
+    for (int l = 0; l < nlev; ++l) {
+        if (!(C[l] > 0) || V[l] < 0) return MLMC_EINVAL;
+        S += std::sqrt(V[l] * C[l]);
+    }
+    for (int l = 0; l < nlev; ++l) N_out[l] = std::sqrt(V[l] / C[l]) * (2.0 / (tol * tol)) * S;
+    return MLMC_OK;
+}
+
+int mlmc_kl_modes(double sigma2, double corr_len, int m, int32_t* ik, int32_t* jk, double* lam, double* w, int nroots) {
+    KLModes kl;
+    int rc = kl_modes(sigma2, corr_len, m, kl);
+    if (rc) return rc;
+    for (int k = 0; k < m; ++k) {
+        if (ik) ik[k] = kl.ik[k];
+        if (jk) jk[k] = kl.jk[k];
+        if (lam) lam[k] = kl.lam[k];
+    }
+    if (w) for (int k = 0; k < nroots && k < (int)kl.w.size(); ++k) w[k] = kl.w[k];
+    return MLMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// controller.cpp -- Algorithm 2 (adaptive MPML) on top of mlmc_sample_level.
+//
+// Readings: R1 bias constant (r m^alpha - 1)/sqrt(2) with
+// r = 1; R2 stop when both tests pass, ELMAX if the bias test still fails at
+// L_max once the variance test passes; R3 draw max(0, ceil(N_l) - N_l^done)
+// new samples, N_l never decreases; R4 V_l = s_l^2 with 1/N_l; R5/R21 C_l =
+// mean deterministic work of one coupled sample; R6 N_init = 100; R8 coarse
+// half at eps_{l-1}; R20 samples already drawn keep their tolerance; R23 the
+// global per-level index counts all rounds; R25 the variance test uses the N_l
+// drawn so far.  Every rank runs this loop on identical all-reduced sums, so
+// every rank takes the same decisions without a broadcast.
+#include <chrono>
+#include <cstring>
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+struct LevelAcc {
+    double s[MLMC_SUMS_LEN] = {0};
+    uint64_t drawn = 0;
+};
+
+mlmc_precision minres_prec() { return mlmc_precision{MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0}; }
+
+// Table 1 (right) quads on the levels where the shared-memory
+// banded factor exists (N <= 32); u = u_r = binary64 here (the paper's level
+// 0/1 working precisions h/s are not implemented), MINRES beyond.
+mlmc_precision policy_prec(int policy, int level, int N) {
+    if (policy == 1 && N <= 32) {
+        if (level == 0) return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0};
+        if (level == 1) return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0};
+        return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0};
+    }
+    return minres_prec();
+}
+
+}  // namespace
+
+extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
+                                 mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
+    if (!ctx || !opts || !out || !(eps > 0.0)) return MLMC_EINVAL;
+    const mlmc_adaptive_opts o = *opts;
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return MLMC_EINVAL;
+    if (o.world > 1 && !allreduce) return MLMC_EINVAL;
+    mlmc_level_info li0;
+    if (mlmc_level_info_get(ctx, 0, &li0) != MLMC_OK) return MLMC_EINVAL;
+    int L_max = 0;
+    {
+        mlmc_level_info li;
+        while (L_max + 1 < MLMC_MAX_LEVELS && mlmc_level_info_get(ctx, L_max + 1, &li) == MLMC_OK) ++L_max;
+    }
+    if (L_max < 1) return MLMC_EINVAL;
+    const double h0 = li0.h, TOL = eps;
+    const int N_init = o.N_init > 0 ? o.N_init : 100;
+    const int max_rounds = o.max_rounds > 0 ? o.max_rounds : 100;
+    const double r_bias = o.r_bias > 0 ? o.r_bias : 1.0;
+    const double alpha = 2.0, mref = 2.0;
+    const double bias_c = (r_bias * std::pow(mref, alpha) - 1.0) / std::sqrt(2.0);
+
+    std::vector<LevelAcc> acc(2);
+    std::vector<double> target(2, (double)N_init);
+    std::vector<double> epsl;
+    int L = 1, rounds = 0, code = MLMC_OK;
+    double solve_s = 0.0;
+    bool failed = false;
+
+    auto stats = [&](int l, double& mean, double& var, double& cost) {
+        const double n = acc[l].s[5];
+        mean = acc[l].s[0] / n;
+        var = std::max(0.0, acc[l].s[1] / n - mean * mean);   // Eq. (4) with 1/N_l (R4)
+        cost = acc[l].s[4] / n;
+    };
+
+    while (L <= L_max && rounds < max_rounds) {
+        ++rounds;
+        epsl.assign(L + 1, o.fixed_tol > 0 ? o.fixed_tol : 1e-10);
+        if (o.k_p > 0.0) mlmc_eps_schedule(L, h0, o.k_p, epsl.data());   // step 2, Eq. (16)
+        std::vector<double> round_sums((size_t)(L + 1) * MLMC_SUMS_LEN, 0.0);
+        std::vector<uint64_t> dN(L + 1, 0);
+        for (int l = 0; l <= L; ++l) {   // steps 3-4
+            const double want = std::ceil(target[l]);
+            dN[l] = want > (double)acc[l].drawn ? (uint64_t)(want - (double)acc[l].drawn) : 0;
+            if (dN[l] == 0) continue;
+            const uint64_t lo = acc[l].drawn + dN[l] * (uint64_t)o.rank / (uint64_t)o.world;
+            const uint64_t hi = acc[l].drawn + dN[l] * (uint64_t)(o.rank + 1) / (uint64_t)o.world;
+            mlmc_level_info lf, lc;
+            mlmc_level_info_get(ctx, l, &lf);
+            if (l > 0) mlmc_level_info_get(ctx, l - 1, &lc);
+            mlmc_precision pf = policy_prec(o.policy, l, lf.N);
+            mlmc_precision pc = l > 0 ? policy_prec(o.policy, l - 1, lc.N) : pf;
+            mlmc_level_sums s{};
+            auto t0 = std::chrono::steady_clock::now();
+            int rc = mlmc_sample_level(ctx, l, hi - lo, o.seed, lo, &pf, &pc, epsl[l], l > 0 ? epsl[l - 1] : epsl[l], &s,
+                                       nullptr);
+            solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (rc) return rc;
+            std::memcpy(&round_sums[(size_t)l * MLMC_SUMS_LEN], &s, sizeof(s));
+        }
+        // one exchange per round: SUM of the additive fields, MAX of the two maxima
+        if (o.world > 1) {
+            std::vector<double> mx((size_t)(L + 1) * 2);
+            for (int l = 0; l <= L; ++l) {
+                mx[2 * l] = round_sums[(size_t)l * MLMC_SUMS_LEN + 9];
+                mx[2 * l + 1] = round_sums[(size_t)l * MLMC_SUMS_LEN + 10];
+                round_sums[(size_t)l * MLMC_SUMS_LEN + 9] = 0.0;
+                round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = 0.0;
+            }
+            if (allreduce(round_sums.data(), (int)round_sums.size(), 0, user) != 0) return MLMC_ECUDA;
+            if (allreduce(mx.data(), (int)mx.size(), 1, user) != 0) return MLMC_ECUDA;
+            for (int l = 0; l <= L; ++l) {
+                round_sums[(size_t)l * MLMC_SUMS_LEN + 9] = mx[2 * l];
+                round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = mx[2 * l + 1];
+            }
+        }
+        for (int l = 0; l <= L; ++l) {
+            const double* rs = &round_sums[(size_t)l * MLMC_SUMS_LEN];
+            for (int k = 0; k < MLMC_SUMS_LEN; ++k)
+                acc[l].s[k] = (k == 9 || k == 10) ? std::max(acc[l].s[k], rs[k]) : acc[l].s[k] + rs[k];
+            acc[l].drawn += dN[l];
+            if (rs[6] > 0) failed = true;
+        }
+        if (failed) { code = MLMC_ESOLVER; break; }
+        // steps 5-7
+        std::vector<double> mean(L + 1), V(L + 1), C(L + 1), Nopt(L + 1);
+        for (int l = 0; l <= L; ++l) stats(l, mean[l], V[l], C[l]);
+        mlmc_optimal_samples(L + 1, V.data(), C.data(), TOL, Nopt.data());
+        for (int l = 0; l <= L; ++l) target[l] = std::max((double)acc[l].drawn, Nopt[l]);   // R3
+        const bool bias_fail = std::fabs(mean[L]) > bias_c * TOL;                          // step 8
+        double vsum = 0.0;
+        for (int l = 0; l <= L; ++l) vsum += V[l] / (double)acc[l].drawn;                 // R25
+        const bool var_ok = vsum <= TOL * TOL / 2.0;
+        if (!bias_fail && var_ok) { code = MLMC_OK; break; }                                // steps 12-13
+        if (bias_fail) {
+            if (L == L_max) {
+                code = MLMC_ELMAX;
+                if (var_ok) break;
+                continue;
+            }
+            ++L;                                                                            // steps 9-10
+            acc.emplace_back();
+            target.push_back((double)N_init);
+        }
+        if (rounds == max_rounds) code = MLMC_ELMAX;
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->L = L;
+    out->rounds = rounds;
+    out->code = code;
+    out->solve_seconds = solve_s;
+    double est = 0.0;
+    for (int l = 0; l <= L && l < MLMC_MAX_LEVELS; ++l) {
+        double m_, v_, c_;
+        stats(l, m_, v_, c_);
+        out->N[l] = acc[l].drawn;
+        out->mean[l] = m_;
+        out->var[l] = v_;
+        out->cost[l] = c_;
+        out->eps[l] = l < (int)epsl.size() ? epsl[l] : 0.0;
+        est += m_;   // Eq. (3)
+    }
+    out->estimate = est;
+    return code;
+}

@@ -1,0 +1,50 @@
+// internal.h -- declarations shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/mlmc.h"
+
+namespace mlmc {
+
+// ---------------------------------------------------------------- host KL (host_kl.cpp)
+struct KLModes {
+    std::vector<int32_t> ik, jk;     // 1-based 1D mode indices
+    std::vector<double> lam;         // 2D eigenvalues, descending (R11 tie-break)
+    std::vector<double> w;           // 1D roots, w[i-1] belongs to 1D mode i
+    std::vector<double> nrm;         // 1D normalisation constants
+    double c = 0.0;                  // 1/corr_len
+};
+int kl_modes(double sigma2, double corr_len, int m, KLModes& out);
+// Phi[p*m + k] for the 2N^2 triangle centroids of an N x N mesh (R10 ordering).
+void build_phi(const mlmc_problem& pr, const KLModes& kl, int N, std::vector<double>& phi);
+
+// ---------------------------------------------------------------- kernels
+// K0: xi[b*m + k] ~ N(0,1), b < nb, for global index first_index + b.
+cudaError_t launch_rng(double* xi, int m, uint64_t nb, uint64_t seed, int level, uint64_t first_index,
+                       cudaStream_t s);
+// K1+K2: a[b*P + p] = exp(sum_k xi[b*m+k] * phi[p*m+k]).
+cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
+                         cudaStream_t s);
+// K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].
+cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
+                          int slot, unsigned* job_counter, cudaStream_t s);
+bool minres_supported(int N);
+// K4: banded Cholesky in u_f + Algorithm 1 refinement.
+cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max,
+                           double* out, int slot, unsigned* job_counter, cudaStream_t s);
+bool chol_supported(int N, int u_f, int u_s);
+// K5: per-level sums of the per-sample records into sums (accumulate = add to existing).
+cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,
+                              double cost_f_fixed, double cost_f_step, double cost_c_fixed,
+                              double cost_c_step, double* chunk_scratch, double* sums, bool accumulate,
+                              cudaStream_t s);
+
+constexpr int kSumsLen = MLMC_SUMS_LEN;
+constexpr int kRecLen = MLMC_SAMPLE_LEN;
+constexpr uint64_t kChunk = 4096;
+
+}  // namespace mlmc

@@ -1,0 +1,126 @@
+// k_field.cu -- K0 (counter-based normals) and K1+K2 (KL synthesis + exp).
+//
+// K0: xi ~ N(0,1)^m per sample from Philox4x32-10 keyed by the seed, counter
+//     (t, index_lo, index_hi, level), Box-Muller on 53-bit uniforms (R12).
+//     The paper draws omega_j ~ N(0, sigma^2); the variance is folded
+//     into the synthesis matrix Phi.
+// K1+K2: log a at the 2N^2 triangle centroids is the dense contraction
+//     G[b][p] = sum_k xi[b][k] Phi[p][k]   (truncated KL)
+//     followed by a = exp(G) (lognormal coefficient).  All binary64
+//     ("apart from the linear solver, all calculations ... in double").
+//     Register-tiled FFMA64: a 64(b) x 64(p) output tile per 256-thread CTA,
+//     4x4 outputs per thread, k staged through shared memory in chunks of 16.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace mlmc {
+
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                             uint32_t k0, uint32_t k1) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+    uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+}
+
+__device__ __forceinline__ void philox10(uint32_t ctr[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        philox_round(ctr[0], ctr[1], ctr[2], ctr[3], k0, k1);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+__global__ void rng_kernel(double* __restrict__ xi, int m, uint64_t nb, uint64_t seed, int level,
+                           uint64_t first_index) {
+    const int pairs = (m + 1) / 2;
+    const uint64_t total = nb * (uint64_t)pairs;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t b = g / pairs;
+        int t = (int)(g - b * pairs);
+        uint64_t idx = first_index + b;
+        uint32_t ctr[4] = {(uint32_t)t, (uint32_t)idx, (uint32_t)(idx >> 32), (uint32_t)level};
+        philox10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
+        const double two53inv = 1.0 / 9007199254740992.0;
+        double u1 = (fma((double)(ctr[0] >> 5), 67108864.0, (double)(ctr[1] >> 6)) + 0.5) * two53inv;
+        double u2 = (fma((double)(ctr[2] >> 5), 67108864.0, (double)(ctr[3] >> 6)) + 0.5) * two53inv;
+        double rad = sqrt(-2.0 * log(u1));
+        double s, c;
+        sincospi(2.0 * u2, &s, &c);
+        double* o = xi + b * (uint64_t)m;
+        o[2 * t] = rad * c;
+        if (2 * t + 1 < m) o[2 * t + 1] = rad * s;
+    }
+}
+
+cudaError_t launch_rng(double* xi, int m, uint64_t nb, uint64_t seed, int level, uint64_t first_index,
+                       cudaStream_t s) {
+    if (nb == 0) return cudaSuccess;
+    uint64_t total = nb * (uint64_t)((m + 1) / 2);
+    unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    rng_kernel<<<grid, 256, 0, s>>>(xi, m, nb, seed, level, first_index);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------- K1 + K2
+constexpr int FT_B = 64, FT_P = 64, FT_K = 16;
+
+__global__ void __launch_bounds__(256) field_kernel(const double* __restrict__ phi, const double* __restrict__ xi,
+                                                    double* __restrict__ a, int P, int m, int nb) {
+    __shared__ double sX[FT_K][FT_B + 1];
+    __shared__ double sP[FT_K][FT_P + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // tx -> p, ty -> b
+    const int b0 = blockIdx.y * FT_B, p0 = blockIdx.x * FT_P;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < m; k0 += FT_K) {
+        // stage xi[b0.., k0..] and phi[p0.., k0..] transposed to [k][row]
+        for (int e = threadIdx.x; e < FT_K * FT_B; e += 256) {
+            int r = e / FT_K, k = e % FT_K;
+            int b = b0 + r, kk = k0 + k;
+            sX[k][r] = (b < nb && kk < m) ? xi[(size_t)b * m + kk] : 0.0;
+            int p = p0 + r;
+            sP[k][r] = (p < P && kk < m) ? phi[(size_t)p * m + kk] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < FT_K; ++k) {
+            double xb[4], pp[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { xb[i] = sX[k][ty + 16 * i]; pp[i] = sP[k][tx + 16 * i]; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(xb[i], pp[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int b = b0 + ty + 16 * i;
+        if (b >= nb) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int p = p0 + tx + 16 * j;
+            if (p < P) a[(size_t)b * P + p] = exp(acc[i][j]);
+        }
+    }
+}
+
+cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
+                         cudaStream_t s) {
+    if (nb == 0) return cudaSuccess;
+    dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nb + FT_B - 1) / FT_B));
+    field_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb);
+    return cudaGetLastError();
+}
+
+}  // namespace mlmc

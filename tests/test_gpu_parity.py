@@ -1,0 +1,279 @@
+"""GPU parity of the C-ABI hot path against the CPU oracle (-m gpu).
+
+Inputs are the seeded synthetic workloads of BASELINE.json (see DESIGN.md
+section 5); every expected value comes from oracle/ (never from the CUDA path).
+Tolerances:
+  * RNG normals / field coefficients: binary64 rounding of different libm
+    implementations (1e-13 relative);
+  * fp64 mode (tol 1e-12): per-sample QoI to 1e-10 relative (north star);
+  * reduced-accuracy modes: |Q_gpu - Q_exact| <= tol ||b|| ||x_exact|| (1 + 1e-6)
+    + 1e-14 Q, the rigorous per-sample bound of DESIGN.md section 4 (w = b, A SPD).
+"""
+import math
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import core as oc  # noqa: E402
+from paper_2503_05533_b200 import Context, precision  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _ctx(cfg, L_max=None, ws=256 << 20):
+    return Context(field=cfg["field"], m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                   q_decay=cfg.get("q_decay", 2.0), h0_inv=cfg["h0_inv"],
+                   L_max=cfg["L_max"] if L_max is None else L_max, device=0, workspace_bytes=ws)
+
+
+def _oracle(cfg):
+    return oc.OracleProblem(cfg["field_code"], cfg["m"], cfg["sigma2"], cfg["corr_len"], cfg.get("q_decay", 2.0),
+                            cfg["h0_inv"])
+
+
+def _exact(P, N, xi):
+    """Direct fp64 solve (O-exact): Q, ||b||, ||x||."""
+    a = P.field_triangles(N, xi)
+    AB, _, b = oc.assemble(N, a)
+    x, _ = oc.chol_band_solve(AB, b)
+    return (1.0 / N) ** 2 * x.sum(), np.linalg.norm(b), np.linalg.norm(x)
+
+
+def _pmap(f, xs):
+    with ThreadPoolExecutor(8) as ex:
+        return list(ex.map(f, xs))
+
+
+# ============================================================================ K0 / K1+K2
+@pytest.mark.parametrize("cfg_name", ["C1", "C2", "C4", "EQ20"])
+def test_rng_and_field_match_oracle(cfg_name):
+    cfg = W.CONFIGS[cfg_name]
+    ctx = _ctx(cfg, L_max=2)
+    P = _oracle(cfg)
+    for level, mesh in ((0, 0), (2, 2), (2, 1)):
+        n = 37
+        xi, a = ctx.debug_field(level, mesh, n, seed=11, first_index=1000)
+        xi, a = xi.cpu().numpy(), a.cpu().numpy()
+        N = cfg["h0_inv"] << mesh
+        for k in (0, 5, 36):
+            ref_xi = oc.normals(11, level, 1000 + k, cfg["m"])
+            assert np.allclose(xi[k], ref_xi, rtol=1e-13, atol=1e-14)
+            ref_a = P.field_triangles(N, ref_xi)
+            assert np.max(np.abs(a[k] / ref_a - 1)) < 1e-12
+    ctx.close()
+
+
+# ============================================================================ C1: fp64 parity 1e-10
+def test_C1_fp64_per_sample_parity_and_sums():
+    cfg = W.CONFIGS["C1"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    for level, n in ((0, cfg["N"][0]), (1, cfg["N"][1])):
+        r = ctx.sample_level(level, n, seed=cfg["seed"], prec_fine="minres", tol_fine=1e-12, tol_coarse=1e-12,
+                             per_sample=True)
+        ps = r.per_sample
+        assert np.all(ps[:, 6:8] == 0)
+        assert np.all(ps[:, 4] <= 1e-12 * 1.01)
+        idx = list(range(0, n, max(1, n // 150))) + [n - 1]
+        refs = _pmap(lambda k: P.coupled_sample(level, cfg["seed"], k), idx)
+        for k, ref in zip(idx, refs):
+            assert abs(ps[k, 0] / ref[0] - 1) < 1e-10, (level, k, ps[k, 0], ref[0])
+            if level > 0:
+                assert abs(ps[k, 1] / ref[1] - 1) < 1e-10
+            else:
+                assert ps[k, 1] == 0.0
+        y = ps[:, 0] - ps[:, 1]
+        s = r.sums
+        assert s["n"] == n and s["n_fail"] == 0
+        assert abs(s["sum_y"] - y.sum()) <= 1e-13 * np.abs(y).sum()
+        assert abs(s["sum_y2"] - (y * y).sum()) <= 1e-13 * (y * y).sum()
+        assert s["iters_f"] == ps[:, 2].sum() and s["iters_f_max"] == ps[:, 2].max()
+        nf = (cfg["h0_inv"] << level) - 1
+        expect_cost = (ps[:, 2] * nf ** 2).sum() + (ps[:, 3] * ((cfg["h0_inv"] << (level - 1)) - 1) ** 2).sum() \
+            if level else (ps[:, 2] * nf ** 2).sum()
+        assert abs(s["sum_cost"] - expect_cost) <= 1e-12 * expect_cost
+    ctx.close()
+
+
+def test_minres_iteration_counts_track_oracle():
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    for level, tf, tc in ((1, 1e-5, 1e-4), (2, 1e-6, 1e-5), (3, 1e-8, 1e-6)):
+        n = 12
+        ps = ctx.sample_level(level, n, seed=1, tol_fine=tf, tol_coarse=tc, per_sample=True).per_sample
+        refs = _pmap(lambda k: P.coupled_sample(level, 1, k, solver=oc.SOLVER_MINRES, tol_f=tf, tol_c=tc), range(n))
+        for k, ref in enumerate(refs):
+            assert abs(ps[k, 2] - ref[2]) <= 2 and abs(ps[k, 3] - ref[3]) <= 2, (level, k, ps[k, 2:4], ref[2:4])
+            assert abs(ps[k, 0] - ref[0]) <= 2.5 * tf * ref[0]
+    ctx.close()
+
+
+# ============================================================================ C2: reduced accuracy bound
+@pytest.mark.parametrize("level", [0, 1, 2, 3])
+def test_C2_reduced_accuracy_within_residual_bound(level):
+    cfg = W.CONFIGS["C2"]
+    tols = cfg["tols"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    n = {0: 4097, 1: 600, 2: 120, 3: 24}[level]             # spans several chunks / a ragged tail
+    tf = tols[level]
+    tc = tols[level - 1] if level else tf
+    r = ctx.sample_level(level, n, seed=cfg["seed"], tol_fine=tf, tol_coarse=tc, per_sample=True)
+    ps = r.per_sample
+    assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
+    assert np.all(ps[:, 4] <= tf * 1.01)
+    if level:
+        assert np.all(ps[:, 5] <= tc * 1.01)
+    idx = sorted(set(list(range(0, n, max(1, n // 40))) + [n - 1]))
+    Nf = cfg["h0_inv"] << level
+
+    def chk(k):
+        xi = oc.normals(cfg["seed"], level, k, cfg["m"])
+        out = [_exact(P, Nf, xi)]
+        if level:
+            out.append(_exact(P, Nf // 2, xi))
+        return out
+
+    for k, ex in zip(idx, _pmap(chk, idx)):
+        qf, bn, xn = ex[0]
+        assert abs(ps[k, 0] - qf) <= tf * bn * xn * (1 + 1e-6) + 1e-14 * qf, (level, k)
+        if level:
+            qc, bn, xn = ex[1]
+            assert abs(ps[k, 1] - qc) <= tc * bn * xn * (1 + 1e-6) + 1e-14 * qc
+    ctx.close()
+
+
+# ============================================================================ C3: Cholesky + IR
+@pytest.mark.parametrize("uf,us", [("h", "s"), ("s", "s"), ("s", "d"), ("h", "d")])
+def test_C3_cholesky_ir_parity(uf, us):
+    cfg = W.CONFIGS["C3"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    prec = precision("chol_ir", uf, us)
+    for level, n in ((0, 3000), (1, 300), (2, 40)):
+        r = ctx.sample_level(level, n, seed=3, prec_fine=prec, prec_coarse=prec, tol_fine=1e-10, tol_coarse=1e-10,
+                             per_sample=True)
+        ps = r.per_sample
+        assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
+        assert np.all(ps[:, 4] < 1e-10) and (level == 0 or np.all(ps[:, 5] < 1e-10))
+        steps = ps[:, 2]
+        if uf == "s":
+            assert steps.max() <= 3                                   # SC-9: 1-2 steps
+        else:
+            assert steps.mean() <= 1.5 * {0: 4.0, 1: 6.2, 2: 11.9}[level] + 1
+        idx = list(range(0, n, max(1, n // 25)))
+        Nf = cfg["h0_inv"] << level
+        exs = _pmap(lambda k: _exact(P, Nf, oc.normals(3, level, k, cfg["m"])), idx)
+        for k, (q, bn, xn) in zip(idx, exs):
+            assert abs(ps[k, 0] - q) <= 1e-10 * bn * xn * (1 + 1e-6) + 1e-14 * q
+        # the oracle's emulated Algorithm 1 converges to the same tolerance on the same systems
+        for k in idx[:3]:
+            xi = oc.normals(3, level, k, cfg["m"])
+            o = P.solve_mesh(Nf, xi, oc.SOLVER_IR, tol=1e-10, quad=uf + us + "dd", max_iter=50)
+            assert o["status"] == 0 and abs(o["iters"] - steps[k]) <= max(2, 0.5 * o["iters"])
+    ctx.close()
+
+
+def test_ir_limiting_accuracy_reported_as_failure():
+    """Corollary 3.3: an fp16 factor with fp32 corrections cannot reach 1e-14."""
+    cfg = W.CONFIGS["C3"]
+    ctx = _ctx(cfg)
+    r = ctx.sample_level(1, 8, seed=0, prec_fine=precision("chol_ir", "h", "s", max_iter=30),
+                         prec_coarse=precision("chol_ir", "h", "s", max_iter=30), tol_fine=1e-15, tol_coarse=1e-15,
+                         per_sample=True)
+    assert r.sums["n_fail"] == 8 and np.all(r.per_sample[:, 6] == 1)
+    ctx.close()
+
+
+# ============================================================================ edge cases
+def test_edge_cases_empty_ragged_batching_and_determinism():
+    cfg = W.CONFIGS["C2"]
+    small = _ctx(cfg, ws=3 << 20)          # forces several passes per call
+    big = _ctx(cfg)
+    r0 = big.sample_level(1, 0, seed=1, tol_fine=1e-6, tol_coarse=1e-5)
+    assert r0.sums["n"] == 0 and r0.sums["sum_y"] == 0.0
+    a = big.sample_level(1, 1000, seed=1, tol_fine=1e-6, tol_coarse=1e-5, per_sample=True).per_sample
+    b = small.sample_level(1, 1000, seed=1, tol_fine=1e-6, tol_coarse=1e-5, per_sample=True).per_sample
+    c = big.sample_level(1, 1000, seed=1, tol_fine=1e-6, tol_coarse=1e-5, per_sample=True).per_sample
+    assert np.array_equal(a, b) and np.array_equal(a, c)            # batch- and run-independent
+    d = big.sample_level(1, 7, seed=1, first_index=501, tol_fine=1e-6, tol_coarse=1e-5, per_sample=True).per_sample
+    assert np.array_equal(d, a[501:508])                             # counter-based sample identity
+    e = big.sample_level(1, 1, seed=2, tol_fine=1e-6, tol_coarse=1e-5, per_sample=True).per_sample
+    assert not np.array_equal(e[0], a[0])
+    # loose tolerance stops early; max_iter exhaustion is counted as a failure, not an error
+    f = big.sample_level(2, 5, seed=1, tol_fine=0.5, tol_coarse=0.5, per_sample=True).per_sample
+    assert np.all(f[:, 2] <= 3)
+    g = big.sample_level(2, 5, seed=1, prec_fine=precision("minres", max_iter=3),
+                         prec_coarse=precision("minres", max_iter=3), tol_fine=1e-12, tol_coarse=1e-12)
+    assert g.sums["n_fail"] == 5
+    with pytest.raises(RuntimeError):
+        big.sample_level(9, 5, seed=1)                              # level beyond L_max
+    with pytest.raises(RuntimeError):
+        big.sample_level(1, 5, seed=1, tol_fine=0.0)
+    # device-resident per-sample export equals the host export
+    dev = big.sample_level(1, 1000, seed=1, tol_fine=1e-6, tol_coarse=1e-5, per_sample="device").per_sample
+    assert np.array_equal(dev.cpu().numpy(), a)
+    small.close()
+    big.close()
+
+
+def test_full_size_C2_step_sampled_parity():
+    """BASELINE configs[1] at full size in the launch configuration bench.py times
+    (one call per level); sampled outputs against the oracle bound."""
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    P = _oracle(cfg)
+    tols = cfg["tols"]
+    for level, n in enumerate(cfg["N"]):
+        tf, tc = tols[level], (tols[level - 1] if level else tols[0])
+        r = ctx.sample_level(level, n, seed=cfg["seed"], tol_fine=tf, tol_coarse=tc, per_sample=True)
+        ps = r.per_sample
+        assert r.sums["n"] == n and r.sums["n_fail"] == 0
+        rng = np.random.default_rng(level)
+        idx = sorted(rng.choice(n, size=min(n, 6), replace=False))
+        Nf = cfg["h0_inv"] << level
+        for k in idx:
+            q, bn, xn = _exact(P, Nf, oc.normals(cfg["seed"], level, int(k), cfg["m"]))
+            assert abs(ps[k, 0] - q) <= tf * bn * xn * (1 + 1e-6) + 1e-14 * q
+        y = ps[:, 0] - ps[:, 1]
+        assert abs(r.sums["sum_y"] - y.sum()) <= 1e-12 * np.abs(y).sum()
+    ctx.close()
+
+
+# ============================================================================ Algorithm 2 end to end
+def test_adaptive_C4_matches_oracle_controller():
+    """Algorithm 2 through the C-ABI vs the oracle's Algorithm 2 driven by oracle
+    MINRES samples (same seeds): identical decisions, estimate within 1e-9."""
+    from oracle import mlmc as om
+    cfg = W.CONFIGS["C4"]
+    ctx = _ctx(cfg, ws=512 << 20)
+    g = ctx.adaptive_run(cfg["eps"], k_p=0.05, N_init=100, seed=4)
+    assert g["code"] == 0
+    P = _oracle(cfg)
+
+    def sampler(l, first, count, tf, tc):
+        outs = _pmap(lambda k: P.coupled_sample(l, 4, k, solver=oc.SOLVER_MINRES, tol_f=tf, tol_c=tc),
+                     range(first, first + count))
+        nf = ((cfg["h0_inv"] << l) - 1) ** 2
+        nc = ((cfg["h0_inv"] << (l - 1)) - 1) ** 2 if l else 0
+        return [o[0] - o[1] for o in outs], [o[2] * nf + o[3] * nc for o in outs]
+
+    o = om.adaptive_mpml(sampler, cfg["eps"], 1 / cfg["h0_inv"], 0.05, L_max=cfg["L_max"], N_init=100)
+    assert o.L == g["L"]
+    if o.N == g["N"]:
+        assert abs(o.estimate - g["estimate"]) < 1e-9
+    else:   # a +-1 MINRES iteration can move C_l and hence ceil(N_l) by a sample or two
+        assert all(abs(a - b) <= max(2, 0.02 * b) for a, b in zip(o.N, g["N"])), (o.N, g["N"])
+        assert abs(o.estimate - g["estimate"]) < 0.1 * cfg["eps"]
+    assert 0.030 < g["estimate"] < 0.038
+    ctx.close()
