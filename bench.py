@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py -- one JSON line for the MPML hot path on B200 (contract in DESIGN.md section 8).
+
+Step = one pass of the whole hot path over BASELINE.json configs[1] (C2): for
+each level l = 0..3 of h = 1/8..1/64, N_l = (20000, 5000, 1200, 300) coupled
+samples: Philox normals -> KL field (m = 64) on both meshes -> P1 assembly ->
+fp64 MINRES to the level tolerance (1e-4, 1e-5, 1e-6, 1e-8; coarse half at
+tol_{l-1}) -> QoI -> level sums; with N > 1 ranks each rank draws its own
+index range (weak scaling) and the level sums are all-reduced over NCCL once
+per step (the method's only exchange).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle (oracle/, plain C) on a bounded sample of
+the same workload on this box's host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "coupled level samples/sec per level and time-to-eps at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "coupled samples/s"
+FLOPS_PER_NODE_ITER = 25.0       # algorithmic fp64 flops of one MINRES iteration per unknown
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+CPU_SAMPLE = {0: 2048, 1: 384, 2: 96, 3: 24}       # cpu_baseline: bounded oracle sample per level
+REF_SAMPLE = {0: 256, 1: 64, 2: 16, 3: 8}          # --impl reference: per-step oracle sample per level
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip cpu_baseline / e2e / time-to-eps")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        t0 = time.time()
+        while self.p and time.time() - t0 < 5 and os.path.getsize(self.f.name) == 0:
+            time.sleep(0.05)
+
+    def stop(self) -> dict:
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+        rows = []
+        for ln in open(self.f.name):
+            v = [x.strip() for x in ln.split(",")]
+            if len(v) >= 7 and v[0].isdigit():
+                rows.append(v)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_rate(sample: dict, seed: int, threads: int) -> dict:
+    """Run the oracle's MINRES path (same algorithm, same tolerances) on `sample[l]`
+    coupled samples per level; returns per-level rates and the C2-mix rate."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import core as oc
+    cfg = W.CONFIGS["C2"]
+    P = oc.OracleProblem(0, cfg["m"], cfg["sigma2"], cfg["corr_len"], 2.0, cfg["h0_inv"])
+    tols = cfg["tols"]
+    rates = {}
+    cpu_s = 0.0
+    with ThreadPoolExecutor(threads) as ex:
+        for l, s in sample.items():
+            tf, tc = tols[l], (tols[l - 1] if l else tols[0])
+            t0 = time.perf_counter()
+            c0 = time.process_time()
+            list(ex.map(lambda k: P.coupled_sample(l, seed, 10_000_000 + k, solver=oc.SOLVER_MINRES, tol_f=tf,
+                                                   tol_c=tc), range(s)))
+            cpu_s += time.process_time() - c0
+            rates[l] = s / (time.perf_counter() - t0)
+    step_s = sum(cfg["N"][l] / rates[l] for l in rates)
+    return {"rates": rates, "value": sum(cfg["N"]) / step_s, "cpu_seconds": cpu_s}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import core as oc
+    oc.build()
+    threads = os.cpu_count() or 1
+    cfg = W.CONFIGS["C2"]
+    for _ in range(args.warmup):
+        oracle_rate({0: 16, 1: 4, 2: 2, 3: 1}, cfg["seed"], threads)
+    t0 = time.perf_counter()
+    vals = [oracle_rate(REF_SAMPLE, cfg["seed"], threads)["value"] for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    sample = "per step: " + ", ".join(f"{REF_SAMPLE[l]} level-{l} samples" for l in REF_SAMPLE) + \
+             " of configs[1], rate extrapolated to the (20000,5000,1200,300) mix"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(cfg["N"]) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1] (C2): 4-level MLMC h=1/8..1/64, KL m=64, fixed N, MINRES tols "
+                                   "1e-4/1e-5/1e-6/1e-8", "engine": "CPU oracle (oracle/oracle.c), textbook MINRES"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "--gpus > 1 must be launched with torch.distributed.run"}))
+        sys.exit(2)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import __graft_entry__
+    if rank == 0 or world == 1:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2503_05533_b200 import Context, precision
+
+    cfg = W.CONFIGS["C2"]
+    Nl, tols, seed, m = cfg["N"], cfg["tols"], cfg["seed"], cfg["m"]
+    L = len(Nl)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(field="expcov", m=m, sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
+                  L_max=L - 1, device=local, workspace_bytes=2 << 30, stream=stream)
+    minres = precision("minres")
+    sums = torch.zeros((L, 12), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
+
+    def step(i, evs=None):
+        for l in range(L):
+            first = (i * world + rank) * Nl[l]
+            ctx.sample_level_async(l, Nl[l], seed, first, minres, minres, tols[l], tols[l - 1] if l else tols[0],
+                                   sums_out=sums[l])
+            if evs is not None:
+                evs[l].record(stream)
+        if world > 1:
+            dist.all_reduce(sums)
+
+    clocks = ClockSampler(local)
+    for i in range(args.warmup):
+        step(10_000 + i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.profile_enable(True)
+    total_ms, level_ms = 0.0, [0.0] * L
+    iters_f = [0.0] * L
+    iters_c = [0.0] * L
+    for i in range(args.steps):
+        flush.zero_()                                                   # L2 flush between timed steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(L)]
+        e_end = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(i, evs)
+        e_end.record(stream)                                            # after the NCCL all-reduce (N > 1)
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e_end)
+        prev = e0
+        for l in range(L):
+            level_ms[l] += prev.elapsed_time(evs[l])
+            prev = evs[l]
+        s = sums.cpu().numpy()
+        for l in range(L):
+            iters_f[l] += s[l, 7]
+            iters_c[l] += s[l, 8]
+    torch.cuda.synchronize()
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    clk = clocks.stop()
+
+    n_step = sum(Nl)
+    value = world * n_step * args.steps / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+    per_level = {f"l{l}": {"h": f"1/{cfg['h0_inv'] << l}", "N": Nl[l], "tol_fine": tols[l],
+                           "samples_per_s": world * Nl[l] * args.steps / (level_ms[l] / 1e3),
+                           "ms": level_ms[l] / args.steps,
+                           "mean_iters_fine": iters_f[l] / (Nl[l] * args.steps),
+                           "mean_iters_coarse": iters_c[l] / (Nl[l] * args.steps) if l else 0.0}
+                 for l in range(L)}
+
+    # ---- roofline of the dominant kernel (largest device time in the timed region)
+    kern = sorted(prof, key=lambda r: -r[3])
+    top = kern[0]
+    n_of = lambda N: (N - 1) ** 2
+    work = 0.0                                                          # node-iterations of this kernel class
+    if top[0] == "minres":
+        for l in range(L):
+            if (cfg["h0_inv"] << l) == top[1]:
+                work += iters_f[l] * n_of(top[1])
+            if l and (cfg["h0_inv"] << (l - 1)) == top[1]:
+                work += iters_c[l] * n_of(top[1])
+    flops_per_launch = FLOPS_PER_NODE_ITER * work / max(top[2], 1)
+    ms_per_launch = top[3] / max(top[2], 1)
+    achieved = flops_per_launch / (ms_per_launch / 1e3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{top[0]}_N{top[1]}")
+        except Exception:
+            traffic = None
+    roofline = {"kernel": f"{top[0]} N={top[1]}", "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md section 6)",
+                "share_of_step": top[3] / total_ms if world == 1 else None,
+                "launches": top[2], "ms_per_launch": ms_per_launch}
+    kernels = [{"kernel": f"{k}", "N": N, "launches": n, "ms_total": ms, "share": ms / total_ms}
+               for (k, N, n, ms) in kern]
+    gpu_launches = int(sum(r[2] for r in prof))
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1] (C2): 4-level MLMC h=1/8..1/64, KL m=64 (var 1, corr 0.3), "
+                                   "N=(20000,5000,1200,300) per GPU, fp64 MINRES tols 1e-4/1e-5/1e-6/1e-8",
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"samples sharded, {world} rank(s), NCCL all-reduce of level sums"},
+            "per_level": per_level, "roofline": roofline, "kernels": kernels, "gpu_launches": gpu_launches,
+            "clocks": clk}
+
+    if not args.no_extras:
+        line["e2e"] = e2e_leg(ctx, cfg, args, world, rank, torch, np, dist)
+        line["time_to_eps"] = adaptive_leg(args, world, rank, local, torch, dist)
+        if rank == 0 and world == 1:
+            from oracle import core as oc
+            oc.build()
+            threads = os.cpu_count() or 1
+            r = oracle_rate(CPU_SAMPLE, seed, threads)
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "oracle",
+                                    "sample": ", ".join(f"{CPU_SAMPLE[l]} level-{l}" for l in CPU_SAMPLE) +
+                                              " coupled samples of configs[1] through the oracle's textbook MINRES "
+                                              "(same tolerances), rate extrapolated to the full step mix",
+                                    "cpu_seconds": r["cpu_seconds"],
+                                    "per_level_samples_per_s": r["rates"]}
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_leg(ctx, cfg, args, world, rank, torch, np, dist):
+    """Same metric through the public C-ABI call with HOST buffers: pinned host xi in,
+    per-sample records + level sums out, copies inside the timed region."""
+    Nl, tols, m = cfg["N"], cfg["tols"], cfg["m"]
+    rng = np.random.default_rng(1000 + rank)
+    xs = [torch.from_numpy(rng.standard_normal((n, m))).pin_memory() for n in Nl]
+    outs = [torch.zeros((n, 8), dtype=torch.float64).pin_memory() for n in Nl]
+    from paper_2503_05533_b200 import precision
+    mr = precision("minres")
+
+    def step():
+        for l in range(len(Nl)):
+            ctx.sample_level_xi(l, xs[l], mr, mr, tols[l], tols[l - 1] if l else tols[0], per_sample=outs[l])
+    for _ in range(max(1, args.warmup)):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    return {"value": world * sum(Nl) * args.steps / el, "unit": UNIT,
+            "h2d_bytes_per_step": int(sum(Nl) * m * 8), "d2h_bytes_per_step": int(sum(Nl) * 8 * 8 + len(Nl) * 96),
+            "api": "mlmc_sample_level_xi (host pinned xi in, host per-sample records + level sums out)",
+            "clock": "host wall clock around the synchronous calls, max over ranks"}
+
+
+def adaptive_leg(args, world, rank, local, torch, dist):
+    """Time-to-eps of Algorithm 2 for configs[3] (C4) and configs[4] (C5), wall clock, max over ranks."""
+    from paper_2503_05533_b200 import Context
+    out = {}
+    for name in ("C4", "C5"):
+        cfg = W.CONFIGS[name]
+        ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                      h0_inv=cfg["h0_inv"], L_max=cfg["L_max"], device=local, workspace_bytes=1 << 30)
+        for l in range(4):                                   # plan warm-up: Phi_l uploaded before timing
+            ctx.sample_level(l, 1, cfg["seed"] + 99, tol_fine=1e-2, tol_coarse=1e-2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = ctx.adaptive_run(cfg["eps"], k_p=cfg["k_p"], N_init=100, seed=cfg["seed"],
+                             group=dist.group.WORLD if world > 1 else None)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=torch.device("cuda", local))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        out[name] = {"eps": cfg["eps"], "seconds": el, "L": r["L"], "N": r["N"], "rounds": r["rounds"],
+                     "estimate": r["estimate"], "code": r["code"]}
+        ctx.close()
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,27 @@ int mlmc_sample_level_async(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed,
                             double tol_fine, double tol_coarse,
                             double* sums_dev, double* per_sample_dev);
 
+/* Caller-supplied random inputs (the SPEC's coupled_sample(l, omega)): exactly
+ * mlmc_sample_level, except that xi (n*m doubles, sample-major, host or dev;
+ * standard normals, the field's omega = sqrt(sigma2) xi) replaces the Philox
+ * draw.  Host xi is copied to the device inside the call (pinned memory makes
+ * the copy asynchronous).  Errors as mlmc_sample_level; EINVAL if xi is NULL. */
+int mlmc_sample_level_xi(mlmc_ctx* ctx, int level, uint64_t n, const double* xi,
+                         const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse,
+                         double tol_fine, double tol_coarse,
+                         mlmc_level_sums* out_sums, double* per_sample);
+
+/* ---- per-kernel accounting -------------------------------------------------
+ * Every kernel the library launches is counted per (kind, mesh N); with
+ * profiling on, each launch is also bracketed by CUDA events on the bound
+ * stream and its device time accumulated.  mlmc_profile_enable resets the
+ * table; mlmc_profile_read synchronises the stream and copies at most `max`
+ * entries (count = entries available).                                       */
+enum { MLMC_K_RNG = 0, MLMC_K_FIELD = 1, MLMC_K_MINRES = 2, MLMC_K_CHOL_IR = 3, MLMC_K_SUMS = 4 };
+typedef struct { int32_t kind; int32_t N; uint64_t launches; double ms; } mlmc_kernel_stat;
+int mlmc_profile_enable(mlmc_ctx* ctx, int on);
+int mlmc_profile_read(mlmc_ctx* ctx, mlmc_kernel_stat* stats, int max, int* count);
+
 /* ---- Algorithm 2 -------------------------------------------------
  * Cross-rank reduction callback: reduce `count` doubles in place across all
  * ranks (op 0 = SUM, 1 = MAX); return 0 on success.  Called once per round

@@ -52,7 +52,13 @@ class Result(C.Structure):
                 ("cost", C.c_double * MLMC_MAX_LEVELS), ("solve_seconds", C.c_double)]
 
 
-ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_void_p)
+class KernelStat(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("N", C.c_int32), ("launches", C.c_uint64), ("ms", C.c_double)]
+
+
+KERNEL_KINDS = {0: "rng", 1: "field", 2: "minres", 3: "chol_ir", 4: "sums"}
+
+ALLREDUCE_FN =C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_void_p)
 
 _lib = None
 
@@ -95,6 +101,10 @@ def lib():
     L.mlmc_kl_modes.argtypes = [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), dp, dp,
                                 C.c_int]
     L.mlmc_debug_field.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]
+    L.mlmc_sample_level_xi.argtypes = [vp, C.c_int, C.c_uint64, vp, C.POINTER(Precision), C.POINTER(Precision),
+                                       C.c_double, C.c_double, C.POINTER(LevelSums), vp]
+    L.mlmc_profile_enable.argtypes = [vp, C.c_int]
+    L.mlmc_profile_read.argtypes = [vp, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)]
     _lib = L
     return L
 

@@ -127,6 +127,35 @@ class Context:
         K.check(rc, self.ctx)
         return out
 
+    def sample_level_xi(self, level: int, xi, prec_fine="minres", prec_coarse=None, tol_fine: float = 1e-8,
+                        tol_coarse: Optional[float] = None, per_sample=None) -> LevelResult:
+        """mlmc_sample_level_xi: caller-supplied standard normals xi [n, m] (host numpy / pinned torch
+        tensor, or a device tensor) instead of the Philox draw.  per_sample: None, a host buffer
+        (numpy / pinned tensor, [n, 8] float64) or a device tensor, filled in place."""
+        pf = _as_prec(prec_fine)
+        pc = _as_prec(prec_coarse if prec_coarse is not None else prec_fine)
+        tc = tol_coarse if tol_coarse is not None else tol_fine
+        n = int(xi.shape[0])
+        xptr = xi.ctypes.data if isinstance(xi, np.ndarray) else xi.data_ptr()
+        pptr = None
+        if per_sample is not None:
+            pptr = per_sample.ctypes.data if isinstance(per_sample, np.ndarray) else per_sample.data_ptr()
+        sums = K.LevelSums()
+        K.check(K.lib().mlmc_sample_level_xi(self.ctx, level, n, C.c_void_p(xptr), C.byref(pf), C.byref(pc),
+                                             tol_fine, tc, C.byref(sums), C.c_void_p(pptr) if pptr else None),
+                self.ctx)
+        return LevelResult({f: getattr(sums, f) for f in SUM_FIELDS}, per_sample)
+
+    def profile_enable(self, on: bool = True):
+        K.check(K.lib().mlmc_profile_enable(self.ctx, 1 if on else 0), self.ctx)
+
+    def profile_read(self) -> list:
+        """[(kind, N, launches, ms)] per kernel class since profile_enable (synchronises the stream)."""
+        arr = (K.KernelStat * 64)()
+        cnt = C.c_int()
+        K.check(K.lib().mlmc_profile_read(self.ctx, arr, 64, C.byref(cnt)), self.ctx)
+        return [(K.KERNEL_KINDS.get(s.kind, str(s.kind)), s.N, s.launches, s.ms) for s in arr[:min(cnt.value, 64)]]
+
     def debug_field(self, level: int, mesh_level: int, n: int, seed: int, first_index: int = 0):
         """mlmc_debug_field: (xi [n, m], a [n, 2N^2]) device tensors."""
         t = self._torch

@@ -24,6 +24,12 @@ struct mlmc_ctx {
     size_t ws_bytes = 0;
     double* sums_dev = nullptr;          // owned: MLMC_MAX_LEVELS * kSumsLen
     std::string err;
+    // per-kernel accounting
+    bool prof_on = false;
+    std::vector<mlmc_kernel_stat> stats;
+    struct Pending { int idx; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace {
@@ -43,6 +49,46 @@ int fail(mlmc_ctx* c, int code, const std::string& msg) {
     } while (0)
 
 int level_N(const mlmc_ctx* c, int level) { return c->pr.h0_inv << level; }
+
+int stat_index(mlmc_ctx* c, int kind, int N) {
+    for (size_t i = 0; i < c->stats.size(); ++i)
+        if (c->stats[i].kind == kind && c->stats[i].N == N) return (int)i;
+    c->stats.push_back(mlmc_kernel_stat{kind, N, 0, 0.0});
+    return (int)c->stats.size() - 1;
+}
+
+cudaEvent_t take_event(mlmc_ctx* c) {
+    if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void drain_pending(mlmc_ctx* c) {
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess)
+            c->stats[p.idx].ms += ms;
+        c->ev_pool.push_back(p.a);
+        c->ev_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
+// Launch through f(), counting it and (profiling on) timing it with events on the ctx stream.
+template <class F>
+cudaError_t counted(mlmc_ctx* c, int kind, int N, F&& f) {
+    int idx = stat_index(c, kind, N);
+    c->stats[idx].launches++;
+    if (!c->prof_on) return f();
+    cudaEvent_t a = take_event(c), b = take_event(c);
+    cudaEventRecord(a, c->stream);
+    cudaError_t e = f();
+    cudaEventRecord(b, c->stream);
+    c->pending.push_back({idx, a, b});
+    if (c->pending.size() > 4096) drain_pending(c);
+    return e;
+}
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -118,17 +164,19 @@ int solve_mesh(mlmc_ctx* ctx, int N, const mlmc_precision* p, double tol, const 
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
-        CU(launch_minres(N, a, nb, tol, mi, rec, slot, ctr, ctx->stream));
+        CU(counted(ctx, MLMC_K_MINRES, N, [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, ctx->stream); }));
     } else {
         int mi = p->max_iter > 0 ? p->max_iter : 50;
-        CU(launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ctx->stream));
+        CU(counted(ctx, MLMC_K_CHOL_IR, N,
+                   [&] { return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ctx->stream); }));
     }
     return MLMC_OK;
 }
 
 int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint64_t first_index,
                       const mlmc_precision* pf, const mlmc_precision* pc, double tol_f, double tol_c, double* sums_dev,
-                      double* per_sample, bool per_sample_is_dev) {
+                      double* per_sample, bool per_sample_is_dev, const double* xi_in = nullptr,
+                      bool xi_in_is_dev = false) {
     if (!ctx) return MLMC_EINVAL;
     if (level < 0 || level > ctx->pr.L_max) return fail(ctx, MLMC_EINVAL, "level out of range");
     const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
@@ -154,13 +202,23 @@ int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
     CU(cudaMemsetAsync(sums_dev, 0, sizeof(double) * kSumsLen, ctx->stream));
     for (uint64_t done = 0; done < n;) {
         const uint64_t nb = std::min<uint64_t>(B, n - done);
-        CU(launch_rng(xi, m, nb, seed, level, first_index + done, ctx->stream));
-        CU(launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, ctx->stream));
-        if (level > 0) CU(launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, ctx->stream));
+        CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, ctx->stream));
+        if (xi_in) {
+            CU(cudaMemcpyAsync(xi, xi_in + done * m, sizeof(double) * m * nb,
+                               xi_in_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+        } else {
+            CU(counted(ctx, MLMC_K_RNG, 0, [&] { return launch_rng(xi, m, nb, seed, level, first_index + done, ctx->stream); }));
+        }
+        CU(counted(ctx, MLMC_K_FIELD, Nf, [&] { return launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, ctx->stream); }));
+        if (level > 0)
+            CU(counted(ctx, MLMC_K_FIELD, Nc,
+                       [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, ctx->stream); }));
         if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, ctx->stream));
         if ((rc = solve_mesh(ctx, Nf, pf, tol_f, af, nb, rec, 0, ctr))) return rc;
         if (level > 0 && (rc = solve_mesh(ctx, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4))) return rc;
-        CU(launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, ctx->stream));
+        CU(counted(ctx, MLMC_K_SUMS, Nf, [&] {
+            return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, ctx->stream);
+        }));
         if (per_sample) {
             double* dst = per_sample + done * kRecLen;
             CU(cudaMemcpyAsync(dst, rec, sizeof(double) * kRecLen * nb,
@@ -235,6 +293,9 @@ int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
 
 void mlmc_destroy(mlmc_ctx* ctx) {
     if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    drain_pending(ctx);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (double* d : ctx->phi_dev) if (d) cudaFree(d);
     if (ctx->sums_dev) cudaFree(ctx->sums_dev);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -283,6 +344,39 @@ int mlmc_sample_level(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
     if (rc) return rc;
     CU(cudaMemcpyAsync(out_sums, ctx->sums_dev, sizeof(double) * kSumsLen, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    return MLMC_OK;
+}
+
+int mlmc_sample_level_xi(mlmc_ctx* ctx, int level, uint64_t n, const double* xi, const mlmc_precision* prec_fine,
+                         const mlmc_precision* prec_coarse, double tol_fine, double tol_coarse, mlmc_level_sums* out_sums,
+                         double* per_sample) {
+    if (!ctx || !out_sums || (!xi && n > 0)) return fail(ctx, MLMC_EINVAL, "NULL argument");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    bool dev = per_sample ? is_device_ptr(per_sample) : false;
+    bool xdev = xi ? is_device_ptr(xi) : false;
+    int rc = sample_level_impl(ctx, level, n, 0, 0, prec_fine, prec_coarse, tol_fine, tol_coarse, ctx->sums_dev,
+                               per_sample, dev, xi, xdev);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(out_sums, ctx->sums_dev, sizeof(double) * kSumsLen, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MLMC_OK;
+}
+
+int mlmc_profile_enable(mlmc_ctx* ctx, int on) {
+    if (!ctx) return MLMC_EINVAL;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    drain_pending(ctx);
+    ctx->stats.clear();
+    ctx->prof_on = on != 0;
+    return MLMC_OK;
+}
+
+int mlmc_profile_read(mlmc_ctx* ctx, mlmc_kernel_stat* stats, int max, int* count) {
+    if (!ctx || !count) return MLMC_EINVAL;
+    CU(cudaStreamSynchronize(ctx->stream));
+    drain_pending(ctx);
+    *count = (int)ctx->stats.size();
+    for (int i = 0; i < max && i < (int)ctx->stats.size(); ++i) stats[i] = ctx->stats[i];
     return MLMC_OK;
 }
 

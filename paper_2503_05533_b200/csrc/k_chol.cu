@@ -251,7 +251,6 @@ static cudaError_t run_chol(const double* a, uint64_t nb, double tol, int i_max,
     uint64_t need = (nb + C::WARPS - 1) / C::WARPS;
     uint64_t grid = std::min<uint64_t>(need, (uint64_t)bps * sms);
     if (grid == 0) return cudaSuccess;
-    cudaMemsetAsync(ctr, 0, sizeof(unsigned), s);
     kern<<<(unsigned)grid, 32 * C::WARPS, C::SMEM, s>>>(a, (int)nb, tol, i_max, out, slot, ctr);
     return cudaGetLastError();
 }

@@ -278,7 +278,6 @@ static cudaError_t run_minres(const double* a, uint64_t nb, double tol, int max_
     uint64_t need = (nb + C::GROUPS - 1) / C::GROUPS;
     uint64_t grid = std::min<uint64_t>(need, (uint64_t)blocks_per_sm * sms);
     if (grid == 0) return cudaSuccess;
-    cudaMemsetAsync(ctr, 0, sizeof(unsigned), s);
     kern<<<(unsigned)grid, C::BLOCK, C::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr);
     return cudaGetLastError();
 }
