@@ -80,14 +80,21 @@ typedef struct {
  *   u_f (MLMC_FMT_F16 / F32 / F64), initial and correction substitutions in
  *   u_s (F32 or F64, R24), residual in u_r and x in u (both F64), stop when
  *   ||r||/||b|| < tol, at most max_iter refinement steps.
- * max_iter = 0 selects the default (MINRES: 4n+100, IR: 50).                 */
+ * max_iter = 0 selects the default (MINRES: 4n+100, IR: 50).
+ * MINRES reports phibar_k/||b|| (the stopping quantity) as the residual and
+ * computes Q from the scalar recurrence of 1^T x_k (R26); with
+ * MLMC_FLAG_VERIFY it also carries x_k and reports ||b - A x_k||/||b||, with
+ * bit-identical Q.                                                          */
 typedef enum { MLMC_FMT_E4M3 = 0, MLMC_FMT_F16 = 1, MLMC_FMT_F32 = 2, MLMC_FMT_F64 = 3 } mlmc_fmt;
 typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1 } mlmc_solver;
+
+#define MLMC_FLAG_VERIFY 1   /* MINRES: also keep x_k and report the true residual */
 
 typedef struct {
     int32_t solver;
     int32_t u_f, u_s, u, u_r;   /* mlmc_fmt codes */
     int32_t max_iter;
+    int32_t flags;              /* MLMC_FLAG_* */
 } mlmc_precision;
 
 /* ---- per-level accumulators (Algorithm 2 steps 5-6) -------------
@@ -108,7 +115,8 @@ typedef struct {
 
 /* per-sample record (MLMC_SAMPLE_LEN doubles, sample-major):
  *   [0] Q_f   [1] Q_c (0 at level 0)   [2] iters_f   [3] iters_c
- *   [4] true relative residual ||b-Ax||/||b|| of the fine solve  [5] coarse
+ *   [4] relative residual of the fine solve (MINRES: phibar/||b||, or the true
+ *       ||b-Ax||/||b|| with MLMC_FLAG_VERIFY; IR: the true residual)  [5] coarse
  *   [6] status_f  [7] status_c   (0 ok, 1 max_iter, 2 breakdown, 3 non-finite) */
 
 typedef struct mlmc_ctx mlmc_ctx;   /* opaque */
@@ -134,9 +142,10 @@ int mlmc_level_info_get(const mlmc_ctx* ctx, int level, mlmc_level_info* out);
  * kernel pass (larger n are processed in passes).  Host-only.               */
 int mlmc_workspace_bytes(const mlmc_ctx* ctx, int level, uint64_t batch, size_t* out);
 
-/* Lend the library a device buffer (>= 256-byte aligned) and a cudaStream_t
- * (NULL = the ctx's own stream).  The buffer stays borrowed until rebound or
- * mlmc_destroy.  Errors: EINVAL (NULL buffer / misaligned).                  */
+/* Lend the library a device buffer (>= 256-byte aligned) and the cudaStream_t
+ * all later work is ordered on (NULL = the legacy default stream; before the
+ * first bind the ctx uses a private stream).  The buffer stays borrowed until
+ * rebound or mlmc_destroy.  Errors: EINVAL (NULL buffer / misaligned).       */
 int mlmc_bind_workspace(mlmc_ctx* ctx, void* dev_ptr, size_t bytes, void* cuda_stream);
 
 /* ---- the hot path -----------------------------------------------------------
@@ -164,6 +173,19 @@ int mlmc_sample_level_async(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed,
                             const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse,
                             double tol_fine, double tol_coarse,
                             double* sums_dev, double* per_sample_dev);
+
+/* Several levels in one call (one round of Algorithm 2 step 4 / one fixed-N
+ * MLMC pass): entry q processes n[q] samples of levels[q] from first_index[q]
+ * with prec_fine[q]/prec_coarse[q] and tol_fine[q]/tol_coarse[q] exactly as
+ * mlmc_sample_level would, and writes its sums to sums_dev + q*MLMC_SUMS_LEN
+ * (dev).  The levels run concurrently on internal priority streams (largest
+ * work first) forked from and joined back into the bound stream; the bound
+ * workspace is split between them (each level still processes its samples in
+ * passes if its slice is small).  Asynchronous; errors as mlmc_sample_level. */
+int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, uint64_t seed,
+                             const uint64_t* first_index, const mlmc_precision* prec_fine,
+                             const mlmc_precision* prec_coarse, const double* tol_fine,
+                             const double* tol_coarse, double* sums_dev);
 
 /* Caller-supplied random inputs (the SPEC's coupled_sample(l, omega)): exactly
  * mlmc_sample_level, except that xi (n*m doubles, sample-major, host or dev;
@@ -221,6 +243,18 @@ typedef struct {
  * ELMAX (result still filled).                                              */
 int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
                       mlmc_allreduce_fn allreduce, void* user, mlmc_result* out);
+
+/* The same controller over a caller-supplied host sampler instead of the GPU
+ * (CPU tests of Algorithm 2 and of the multi-rank exchange).  The sampler must
+ * draw n coupled samples of `level` from global index first_index with the
+ * given precisions / tolerances and write MLMC_SUMS_LEN sums; return 0 on
+ * success.  Levels 0..L_max, h_l = 1/(h0_inv 2^l).  Host-only.              */
+typedef int (*mlmc_level_sampler_fn)(int level, uint64_t n, uint64_t first_index,
+                                     const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse,
+                                     double tol_fine, double tol_coarse, double* sums, void* user);
+int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts* opts,
+                           mlmc_level_sampler_fn sampler, void* sampler_user,
+                           mlmc_allreduce_fn allreduce, void* user, mlmc_result* out);
 
 /* ---- host-only helpers (no device needed; used by the controller) ---------- */
 /* Eq. (16): eps[l] = sqrt(k_p) h_l^2 for l < L, eps[L] = k_p h_L^2. */

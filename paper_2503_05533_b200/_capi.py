@@ -17,6 +17,7 @@ MLMC_MAX_LEVELS, MLMC_SUMS_LEN, MLMC_SAMPLE_LEN = 16, 12, 8
 FIELD_EXPCOV_KL, FIELD_PAPER_EQ20 = 0, 1
 FMT = {"q": 0, "h": 1, "s": 2, "d": 3}
 SOLVER_MINRES, SOLVER_CHOL_IR = 0, 1
+FLAG_VERIFY = 1
 
 
 class Problem(C.Structure):
@@ -27,7 +28,7 @@ class Problem(C.Structure):
 
 class Precision(C.Structure):
     _fields_ = [("solver", C.c_int32), ("u_f", C.c_int32), ("u_s", C.c_int32), ("u", C.c_int32),
-                ("u_r", C.c_int32), ("max_iter", C.c_int32)]
+                ("u_r", C.c_int32), ("max_iter", C.c_int32), ("flags", C.c_int32)]
 
 
 class LevelSums(C.Structure):
@@ -58,7 +59,9 @@ class KernelStat(C.Structure):
 
 KERNEL_KINDS = {0: "rng", 1: "field", 2: "minres", 3: "chol_ir", 4: "sums"}
 
-ALLREDUCE_FN =C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_void_p)
+LEVEL_SAMPLER_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(Precision),
+                               C.POINTER(Precision), C.c_double, C.c_double, C.POINTER(C.c_double), C.c_void_p)
 
 _lib = None
 
@@ -103,6 +106,11 @@ def lib():
     L.mlmc_debug_field.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]
     L.mlmc_sample_level_xi.argtypes = [vp, C.c_int, C.c_uint64, vp, C.POINTER(Precision), C.POINTER(Precision),
                                        C.c_double, C.c_double, C.POINTER(LevelSums), vp]
+    L.mlmc_sample_levels_async.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.c_uint64,
+                                           C.POINTER(C.c_uint64), C.POINTER(Precision), C.POINTER(Precision), dp, dp,
+                                           vp]
+    L.mlmc_adaptive_run_host.argtypes = [C.c_int, C.c_int, C.c_double, C.POINTER(AdaptiveOpts), LEVEL_SAMPLER_FN, vp,
+                                         ALLREDUCE_FN, vp, C.POINTER(Result)]
     L.mlmc_profile_enable.argtypes = [vp, C.c_int]
     L.mlmc_profile_read.argtypes = [vp, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)]
     _lib = L

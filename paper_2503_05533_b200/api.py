@@ -24,10 +24,11 @@ SUM_FIELDS = ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail", 
 
 
 def precision(solver: str = "minres", u_f: str = "s", u_s: str = "s", u: str = "d", u_r: str = "d",
-              max_iter: int = 0) -> K.Precision:
-    """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad."""
+              max_iter: int = 0, verify: bool = False) -> K.Precision:
+    """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad.
+    verify=True (MINRES): also carry x_k and report the true residual."""
     s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR}[solver]
-    return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter)
+    return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter, K.FLAG_VERIFY if verify else 0)
 
 
 def _as_prec(p) -> K.Precision:
@@ -127,6 +128,19 @@ class Context:
         K.check(rc, self.ctx)
         return out
 
+    def sample_levels_async(self, levels, n, seed: int, first_index, prec_fine, prec_coarse, tol_fine, tol_coarse,
+                            sums_out):
+        """mlmc_sample_levels_async: all listed levels concurrently; sums_out is a device tensor
+        [len(levels), 12] (row q = levels[q])."""
+        k = len(levels)
+        pf = (K.Precision * k)(*[_as_prec(p) for p in prec_fine])
+        pc = (K.Precision * k)(*[_as_prec(p) for p in prec_coarse])
+        rc = K.lib().mlmc_sample_levels_async(self.ctx, k, (C.c_int * k)(*levels), (C.c_uint64 * k)(*n), seed,
+                                              (C.c_uint64 * k)(*first_index), pf, pc, (C.c_double * k)(*tol_fine),
+                                              (C.c_double * k)(*tol_coarse), C.c_void_p(sums_out.data_ptr()))
+        K.check(rc, self.ctx)
+        return sums_out
+
     def sample_level_xi(self, level: int, xi, prec_fine="minres", prec_coarse=None, tol_fine: float = 1e-8,
                         tol_coarse: Optional[float] = None, per_sample=None) -> LevelResult:
         """mlmc_sample_level_xi: caller-supplied standard normals xi [n, m] (host numpy / pinned torch
@@ -170,37 +184,71 @@ class Context:
                      fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None) -> dict:
         """mlmc_adaptive_run (Algorithm 2).  With a torch.distributed group the per-round level sums are
         all-reduced through it (NCCL on GPU tensors, gloo on CPU tensors)."""
-        t = self._torch
-        rank, world = 0, 1
-        cb = K.ALLREDUCE_FN(0)
-        keep = None
-        if group is not None or (t.distributed.is_available() and t.distributed.is_initialized()):
-            import torch.distributed as dist
-            rank, world = dist.get_rank(group), dist.get_world_size(group)
-            backend = dist.get_backend(group)
-            dev = self.device if backend == "nccl" else t.device("cpu")
-
-            def _allreduce(buf, count, op, user):
-                try:
-                    arr = np.ctypeslib.as_array(buf, shape=(count,))
-                    ten = t.from_numpy(arr.copy()).to(dev)
-                    dist.all_reduce(ten, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
-                    arr[:] = ten.cpu().numpy()
-                    return 0
-                except Exception:  # noqa: BLE001 -- reported to the C side as a failure
-                    return 1
-
-            keep = cb = K.ALLREDUCE_FN(_allreduce)
+        rank, world, cb = _allreduce_callback(group, self.device)
         opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed)
         res = K.Result()
         rc = K.lib().mlmc_adaptive_run(self.ctx, eps, C.byref(opts), cb, None, C.byref(res))
-        del keep
         if rc not in (K.MLMC_OK, K.MLMC_ELMAX):
             K.check(rc, self.ctx)
-        L = res.L
-        return {"estimate": res.estimate, "L": L, "rounds": res.rounds, "code": res.code,
-                "N": list(res.N[:L + 1]), "eps": list(res.eps[:L + 1]), "mean": list(res.mean[:L + 1]),
-                "var": list(res.var[:L + 1]), "cost": list(res.cost[:L + 1]), "solve_seconds": res.solve_seconds}
+        return _result_dict(res)
+
+
+def _result_dict(res) -> dict:
+    L = res.L
+    return {"estimate": res.estimate, "L": L, "rounds": res.rounds, "code": res.code,
+            "N": list(res.N[:L + 1]), "eps": list(res.eps[:L + 1]), "mean": list(res.mean[:L + 1]),
+            "var": list(res.var[:L + 1]), "cost": list(res.cost[:L + 1]), "solve_seconds": res.solve_seconds}
+
+
+def _allreduce_callback(group, device):
+    """(rank, world, mlmc_allreduce_fn) for the torch.distributed group (or the default one if
+    initialised); NCCL groups reduce a tensor on `device`, others (gloo) on the CPU."""
+    import torch as t
+    if group is None and not (t.distributed.is_available() and t.distributed.is_initialized()):
+        return 0, 1, K.ALLREDUCE_FN(0)
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = device if dist.get_backend(group) == "nccl" else t.device("cpu")
+
+    def _allreduce(buf, count, op, user):
+        try:
+            arr = np.ctypeslib.as_array(buf, shape=(count,))
+            ten = t.from_numpy(arr.copy()).to(dev)
+            dist.all_reduce(ten, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+            arr[:] = ten.cpu().numpy()
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the C side as a failure
+            return 1
+
+    return rank, world, K.ALLREDUCE_FN(_allreduce)
+
+
+def mlmc_adaptive_run_host(h0_inv: int, L_max: int, eps: float, sampler, k_p: float = 0.05, N_init: int = 100,
+                           policy: int = 0, seed: int = 0, fixed_tol: float = 1e-10, r_bias: float = 1.0,
+                           max_rounds: int = 100, group=None) -> dict:
+    """The library's Algorithm 2 over a host sampler (no GPU): ``sampler(level, n, first_index, prec_fine,
+    prec_coarse, tol_fine, tol_coarse) -> 12 level sums``.  Used by the CPU tests of the controller and
+    of the multi-rank exchange (gloo)."""
+    rank, world, cb = _allreduce_callback(group, None)
+
+    def _cb(level, n, first, pf, pc, tf, tc, sums, user):
+        try:
+            out = sampler(level, int(n), int(first), pf.contents, pc.contents, tf, tc)
+            for k in range(K.MLMC_SUMS_LEN):
+                sums[k] = float(out[k])
+            return 0
+        except Exception:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    scb = K.LEVEL_SAMPLER_FN(_cb)
+    opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed)
+    res = K.Result()
+    rc = K.lib().mlmc_adaptive_run_host(h0_inv, L_max, eps, C.byref(opts), scb, None, cb, None, C.byref(res))
+    if rc not in (K.MLMC_OK, K.MLMC_ELMAX):
+        K.check(rc)
+    return _result_dict(res)
 
 
 # ---------------------------------------------------------------------- C-ABI names

@@ -30,6 +30,10 @@ struct mlmc_ctx {
     struct Pending { int idx; cudaEvent_t a, b; };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> ev_pool;
+    // concurrent levels (mlmc_sample_levels_async): priority streams + fork/join events
+    std::vector<cudaStream_t> aux;
+    std::vector<cudaEvent_t> join_ev;
+    cudaEvent_t fork_ev = nullptr;
 };
 
 namespace {
@@ -75,16 +79,16 @@ void drain_pending(mlmc_ctx* c) {
     c->pending.clear();
 }
 
-// Launch through f(), counting it and (profiling on) timing it with events on the ctx stream.
+// Launch through f(), counting it and (profiling on) timing it with events on its stream.
 template <class F>
-cudaError_t counted(mlmc_ctx* c, int kind, int N, F&& f) {
+cudaError_t counted(mlmc_ctx* c, cudaStream_t st, int kind, int N, F&& f) {
     int idx = stat_index(c, kind, N);
     c->stats[idx].launches++;
     if (!c->prof_on) return f();
     cudaEvent_t a = take_event(c), b = take_event(c);
-    cudaEventRecord(a, c->stream);
+    cudaEventRecord(a, st);
     cudaError_t e = f();
-    cudaEventRecord(b, c->stream);
+    cudaEventRecord(b, st);
     c->pending.push_back({idx, a, b});
     if (c->pending.size() > 4096) drain_pending(c);
     return e;
@@ -110,16 +114,22 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch) {
     return L;
 }
 
-uint64_t max_batch(const mlmc_ctx* c, int level) {
-    if (!c->ws) return 0;
+uint64_t max_batch(const mlmc_ctx* c, int level, size_t bytes) {
     uint64_t lo = 0, hi = 1;
-    while (ws_layout(c, level, hi).total <= c->ws_bytes && hi < (1ull << 40)) { lo = hi; hi *= 2; }
+    while (ws_layout(c, level, hi).total <= bytes && hi < (1ull << 40)) { lo = hi; hi *= 2; }
     while (hi - lo > 1) {
         uint64_t mid = lo + (hi - lo) / 2;
-        if (ws_layout(c, level, mid).total <= c->ws_bytes) lo = mid; else hi = mid;
+        if (ws_layout(c, level, mid).total <= bytes) lo = mid; else hi = mid;
     }
     return lo;
 }
+
+// Where one level's pipeline runs: a slice of the workspace and a stream.
+struct Exec {
+    unsigned char* ws;
+    size_t bytes;
+    cudaStream_t st;
+};
 
 int ensure_phi(mlmc_ctx* ctx, int level) {
     if (ctx->phi_dev[level]) return MLMC_OK;
@@ -159,16 +169,84 @@ void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
     else { fixed = n * bw * bw * fmt_bits(p->u_f) / 64.0; step = 4.0 * n * bw; }
 }
 
-int solve_mesh(mlmc_ctx* ctx, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb, double* rec,
-               int slot, unsigned* ctr) {
+int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
+               double* rec, int slot, unsigned* ctr) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
-        CU(counted(ctx, MLMC_K_MINRES, N, [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, ctx->stream); }));
+        bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
+        CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
+                   [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, ex.st); }));
     } else {
         int mi = p->max_iter > 0 ? p->max_iter : 50;
-        CU(counted(ctx, MLMC_K_CHOL_IR, N,
-                   [&] { return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ctx->stream); }));
+        CU(counted(ctx, ex.st, MLMC_K_CHOL_IR, N,
+                   [&] { return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ex.st); }));
+    }
+    return MLMC_OK;
+}
+
+int validate_level(mlmc_ctx* ctx, int level, const mlmc_precision* pf, const mlmc_precision* pc, double tol_f,
+                   double tol_c) {
+    if (level < 0 || level > ctx->pr.L_max) return fail(ctx, MLMC_EINVAL, "level out of range");
+    const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
+    int rc = check_prec(ctx, pf, Nf, tol_f);
+    if (rc) return rc;
+    if (level > 0 && (rc = check_prec(ctx, pc, Nc, tol_c))) return rc;
+    if ((rc = ensure_phi(ctx, level))) return rc;
+    if (level > 0 && (rc = ensure_phi(ctx, level - 1))) return rc;
+    return MLMC_OK;
+}
+
+// One level's pipeline (K0 -> K1 -> K3/K4 fine + coarse -> K5) in passes that fit ex.ws, on ex.st.
+int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t seed, uint64_t first_index,
+              const mlmc_precision* pf, const mlmc_precision* pc, double tol_f, double tol_c, double* sums_dev,
+              double* per_sample, bool per_sample_is_dev, const double* xi_in, bool xi_in_is_dev) {
+    const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
+    uint64_t B = max_batch(ctx, level, ex.bytes);
+    if (B == 0 && n > 0) return fail(ctx, MLMC_ENOMEM, "workspace too small for one sample");
+    // passes made of whole 4096-sample chunks: the chunked sums then do not depend on the pass size
+    if (B > kChunk && B < n) B = (B / kChunk) * kChunk;
+    const WsLayout L = ws_layout(ctx, level, std::max<uint64_t>(B, 1));
+    double* xi = reinterpret_cast<double*>(ex.ws + L.xi);
+    double* af = reinterpret_cast<double*>(ex.ws + L.a_f);
+    double* ac = reinterpret_cast<double*>(ex.ws + L.a_c);
+    double* rec = reinterpret_cast<double*>(ex.ws + L.rec);
+    double* chunks = reinterpret_cast<double*>(ex.ws + L.chunks);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ex.ws + L.ctr);
+    double cff, cfs, ccf = 0, ccs = 0;
+    cost_model(pf, Nf, cff, cfs);
+    if (level > 0) cost_model(pc, Nc, ccf, ccs);
+    const int m = ctx->pr.m;
+    const cudaStream_t st = ex.st;
+    int rc;
+    CU(cudaMemsetAsync(sums_dev, 0, sizeof(double) * kSumsLen, st));
+    for (uint64_t done = 0; done < n;) {
+        const uint64_t nb = std::min<uint64_t>(B, n - done);
+        CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, st));
+        if (xi_in) {
+            CU(cudaMemcpyAsync(xi, xi_in + done * m, sizeof(double) * m * nb,
+                               xi_in_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        } else {
+            CU(counted(ctx, st, MLMC_K_RNG, 0,
+                       [&] { return launch_rng(xi, m, nb, seed, level, first_index + done, st); }));
+        }
+        CU(counted(ctx, st, MLMC_K_FIELD, Nf,
+                   [&] { return launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, st); }));
+        if (level > 0)
+            CU(counted(ctx, st, MLMC_K_FIELD, Nc,
+                       [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, st); }));
+        if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, st));
+        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr))) return rc;
+        if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4))) return rc;
+        CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
+            return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, st);
+        }));
+        if (per_sample) {
+            double* dst = per_sample + done * kRecLen;
+            CU(cudaMemcpyAsync(dst, rec, sizeof(double) * kRecLen * nb,
+                               per_sample_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        }
+        done += nb;
     }
     return MLMC_OK;
 }
@@ -178,56 +256,22 @@ int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
                       double* per_sample, bool per_sample_is_dev, const double* xi_in = nullptr,
                       bool xi_in_is_dev = false) {
     if (!ctx) return MLMC_EINVAL;
-    if (level < 0 || level > ctx->pr.L_max) return fail(ctx, MLMC_EINVAL, "level out of range");
-    const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
-    int rc = check_prec(ctx, pf, Nf, tol_f);
+    int rc = validate_level(ctx, level, pf, pc, tol_f, tol_c);
     if (rc) return rc;
-    if (level > 0 && (rc = check_prec(ctx, pc, Nc, tol_c))) return rc;
     if (!ctx->ws) return fail(ctx, MLMC_ENOMEM, "no workspace bound");
-    const uint64_t B = max_batch(ctx, level);
-    if (B == 0 && n > 0) return fail(ctx, MLMC_ENOMEM, "workspace too small for one sample");
-    if ((rc = ensure_phi(ctx, level))) return rc;
-    if (level > 0 && (rc = ensure_phi(ctx, level - 1))) return rc;
-    const WsLayout L = ws_layout(ctx, level, std::max<uint64_t>(B, 1));
-    double* xi = reinterpret_cast<double*>(ctx->ws + L.xi);
-    double* af = reinterpret_cast<double*>(ctx->ws + L.a_f);
-    double* ac = reinterpret_cast<double*>(ctx->ws + L.a_c);
-    double* rec = reinterpret_cast<double*>(ctx->ws + L.rec);
-    double* chunks = reinterpret_cast<double*>(ctx->ws + L.chunks);
-    unsigned* ctr = reinterpret_cast<unsigned*>(ctx->ws + L.ctr);
-    double cff, cfs, ccf = 0, ccs = 0;
-    cost_model(pf, Nf, cff, cfs);
-    if (level > 0) cost_model(pc, Nc, ccf, ccs);
-    const int m = ctx->pr.m;
-    CU(cudaMemsetAsync(sums_dev, 0, sizeof(double) * kSumsLen, ctx->stream));
-    for (uint64_t done = 0; done < n;) {
-        const uint64_t nb = std::min<uint64_t>(B, n - done);
-        CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, ctx->stream));
-        if (xi_in) {
-            CU(cudaMemcpyAsync(xi, xi_in + done * m, sizeof(double) * m * nb,
-                               xi_in_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
-        } else {
-            CU(counted(ctx, MLMC_K_RNG, 0, [&] { return launch_rng(xi, m, nb, seed, level, first_index + done, ctx->stream); }));
-        }
-        CU(counted(ctx, MLMC_K_FIELD, Nf, [&] { return launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, ctx->stream); }));
-        if (level > 0)
-            CU(counted(ctx, MLMC_K_FIELD, Nc,
-                       [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, ctx->stream); }));
-        if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, ctx->stream));
-        if ((rc = solve_mesh(ctx, Nf, pf, tol_f, af, nb, rec, 0, ctr))) return rc;
-        if (level > 0 && (rc = solve_mesh(ctx, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4))) return rc;
-        CU(counted(ctx, MLMC_K_SUMS, Nf, [&] {
-            return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, ctx->stream);
-        }));
-        if (per_sample) {
-            double* dst = per_sample + done * kRecLen;
-            CU(cudaMemcpyAsync(dst, rec, sizeof(double) * kRecLen * nb,
-                               per_sample_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
-        }
-        done += nb;
-    }
+    return run_level(ctx, Exec{ctx->ws, ctx->ws_bytes, ctx->stream}, level, n, seed, first_index, pf, pc, tol_f, tol_c,
+                     sums_dev, per_sample, per_sample_is_dev, xi_in, xi_in_is_dev);
+}
+
+}  // namespace
+
+int mlmc::copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host) {
+    CU(cudaMemcpyAsync(host, dev, sizeof(double) * kSumsLen * nlev, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return MLMC_OK;
 }
+
+namespace {
 
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes at{};
@@ -293,7 +337,10 @@ int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
 
 void mlmc_destroy(mlmc_ctx* ctx) {
     if (!ctx) return;
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    for (cudaStream_t s : ctx->aux) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    for (cudaEvent_t e : ctx->join_ev) cudaEventDestroy(e);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     drain_pending(ctx);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (double* d : ctx->phi_dev) if (d) cudaFree(d);
@@ -320,7 +367,7 @@ int mlmc_bind_workspace(mlmc_ctx* ctx, void* dev_ptr, size_t bytes, void* cuda_s
     if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 255)) return fail(ctx, MLMC_EINVAL, "workspace NULL or not 256-byte aligned");
     ctx->ws = static_cast<unsigned char*>(dev_ptr);
     ctx->ws_bytes = bytes;
-    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);   // NULL = the legacy default stream
     return MLMC_OK;
 }
 
@@ -344,6 +391,73 @@ int mlmc_sample_level(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
     if (rc) return rc;
     CU(cudaMemcpyAsync(out_sums, ctx->sums_dev, sizeof(double) * kSumsLen, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    return MLMC_OK;
+}
+
+int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, uint64_t seed,
+                             const uint64_t* first_index, const mlmc_precision* prec_fine,
+                             const mlmc_precision* prec_coarse, const double* tol_fine, const double* tol_coarse,
+                             double* sums_dev) {
+    if (!ctx || nlev < 1 || nlev > MLMC_MAX_LEVELS || !levels || !n || !first_index || !prec_fine || !prec_coarse ||
+        !tol_fine || !tol_coarse || !sums_dev)
+        return fail(ctx, MLMC_EINVAL, "NULL / bad argument");
+    if (!ctx->ws) return fail(ctx, MLMC_ENOMEM, "no workspace bound");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    for (int q = 0; q < nlev; ++q) {
+        int rc = validate_level(ctx, levels[q], &prec_fine[q], &prec_coarse[q], tol_fine[q], tol_coarse[q]);
+        if (rc) return rc;
+    }
+    // largest work first (proxy: samples x unknowns x N, i.e. ~ iterations x unknowns)
+    std::vector<int> order(nlev);
+    std::vector<double> cost(nlev);
+    for (int q = 0; q < nlev; ++q) {
+        order[q] = q;
+        const double N = (double)level_N(ctx, levels[q]);
+        cost[q] = (double)n[q] * (N - 1) * (N - 1) * N;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    // workspace slices: each level's single-pass need if everything fits, else proportional
+    std::vector<size_t> need(nlev);
+    size_t total = 0;
+    for (int q = 0; q < nlev; ++q) {
+        need[q] = ws_layout(ctx, levels[q], std::max<uint64_t>(n[q], 1)).total;
+        total += need[q];
+    }
+    std::vector<size_t> slice(nlev);
+    for (int q = 0; q < nlev; ++q)
+        slice[q] = total <= ctx->ws_bytes ? need[q]
+                                          : (size_t)((double)ctx->ws_bytes * ((double)need[q] / (double)total)) & ~(size_t)255;
+    // streams: one per level, highest priority for the largest level
+    if ((int)ctx->aux.size() < nlev) {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        while ((int)ctx->aux.size() < nlev) {
+            const int k = (int)ctx->aux.size();
+            const int prio = std::max(greatest, least - (least - greatest) * (MLMC_MAX_LEVELS - k) / MLMC_MAX_LEVELS);
+            cudaStream_t s;
+            CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, k == 0 ? greatest : prio));
+            ctx->aux.push_back(s);
+            cudaEvent_t e;
+            CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->join_ev.push_back(e);
+        }
+        if (!ctx->fork_ev) CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
+    size_t off = 0;
+    std::vector<size_t> offs(nlev);
+    for (int q = 0; q < nlev; ++q) { offs[q] = off; off += slice[q]; }
+    for (int k = 0; k < nlev; ++k) {
+        const int q = order[k];
+        cudaStream_t st = ctx->aux[k];
+        CU(cudaStreamWaitEvent(st, ctx->fork_ev, 0));
+        int rc = run_level(ctx, Exec{ctx->ws + offs[q], slice[q], st}, levels[q], n[q], seed, first_index[q],
+                           &prec_fine[q], &prec_coarse[q], tol_fine[q], tol_coarse[q], sums_dev + (size_t)q * kSumsLen,
+                           nullptr, false, nullptr, false);
+        if (rc) return rc;
+        CU(cudaEventRecord(ctx->join_ev[k], st));
+    }
+    for (int k = 0; k < nlev; ++k) CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[k], 0));
     return MLMC_OK;
 }
 

@@ -1,4 +1,4 @@
-// controller.cpp -- Algorithm 2 (adaptive MPML) on top of mlmc_sample_level.
+// controller.cpp -- Algorithm 2 (adaptive MPML) on top of the per-level sampler.
 //
 // Readings: R1 bias constant (r m^alpha - 1)/sqrt(2) with
 // r = 1; R2 stop when both tests pass, ELMAX if the bias test still fails at
@@ -6,13 +6,18 @@
 // new samples, N_l never decreases; R4 V_l = s_l^2 with 1/N_l; R5/R21 C_l =
 // mean deterministic work of one coupled sample; R6 N_init = 100; R8 coarse
 // half at eps_{l-1}; R20 samples already drawn keep their tolerance; R23 the
-// global per-level index counts all rounds; R25 the variance test uses the N_l
-// drawn so far.  Every rank runs this loop on identical all-reduced sums, so
-// every rank takes the same decisions without a broadcast.
-#include <chrono>
-#include <cstring>
+// global per-level index counts all rounds, ranks take contiguous slices; R25
+// the variance test uses the N_l drawn so far.  Every rank runs this loop on
+// identical all-reduced sums, so every rank takes the same decisions without a
+// broadcast.  The same loop runs over the GPU (mlmc_adaptive_run: every level
+// of a round in one mlmc_sample_levels_async call) or over a caller-supplied
+// host sampler (mlmc_adaptive_run_host: CPU tests of the controller and of the
+// multi-rank exchange).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstring>
+#include <functional>
 #include <vector>
 
 #include "internal.h"
@@ -24,37 +29,36 @@ struct LevelAcc {
     uint64_t drawn = 0;
 };
 
-mlmc_precision minres_prec() { return mlmc_precision{MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0}; }
+mlmc_precision minres_prec() {
+    return mlmc_precision{MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
+}
 
 // Table 1 (right) quads on the levels where the shared-memory
 // banded factor exists (N <= 32); u = u_r = binary64 here (the paper's level
-// 0/1 working precisions h/s are not implemented), MINRES beyond.
+// 0/1 working precisions h/s are not implemented), MINRES beyond (R14).
 mlmc_precision policy_prec(int policy, int level, int N) {
     if (policy == 1 && N <= 32) {
-        if (level == 0) return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0};
-        if (level == 1) return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0};
-        return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0};
+        if (level == 0)
+            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
+        if (level == 1)
+            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
+        return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
     }
     return minres_prec();
 }
 
-}  // namespace
+// Draw one round: for each q, n[q] samples of levels[q] from first[q]; write
+// MLMC_SUMS_LEN sums per entry to sums (host).
+using RoundSampler = std::function<int(int nlev, const int* levels, const uint64_t* n, const uint64_t* first,
+                                       const mlmc_precision* pf, const mlmc_precision* pc, const double* tf,
+                                       const double* tc, double* sums)>;
 
-extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
-                                 mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
-    if (!ctx || !opts || !out || !(eps > 0.0)) return MLMC_EINVAL;
-    const mlmc_adaptive_opts o = *opts;
-    if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return MLMC_EINVAL;
+int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o, const RoundSampler& sampler,
+                  mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
+    if (!(eps > 0.0) || o.world < 1 || o.rank < 0 || o.rank >= o.world || L_max < 1 || h0_inv < 2)
+        return MLMC_EINVAL;
     if (o.world > 1 && !allreduce) return MLMC_EINVAL;
-    mlmc_level_info li0;
-    if (mlmc_level_info_get(ctx, 0, &li0) != MLMC_OK) return MLMC_EINVAL;
-    int L_max = 0;
-    {
-        mlmc_level_info li;
-        while (L_max + 1 < MLMC_MAX_LEVELS && mlmc_level_info_get(ctx, L_max + 1, &li) == MLMC_OK) ++L_max;
-    }
-    if (L_max < 1) return MLMC_EINVAL;
-    const double h0 = li0.h, TOL = eps;
+    const double h0 = 1.0 / h0_inv, TOL = eps;
     const int N_init = o.N_init > 0 ? o.N_init : 100;
     const int max_rounds = o.max_rounds > 0 ? o.max_rounds : 100;
     const double r_bias = o.r_bias > 0 ? o.r_bias : 1.0;
@@ -66,13 +70,12 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
     std::vector<double> epsl;
     int L = 1, rounds = 0, code = MLMC_OK;
     double solve_s = 0.0;
-    bool failed = false;
 
     auto stats = [&](int l, double& mean, double& var, double& cost) {
         const double n = acc[l].s[5];
-        mean = acc[l].s[0] / n;
-        var = std::max(0.0, acc[l].s[1] / n - mean * mean);   // Eq. (4) with 1/N_l (R4)
-        cost = acc[l].s[4] / n;
+        mean = n > 0 ? acc[l].s[0] / n : 0.0;
+        var = n > 0 ? std::max(0.0, acc[l].s[1] / n - mean * mean) : 0.0;   // Eq. (4) with 1/N_l (R4)
+        cost = n > 0 ? acc[l].s[4] / n : 0.0;
     };
 
     while (L <= L_max && rounds < max_rounds) {
@@ -81,24 +84,35 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
         if (o.k_p > 0.0) mlmc_eps_schedule(L, h0, o.k_p, epsl.data());   // step 2, Eq. (16)
         std::vector<double> round_sums((size_t)(L + 1) * MLMC_SUMS_LEN, 0.0);
         std::vector<uint64_t> dN(L + 1, 0);
-        for (int l = 0; l <= L; ++l) {   // steps 3-4
+        // steps 3-4: this rank's slice of every level's new indices, all levels in one call
+        std::vector<int> lv;
+        std::vector<uint64_t> cnt, first;
+        std::vector<mlmc_precision> pf, pc;
+        std::vector<double> tf, tc;
+        for (int l = 0; l <= L; ++l) {
             const double want = std::ceil(target[l]);
             dN[l] = want > (double)acc[l].drawn ? (uint64_t)(want - (double)acc[l].drawn) : 0;
             if (dN[l] == 0) continue;
             const uint64_t lo = acc[l].drawn + dN[l] * (uint64_t)o.rank / (uint64_t)o.world;
             const uint64_t hi = acc[l].drawn + dN[l] * (uint64_t)(o.rank + 1) / (uint64_t)o.world;
-            mlmc_level_info lf, lc;
-            mlmc_level_info_get(ctx, l, &lf);
-            if (l > 0) mlmc_level_info_get(ctx, l - 1, &lc);
-            mlmc_precision pf = policy_prec(o.policy, l, lf.N);
-            mlmc_precision pc = l > 0 ? policy_prec(o.policy, l - 1, lc.N) : pf;
-            mlmc_level_sums s{};
+            lv.push_back(l);
+            cnt.push_back(hi - lo);
+            first.push_back(lo);
+            pf.push_back(policy_prec(o.policy, l, h0_inv << l));
+            pc.push_back(l > 0 ? policy_prec(o.policy, l - 1, h0_inv << (l - 1)) : pf.back());
+            tf.push_back(epsl[l]);
+            tc.push_back(l > 0 ? epsl[l - 1] : epsl[l]);
+        }
+        if (!lv.empty()) {
+            std::vector<double> s(lv.size() * MLMC_SUMS_LEN, 0.0);
             auto t0 = std::chrono::steady_clock::now();
-            int rc = mlmc_sample_level(ctx, l, hi - lo, o.seed, lo, &pf, &pc, epsl[l], l > 0 ? epsl[l - 1] : epsl[l], &s,
-                                       nullptr);
+            int rc = sampler((int)lv.size(), lv.data(), cnt.data(), first.data(), pf.data(), pc.data(), tf.data(),
+                             tc.data(), s.data());
             solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             if (rc) return rc;
-            std::memcpy(&round_sums[(size_t)l * MLMC_SUMS_LEN], &s, sizeof(s));
+            for (size_t q = 0; q < lv.size(); ++q)
+                std::memcpy(&round_sums[(size_t)lv[q] * MLMC_SUMS_LEN], &s[q * MLMC_SUMS_LEN],
+                            sizeof(double) * MLMC_SUMS_LEN);
         }
         // one exchange per round: SUM of the additive fields, MAX of the two maxima
         if (o.world > 1) {
@@ -116,6 +130,7 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = mx[2 * l + 1];
             }
         }
+        bool failed = false;
         for (int l = 0; l <= L; ++l) {
             const double* rs = &round_sums[(size_t)l * MLMC_SUMS_LEN];
             for (int k = 0; k < MLMC_SUMS_LEN; ++k)
@@ -123,7 +138,7 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
             acc[l].drawn += dN[l];
             if (rs[6] > 0) failed = true;
         }
-        if (failed) { code = MLMC_ESOLVER; break; }
+        if (failed) { code = MLMC_ESOLVER; break; }   // a failed solve is never resampled (R15)
         // steps 5-7
         std::vector<double> mean(L + 1), V(L + 1), C(L + 1), Nopt(L + 1);
         for (int l = 0; l <= L; ++l) stats(l, mean[l], V[l], C[l]);
@@ -164,4 +179,44 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
     }
     out->estimate = est;
     return code;
+}
+
+}  // namespace
+
+extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
+                                 mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
+    if (!ctx || !opts || !out) return MLMC_EINVAL;
+    mlmc_level_info li0;
+    if (mlmc_level_info_get(ctx, 0, &li0) != MLMC_OK) return MLMC_EINVAL;
+    int L_max = 0;
+    mlmc_level_info li;
+    while (L_max + 1 < MLMC_MAX_LEVELS && mlmc_level_info_get(ctx, L_max + 1, &li) == MLMC_OK) ++L_max;
+    double* dev = nullptr;
+    if (cudaMalloc(&dev, sizeof(double) * MLMC_MAX_LEVELS * MLMC_SUMS_LEN) != cudaSuccess) return MLMC_ECUDA;
+    const uint64_t seed = opts->seed;
+    RoundSampler gpu = [&](int nlev, const int* lv, const uint64_t* n, const uint64_t* first, const mlmc_precision* pf,
+                           const mlmc_precision* pc, const double* tf, const double* tc, double* sums) -> int {
+        int rc = mlmc_sample_levels_async(ctx, nlev, lv, n, seed, first, pf, pc, tf, tc, dev);
+        if (rc) return rc;
+        return mlmc::copy_sums_to_host(ctx, dev, nlev, sums);
+    };
+    int rc = adaptive_core(li0.N, L_max, eps, *opts, gpu, allreduce, user, out);
+    cudaFree(dev);
+    return rc;
+}
+
+extern "C" int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts* opts,
+                                      mlmc_level_sampler_fn sampler, void* sampler_user, mlmc_allreduce_fn allreduce,
+                                      void* user, mlmc_result* out) {
+    if (!opts || !out || !sampler) return MLMC_EINVAL;
+    RoundSampler host = [&](int nlev, const int* lv, const uint64_t* n, const uint64_t* first, const mlmc_precision* pf,
+                            const mlmc_precision* pc, const double* tf, const double* tc, double* sums) -> int {
+        for (int q = 0; q < nlev; ++q) {
+            int rc = sampler(lv[q], n[q], first[q], &pf[q], &pc[q], tf[q], tc[q], sums + (size_t)q * MLMC_SUMS_LEN,
+                             sampler_user);
+            if (rc) return rc;
+        }
+        return MLMC_OK;
+    };
+    return adaptive_core(h0_inv, L_max, eps, *opts, host, allreduce, user, out);
 }

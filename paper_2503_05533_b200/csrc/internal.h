@@ -31,7 +31,7 @@ cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, 
                          cudaStream_t s);
 // K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].
 cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                          int slot, unsigned* job_counter, cudaStream_t s);
+                          int slot, unsigned* job_counter, bool verify, cudaStream_t s);
 bool minres_supported(int N);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max,
@@ -42,6 +42,9 @@ cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double 
                               double cost_f_fixed, double cost_f_step, double cost_c_fixed,
                               double cost_c_step, double* chunk_scratch, double* sums, bool accumulate,
                               cudaStream_t s);
+
+// Copy nlev level-sum records from the device to the host on the ctx's stream and wait.
+int copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host);
 
 constexpr int kSumsLen = MLMC_SUMS_LEN;
 constexpr int kRecLen = MLMC_SAMPLE_LEN;

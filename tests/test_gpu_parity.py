@@ -77,12 +77,18 @@ def test_C1_fp64_per_sample_parity_and_sums():
     cfg = W.CONFIGS["C1"]
     ctx = _ctx(cfg)
     P = _oracle(cfg)
+    vprec = precision("minres", verify=True)
     for level, n in ((0, cfg["N"][0]), (1, cfg["N"][1])):
         r = ctx.sample_level(level, n, seed=cfg["seed"], prec_fine="minres", tol_fine=1e-12, tol_coarse=1e-12,
                              per_sample=True)
         ps = r.per_sample
         assert np.all(ps[:, 6:8] == 0)
-        assert np.all(ps[:, 4] <= 1e-12 * 1.01)
+        assert np.all(ps[:, 4] <= 1e-12)                     # phibar / ||b||, the stopping quantity
+        # VERIFY instantiation: same Q bits, plus the true residual ||b - A x|| / ||b||
+        rv = ctx.sample_level(level, n, seed=cfg["seed"], prec_fine=vprec, prec_coarse=vprec, tol_fine=1e-12,
+                              tol_coarse=1e-12, per_sample=True).per_sample
+        assert np.array_equal(rv[:, [0, 1, 2, 3, 6, 7]], ps[:, [0, 1, 2, 3, 6, 7]])
+        assert np.all(rv[:, 4] <= 1e-12 * 1.05) and (level == 0 or np.all(rv[:, 5] <= 1e-12 * 1.05))
         idx = list(range(0, n, max(1, n // 150))) + [n - 1]
         refs = _pmap(lambda k: P.coupled_sample(level, cfg["seed"], k), idx)
         for k, ref in zip(idx, refs):
@@ -134,9 +140,13 @@ def test_C2_reduced_accuracy_within_residual_bound(level):
     r = ctx.sample_level(level, n, seed=cfg["seed"], tol_fine=tf, tol_coarse=tc, per_sample=True)
     ps = r.per_sample
     assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
-    assert np.all(ps[:, 4] <= tf * 1.01)
+    vp = precision("minres", verify=True)
+    pv = ctx.sample_level(level, n, seed=cfg["seed"], prec_fine=vp, prec_coarse=vp, tol_fine=tf, tol_coarse=tc,
+                          per_sample=True).per_sample
+    assert np.array_equal(pv[:, 0:4], ps[:, 0:4])
+    assert np.all(pv[:, 4] <= tf * 1.01)                        # true residual meets Eq. (2)
     if level:
-        assert np.all(ps[:, 5] <= tc * 1.01)
+        assert np.all(pv[:, 5] <= tc * 1.01)
     idx = sorted(set(list(range(0, n, max(1, n // 40))) + [n - 1]))
     Nf = cfg["h0_inv"] << level
 
@@ -231,6 +241,32 @@ def test_edge_cases_empty_ragged_batching_and_determinism():
     big.close()
 
 
+def test_concurrent_levels_equal_sequential_levels():
+    """mlmc_sample_levels_async (levels on concurrent streams, split workspace) gives bit-identical
+    level sums to one mlmc_sample_level call per level; small workspace forces multi-pass slices."""
+    cfg = W.CONFIGS["C2"]
+    tols = cfg["tols"]
+    Nl = [2000, 500, 120, 30]
+    tc = [tols[l - 1] if l else tols[0] for l in range(4)]
+    mr = precision("minres")
+    for ws in (512 << 20, 6 << 20):
+        ctx = _ctx(cfg, ws=ws)
+        sums = torch.zeros((4, 12), dtype=torch.float64, device="cuda")
+        ctx.sample_levels_async([3, 1, 0, 2], [Nl[3], Nl[1], Nl[0], Nl[2]], 1, [7, 5, 3, 11], [mr] * 4, [mr] * 4,
+                                [tols[3], tols[1], tols[0], tols[2]], [tc[3], tc[1], tc[0], tc[2]], sums)
+        torch.cuda.synchronize()
+        got = sums.cpu().numpy()
+        for q, (l, first) in enumerate(zip([3, 1, 0, 2], [7, 5, 3, 11])):
+            ref = ctx.sample_level(l, Nl[l], seed=1, first_index=first, tol_fine=tols[l], tol_coarse=tc[l]).sums
+            ref = np.array([ref[f] for f in ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail",
+                                             "iters_f", "iters_c", "iters_f_max", "iters_c_max", "reserved")])
+            if ws > (64 << 20):      # one pass on both sides: bit-identical
+                assert np.array_equal(got[q], ref), (ws, l)
+            else:                    # passes smaller than a 4096-chunk: summation order differs
+                assert np.array_equal(got[q][4:], ref[4:]) and np.allclose(got[q], ref, rtol=1e-13, atol=0)
+        ctx.close()
+
+
 def test_full_size_C2_step_sampled_parity():
     """BASELINE configs[1] at full size in the launch configuration bench.py times
     (one call per level); sampled outputs against the oracle bound."""
@@ -274,8 +310,11 @@ def test_adaptive_C4_matches_oracle_controller():
 
     o = om.adaptive_mpml(sampler, cfg["eps"], 1 / cfg["h0_inv"], 0.05, L_max=cfg["L_max"], N_init=100)
     assert o.L == g["L"]
+    # both sides solve every sample to relative residual eps_l, so each Q differs from the exact one by at
+    # most eps_l ||b|| ||x|| <= 1.5 eps_l Q; Q < 0.06 for these fields
+    bound = sum(2 * 1.5 * 0.06 * (e + (g["eps"][l - 1] if l else 0.0)) for l, e in enumerate(g["eps"]))
     if o.N == g["N"]:
-        assert abs(o.estimate - g["estimate"]) < 1e-9
+        assert abs(o.estimate - g["estimate"]) < bound
     else:   # a +-1 MINRES iteration can move C_l and hence ceil(N_l) by a sample or two
         assert all(abs(a - b) <= max(2, 0.02 * b) for a, b in zip(o.N, g["N"])), (o.N, g["N"])
         assert abs(o.estimate - g["estimate"]) < 0.1 * cfg["eps"]
