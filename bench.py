@@ -287,6 +287,7 @@ def run_ours(args):
     if not args.no_extras:
         line["e2e"] = e2e_leg(ctx, cfg, args, world, rank, torch, np, dist)
         line["time_to_eps"] = adaptive_leg(args, world, rank, local, torch, dist)
+        line["c3_cholesky_ir"] = c3_leg(local, torch)
         if rank == 0 and world == 1:
             from oracle import core as oc
             oc.build()
@@ -337,6 +338,34 @@ def e2e_leg(ctx, cfg, args, world, rank, torch, np, dist):
             "h2d_bytes_per_step": int(sum(Nl) * m * 8), "d2h_bytes_per_step": int(sum(Nl) * 8 * 8 + len(Nl) * 96),
             "api": "mlmc_sample_level_xi (host pinned xi in, host per-sample records + level sums out)",
             "clock": "host wall clock around the synchronous calls, max over ranks"}
+
+
+def c3_leg(local, torch):
+    """configs[2]: 100000 coupled samples per level, h = 1/8, 1/16, 1/32, banded Cholesky in fp16 / fp32
+    with fp64 iterative refinement to 1e-10 (substitutions in fp32); device-timed per level."""
+    from paper_2503_05533_b200 import Context, precision
+    cfg = W.CONFIGS["C3"]
+    ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
+                  L_max=cfg["L_max"], device=local, workspace_bytes=4 << 30)
+    stream = torch.cuda.current_stream()
+    sums = torch.zeros(12, dtype=torch.float64, device=torch.device("cuda", local))
+    out = {}
+    for uf in ("h", "s"):
+        prec = precision("chol_ir", uf, "s")
+        for l, n in enumerate(cfg["N"]):
+            ctx.sample_level_async(l, 2000, cfg["seed"], 10**7, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            ctx.sample_level_async(l, n, cfg["seed"], 0, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            s = sums.cpu().numpy()
+            ms = a0.elapsed_time(a1)
+            out[f"l{l}_{'fp16' if uf == 'h' else 'fp32'}"] = {
+                "h": f"1/{cfg['h0_inv'] << l}", "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
+                "mean_ir_steps_fine": s[7] / n, "max_ir_steps_fine": s[9], "failures": s[6]}
+    ctx.close()
+    return out
 
 
 def adaptive_leg(args, world, rank, local, torch, dist):

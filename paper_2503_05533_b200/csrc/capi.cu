@@ -17,6 +17,7 @@ struct mlmc_ctx {
     mlmc_problem pr{};
     KLModes kl;
     int device = 0;
+    int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     std::vector<double*> phi_dev;        // per level, lazily built
@@ -98,7 +99,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Workspace layout for one pass of `batch` samples of `level`.
 struct WsLayout {
-    size_t xi, a_f, a_c, rec, chunks, ctr, total;
+    size_t xi, a_f, a_c, rec, chunks, ctr, gm, total;
+    int gm_ctas;
 };
 WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch) {
     WsLayout L{};
@@ -110,6 +112,12 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch) {
     L.rec = off;    off += align256(sizeof(double) * batch * kRecLen);
     L.chunks = off; off += align256(sizeof(double) * kSumsLen * ((batch + kChunk - 1) / kChunk + 1));
     L.ctr = off;    off += align256(sizeof(unsigned) * 16);
+    L.gm = off;
+    L.gm_ctas = 0;
+    if (Nf >= kGmMinN) {   // per-CTA vector scratch of the global-memory MINRES (fine and coarse share it)
+        L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1));
+        off += align256(minres_gm_scratch_per_cta(Nf) * L.gm_ctas);
+    }
     L.total = off;
     return L;
 }
@@ -170,13 +178,18 @@ void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
 }
 
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
-               double* rec, int slot, unsigned* ctr) {
+               double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
         bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
-        CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
-                   [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, ex.st); }));
+        if (N >= kGmMinN)
+            CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
+                return launch_minres_gm(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st);
+            }));
+        else
+            CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
+                       [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, ex.st); }));
     } else {
         int mi = p->max_iter > 0 ? p->max_iter : 50;
         CU(counted(ctx, ex.st, MLMC_K_CHOL_IR, N,
@@ -213,6 +226,7 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
     double* rec = reinterpret_cast<double*>(ex.ws + L.rec);
     double* chunks = reinterpret_cast<double*>(ex.ws + L.chunks);
     unsigned* ctr = reinterpret_cast<unsigned*>(ex.ws + L.ctr);
+    double* gm = reinterpret_cast<double*>(ex.ws + L.gm);
     double cff, cfs, ccf = 0, ccs = 0;
     cost_model(pf, Nf, cff, cfs);
     if (level > 0) cost_model(pc, Nc, ccf, ccs);
@@ -236,8 +250,8 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
             CU(counted(ctx, st, MLMC_K_FIELD, Nc,
                        [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, st); }));
         if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, st));
-        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr))) return rc;
-        if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4))) return rc;
+        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas))) return rc;
+        if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas))) return rc;
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
             return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, st);
         }));
@@ -322,6 +336,7 @@ int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
         if (rc) { delete ctx; return fail(nullptr, rc, "KL eigenpairs failed"); }
     }
     ctx->phi_dev.assign(p.L_max + 1, nullptr);
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, p.device);
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->sums_dev, sizeof(double) * kSumsLen * MLMC_MAX_LEVELS);

@@ -33,6 +33,11 @@ cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, 
 cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
                           int slot, unsigned* job_counter, bool verify, cudaStream_t s);
 bool minres_supported(int N);
+// K3 for N >= 128: vectors in a per-CTA global scratch (nctas CTAs, minres_gm_scratch_per_cta(N) bytes each).
+constexpr int kGmMinN = 128;
+size_t minres_gm_scratch_per_cta(int N);
+cudaError_t launch_minres_gm(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                             unsigned* job_counter, double* scratch, int nctas, cudaStream_t s);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max,
                            double* out, int slot, unsigned* job_counter, cudaStream_t s);

@@ -53,8 +53,9 @@ __device__ __forceinline__ double warp_allsum(double v) {
 // carries SPW = floor(32 / C) strips side by side (lane = strip * C + column),
 // for C > 32 a strip spans WPR warps (lane = column).  Idle lanes act as a
 // phantom strip S (zeros) and never touch a node's cell.
-template <int N, int R, int MINB_>
+template <int N, int R, int MINB_, bool CS_ = false>
 struct StripCfg {
+    static constexpr bool CS = CS_;                       // all conductances from shared grids (frees registers)
     static constexpr int C = N - 1;                       // interior columns / rows
     static constexpr int S = (C + R - 1) / R;             // strips per column
     static constexpr bool NARROW = C <= 32;
@@ -67,9 +68,10 @@ struct StripCfg {
     static constexpr int MINB = MINB_;                    // resident CTAs per SM the register budget must allow
     static constexpr int G = NARROW ? N + 1 : 32 * WPR + 2;   // grid pitch
     static constexpr int GR = S * R + R + 2;              // grid rows (phantom strip S for idle lanes)
-    static constexpr bool CW_SMEM = N >= 32;              // west conductance from the shared cE grid
-    // cE grid rows 0..GR-1 (rows >= N, read by phantom rows / idle lanes, hold 0)
-    static constexpr int SMEM_PER_GROUP = G * GR + 2 * NW + 2 + (CW_SMEM ? N * GR : 0);
+    static constexpr bool CW_SMEM = CS || N >= 32;        // west conductance from the shared cE grid
+    static constexpr int GP = 32 * WPR + 2 > N + 2 ? 32 * WPR + 2 : N + 2;   // conductance grid pitch
+    // cE (and with CS cN) grids [row * GP + col], rows 0..GR-1; entries that are not edges hold 0
+    static constexpr int SMEM_PER_GROUP = G * GR + 2 * NW + 2 + (CW_SMEM ? GP * GR : 0) + (CS ? GP * GR : 0);
     static constexpr size_t SMEM = sizeof(double) * SMEM_PER_GROUP * GROUPS + 16 * GROUPS;
     static_assert(S * R == C || S * R == C + 1, "strips must end at row C or at the boundary row N");
 };
@@ -101,18 +103,20 @@ __device__ __forceinline__ double gsum(double a, double* buf, int tg, int g) {
     }
 }
 
-template <int N, int R, int MINB, bool VERIFY>
-__global__ void __launch_bounds__(StripCfg<N, R, MINB>::BLOCK, MINB)
+template <int N, int R, int MINB, bool VERIFY, bool PIPE, bool CS>
+__global__ void __launch_bounds__(StripCfg<N, R, MINB, CS>::BLOCK, MINB)
 minres_strip_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
                     int slot, unsigned* __restrict__ job_counter) {
-    using K = StripCfg<N, R, MINB>;
+    using K = StripCfg<N, R, MINB, CS>;
+    constexpr int GP = K::GP;
     constexpr int C = K::C, G = K::G, TPG = K::TPG, GROUPS = K::GROUPS, NW = K::NW, P = 2 * N * N;
     extern __shared__ double smem[];
     const int g = threadIdx.x / TPG, tg = threadIdx.x % TPG;
     double* Sg = smem + g * K::SMEM_PER_GROUP;          // zero-padded exchange grid [row * G + col]
     double* redA = Sg + G * K::GR;                       // alpha partials
     double* redB = redA + NW;                            // ||r2||^2 partials
-    double* cEg = redB + NW + 2;                         // CW_SMEM: cE edge grid [j*N + i]
+    double* cEg = redB + NW + 2;                         // CW_SMEM: cE edge grid [j*GP + i]
+    double* cNg = cEg + GP * K::GR;                      // CS: cN edge grid [j*GP + i]
     int* jobslot = reinterpret_cast<int*>(smem + K::SMEM_PER_GROUP * GROUPS) + 4 * g;
 
     // ---- this thread's strip: column i, rows j0 .. j0 + R - 1 (nrows of them are nodes)
@@ -145,29 +149,37 @@ minres_strip_kernel(const double* __restrict__ a_all, int nb, double tol, int ma
 
         // ---- prologue: zero the exchange grid, load conductances (registers + cE grid)
         for (int e = tg; e < G * K::GR; e += TPG) Sg[e] = 0.0;
-        if constexpr (K::CW_SMEM) {
-            for (int e = tg; e < N * K::GR; e += TPG) {
-                const int ii = e % N, jj = e / N;
-                cEg[e] = (jj >= 1 && jj < N) ? 0.5 * (__ldg(a + 2 * (jj * N + ii)) + __ldg(a + 2 * ((jj - 1) * N + ii) + 1)) : 0.0;
-            }
-        }
-        double cE[R], cN[R], cW[K::CW_SMEM ? 1 : R];
-        double cS0 = 0.0;
         auto aL = [&](int ii, int jj) { return __ldg(a + 2 * (jj * N + ii)); };
         auto aU = [&](int ii, int jj) { return __ldg(a + 2 * (jj * N + ii) + 1); };
+        if constexpr (K::CW_SMEM) {
+            for (int e = tg; e < GP * K::GR; e += TPG) {
+                const int ii = e % GP, jj = e / GP;
+                // edge (ii,jj)-(ii+1,jj): lower tri of cell (ii,jj) + upper tri of cell (ii,jj-1)
+                cEg[e] = (ii < N && jj >= 1 && jj < N) ? 0.5 * (aL(ii, jj) + aU(ii, jj - 1)) : 0.0;
+                // edge (ii,jj)-(ii,jj+1): upper tri of cell (ii,jj) + lower tri of cell (ii-1,jj)
+                if constexpr (K::CS) cNg[e] = (ii >= 1 && ii < N && jj < N) ? 0.5 * (aU(ii, jj) + aL(ii - 1, jj)) : 0.0;
+            }
+        }
+        constexpr int RR = K::CS ? 1 : R;
+        double cE[RR], cN[RR], cW[K::CW_SMEM ? 1 : R];
+        double cS0 = 0.0, cSlast = 0.0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < RR; ++r) {
             cE[r] = 0.0;
             cN[r] = 0.0;
-            if constexpr (!K::CW_SMEM) cW[r] = 0.0;
-            if (r < nrows) {
+            if constexpr (!K::CW_SMEM) cW[K::CW_SMEM ? 0 : r] = 0.0;
+            if (!K::CS && r < nrows) {
                 const int j = j0 + r;
                 cE[r] = 0.5 * (aL(i, j) + aU(i, j - 1));
                 cN[r] = 0.5 * (aU(i, j) + aL(i - 1, j));
-                if constexpr (!K::CW_SMEM) cW[r] = 0.5 * (aL(i - 1, j) + aU(i - 1, j - 1));
+                if constexpr (!K::CW_SMEM) cW[K::CW_SMEM ? 0 : r] = 0.5 * (aL(i - 1, j) + aU(i - 1, j - 1));
             }
         }
         if (nrows > 0) cS0 = 0.5 * (aU(i, j0 - 1) + aL(i - 1, j0 - 1));
+        // South conductance of the strip's top row: 0 if that row is the phantom boundary row,
+        // which then has only zero couplings and zero entries, so its y stays exactly 0.
+        if (R > 1 && live_last) cSlast = 0.5 * (aU(i, j0 + R - 2) + aL(i - 1, j0 + R - 2));
+        if (R == 1) cSlast = cS0;
         gsync<TPG, GROUPS>(g);
 
         // ---- MINRES state: r1 = r2 = b, w = w2 = 0 (x itself only in VERIFY)
@@ -194,22 +206,38 @@ minres_strip_kernel(const double* __restrict__ a_all, int nb, double tol, int ma
         // chain of k hides behind the stencil of k+1.  Same operations, same order per
         // value as the plain loop.
         const double* Sc = Sg + c0;
+        // CW_SMEM: [r*GP] west, [r*GP + 1] own (CS) cE.  An idle lane of a wide layout sits in
+        // column N: it reads the all-zero columns N, N+1 so that its entries stay exactly 0.
+        const double* cEw = cEg + j0 * GP + (live ? i - 1 : i);
+        const double* cNw = cNg + j0 * GP + i;              // CS: [r*GP] own cN
+        // conductances of row r: east, west, north, south (south of row r = north of row r-1)
+        auto coef = [&](int r, double& ce, double& cw, double& cn, double& cs_) {
+            if constexpr (K::CS) {
+                ce = cEw[r * GP + 1];
+                cn = cNw[r * GP];
+            } else {
+                ce = cE[K::CS ? 0 : r];
+                cn = cN[K::CS ? 0 : r];
+            }
+            if constexpr (K::CW_SMEM) cw = cEw[r * GP]; else cw = cW[K::CW_SMEM ? 0 : r];
+            if (r == R - 1) cs_ = cSlast;
+            else if (r == 0) cs_ = cS0;
+            else if constexpr (K::CS) cs_ = cNw[(r - 1) * GP];
+            else cs_ = cN[K::CS ? 0 : r - 1];
+        };
         // phase A of iteration k: y = A v - cr1 r1, v = r2 * invb; y parked in r1; alpha partial
         auto phaseA = [&](int r, double cr1, double& pa) {
-            const bool alive = (r < R - 1) ? live : live_last;
             const double vC = r2[r];
             const double vN = (r + 1 < R) ? r2[r + 1 < R ? r + 1 : r] : Sc[r * G + G];
             const double vS = (r > 0) ? r2[r > 0 ? r - 1 : 0] : Sc[-G];
             const double vE = Sc[r * G + 1], vW = Sc[r * G - 1];
-            const double cs_ = (r > 0) ? cN[r > 0 ? r - 1 : 0] : cS0;
-            double cw_;
-            if constexpr (K::CW_SMEM) cw_ = cEg[(j0 + r) * N + i - 1]; else cw_ = cW[K::CW_SMEM ? 0 : r];
-            const double d = (cE[r] + cw_) + (cN[r] + cs_);
-            const double t = fma(cE[r], vE, cw_ * vW);
-            const double u = fma(cN[r], vN, cs_ * vS);
+            double ce, cw_, cn, cs_;
+            coef(r, ce, cw_, cn, cs_);
+            const double d = (ce + cw_) + (cn + cs_);
+            const double t = fma(ce, vE, cw_ * vW);
+            const double u = fma(cn, vN, cs_ * vS);
             const double Av = fma(d, vC, -(t + u));
-            double y = fma(Av, invb, -(cr1 * r1[r]));
-            y = alive ? y : 0.0;
+            const double y = fma(Av, invb, -(cr1 * r1[r]));
             r1[r] = y;
             pa = fma(vC * invb, y, pa);
         };
@@ -274,10 +302,17 @@ minres_strip_kernel(const double* __restrict__ a_all, int nb, double tol, int ma
             const double cr1 = beta * inv_oldb;            // beta_{k+1} / beta_k
             pa0 = 0.0;
             pa1 = 0.0;
+            if constexpr (PIPE) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                phaseC(r);
-                phaseA(r, cr1, (r & 1) ? pa1 : pa0);
+                for (int r = 0; r < R; ++r) {
+                    phaseC(r);
+                    phaseA(r, cr1, (r & 1) ? pa1 : pa0);
+                }
+            } else {                                        // fewer live registers
+#pragma unroll
+                for (int r = 0; r < R; ++r) phaseC(r);
+#pragma unroll
+                for (int r = 0; r < R; ++r) phaseA(r, cr1, (r & 1) ? pa1 : pa0);
             }
             Xt = fma(phi, sw, Xt);
             ++k;
@@ -294,14 +329,13 @@ minres_strip_kernel(const double* __restrict__ a_all, int nb, double tol, int ma
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const bool alive = (r < R - 1) ? live : live_last;
-                const double cs_ = (r > 0) ? cN[r > 0 ? r - 1 : 0] : cS0;
-                double cw_;
-                if constexpr (K::CW_SMEM) cw_ = cEg[(j0 + r) * N + i - 1]; else cw_ = cW[K::CW_SMEM ? 0 : r];
-                const double d = (cE[r] + cw_) + (cN[r] + cs_);
+                double ce, cw_, cn, cs_;
+                coef(r, ce, cw_, cn, cs_);
+                const double d = (ce + cw_) + (cn + cs_);
                 double Ax = d * Sc[r * G];
-                Ax = fma(-cE[r], Sc[r * G + 1], Ax);
+                Ax = fma(-ce, Sc[r * G + 1], Ax);
                 Ax = fma(-cw_, Sc[r * G - 1], Ax);
-                Ax = fma(-cN[r], Sc[r * G + G], Ax);
+                Ax = fma(-cn, Sc[r * G + G], Ax);
                 Ax = fma(-cs_, Sc[r * G - G], Ax);
                 const double res = alive ? h2 - Ax : 0.0;
                 rr = fma(res, res, rr);
@@ -320,11 +354,11 @@ minres_strip_kernel(const double* __restrict__ a_all, int nb, double tol, int ma
     }
 }
 
-template <int N, int R, int MINB, bool VERIFY>
+template <int N, int R, int MINB, bool VERIFY, bool PIPE = true, bool CS = false>
 static cudaError_t run_minres(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                               unsigned* ctr, cudaStream_t s) {
-    using K = StripCfg<N, R, MINB>;
-    auto kern = minres_strip_kernel<N, R, MINB, VERIFY>;
+    using K = StripCfg<N, R, MINB, CS>;
+    auto kern = minres_strip_kernel<N, R, MINB, VERIFY, PIPE, CS>;
     static int blocks_per_sm = -1, sms = 0;
     if (blocks_per_sm < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
@@ -343,7 +377,9 @@ static cudaError_t run_minres(const double* a, uint64_t nb, double tol, int max_
     return cudaGetLastError();
 }
 
-bool minres_supported(int N) { return N == 2 || N == 4 || N == 8 || N == 16 || N == 32 || N == 64; }
+bool minres_supported(int N) {
+    return N == 2 || N == 4 || N == 8 || N == 16 || N == 32 || N == 64 || N == 128 || N == 256 || N == 512;
+}
 
 // Kernel shape per mesh (rows per thread R, register budget MINB); alternatives
 // selectable with MLMC_MINRES_VARIANT_N<N>=<index> for tuning runs.
@@ -367,22 +403,26 @@ static cudaError_t minres_dispatch(int N, const double* a, uint64_t nb, double t
         case 2:  return run_minres<2, 1, 8, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 4:  return run_minres<4, 1, 8, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 8:
-            if (var == 1) return run_minres<8, 2, 4, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_minres<8, 2, 6, V, false>(a, nb, tol, max_iter, out, slot, ctr, s);
             if (var == 2) return run_minres<8, 2, 8, V>(a, nb, tol, max_iter, out, slot, ctr, s);
             return run_minres<8, 2, 6, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 16:
-            if (var == 1) return run_minres<16, 4, 4, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_minres<16, 8, 2, V, false>(a, nb, tol, max_iter, out, slot, ctr, s);
             if (var == 2) return run_minres<16, 8, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 3) return run_minres<16, 4, 2, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 3) return run_minres<16, 4, 4, V>(a, nb, tol, max_iter, out, slot, ctr, s);
             return run_minres<16, 8, 2, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 32:
-            if (var == 1) return run_minres<32, 8, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 2) return run_minres<32, 4, 2, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 3) return run_minres<32, 8, 2, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_minres<32, 16, 2, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            // measured (tools/tune_minres.py, configs[1] level 2): v0 1.00 ms, v1 1.14, v2 1.14, v3 1.01
+            if (var == 1) return run_minres<32, 8, 3, V, true>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 2) return run_minres<32, 8, 4, V, true, true>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 3) return run_minres<32, 16, 2, V, true, true>(a, nb, tol, max_iter, out, slot, ctr, s);
+            return run_minres<32, 8, 3, V, false>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 64:
-            if (var == 1) return run_minres<64, 8, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_minres<64, 16, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            // measured (configs[1] level 3, 300 systems): v0 3.24 ms, v1 3.78, v2 4.05, v3 3.62
+            if (var == 1) return run_minres<64, 8, 1, V, true, true>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 2) return run_minres<64, 16, 1, V, false>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 3) return run_minres<64, 8, 1, V, false, true>(a, nb, tol, max_iter, out, slot, ctr, s);
+            return run_minres<64, 16, 1, V, true, true>(a, nb, tol, max_iter, out, slot, ctr, s);
         default: return cudaErrorNotSupported;
     }
 }
