@@ -1,4 +1,4 @@
-"""Time the MINRES kernel variants (MLMC_MINRES_VARIANT_N<N>) on the configs[1] workload.
+"""Time the MINRES kernel variants (MLMC_MINRES_TILE_N<N>) on the configs[1] workload.
 
 Usage: python tools/tune_minres.py            (spawns one process per variant)
        python tools/tune_minres.py --one N L n (internal: time one level's solves)
@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 
 # (mesh N, level whose FINE mesh is N, samples, tolerance) from configs[1]
 CASES = {8: (0, 20000, 1e-4), 16: (1, 5000, 1e-5), 32: (2, 1200, 1e-6), 64: (3, 300, 1e-8)}
-VARIANTS = {8: [0, 1, 2], 16: [0, 1, 2, 3], 32: [0, 1, 2, 3], 64: [0, 1, 2, 3]}
+VARIANTS = {16: [-1, 0, 1], 32: [-1, 0, 1, 2, 3], 64: [-1, 0, 1, 2]}
 
 
 def one(N):
@@ -39,7 +39,7 @@ def one(N):
     ms = [p for p in prof if p[0] == "minres" and p[1] == N][0]
     per = ms[3] / ms[2]
     nodes = (N - 1) ** 2
-    print(json.dumps({"N": N, "variant": int(os.environ.get(f"MLMC_MINRES_VARIANT_N{N}", "0")),
+    print(json.dumps({"N": N, "variant": int(os.environ.get(f"MLMC_MINRES_TILE_N{N}", "0")),
                       "ms_per_launch": per, "node_iters_per_s": its / reps * nodes / (per / 1e3),
                       "fp64_tflops_alg": 25 * its / reps * nodes / (per / 1e3) / 1e12}), flush=True)
 
@@ -50,7 +50,7 @@ def main():
         return
     for N, vs in VARIANTS.items():
         for v in vs:
-            env = dict(os.environ, **{f"MLMC_MINRES_VARIANT_N{N}": str(v)})
+            env = dict(os.environ, **{f"MLMC_MINRES_TILE_N{N}": str(v)})
             r = subprocess.run([sys.executable, __file__, "--one", str(N)], env=env, capture_output=True, text=True)
             out = [l for l in r.stdout.splitlines() if l.startswith("{")]
             print(out[-1] if out else json.dumps({"N": N, "variant": v, "error": r.stderr[-400:]}), flush=True)
