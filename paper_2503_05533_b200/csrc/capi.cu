@@ -35,6 +35,10 @@ struct mlmc_ctx {
     std::vector<cudaStream_t> aux;
     std::vector<cudaEvent_t> join_ev;
     cudaEvent_t fork_ev = nullptr;
+    // per level slot: a second stream for the coarse solve, its fork/join events, and the
+    // "fields ready" event that gates the other levels' solves behind the largest level's
+    std::vector<cudaStream_t> aux_c;
+    std::vector<cudaEvent_t> cfork_ev, cjoin_ev, prep_ev;
 };
 
 namespace {
@@ -139,6 +143,15 @@ struct Exec {
     cudaStream_t st;
 };
 
+// Optional scheduling of a single-pass level inside mlmc_sample_levels_async: the coarse solve
+// forks onto st_c (fine and coarse solves are independent), `prep` is recorded once the fields
+// are on HBM, and the solves wait for `gate` (the largest level's prep) so that the longest
+// solve is the first one eligible for the SMs.
+struct LevelSched {
+    cudaStream_t st_c = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, prep = nullptr, gate = nullptr;
+};
+
 int ensure_phi(mlmc_ctx* ctx, int level) {
     if (ctx->phi_dev[level]) return MLMC_OK;
     int N = level_N(ctx, level);
@@ -213,7 +226,8 @@ int validate_level(mlmc_ctx* ctx, int level, const mlmc_precision* pf, const mlm
 // One level's pipeline (K0 -> K1 -> K3/K4 fine + coarse -> K5) in passes that fit ex.ws, on ex.st.
 int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t seed, uint64_t first_index,
               const mlmc_precision* pf, const mlmc_precision* pc, double tol_f, double tol_c, double* sums_dev,
-              double* per_sample, bool per_sample_is_dev, const double* xi_in, bool xi_in_is_dev) {
+              double* per_sample, bool per_sample_is_dev, const double* xi_in, bool xi_in_is_dev,
+              const LevelSched* sch = nullptr) {
     const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
     uint64_t B = max_batch(ctx, level, ex.bytes);
     if (B == 0 && n > 0) return fail(ctx, MLMC_ENOMEM, "workspace too small for one sample");
@@ -250,8 +264,24 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
             CU(counted(ctx, st, MLMC_K_FIELD, Nc,
                        [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, st); }));
         if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, st));
+        const bool sched = sch && nb == n;               // single pass only
+        if (sched && sch->prep) CU(cudaEventRecord(sch->prep, st));
+        if (sched && sch->gate) CU(cudaStreamWaitEvent(st, sch->gate, 0));
+        // the global-memory MINRES shares one scratch between the fine and coarse solves: no fork then
+        const bool fork = sched && level > 0 && sch->st_c && Nf < kGmMinN;
+        if (fork) {
+            CU(cudaEventRecord(sch->fork, st));
+            CU(cudaStreamWaitEvent(sch->st_c, sch->fork, 0));
+        }
         if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas))) return rc;
-        if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas))) return rc;
+        if (fork) {
+            const Exec exc{ex.ws, ex.bytes, sch->st_c};
+            if ((rc = solve_mesh(ctx, exc, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas))) return rc;
+            CU(cudaEventRecord(sch->join, sch->st_c));
+            CU(cudaStreamWaitEvent(st, sch->join, 0));
+        } else if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas))) {
+            return rc;
+        }
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
             return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, st);
         }));
@@ -354,6 +384,9 @@ void mlmc_destroy(mlmc_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
     for (cudaStream_t s : ctx->aux) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    for (cudaStream_t s : ctx->aux_c) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    for (auto* v : {&ctx->cfork_ev, &ctx->cjoin_ev, &ctx->prep_ev})
+        for (cudaEvent_t e : *v) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->join_ev) cudaEventDestroy(e);
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     drain_pending(ctx);
@@ -452,9 +485,15 @@ int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const u
             cudaStream_t s;
             CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, k == 0 ? greatest : prio));
             ctx->aux.push_back(s);
+            CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, k == 0 ? greatest : prio));
+            ctx->aux_c.push_back(s);
             cudaEvent_t e;
             CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             ctx->join_ev.push_back(e);
+            for (auto* v : {&ctx->cfork_ev, &ctx->cjoin_ev, &ctx->prep_ev}) {
+                CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                v->push_back(e);
+            }
         }
         if (!ctx->fork_ev) CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
     }
@@ -466,9 +505,17 @@ int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const u
         const int q = order[k];
         cudaStream_t st = ctx->aux[k];
         CU(cudaStreamWaitEvent(st, ctx->fork_ev, 0));
+        LevelSched sch;
+        sch.st_c = ctx->aux_c[k];
+        sch.fork = ctx->cfork_ev[k];
+        sch.join = ctx->cjoin_ev[k];
+        sch.prep = k == 0 ? ctx->prep_ev[0] : nullptr;
+        sch.gate = k == 0 ? nullptr : ctx->prep_ev[0];
+        const bool top_single = max_batch(ctx, levels[order[0]], slice[order[0]]) >= n[order[0]];
+        if (!top_single) sch.prep = sch.gate = nullptr;   // the largest level runs in passes: no gate
         int rc = run_level(ctx, Exec{ctx->ws + offs[q], slice[q], st}, levels[q], n[q], seed, first_index[q],
                            &prec_fine[q], &prec_coarse[q], tol_fine[q], tol_coarse[q], sums_dev + (size_t)q * kSumsLen,
-                           nullptr, false, nullptr, false);
+                           nullptr, false, nullptr, false, &sch);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->join_ev[k], st));
     }
