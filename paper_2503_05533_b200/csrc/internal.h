@@ -33,7 +33,7 @@ cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, 
 cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
                           int slot, unsigned* job_counter, bool verify, cudaStream_t s);
 bool minres_supported(int N);
-// K3 v2 (k_minres_tile.cu): 2-column register tiles for N = 16, 32, 64; variant < 0 = not used for N.
+// K3 v2 (k_minres_tile.cu): 2-column register tiles for N = 8, 16, 32, 64; variant < 0 = not used for N.
 int minres_tile_variant(int N);
 cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
                                int slot, unsigned* job_counter, bool verify, cudaStream_t s);

@@ -1,4 +1,4 @@
-// k_minres_tile.cu -- K3 v2: batched MINRES with 2-column register tiles (h = 1/16 .. 1/64).
+// k_minres_tile.cu -- K3 v2: batched MINRES with 2-column register tiles (h = 1/8 .. 1/64).
 //
 // Same method as k_minres.cu (Eq. (2), R9, R10, R26): unpreconditioned
 // binary64 MINRES from x0 = 0 on the P1 stiffness matrix of the uniform SW-NE
@@ -44,9 +44,9 @@ struct TileCfg {
     static constexpr int PAIRS = N / 2;                   // pair p: columns 2p+1, 2p+2 (column N is a phantom)
     static constexpr int S = (C + R - 1) / R;             // row strips
     static constexpr int TPS = PAIRS * S;                 // threads per system
-    static_assert(TPS % 32 == 0, "a system must fill whole warps");
+    static_assert(TPS % 32 == 0 || TPS == 16, "a system fills whole warps or one half-warp");
     static_assert(S * R == C || S * R == C + 1, "strips end at row C or at the boundary row N");
-    static constexpr int NW = TPS / 32;
+    static constexpr int NW = TPS >= 32 ? TPS / 32 : 1;
     static constexpr int GROUPS = TPS >= 128 ? 1 : 128 / TPS;
     static constexpr int BLOCK = TPS * GROUPS;
     static constexpr int MINB = MINB_;
@@ -61,16 +61,26 @@ struct TileCfg {
     static constexpr size_t SMEM = sizeof(double) * SMEM_PER_GROUP * GROUPS + 16 * GROUPS;
 };
 
+// Butterfly over the lanes of one system inside a warp (all 32, or one half-warp when TPS = 16:
+// two systems share a warp and may diverge, so the half-warp mask is used).
+template <int TPS>
+__device__ __forceinline__ unsigned lane_mask() {
+    if constexpr (TPS >= 32) return 0xffffffffu;
+    else return 0xffffu << (threadIdx.x & 16);
+}
+template <int TPS>
 __device__ __forceinline__ double warp_sum_all(double v) {
+    constexpr int W = TPS >= 32 ? 32 : TPS;
+    const unsigned m = lane_mask<TPS>();
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
     return v;
 }
 
 template <int TPS, int GROUPS>
 __device__ __forceinline__ void tsync(int g) {
-    if constexpr (TPS == 32) {
-        __syncwarp();
+    if constexpr (TPS <= 32) {
+        __syncwarp(lane_mask<TPS>());
     } else if constexpr (GROUPS == 1) {
         __syncthreads();
     } else {
@@ -98,8 +108,8 @@ __device__ __forceinline__ double2 sum_partials(const double* buf) {
 
 template <int TPS, int GROUPS>
 __device__ __forceinline__ double tsum1(double a, double* buf, int tg, int g) {
-    a = warp_sum_all(a);
-    if constexpr (TPS == 32) {
+    a = warp_sum_all<TPS>(a);
+    if constexpr (TPS <= 32) {
         return a;
     } else {
         if ((tg & 31) == 0) reinterpret_cast<double2*>(buf)[tg >> 5] = make_double2(a, 0.0);
@@ -405,8 +415,8 @@ cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, dou
 // -1 hands the mesh back to the column-strip kernel (k_minres.cu).
 int minres_tile_variant(int N) {
     static int v[4] = {-2, -2, -2, -2};
-    const int slot = N == 16 ? 0 : N == 32 ? 1 : N == 64 ? 2 : 3;
-    if (slot == 3) return -1;
+    const int slot = N == 8 ? 3 : N == 16 ? 0 : N == 32 ? 1 : N == 64 ? 2 : -1;
+    if (slot < 0) return -1;
     if (v[slot] == -2) {
         char name[64];
         std::snprintf(name, sizeof(name), "MLMC_MINRES_TILE_N%d", N);
@@ -421,6 +431,9 @@ template <bool V>
 static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, double tol, int max_iter, double* out,
                                  int slot, unsigned* ctr, cudaStream_t s) {
     switch (N) {
+        case 8:   // two systems per warp (16 threads each)
+            if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 16:
             // measured (configs[1] level 1, 5000 systems): v0 0.28 ms, v1 0.31; strip 0.31
             if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
