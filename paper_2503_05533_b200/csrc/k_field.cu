@@ -12,6 +12,8 @@
 //     4x4 outputs per thread, k staged through shared memory in chunks of 16.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -115,11 +117,90 @@ __global__ void __launch_bounds__(256) field_kernel(const double* __restrict__ p
     }
 }
 
+// K1 on the FP64 tensor cores: DMMA (mma.sync m8n8k4 f64; tcgen05 has no f64 kind).
+// A CTA computes a 64-sample x 64-centroid tile of G = Xi Phi^T with 8 warps (2 along the
+// samples x 4 along the centroids, 32 x 16 each = 4 x 2 MMA tiles), K staged through shared
+// memory 16 at a time with a pitch of 68 doubles (= 4 mod 16: conflict-free fragment loads);
+// the epilogue applies exp (K2) and stores a[b * P + p].
+constexpr int FD_B = 64, FD_P = 64, FD_K = 16, FD_PITCH = 68;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) field_dmma_kernel(const double* __restrict__ phi, const double* __restrict__ xi,
+                                                         double* __restrict__ a, int P, int m, int nb) {
+    __shared__ double sX[FD_K][FD_PITCH];
+    __shared__ double sP[FD_K][FD_PITCH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wb = warp >> 2, wp = warp & 3;            // warp tile: samples 32*wb.., centroids 16*wp..
+    const int gq = lane >> 2, tq = lane & 3;            // fragment row group / thread in group
+    const int b0 = blockIdx.y * FD_B, p0 = blockIdx.x * FD_P;
+    double acc[4][2][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+    for (int k0 = 0; k0 < m; k0 += FD_K) {
+        for (int e = threadIdx.x; e < FD_K * FD_B; e += 256) {
+            const int r = e / FD_K, k = e % FD_K;
+            const int kk = k0 + k, b = b0 + r, pp = p0 + r;
+            sX[k][r] = (b < nb && kk < m) ? xi[(size_t)b * m + kk] : 0.0;
+            sP[k][r] = (pp < P && kk < m) ? phi[(size_t)pp * m + kk] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k4 = 0; k4 < FD_K; k4 += 4) {
+            double fa[4], fb[2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) fa[t] = sX[k4 + tq][32 * wb + 8 * t + gq];   // A[row = b][col = k]
+#pragma unroll
+            for (int u = 0; u < 2; ++u) fb[u] = sP[k4 + tq][16 * wp + 8 * u + gq];   // B[row = k][col = p]
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) dmma(acc[t][u][0], acc[t][u][1], fa[t], fb[u]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int b = b0 + 32 * wb + 8 * t + gq;
+        if (b >= nb) continue;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int p = p0 + 16 * wp + 8 * u + 2 * tq;
+            double* dst = a + (size_t)b * P + p;
+            if (p + 1 < P) {
+                *reinterpret_cast<double2*>(dst) = make_double2(exp(acc[t][u][0]), exp(acc[t][u][1]));
+            } else if (p < P) {
+                dst[0] = exp(acc[t][u][0]);
+            }
+        }
+    }
+}
+
+static bool field_use_ffma() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("MLMC_FIELD_KERNEL");
+        v = (e && std::strcmp(e, "ffma") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
                          cudaStream_t s) {
     if (nb == 0) return cudaSuccess;
-    dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nb + FT_B - 1) / FT_B));
-    field_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb);
+    if (field_use_ffma() || (P & 1)) {
+        dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nb + FT_B - 1) / FT_B));
+        field_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb);
+    } else {
+        dim3 grid((P + FD_P - 1) / FD_P, (unsigned)((nb + FD_B - 1) / FD_B));
+        field_dmma_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb);
+    }
     return cudaGetLastError();
 }
 
