@@ -56,7 +56,7 @@ struct TileCfg {
     static constexpr int GRID = ROWS * RP;
     static constexpr int DGRID = DS ? S * R * 2 * PAIRS : 0;   // d at [(row-1) * 2 * PAIRS + parity * PAIRS + pair]
     static constexpr int WGRID = WS ? S * R * PAIRS : 0;       // -cW of column 0 at [(row-1) * PAIRS + pair]
-    static constexpr int RED = 4 * NW;                         // two reduction buffers of NW (value, value) pairs
+    static constexpr int RED = 4 * NW;                         // reduction buffer: NW x (3 partials + pad)
     static constexpr int SMEM_PER_GROUP = GRID + DGRID + WGRID + RED;
     static constexpr size_t SMEM = sizeof(double) * SMEM_PER_GROUP * GROUPS + 16 * GROUPS;
 };
@@ -68,15 +68,6 @@ __device__ __forceinline__ unsigned lane_mask() {
     if constexpr (TPS >= 32) return 0xffffffffu;
     else return 0xffffu << (threadIdx.x & 16);
 }
-template <int TPS>
-__device__ __forceinline__ double warp_sum_all(double v) {
-    constexpr int W = TPS >= 32 ? 32 : TPS;
-    const unsigned m = lane_mask<TPS>();
-#pragma unroll
-    for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
-    return v;
-}
-
 template <int TPS, int GROUPS>
 __device__ __forceinline__ void tsync(int g) {
     if constexpr (TPS <= 32) {
@@ -88,46 +79,51 @@ __device__ __forceinline__ void tsync(int g) {
     }
 }
 
-// Fixed-order sum of the NW warp partials held in buf[2w + c] (every thread reads all of them,
-// so every thread ends with the same bits).
-template <int NW>
-__device__ __forceinline__ double2 sum_partials(const double* buf) {
-    double2 v[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) v[w] = reinterpret_cast<const double2*>(buf)[w];
-#pragma unroll
-    for (int st = 1; st < NW; st *= 2) {
-#pragma unroll
-        for (int w = 0; w + st < NW; w += 2 * st) {
-            v[w].x += v[w + st].x;
-            v[w].y += v[w + st].y;
-        }
-    }
-    return v[0];
-}
-
+// Sums of (a, b, c) over the system's threads, bit-identical in every thread: butterflies inside
+// each warp, then every thread adds the NW warp partials in the same fixed (pairwise) order.
 template <int TPS, int GROUPS>
-__device__ __forceinline__ double tsum1(double a, double* buf, int tg, int g) {
-    a = warp_sum_all<TPS>(a);
+__device__ __forceinline__ double4 tsum3(double a, double b, double c, double* buf, int tg, int g) {
+    constexpr int W = TPS >= 32 ? 32 : TPS;
+    const unsigned msk = lane_mask<TPS>();
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(msk, a, o);
+        b += __shfl_xor_sync(msk, b, o);
+        c += __shfl_xor_sync(msk, c, o);
+    }
     if constexpr (TPS <= 32) {
-        return a;
+        return make_double4(a, b, c, 0.0);
     } else {
-        if ((tg & 31) == 0) reinterpret_cast<double2*>(buf)[tg >> 5] = make_double2(a, 0.0);
+        constexpr int NW = TPS / 32;
+        if ((tg & 31) == 0) reinterpret_cast<double4*>(buf)[tg >> 5] = make_double4(a, b, c, 0.0);
         tsync<TPS, GROUPS>(g);
-        return sum_partials<TPS / 32>(buf).x;
+        double4 v[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v[w] = reinterpret_cast<const double4*>(buf)[w];
+#pragma unroll
+        for (int st = 1; st < NW; st *= 2) {
+#pragma unroll
+            for (int w = 0; w + st < NW; w += 2 * st) {
+                v[w].x += v[w + st].x;
+                v[w].y += v[w + st].y;
+                v[w].z += v[w + st].z;
+            }
+        }
+        return v[0];
     }
 }
 
-// Iteration k of MINRES, written so that the Givens chain is off the critical path:
-//  A(k)   y = A p_k / beta_k - (beta_k / beta_{k-1}) p_{k-1}          (p_k = beta_k v_k, unnormalised)
-//  alpha_k = v_k . y                                                   [reduction]
-//  B(k)   p_{k+1} = y - alpha_k v_k
-//  C(k)   wt_k = v_k - (eps_k / gamma_{k-2}) wt_{k-2} - (delta_k / gamma_{k-1}) wt_{k-1}
-//         (wt_k = gamma_k w_k: delta_k and eps_k are known once alpha_k is, gamma_k is not)
-//  beta_{k+1} = ||p_{k+1}||                                            [reduction]
-//  Givens: gamma_k, phi_k; 1^T x_k = 1^T x_{k-1} + (phi_k / gamma_k) 1^T wt_k
-// (A one-reduction variant, beta_{k+1}^2 = ||y||^2 - alpha_k^2, was tried and rejected: without
-// re-normalisation the error of ||v_k|| = 1 grows by ~alpha^2/beta^2 per step and the solve diverges.)
+// One MINRES step per stencil, one reduction per step (R27):
+//   step j:  t = A p_j;  reduce (p_j . t, p_j . p_j, 1 . p_j)           [the only reduction]
+//            beta_j = ||p_j||, alpha_j = p_j.t / p_j.p_j (= v_j^T A v_j), sigma_j = 1^T v_j
+//            Givens rotation of MINRES iteration k = j-1 (needs alpha_{j-1}, beta_j), stopping test
+//            Q += phi_k s_k with s_k = 1^T w_k from s_k = (sigma_k - eps_k s_{k-2} - delta_k s_{k-1}) / gamma_k
+//            p_{j+1} = t / beta_j - (alpha_j / beta_j) p_j - (beta_j / beta_{j-1}) p_{j-1}
+//            exchange p_{j+1} through shared memory                    [plain barrier]
+// p_j = beta_j v_j keeps its true norm (beta from the stored vector, no drift); alpha is the
+// Rayleigh quotient (Lanczos variant "A1") instead of v^T (A v - beta v_prev).  Three vectors per
+// node (p_{j-1}, p_j, t) instead of five; 11 fp64 operations per node and step.  VERIFY also
+// carries w_k and x_k (textbook updates) to report the true residual.
 template <int N, int R, int MINB, int CM, bool VERIFY>
 __global__ void __launch_bounds__(TileCfg<N, R, MINB, CM>::BLOCK, MINB)
 minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
@@ -141,8 +137,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
     double* Sg = smem + g * K::SMEM_PER_GROUP;           // exchange grid [row * RP + parity * PW + pair + 1]
     double* Dg = Sg + K::GRID;
     double* Wg = Dg + K::DGRID;
-    double* redA = Wg + K::WGRID;
-    double* redB = redA + 2 * K::NW;
+    double* red = Wg + K::WGRID;                          // NW x 4 doubles (3 partials + pad)
     int* jobslot = reinterpret_cast<int*>(smem + K::SMEM_PER_GROUP * GROUPS) + 4 * g;
 
     const int p = tg % PAIRS, s = tg / PAIRS;
@@ -150,8 +145,6 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
     const bool col1_live = i1 <= K::C;
     const bool top_live = j0 + R - 1 <= K::C;
     const double h = 1.0 / N, h2 = h * h;
-    // own column c of row j at Sg[j*RP + c*PW + p + 1];
-    // west of column i0 = parity-1 plane, pair p-1; east of column i1 = parity-0 plane, pair p+1
     double* const own = Sg + j0 * RP + p + 1;
     const double* const westp = Sg + j0 * RP + PW + p;
     const double* const eastp = Sg + j0 * RP + p + 2;
@@ -203,145 +196,160 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 dg1[DS ? 0 : r] = d1;
             }
         }
+        // y = A v (v = this thread's tile of the grid-exchanged vector held in VA/VB)
+        auto stencil = [&](const double (&VA)[R], const double (&VB)[R], int r, const double* grid_w,
+                           const double* grid_e, const double* grid_own, double& t0, double& t1) {
+            const double vW = grid_w[r * RP], vE = grid_e[r * RP];
+            const double vN0 = (r + 1 < R) ? VA[r + 1 < R ? r + 1 : r] : grid_own[R * RP];
+            const double vN1 = (r + 1 < R) ? VB[r + 1 < R ? r + 1 : r] : grid_own[R * RP + PW];
+            const double vS0 = (r > 0) ? VA[r > 0 ? r - 1 : 0] : grid_own[-RP];
+            const double vS1 = (r > 0) ? VB[r > 0 ? r - 1 : 0] : grid_own[-RP + PW];
+            const double sS0 = (r > 0) ? nN0[r > 0 ? r - 1 : 0] : nS0;
+            const double sS1 = (r > 0) ? nN1[r > 0 ? r - 1 : 0] : nS1;
+            const double d0 = DS ? dgp[r * 2 * PAIRS] : dg0[DS ? 0 : r];
+            const double d1 = DS ? dgp[r * 2 * PAIRS + PAIRS] : dg1[DS ? 0 : r];
+            const double w0 = WS ? wgp[r * PAIRS] : nW0[WS ? 0 : r];
+            t0 = d0 * VA[r];
+            t1 = d1 * VB[r];
+            t0 = fma(nE0[r], VB[r], t0);
+            t1 = fma(nE0[r], VA[r], t1);
+            t0 = fma(w0, vW, t0);
+            t1 = fma(nE1[r], vE, t1);
+            t0 = fma(nN0[r], vN0, t0);
+            t1 = fma(nN1[r], vN1, t1);
+            t0 = fma(sS0, vS0, t0);
+            t1 = fma(sS1, vS1, t1);
+        };
 
-        // ---- MINRES state: X = p_k, Y = p_{k-1} (then y), Wn = wt_{k-1}, Wo = wt_{k-2}
-        double X0[R], X1[R], Y0[R], Y1[R], Wn0[R], Wn1[R], Wo0[R], Wo1[R];
+        // ---- state: X = p_{j-1}, Y = p_j, T = A p_j
+        double X0[R], X1[R], Y0[R], Y1[R], T0[R], T1[R];
+        double Wa0[VERIFY ? R : 1], Wa1[VERIFY ? R : 1], Wb0[VERIFY ? R : 1], Wb1[VERIFY ? R : 1];
         double x0[VERIFY ? R : 1], x1[VERIFY ? R : 1];
-        double pb = 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const bool rl = (r < R - 1) || top_live;
             const double b0 = rl ? h2 : 0.0;
             const double b1 = rl && col1_live ? h2 : 0.0;
-            X0[r] = b0; X1[r] = b1; Y0[r] = 0.0; Y1[r] = 0.0;
-            Wn0[r] = 0.0; Wn1[r] = 0.0; Wo0[r] = 0.0; Wo1[r] = 0.0;
-            if constexpr (VERIFY) { x0[VERIFY ? r : 0] = 0.0; x1[VERIFY ? r : 0] = 0.0; }
+            X0[r] = 0.0; X1[r] = 0.0; Y0[r] = b0; Y1[r] = b1;
+            if constexpr (VERIFY) {
+                Wa0[VERIFY ? r : 0] = Wa1[VERIFY ? r : 0] = Wb0[VERIFY ? r : 0] = Wb1[VERIFY ? r : 0] = 0.0;
+                x0[VERIFY ? r : 0] = x1[VERIFY ? r : 0] = 0.0;
+            }
             own[r * RP] = b0;
             own[r * RP + PW] = b1;
-            pb = fma(b0, b0, fma(b1, b1, pb));
         }
-        pb = tsum1<TPS, GROUPS>(pb, redB, tg, g);          // barrier: the grid holds p_1 = b
-        double invb = pb > 0.0 ? rsqrt(pb) : 0.0;          // 1 / beta_k
-        const double beta1 = pb > 0.0 ? pb * invb : 0.0;
-        const double inv_beta1 = invb, tol_b = tol * beta1;
+        tsync<TPS, GROUPS>(g);                               // the grid holds p_1 = b
         const double m1 = col1_live ? 1.0 : 0.0, mt = top_live ? 1.0 : 0.0;
-        double dbar = 0.0, epsln = 0.0, phibar = beta1, cs = -1.0, sn = 0.0, ig1 = 0.0, ig2 = 0.0;
-        double Xt = 0.0;                                    // this thread's share of 1^T x_k
+        double beta1 = 0.0, tol_b = 0.0, inv_beta1 = 0.0;
+        double invb_prev = 0.0, beta_prev = 0.0, alpha_prev = 0.0, sigma_prev = 0.0;
+        double dbar = 0.0, epsln = 0.0, phibar = 0.0, cs = -1.0, sn = 0.0, s1q = 0.0, s2q = 0.0, Xq = 0.0;
+        int k = 0, status = 1;
 
-        // A: Y <- (A X) / beta_k + ncr * Y; partial of X . y
-        auto phaseA = [&](double (&XA)[R], double (&XB)[R], double (&YA)[R], double (&YB)[R], double ib, double ncr,
-                          double& pa) {
-            const double ib1 = ib * m1, ibt = ib * mt, ibt1 = ibt * m1;
-            double pa0 = 0.0, pa1 = 0.0;
+        // one step j with roles (XA/XB = p_{j-1}, YA/YB = p_j, grid = p_j); false when done
+        auto step = [&](double (&XA)[R], double (&XB)[R], double (&YA)[R], double (&YB)[R]) -> bool {
+            double pa0 = 0.0, pa1 = 0.0, pb0 = 0.0, pb1 = 0.0, pc0 = 0.0, pc1 = 0.0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const double vW = westp[r * RP], vE = eastp[r * RP];
-                const double vN0 = (r + 1 < R) ? XA[r + 1 < R ? r + 1 : r] : own[R * RP];
-                const double vN1 = (r + 1 < R) ? XB[r + 1 < R ? r + 1 : r] : own[R * RP + PW];
-                const double vS0 = (r > 0) ? XA[r > 0 ? r - 1 : 0] : own[-RP];
-                const double vS1 = (r > 0) ? XB[r > 0 ? r - 1 : 0] : own[-RP + PW];
-                const double sS0 = (r > 0) ? nN0[r > 0 ? r - 1 : 0] : nS0;
-                const double sS1 = (r > 0) ? nN1[r > 0 ? r - 1 : 0] : nS1;
-                const double d0 = DS ? dgp[r * 2 * PAIRS] : dg0[DS ? 0 : r];
-                const double d1 = DS ? dgp[r * 2 * PAIRS + PAIRS] : dg1[DS ? 0 : r];
-                const double w0 = WS ? wgp[r * PAIRS] : nW0[WS ? 0 : r];
-                double t0 = d0 * XA[r];
-                double t1 = d1 * XB[r];
-                t0 = fma(nE0[r], XB[r], t0);
-                t1 = fma(nE0[r], XA[r], t1);
-                t0 = fma(w0, vW, t0);
-                t1 = fma(nE1[r], vE, t1);
-                t0 = fma(nN0[r], vN0, t0);
-                t1 = fma(nN1[r], vN1, t1);
-                t0 = fma(sS0, vS0, t0);
-                t1 = fma(sS1, vS1, t1);
-                const double s0 = (r == R - 1) ? ibt : ib;
-                const double s1 = (r == R - 1) ? ibt1 : ib1;
-                const double y0 = fma(t0, s0, ncr * YA[r]);
-                const double y1 = fma(t1, s1, ncr * YB[r]);
-                YA[r] = y0;
-                YB[r] = y1;
-                pa0 = fma(XA[r], y0, pa0);
-                pa1 = fma(XB[r], y1, pa1);
+                double t0, t1;
+                stencil(YA, YB, r, westp, eastp, own, t0, t1);
+                T0[r] = t0;
+                T1[r] = t1;
+                pa0 = fma(YA[r], t0, pa0);
+                pa1 = fma(YB[r], t1, pa1);
+                pb0 = fma(YA[r], YA[r], pb0);
+                pb1 = fma(YB[r], YB[r], pb1);
+                pc0 += YA[r];
+                pc1 += YB[r];
             }
-            pa = pa0 + pa1;
-        };
-
-        int k = 1, status = 1;
-        double pa = 0.0;
-        if (beta1 == 0.0) {
-            status = 0;
-            k = 0;
-        } else {
-            phaseA(X0, X1, Y0, Y1, invb, 0.0, pa);
-        }
-        auto iterate = [&](double (&XA)[R], double (&XB)[R], double (&YA)[R], double (&YB)[R], double (&WnA)[R],
-                           double (&WnB)[R], double (&WoA)[R], double (&WoB)[R]) -> bool {
-            const double alpha = invb * tsum1<TPS, GROUPS>(pa, redA, tg, g);   // all grid reads of A(k) done
-            const double nca = -alpha * invb;
-            const double delta = cs * dbar + sn * alpha;
-            const double gbar = sn * dbar - cs * alpha;
-            const double c1 = invb, c2 = -epsln * ig2, c3 = -delta * ig1;
-            double pb0 = 0.0, pb1 = 0.0, sw0 = 0.0, sw1 = 0.0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {                  // B(k) into Y, C(k) into Wo
-                const double y0 = fma(nca, XA[r], YA[r]);
-                const double y1 = fma(nca, XB[r], YB[r]);
-                YA[r] = y0;
-                YB[r] = y1;
-                own[r * RP] = y0;
-                own[r * RP + PW] = y1;
-                pb0 = fma(y0, y0, pb0);
-                pb1 = fma(y1, y1, pb1);
-                const double w0 = fma(c1, XA[r], fma(c2, WoA[r], c3 * WnA[r]));
-                const double w1 = fma(c1, XB[r], fma(c2, WoB[r], c3 * WnB[r]));
-                WoA[r] = w0;
-                WoB[r] = w1;
-                sw0 += w0;
-                sw1 += w1;
+            const double4 S = tsum3<TPS, GROUPS>(pa0 + pa1, pb0 + pb1, pc0 + pc1, red, tg, g);
+            const double bb = S.y;
+            const double invb = bb > 0.0 ? rsqrt(bb) : 0.0;
+            const double beta = __dmul_rn(bb, invb);         // beta_j = ||p_j||
+            const double alpha = __dmul_rn(S.x, __dmul_rn(invb, invb));   // alpha_j = v_j^T A v_j
+            const double sigma = __dmul_rn(S.z, invb);       // 1^T v_j
+            // ---- Givens rotation of MINRES iteration k = j-1 (Paige-Saunders), gamma_k = hypot(gbar, beta_j);
+            // only the stopping test depends on it, so the p_{j+1} pass below does not wait for it
+            double phi = 0.0, oldeps = 0.0, delta = 0.0, invg = 0.0;
+            if (k > 0) {
+                // explicit roundings: the VERIFY instantiation must produce the same bits
+                oldeps = epsln;
+                delta = __fma_rn(cs, dbar, __dmul_rn(sn, alpha_prev));
+                const double gbar = __fma_rn(sn, dbar, -__dmul_rn(cs, alpha_prev));
+                epsln = __dmul_rn(sn, beta);
+                dbar = -__dmul_rn(cs, beta);
+                const double gg = __fma_rn(gbar, gbar, bb);
+                invg = gg > 0.0 ? rsqrt(gg) : 1.0 / DBL_MIN;
+                cs = __dmul_rn(gbar, invg);
+                sn = __dmul_rn(beta, invg);
+                phi = __dmul_rn(cs, phibar);
+                phibar = __dmul_rn(sn, phibar);
+                // 1^T w_k by the scalar recurrence (R26), Q_k = Q_{k-1} + phi_k 1^T w_k
+                const double sq = __dmul_rn(__fma_rn(-delta, s1q, __fma_rn(-oldeps, s2q, sigma_prev)), invg);
+                s2q = s1q;
+                s1q = sq;
+                Xq = __fma_rn(phi, sq, Xq);
+            } else {                                         // j = 1: beta_1 = ||b||
+                beta1 = beta;
+                inv_beta1 = invb;
+                tol_b = tol * beta1;
+                phibar = beta1;
             }
-            const double b2 = tsum1<TPS, GROUPS>(pb0 + pb1, redB, tg, g);   // grid holds p_{k+1}
-            const double invb_new = b2 > 0.0 ? rsqrt(b2) : 0.0;
-            const double beta = b2 * invb_new;              // beta_{k+1}
-            // ---- Givens rotation (Paige-Saunders); gamma_k = hypot(gbar, beta_{k+1})
-            epsln = sn * beta;
-            dbar = -cs * beta;
-            const double gg = fma(gbar, gbar, b2);
-            const double invg = gg > 0.0 ? rsqrt(gg) : 1.0 / DBL_MIN;
-            cs = gbar * invg;
-            sn = beta * invg;
-            const double phi = cs * phibar;
-            phibar = sn * phibar;
-            const double phig = phi * invg;                 // x_k = x_{k-1} + (phi_k / gamma_k) wt_k
-            Xt = fma(phig, sw0 + sw1, Xt);
-            ig2 = ig1;
-            ig1 = invg;
             if constexpr (VERIFY) {
+                if (k > 0) {
+                    // w_k = (v_k - eps w_{k-2} - delta w_{k-1}) / gamma_k, v_k = p_k / beta_k = X * invb_prev
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    x0[VERIFY ? r : 0] = fma(phig, WoA[r], x0[VERIFY ? r : 0]);
-                    x1[VERIFY ? r : 0] = fma(phig, WoB[r], x1[VERIFY ? r : 0]);
+                    for (int r = 0; r < R; ++r) {
+                        const double u0 = (XA[r] * invb_prev - oldeps * Wb0[VERIFY ? r : 0] - delta * Wa0[VERIFY ? r : 0]) * invg;
+                        const double u1 = (XB[r] * invb_prev - oldeps * Wb1[VERIFY ? r : 0] - delta * Wa1[VERIFY ? r : 0]) * invg;
+                        Wb0[VERIFY ? r : 0] = Wa0[VERIFY ? r : 0];
+                        Wb1[VERIFY ? r : 0] = Wa1[VERIFY ? r : 0];
+                        Wa0[VERIFY ? r : 0] = u0;
+                        Wa1[VERIFY ? r : 0] = u1;
+                        x0[VERIFY ? r : 0] = fma(phi, u0, x0[VERIFY ? r : 0]);
+                        x1[VERIFY ? r : 0] = fma(phi, u1, x1[VERIFY ? r : 0]);
+                    }
                 }
             }
-            if (!(phibar == phibar) || !(beta == beta)) status = 3;
-            else if (phibar <= tol_b) status = 0;           // phibar / ||b|| <= tol
-            if (status != 1 || k >= max_iter) return false; // uniform across the system
-            // A(k+1): X <- A p_{k+1} / beta_{k+1} - (beta_{k+1} / beta_k) p_k
-            phaseA(YA, YB, XA, XB, invb_new, -beta * invb, pa);
-            invb = invb_new;
+            // ---- p_{j+1} = t / beta_j - (alpha_j / beta_j) p_j - (beta_j / beta_{j-1}) p_{j-1}, into X
+            const double ct = invb, c1 = -alpha * invb, c0 = k == 0 ? 0.0 : -beta * invb_prev;
+            const double ct1 = ct * m1, ctt = ct * mt, ctt1 = ctt * m1;   // phantom nodes stay 0
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double sa = (r == R - 1) ? ctt : ct;
+                const double sb = (r == R - 1) ? ctt1 : ct1;
+                const double q0 = fma(sa, T0[r], fma(c1, YA[r], c0 * XA[r]));
+                const double q1 = fma(sb, T1[r], fma(c1, YB[r], c0 * XB[r]));
+                XA[r] = q0;
+                XB[r] = q1;
+                own[r * RP] = q0;
+                own[r * RP + PW] = q1;
+            }
+            // stopping test of iteration k (uniform across the system); the p_{j+1} pass of the
+            // last step is discarded
+            if (k == 0) {
+                if (beta1 == 0.0) { status = 0; return false; }
+            } else {
+                if (!(phibar == phibar) || !(beta == beta)) { status = 3; return false; }
+                if (phibar <= tol_b) { status = 0; return false; }       // phibar / ||b|| <= tol
+                if (k >= max_iter) return false;
+            }
+            tsync<TPS, GROUPS>(g);                           // the grid holds p_{j+1}
+            invb_prev = invb;
+            beta_prev = beta;
+            alpha_prev = alpha;
+            sigma_prev = sigma;
             ++k;
             return true;
         };
-        if (status == 1) {
-            for (;;) {
-                if (!iterate(X0, X1, Y0, Y1, Wn0, Wn1, Wo0, Wo1)) break;
-                if (!iterate(Y0, Y1, X0, X1, Wo0, Wo1, Wn0, Wn1)) break;
-            }
+        for (;;) {
+            if (!step(X0, X1, Y0, Y1)) break;
+            if (!step(Y0, Y1, X0, X1)) break;
         }
+        (void)beta_prev;
         double relres = phibar * inv_beta1;
-        const double Xs = tsum1<TPS, GROUPS>(Xt, redA, tg, g);
         if constexpr (VERIFY) {
-            // true residual ||b - A x|| / ||b|| (the loop's last grid reads precede the barrier above)
+            // true residual ||b - A x|| / ||b||: x goes through the grid (the last step's grid reads
+            // precede its reduction barrier)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 own[r * RP] = x0[VERIFY ? r : 0];
@@ -352,32 +360,18 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const bool rl = (r < R - 1) || top_live;
-                const double v0 = own[r * RP], v1 = own[r * RP + PW];
-                const double sS0 = (r > 0) ? nN0[r > 0 ? r - 1 : 0] : nS0;
-                const double sS1 = (r > 0) ? nN1[r > 0 ? r - 1 : 0] : nS1;
-                const double d0 = DS ? dgp[r * 2 * PAIRS] : dg0[DS ? 0 : r];
-                const double d1 = DS ? dgp[r * 2 * PAIRS + PAIRS] : dg1[DS ? 0 : r];
-                const double w0 = WS ? wgp[r * PAIRS] : nW0[WS ? 0 : r];
-                double t0 = d0 * v0;
-                t0 = fma(nE0[r], v1, t0);
-                t0 = fma(w0, westp[r * RP], t0);
-                t0 = fma(nN0[r], own[r * RP + RP], t0);
-                t0 = fma(sS0, own[r * RP - RP], t0);
-                double t1 = d1 * v1;
-                t1 = fma(nE1[r], eastp[r * RP], t1);
-                t1 = fma(nE0[r], v0, t1);
-                t1 = fma(nN1[r], own[r * RP + RP + PW], t1);
-                t1 = fma(sS1, own[r * RP - RP + PW], t1);
+                double t0, t1;
+                stencil(x0, x1, r, westp, eastp, own, t0, t1);
                 const double res0 = rl ? h2 - t0 : 0.0;
                 const double res1 = rl && col1_live ? h2 - t1 : 0.0;
                 rr = fma(res0, res0, fma(res1, res1, rr));
             }
-            rr = tsum1<TPS, GROUPS>(rr, redB, tg, g);
+            rr = tsum3<TPS, GROUPS>(rr, 0.0, 0.0, red, tg, g).x;
             relres = sqrt(rr) * inv_beta1;
         }
         if (tg == 0) {
             double* o = out + (size_t)job * kRecLen;
-            o[0 + slot] = h2 * Xs;
+            o[0 + slot] = h2 * Xq;
             o[2 + slot] = (double)k;
             o[4 + slot] = relres;
             o[6 + slot] = (double)status;
@@ -435,20 +429,20 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
             return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 16:
-            // measured (configs[1] level 1, 5000 systems): v0 0.28 ms, v1 0.31; strip 0.31
             if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
             return run_tile<16, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 32:
-            // measured (configs[1] level 2, 1200 systems): v0 0.66 ms, v1 0.69, v2 0.75, v3 0.74; strip 1.02
-            if (var == 1) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 2) return run_tile<32, 8, 2, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 3) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
             return run_tile<32, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 64:
-            // measured (configs[1] level 3, 300 systems): v0 2.31 ms, v1 2.40, v2 3.03; strip kernel 3.25
-            if (var == 1) return run_tile<64, 8, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 2) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67
+            if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         default: return cudaErrorNotSupported;
     }
 }
