@@ -9,6 +9,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "list rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-   -k "regex:minres_strip_kernel<.int.(64|32)," -s 6 -c 3 -o gpurun_out/prof_minres -f $CMD > gpurun_out/ncu_full.log 2>&1
+   -k "regex:minres_tile_kernel<.int.(64|32)," -s 6 -c 3 -o gpurun_out/prof_minres -f $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
 tail -3 gpurun_out/ncu_full.log
