@@ -139,8 +139,16 @@ typedef struct { int32_t N, n, P, bw; double h; } mlmc_level_info;
 int mlmc_level_info_get(const mlmc_ctx* ctx, int level, mlmc_level_info* out);
 
 /* Device workspace needed to process `batch` coupled samples of `level` per
- * kernel pass (larger n are processed in passes).  Host-only.               */
+ * kernel pass (larger n are processed in passes) with MINRES solves.
+ * Host-only.                                                                */
 int mlmc_workspace_bytes(const mlmc_ctx* ctx, int level, uint64_t batch, size_t* out);
+
+/* The same for the given fine / coarse precisions (either may be NULL =
+ * MINRES): Cholesky-IR solves (K4) also need a factor scratch of one factor
+ * per resident warp segment -- it depends on the format and on the device's
+ * occupancy, so this query needs the device (ECUDA without one).            */
+int mlmc_workspace_bytes_prec(const mlmc_ctx* ctx, int level, uint64_t batch, const mlmc_precision* prec_fine,
+                              const mlmc_precision* prec_coarse, size_t* out);
 
 /* Lend the library a device buffer (>= 256-byte aligned) and the cudaStream_t
  * all later work is ordered on (NULL = the legacy default stream; before the

@@ -93,6 +93,8 @@ def lib():
     L.mlmc_last_error.restype = C.c_char_p
     L.mlmc_level_info_get.argtypes = [vp, C.c_int, C.POINTER(LevelInfo)]
     L.mlmc_workspace_bytes.argtypes = [vp, C.c_int, C.c_uint64, C.POINTER(C.c_size_t)]
+    L.mlmc_workspace_bytes_prec.argtypes = [vp, C.c_int, C.c_uint64, C.POINTER(Precision), C.POINTER(Precision),
+                                            C.POINTER(C.c_size_t)]
     L.mlmc_bind_workspace.argtypes = [vp, vp, C.c_size_t, vp]
     L.mlmc_sample_level.argtypes = [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(Precision),
                                     C.POINTER(Precision), C.c_double, C.c_double, C.POINTER(LevelSums), vp]

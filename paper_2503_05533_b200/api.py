@@ -91,6 +91,15 @@ class Context:
         K.check(K.lib().mlmc_workspace_bytes(self.ctx, level, batch, C.byref(out)), self.ctx)
         return out.value
 
+    def workspace_bytes_prec(self, level: int, batch: int, prec_fine="minres", prec_coarse=None) -> int:
+        """mlmc_workspace_bytes_prec: includes the Cholesky-IR factor scratch of the given precisions."""
+        pf = _as_prec(prec_fine)
+        pc = _as_prec(prec_coarse if prec_coarse is not None else prec_fine)
+        out = C.c_size_t()
+        K.check(K.lib().mlmc_workspace_bytes_prec(self.ctx, level, batch, C.byref(pf), C.byref(pc), C.byref(out)),
+                self.ctx)
+        return out.value
+
     # ------------------------------------------------------------------ hot path
     def sample_level(self, level: int, n: int, seed: int, first_index: int = 0, prec_fine="minres",
                      prec_coarse=None, tol_fine: float = 1e-8, tol_coarse: Optional[float] = None,

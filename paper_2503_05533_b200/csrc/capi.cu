@@ -103,10 +103,16 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Workspace layout for one pass of `batch` samples of `level`.
 struct WsLayout {
-    size_t xi, a_f, a_c, rec, chunks, ctr, gm, total;
+    size_t xi, a_f, a_c, rec, chunks, ctr, gm, ch_f, ch_c, ch_f_bytes, ch_c_bytes, total;
     int gm_ctas;
 };
-WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch) {
+// Cholesky factor scratch of one solve (0 for MINRES / unsupported combinations)
+size_t chol_bytes(const mlmc_precision* p, int N, uint64_t batch) {
+    if (!p || p->solver != MLMC_SOLVER_CHOL_IR || N < 2) return 0;
+    return chol_scratch_bytes(N, p->u_f, p->u_s, batch);
+}
+WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_precision* pf = nullptr,
+                   const mlmc_precision* pc = nullptr) {
     WsLayout L{};
     int Nf = level_N(c, level), Nc = level > 0 ? level_N(c, level - 1) : 0;
     size_t off = 0;
@@ -122,16 +128,22 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch) {
         L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1));
         off += align256(minres_gm_scratch_per_cta(Nf) * L.gm_ctas);
     }
+    // factor scratch of the Cholesky-IR solves (fine and coarse may run concurrently: two regions)
+    L.ch_f_bytes = chol_bytes(pf, Nf, batch);
+    L.ch_c_bytes = level > 0 ? chol_bytes(pc, Nc, batch) : 0;
+    L.ch_f = off;   off += align256(L.ch_f_bytes);
+    L.ch_c = off;   off += align256(L.ch_c_bytes);
     L.total = off;
     return L;
 }
 
-uint64_t max_batch(const mlmc_ctx* c, int level, size_t bytes) {
+uint64_t max_batch(const mlmc_ctx* c, int level, size_t bytes, const mlmc_precision* pf = nullptr,
+                   const mlmc_precision* pc = nullptr) {
     uint64_t lo = 0, hi = 1;
-    while (ws_layout(c, level, hi).total <= bytes && hi < (1ull << 40)) { lo = hi; hi *= 2; }
+    while (ws_layout(c, level, hi, pf, pc).total <= bytes && hi < (1ull << 40)) { lo = hi; hi *= 2; }
     while (hi - lo > 1) {
         uint64_t mid = lo + (hi - lo) / 2;
-        if (ws_layout(c, level, mid).total <= bytes) lo = mid; else hi = mid;
+        if (ws_layout(c, level, mid, pf, pc).total <= bytes) lo = mid; else hi = mid;
     }
     return lo;
 }
@@ -191,7 +203,8 @@ void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
 }
 
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
-               double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas) {
+               double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas, void* ch_scratch,
+               size_t ch_bytes) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
@@ -206,7 +219,10 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
     } else {
         int mi = p->max_iter > 0 ? p->max_iter : 50;
         CU(counted(ctx, ex.st, MLMC_K_CHOL_IR, N,
-                   [&] { return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ex.st); }));
+                   [&] {
+                       return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ch_scratch, ch_bytes,
+                                             ex.st);
+                   }));
     }
     return MLMC_OK;
 }
@@ -229,11 +245,11 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
               double* per_sample, bool per_sample_is_dev, const double* xi_in, bool xi_in_is_dev,
               const LevelSched* sch = nullptr) {
     const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
-    uint64_t B = max_batch(ctx, level, ex.bytes);
+    uint64_t B = max_batch(ctx, level, ex.bytes, pf, pc);
     if (B == 0 && n > 0) return fail(ctx, MLMC_ENOMEM, "workspace too small for one sample");
     // passes made of whole 4096-sample chunks: the chunked sums then do not depend on the pass size
     if (B > kChunk && B < n) B = (B / kChunk) * kChunk;
-    const WsLayout L = ws_layout(ctx, level, std::max<uint64_t>(B, 1));
+    const WsLayout L = ws_layout(ctx, level, std::max<uint64_t>(B, 1), pf, pc);
     double* xi = reinterpret_cast<double*>(ex.ws + L.xi);
     double* af = reinterpret_cast<double*>(ex.ws + L.a_f);
     double* ac = reinterpret_cast<double*>(ex.ws + L.a_c);
@@ -273,13 +289,17 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
             CU(cudaEventRecord(sch->fork, st));
             CU(cudaStreamWaitEvent(sch->st_c, sch->fork, 0));
         }
-        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas))) return rc;
+        void* chf = ex.ws + L.ch_f;
+        void* chc = ex.ws + L.ch_c;
+        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes))) return rc;
         if (fork) {
             const Exec exc{ex.ws, ex.bytes, sch->st_c};
-            if ((rc = solve_mesh(ctx, exc, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas))) return rc;
+            if ((rc = solve_mesh(ctx, exc, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc, L.ch_c_bytes)))
+                return rc;
             CU(cudaEventRecord(sch->join, sch->st_c));
             CU(cudaStreamWaitEvent(st, sch->join, 0));
-        } else if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas))) {
+        } else if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc,
+                                                 L.ch_c_bytes))) {
             return rc;
         }
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
@@ -410,6 +430,14 @@ int mlmc_workspace_bytes(const mlmc_ctx* ctx, int level, uint64_t batch, size_t*
     return MLMC_OK;
 }
 
+int mlmc_workspace_bytes_prec(const mlmc_ctx* ctx, int level, uint64_t batch, const mlmc_precision* prec_fine,
+                              const mlmc_precision* prec_coarse, size_t* out) {
+    if (!ctx || !out || level < 0 || level > ctx->pr.L_max) return MLMC_EINVAL;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return MLMC_ECUDA;
+    *out = ws_layout(ctx, level, std::max<uint64_t>(batch, 1), prec_fine, prec_coarse).total;
+    return MLMC_OK;
+}
+
 int mlmc_bind_workspace(mlmc_ctx* ctx, void* dev_ptr, size_t bytes, void* cuda_stream) {
     if (!ctx) return MLMC_EINVAL;
     if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 255)) return fail(ctx, MLMC_EINVAL, "workspace NULL or not 256-byte aligned");
@@ -468,7 +496,7 @@ int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const u
     std::vector<size_t> need(nlev);
     size_t total = 0;
     for (int q = 0; q < nlev; ++q) {
-        need[q] = ws_layout(ctx, levels[q], std::max<uint64_t>(n[q], 1)).total;
+        need[q] = ws_layout(ctx, levels[q], std::max<uint64_t>(n[q], 1), &prec_fine[q], &prec_coarse[q]).total;
         total += need[q];
     }
     std::vector<size_t> slice(nlev);
@@ -511,7 +539,8 @@ int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const u
         sch.join = ctx->cjoin_ev[k];
         sch.prep = k == 0 ? ctx->prep_ev[0] : nullptr;
         sch.gate = k == 0 ? nullptr : ctx->prep_ev[0];
-        const bool top_single = max_batch(ctx, levels[order[0]], slice[order[0]]) >= n[order[0]];
+        const bool top_single =
+            max_batch(ctx, levels[order[0]], slice[order[0]], &prec_fine[order[0]], &prec_coarse[order[0]]) >= n[order[0]];
         if (!top_single) sch.prep = sch.gate = nullptr;   // the largest level runs in passes: no gate
         int rc = run_level(ctx, Exec{ctx->ws + offs[q], slice[q], st}, levels[q], n[q], seed, first_index[q],
                            &prec_fine[q], &prec_coarse[q], tol_fine[q], tol_coarse[q], sums_dev + (size_t)q * kSumsLen,

@@ -1,4 +1,4 @@
-// k_chol.cu -- K4: batched banded Cholesky in a low precision u_f + iterative refinement.
+// k_chol.cu -- K4 v2: batched banded Cholesky in a low precision u_f + iterative refinement.
 //
 // Algorithm 1 for the P1 system A x = b of one sample:
 //   1. factorise A = L L^T in precision u_f
@@ -8,286 +8,651 @@
 //   5.   if ||r_i|| / ||b|| < tol: exit
 //   7.   solve A d_i = r_i with the retained factor in u_s
 //   8.   x_{i+1} = x_i + d_i in u (binary64)
-// The matrix is the 5-point P1 operator (R10): natural ordering gives band
-// width bw = N - 1 and the factor fills the band completely, so L is kept as
-// a dense n x (bw+1) band, Lb[r*(bw+1) + d] = L(r, r-d), in shared memory in
-// the factor format (fp16 / fp32 / fp64) -- mixed precision is what makes the
-// factor of the h = 1/32 level fit on chip (61.5 KB fp16, 123 KB fp32).
+// The matrix is the 5-point P1 operator (R10).  In natural ordering its band
+// width is bw = N - 1 and the factor fills the band, so L has W = N entries per
+// column: L(k+d, k), d = 0..W-1.
 //
-// B200 mapping: one warp per sample, lanes = band offsets (bw + 1 <= 32).
-//  * factorisation, right-looking in place: step k computes column k
-//    (lane i: L(k+i,k)) and applies the rank-1 update to the (bw x bw) window,
-//    lane i owning row k+i; every arithmetic op in the factor type.
-//  * substitutions, column-oriented with a sliding register window: lane d
-//    holds the pending right-hand side entry k+d; one broadcast and one
-//    shift per row.
-//  * residual in binary64 with the stencil from the conductances (kept in
-//    shared memory), reductions by xor butterflies.
+// B200 mapping (K4).  One W-lane segment of a warp per
+// sample (W = N <= 32; 32/W samples share a warp and run in lockstep).
+//  * The factor never has to fit on chip: it is written once to a per-segment
+//    global scratch in "column-band" blocks, Lc[k][d] = L(k+d, k), W rows x W
+//    entries = one contiguous block per W columns, and streamed back into a
+//    3-slot shared-memory ring by TMA bulk copies (cp.async.bulk, mbarrier
+//    completion) for every substitution.  The factor format u_f sets the bytes
+//    each substitution moves -- the paper's memory-reference argument
+//    taken literally: fp16 halves them against fp32.
+//  * Factorisation (right-looking, band window in registers): lane l owns the
+//    rows r = l (mod W) currently in the W-row window [k, k+W); row r keeps
+//    A(r, c) for its W band columns in register c mod W, so every step k
+//    addresses the registers with the compile-time index k mod W (the k loop is
+//    unrolled by W).  Step k: pivot from lane k mod W by one shuffle, every lane
+//    divides its column entry by sqrt(pivot) in u_f, the column goes to the
+//    global factor (one coalesced W-entry row) and through shared memory to the
+//    rank-1 update of the window (W-1 FMAs per lane in u_f, no predication:
+//    entries right of a row's diagonal are dead registers).  The pivot lane
+//    then loads row k+W (3 nonzeros of A) into its registers.
+//  * Substitutions (column-oriented, rotating ownership): lane l holds the
+//    pending right-hand-side entry of the window row r = l (mod W); each row
+//    costs one shuffle, one multiply by the (off-chain) reciprocal pivot and one
+//    FMA per lane in u_s (R28); the finished entry is written in place to a
+//    shared-memory vector.  Forward reads Lc[k][*] (a block row), backward
+//    reads row k of L = Lc[k-d][d] (a block diagonal, bank-conflict free).
+//  * Residual and update in binary64 from the shared x and the triangle
+//    coefficients (conductances rebuilt on the fly, L1/L2).
+// The system is padded to n_pad = N(N-1) = (N-1) W rows with identity rows
+// (zero right-hand side), which keeps every loop a whole number of blocks.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
 namespace mlmc {
+namespace {
 
 template <typename T> struct FT;
 template <> struct FT<double> {
     static __device__ __forceinline__ double from(double v) { return v; }
-    static __device__ __forceinline__ double to_d(double v) { return v; }
     static __device__ __forceinline__ double fnma(double a, double b, double c) { return fma(-a, b, c); }
     static __device__ __forceinline__ double div(double a, double b) { return a / b; }
     static __device__ __forceinline__ double sqrt_(double a) { return sqrt(a); }
     static __device__ __forceinline__ bool pos_finite(double a) { return a > 0.0 && a <= DBL_MAX; }
+    static __device__ __forceinline__ float to_f(double v) { return (float)v; }
+    static __device__ __forceinline__ double to_d(double v) { return v; }
 };
 template <> struct FT<float> {
     static __device__ __forceinline__ float from(double v) { return __double2float_rn(v); }
-    static __device__ __forceinline__ double to_d(float v) { return (double)v; }
     static __device__ __forceinline__ float fnma(float a, float b, float c) { return __fmaf_rn(-a, b, c); }
     static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
     static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
     static __device__ __forceinline__ bool pos_finite(float a) { return a > 0.0f && a <= FLT_MAX; }
+    static __device__ __forceinline__ float to_f(float v) { return v; }
+    static __device__ __forceinline__ double to_d(float v) { return (double)v; }
 };
 template <> struct FT<__half> {
     static __device__ __forceinline__ __half from(double v) { return __double2half(v); }
-    static __device__ __forceinline__ double to_d(__half v) { return (double)__half2float(v); }
     static __device__ __forceinline__ __half fnma(__half a, __half b, __half c) { return __hfma(__hneg(a), b, c); }
     static __device__ __forceinline__ __half div(__half a, __half b) { return __hdiv(a, b); }
     static __device__ __forceinline__ __half sqrt_(__half a) { return __float2half_rn(sqrtf(__half2float(a))); }
     static __device__ __forceinline__ bool pos_finite(__half a) {
-        float f = __half2float(a);
+        const float f = __half2float(a);
         return f > 0.0f && f <= 65504.0f;
     }
+    static __device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
+    static __device__ __forceinline__ double to_d(__half v) { return (double)__half2float(v); }
 };
-
-__device__ __forceinline__ double wsum_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+// if (l == u) { cur = nxt; y = yk; } as one setp + two predicated moves, kept in place (volatile) so
+// the compiler does not materialise all W lane predicates of an unrolled block up front
+__device__ __forceinline__ void pivot_take(int l, int u, float& cur, float nxt, float& y, float yk) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\t@p mov.f32 %0, %4;\n\t@p mov.f32 %1, %5;\n}"
+                 : "+f"(cur), "+f"(y)
+                 : "r"(l), "r"(u), "f"(nxt), "f"(yk));
+}
+__device__ __forceinline__ void pivot_take(int l, int u, double& cur, double nxt, double& y, double yk) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\t@p mov.f64 %0, %4;\n\t@p mov.f64 %1, %5;\n}"
+                 : "+d"(cur), "+d"(y)
+                 : "r"(l), "r"(u), "d"(nxt), "d"(yk));
+}
+// correctly rounded reciprocal in the substitution precision (R28)
+__device__ __forceinline__ float rcp_s(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_s(double x) { return __drcp_rn(x); }
+// factor entry -> substitution precision S
+template <typename S, typename F> __device__ __forceinline__ S to_s(F v) {
+    if constexpr (sizeof(S) == 8) return FT<F>::to_d(v);
+    else return FT<F>::to_f(v);
 }
 
-template <int N, typename F>
-struct CholCfg {
+template <int N, typename F, typename S, int NS_ = 3, int WPC_ = 4>
+struct Chol2Cfg {
+    static constexpr int NS = NS_;                     // ring slots (factor blocks in flight + in use)
+    static constexpr int WPC = WPC_;                   // warps per CTA
+    static constexpr int W = N;                        // band entries per column, segment width
     static constexpr int n = (N - 1) * (N - 1);
-    static constexpr int BW = N - 1;
-    static constexpr int W = BW + 1;   // band row length (<= 32)
-    static constexpr size_t band_bytes = ((sizeof(F) * (size_t)n * W + 15) / 16) * 16;
-    // per warp: band, cE, cN (N^2 doubles each), x, r (n doubles each), 2 ints
-    static constexpr size_t per_warp = band_bytes + sizeof(double) * (2 * N * N + 2 * n) + 16;
-    static constexpr int WARPS = (int)((200 * 1024) / per_warp) < 1 ? 1
-                                 : ((int)((200 * 1024) / per_warp) > 8 ? 8 : (int)((200 * 1024) / per_warp));
-    static constexpr size_t SMEM = per_warp * WARPS;
-    static_assert(W <= 32, "band must fit a warp");
+    static constexpr int NB = N - 1;                   // blocks of W rows / columns
+    static constexpr int NPAD = NB * W;                // padded system size N(N-1) >= n
+    static constexpr int SEGS = 32 / W;                // samples per warp
+    static constexpr int FE = W * (int)sizeof(F);      // bytes of one lane row of a block
+    static constexpr int C = FE / 16;                  // 16-byte chunks per lane row (0: scalar access)
+    static constexpr int EPC = 16 / (int)sizeof(F);    // entries per chunk
+    static constexpr int LPR = C >= 8 ? 1 : (C > 0 ? 8 / C : 1);   // lane rows per 128-byte bank row
+    static constexpr int HDR = W * FE;                 // reciprocal pivots (S) after the W lane rows
+    static constexpr int BLK = ((HDR + W * (int)sizeof(S) + 127) / 128) * 128;   // block stride (bytes)
+    static constexpr size_t FBYTES = (size_t)2 * NB * BLK;   // forward + backward layouts per segment
+    // shared memory per segment: ring (NS blocks) | x (binary64) | v (u_s) | column buffer | mbarriers
+    static constexpr int OFF_X = NS * BLK;
+    static constexpr int OFF_V = OFF_X + NPAD * 8;
+    static constexpr int OFF_C = OFF_V + ((NPAD * (int)sizeof(S) + 15) / 16) * 16;
+    static constexpr int OFF_B = OFF_C + ((2 * W * (int)sizeof(F) + 15) / 16) * 16;
+    static constexpr int SEG_BYTES = ((OFF_B + NS * 8 + 127) / 128) * 128;
+    static constexpr int SMEM = SEG_BYTES * SEGS * WPC;
+    static_assert(W >= 2 && W <= 32 && (W & (W - 1)) == 0, "segment width must be a power of two <= 32");
+    // byte offset of entry e of lane row r inside a block: 16-byte chunks rotated per lane row so that
+    // a quarter-warp reading chunk i of 8 consecutive lane rows hits 8 distinct bank groups
+    static __device__ __forceinline__ int off(int r, int e) {
+        if constexpr (C == 0) return r * FE + e * (int)sizeof(F);
+        else return r * FE + (((e / EPC) + r / LPR) % C) * 16 + (e % EPC) * (int)sizeof(F);
+    }
 };
 
-// forward (L y = r) and backward (L^T z = y) substitution in precision S, in place on v (binary64 storage).
-template <int N, typename F, typename S>
-__device__ __forceinline__ void band_solve(const F* __restrict__ Lb, double* __restrict__ v, int lane) {
-    using C = CholCfg<N, F>;
-    constexpr int n = C::n, W = C::W, BW = C::BW;
-    // forward: lane d holds the pending entry k + d
-    S cur = (lane < W && lane < n) ? (S)v[lane] : (S)0;
-    for (int k = 0; k < n; ++k) {
-        S yk = (S)0;
-        if (lane == 0) yk = cur / (S)FT<F>::to_d(Lb[(size_t)k * W]);
-        yk = __shfl_sync(0xffffffffu, yk, 0);
-        if (lane >= 1 && lane <= BW && k + lane < n) cur = cur - (S)FT<F>::to_d(Lb[(size_t)(k + lane) * W + lane]) * yk;
-        if (lane == 0) v[k] = (double)yk;
-        S nxt = __shfl_down_sync(0xffffffffu, cur, 1);
-        if (lane == BW) nxt = (k + W < n) ? (S)v[k + W] : (S)0;
-        cur = nxt;
+// ---- mbarrier / bulk-copy primitives (PTX)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// (A slot is refilled only after every lane of the segment has consumed the values it read from it
+// and passed a __syncwarp, so no proxy fence is issued per fill.)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// FIFO ring of factor blocks for one segment (NS slots).  The blocks are consumed in a fixed
+// sequence -- forward pass LF[0..NB-1], backward pass LB[NB-1..0], forward, ... -- so fill
+// position p goes to slot p % NS and completes phase (p / NS) & 1 of that slot's mbarrier; the
+// producer (the segment's lane 0) keeps NS-1 positions ahead of the consumer.  Counters are
+// absolute across jobs (the mbarrier phases are); P0 is the first position of the current job.
+struct Ring {
+    unsigned char* buf;     // slot 0 (generic address)
+    uint32_t sbuf, bar;     // shared addresses of slot 0 and barrier 0
+    const unsigned char* lf;
+    const unsigned char* lb;
+    unsigned P0, iss, use;
+};
+
+template <int NB, int BLK, int NS>
+__device__ __forceinline__ const unsigned char* ring_acquire(Ring& R, bool leader) {
+    __syncwarp();                                   // all lanes are done with position use-1
+    while (R.iss < R.use + NS) {
+        const unsigned i = R.iss - R.P0, pass = i / NB, j = i % NB;
+        const unsigned char* src = (pass & 1) ? R.lb + (size_t)(NB - 1 - j) * BLK : R.lf + (size_t)j * BLK;
+        if (leader) bulk_load(R.sbuf + (R.iss % NS) * BLK, src, BLK, R.bar + 8 * (R.iss % NS));
+        ++R.iss;
     }
+    mbar_wait(R.bar + 8 * (R.use % NS), (R.use / NS) & 1u);
+    const unsigned char* p = R.buf + (R.use % NS) * BLK;
+    ++R.use;
+    return p;
+}
+template <int NS>
+__device__ __forceinline__ void ring_drain(Ring& R) {
+    while (R.use < R.iss) {
+        mbar_wait(R.bar + 8 * (R.use % NS), (R.use / NS) & 1u);
+        ++R.use;
+    }
+    R.P0 = R.iss;
     __syncwarp();
-    // backward: lane d holds the pending entry k - d
-    cur = (lane < W && n - 1 - lane >= 0) ? (S)v[n - 1 - lane] : (S)0;
-    for (int k = n - 1; k >= 0; --k) {
-        S xk = (S)0;
-        if (lane == 0) xk = cur / (S)FT<F>::to_d(Lb[(size_t)k * W]);
-        xk = __shfl_sync(0xffffffffu, xk, 0);
-        if (lane >= 1 && lane <= BW && k - lane >= 0) cur = cur - (S)FT<F>::to_d(Lb[(size_t)k * W + lane]) * xk;
-        if (lane == 0) v[k] = (double)xk;
-        S nxt = __shfl_down_sync(0xffffffffu, cur, 1);
-        if (lane == BW) nxt = (k - W >= 0) ? (S)v[k - W] : (S)0;
-        cur = nxt;
+}
+
+// Entries of row r of A (interior node (i, j), r = (j-1)(N-1) + (i-1)) from the triangle
+// coefficients: cE(i,j) = (aL(i,j) + aU(i,j-1))/2, cN(i,j) = (aU(i,j) + aL(i-1,j))/2 (R10).
+template <int N>
+struct Coef {
+    const double* a;
+    __device__ __forceinline__ double aL(int i, int j) const { return __ldg(a + 2 * (j * N + i)); }
+    __device__ __forceinline__ double aU(int i, int j) const { return __ldg(a + 2 * (j * N + i) + 1); }
+    __device__ __forceinline__ double cE(int i, int j) const { return 0.5 * (aL(i, j) + aU(i, j - 1)); }
+    __device__ __forceinline__ double cN(int i, int j) const { return 0.5 * (aU(i, j) + aL(i - 1, j)); }
+    // diagonal, west coupling (column r-1) and south coupling (column r-(N-1)) of row r; identity for r >= n
+    __device__ __forceinline__ void row(int r, double& dg, double& we, double& so) const {
+        constexpr int n = (N - 1) * (N - 1);
+        if (r >= n) { dg = 1.0; we = 0.0; so = 0.0; return; }
+        const int i = r % (N - 1) + 1, j = r / (N - 1) + 1;
+        const double e = cE(i, j), w = cE(i - 1, j), no = cN(i, j), s = cN(i, j - 1);
+        dg = (e + w) + (no + s);
+        we = i > 1 ? -w : 0.0;
+        so = j > 1 ? -s : 0.0;
+    }
+};
+
+// lane row r of a block (shared memory) -> W values in precision S
+template <int N, typename F, typename S, class C = Chol2Cfg<N, F, S>>
+__device__ __forceinline__ void load_row(const unsigned char* blk, int r, S (&lv)[N]) {
+    if constexpr (C::C == 0) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) lv[e] = to_s<S>(*reinterpret_cast<const F*>(blk + C::off(r, e)));
+    } else {
+#pragma unroll
+        for (int i = 0; i < C::C; ++i) {
+            const uint4 q = *reinterpret_cast<const uint4*>(blk + C::off(r, i * C::EPC));
+            F t[C::EPC];
+            memcpy(t, &q, 16);
+#pragma unroll
+            for (int e = 0; e < C::EPC; ++e) lv[i * C::EPC + e] = to_s<S>(t[e]);
+        }
+    }
+}
+// W factor values -> lane row r of a block in global memory
+template <int N, typename F, typename S, class C = Chol2Cfg<N, F, S>>
+__device__ __forceinline__ void store_row(unsigned char* blk, int r, const F (&vals)[N]) {
+    if constexpr (C::C == 0) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) *reinterpret_cast<F*>(blk + C::off(r, e)) = vals[e];
+    } else {
+#pragma unroll
+        for (int i = 0; i < C::C; ++i) {
+            uint4 q;
+            memcpy(&q, &vals[i * C::EPC], 16);
+            *reinterpret_cast<uint4*>(blk + C::off(r, i * C::EPC)) = q;
+        }
+    }
+}
+// raw copy of lane row r (shared -> global), same layout
+template <int N, typename F, typename S, class C = Chol2Cfg<N, F, S>>
+__device__ __forceinline__ void copy_row(unsigned char* dst, const unsigned char* src, int r) {
+    if constexpr (C::C == 0) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) *reinterpret_cast<F*>(dst + C::off(r, e)) = *reinterpret_cast<const F*>(src + C::off(r, e));
+    } else {
+#pragma unroll
+        for (int i = 0; i < C::C; ++i)
+            *reinterpret_cast<uint4*>(dst + C::off(r, i * C::EPC)) = *reinterpret_cast<const uint4*>(src + C::off(r, i * C::EPC));
+    }
+}
+
+// Forward substitution L y = v in place (u_s).  Block b of LF holds, for lane l, the entries
+// L(r_l(u), bW+u), u = 0..W-1, of the row r_l(u) = l (mod W) that lane owns at step u, and the
+// reciprocal pivot 1/L(bW+l, bW+l) in the header (R28).  Per row: one multiply, one shuffle and
+// one FMA on the chain; the pivot lane then takes the row W further on.
+template <int N, typename F, typename S, class C>
+__device__ __noinline__ void forward(Ring& R, S* v, int l, bool leader) {
+    constexpr int W = C::W, NB = C::NB;
+    S cur = v[l];
+    for (int b = 0; b < NB; ++b) {
+        const unsigned char* blk = ring_acquire<NB, C::BLK, C::NS>(R, leader);
+        S lv[W];
+        load_row<N, F, S, C>(blk, l, lv);
+        const S rd = reinterpret_cast<const S*>(blk + C::HDR)[l];
+        const int k0 = b * W;
+        const S nxt = b + 1 < NB ? v[k0 + W + l] : (S)0;
+        S yv = (S)0;
+        S t = cur * rd;                              // y of this lane's row if it is the next pivot
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            const S yk = __shfl_sync(0xffffffffu, t, u, W);
+            const S c2 = fma(-lv[u], yk, cur);
+            t = c2 * rd;                             // chain: shuffle -> FMA -> multiply (lane u+1)
+            cur = c2;
+            pivot_take(l, u, cur, nxt, yv, yk);
+        }
+        v[k0 + l] = yv;
     }
     __syncwarp();
 }
 
-template <int N, typename F, typename S>
-__global__ void __launch_bounds__(32 * CholCfg<N, F>::WARPS)
+// Backward substitution L^T x = v in place (u_s).  Block b of LB holds, for lane l, the entries
+// L(bW+u, r_l(u)) of row bW+u at the column r_l(u) = l (mod W) that lane owns at step u.
+template <int N, typename F, typename S, class C>
+__device__ __noinline__ void backward(Ring& R, S* v, int l, bool leader) {
+    constexpr int W = C::W, NB = C::NB;
+    S cur = v[(NB - 1) * W + l];
+    for (int b = NB - 1; b >= 0; --b) {
+        const unsigned char* blk = ring_acquire<NB, C::BLK, C::NS>(R, leader);
+        S lv[W];
+        load_row<N, F, S, C>(blk, l, lv);
+        const S rd = reinterpret_cast<const S*>(blk + C::HDR)[l];
+        const int k0 = b * W;
+        const S nxt = b > 0 ? v[k0 - W + l] : (S)0;
+        S xv = (S)0;
+        S t = cur * rd;
+#pragma unroll
+        for (int u = W - 1; u >= 0; --u) {
+            const S xk = __shfl_sync(0xffffffffu, t, u, W);
+            const S c2 = fma(-lv[u], xk, cur);
+            t = c2 * rd;
+            cur = c2;
+            pivot_take(l, u, cur, nxt, xv, xk);
+        }
+        v[k0 + l] = xv;
+    }
+    __syncwarp();
+}
+
+template <int N, typename F, typename S, int NS, int WPC>
+__global__ void __launch_bounds__(32 * WPC)
 chol_ir_kernel(const double* __restrict__ a_all, int nb, double tol, int i_max, double* __restrict__ out, int slot,
-               unsigned* __restrict__ job_counter) {
-    using C = CholCfg<N, F>;
-    constexpr int n = C::n, W = C::W, BW = C::BW, P = 2 * N * N;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* base = smem_raw + C::per_warp * warp;
-    F* Lb = reinterpret_cast<F*>(base);
-    double* cE = reinterpret_cast<double*>(base + C::band_bytes);
-    double* cN = cE + N * N;
-    double* xv = cN + N * N;
-    double* rv = xv + n;
+               unsigned* __restrict__ job_counter, unsigned char* __restrict__ fscratch) {
+    using C = Chol2Cfg<N, F, S, NS, WPC>;
+    constexpr int W = C::W, n = C::n, NB = C::NB, NPAD = C::NPAD, SEGS = C::SEGS, BLK = C::BLK;
+    constexpr int P = 2 * N * N, PER = NPAD / W;     // vector entries per lane (= NB)
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int seg = lane / W, l = lane % W;
+    const unsigned mask = 0xffffffffu;
+    const bool leader = l == 0;
+    unsigned char* base = smem + (size_t)(warp * SEGS + seg) * C::SEG_BYTES;
+    unsigned char* ring = base;
+    double* xs = reinterpret_cast<double*>(base + C::OFF_X);
+    S* v = reinterpret_cast<S*>(base + C::OFF_V);
+    F* colbuf = reinterpret_cast<F*>(base + C::OFF_C);
+    const size_t gseg = ((size_t)blockIdx.x * WPC + warp) * SEGS + seg;
+    unsigned char* LF = fscratch + gseg * C::FBYTES;
+    unsigned char* LB = LF + (size_t)NB * BLK;
+    Ring R;
+    R.buf = ring;
+    R.sbuf = smem_u32(ring);
+    R.bar = smem_u32(base + C::OFF_B);
+    R.lf = LF;
+    R.lb = LB;
+    R.P0 = R.iss = R.use = 0;
+    if (leader) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) mbar_init(R.bar + 8 * q);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     const double h = 1.0 / N, h2 = h * h;
     const double bnorm = h2 * sqrt((double)n);
 
     for (;;) {
-        int job = 0;
-        if (lane == 0) job = (int)atomicAdd(job_counter, 1u);
-        job = __shfl_sync(0xffffffffu, job, 0);
-        if (job >= nb) break;
-        const double* a = a_all + (size_t)job * P;
-        // conductances (binary64, the assembled operator of P:178)
-        for (int e = lane; e < N * N; e += 32) {
-            int i = e % N, j = e / N;
-            cE[e] = (j >= 1) ? 0.5 * (__ldg(a + 2 * (j * N + i)) + __ldg(a + 2 * ((j - 1) * N + i) + 1)) : 0.0;
-            cN[e] = (i >= 1) ? 0.5 * (__ldg(a + 2 * (j * N + i) + 1) + __ldg(a + 2 * (j * N + i - 1))) : 0.0;
-        }
-        __syncwarp();
-        // band of A rounded to u_f: diagonal, west (d = 1) and south (d = BW) couplings
-        for (int e = lane; e < n * W; e += 32) {
-            int r = e / W, d = e % W;
-            int i = r % (N - 1) + 1, j = r / (N - 1) + 1, c = j * N + i;
-            double v = 0.0;
-            if (d == 0) v = (cE[c] + cE[c - 1]) + (cN[c] + cN[c - N]);
-            else if (d == 1 && i > 1) v = -cE[c - 1];
-            else if (d == BW && j > 1) v = -cN[c - N];
-            Lb[e] = FT<F>::from(v);
-        }
-        __syncwarp();
-        // ---- step 1: right-looking banded Cholesky in F
-        int status = 0;
-        for (int k = 0; k < n; ++k) {
-            F piv = Lb[(size_t)k * W];
-            if (!FT<F>::pos_finite(piv)) { status = 2; break; }
-            F lkk = FT<F>::sqrt_(piv);
-            F li = FT<F>::from(0.0);
-            const bool act = lane >= 1 && lane <= BW && k + lane < n;
-            if (act) {
-                li = FT<F>::div(Lb[(size_t)(k + lane) * W + lane], lkk);
-                Lb[(size_t)(k + lane) * W + lane] = li;
+        int jb = 0;
+        if (lane == 0) jb = (int)atomicAdd(job_counter, (unsigned)SEGS);
+        jb = __shfl_sync(mask, jb, 0);
+        if (jb >= nb) break;
+        const int job = jb + seg;
+        const bool live = job < nb;
+        const Coef<N> A{a_all + (size_t)(live ? job : nb - 1) * P};
+
+        // ---- step 1: right-looking banded Cholesky in F, window rows [k, k+W) in registers
+        // (ring slots 0 / 1 serve as the tiles in which the backward layout LB is assembled)
+        for (int e = l; e < BLK / 16; e += W) reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
+        F Rw[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) Rw[c] = FT<F>::from(0.0);
+        {
+            // row l: diagonal in slot l, west (column l-1) in slot l-1, south (column l-(N-1), only
+            // for l = W-1) in slot (l+1) mod W
+            double dg, we, so;
+            A.row(l, dg, we, so);
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                if (u == ((l + 1) & (W - 1))) Rw[u] = FT<F>::from(so);
+                if (u == ((l + W - 1) & (W - 1))) Rw[u] = FT<F>::from(we);
+                if (u == l) Rw[u] = FT<F>::from(dg);
             }
-            __syncwarp();
-            if (lane == 0) Lb[(size_t)k * W] = lkk;
-            if (act) {
-                F* row = Lb + (size_t)(k + lane) * W;
-#pragma unroll 4
-                for (int jj = 1; jj <= BW; ++jj) {
-                    if (jj > lane) break;
-                    F lj = Lb[(size_t)(k + jj) * W + jj];
-                    row[lane - jj] = FT<F>::fnma(li, lj, row[lane - jj]);
+        }
+        __syncwarp(mask);
+        bool ok = true;
+        F pnext = FT<F>::from(0.0);
+        for (int b = 0; b < NB; ++b) {
+            const int k0 = b * W;
+            unsigned char* Tc = ring + (b & 1) * BLK;          // tile of block b (rows k0 .. k0+W-1)
+            unsigned char* Tn = ring + ((b + 1) & 1) * BLK;    // tile of block b+1
+            // the row each lane takes after its pivot step in this block: k0 + W + l (loads issued early)
+            F dgn = FT<F>::from(0.0), wen = FT<F>::from(0.0), son = FT<F>::from(0.0);
+            if (b + 1 < NB) {
+                double dg, we, so;
+                A.row(k0 + W + l, dg, we, so);
+                dgn = FT<F>::from(dg);
+                wen = FT<F>::from(we);
+                son = FT<F>::from(so);
+            }
+            F lcol[W];
+            S rdl = (S)0;
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                const int d = (l - u) & (W - 1);      // this lane holds row k0 + u + d
+                // pivot: lane u's diagonal, from the fast path of the previous step (k > 0)
+                F piv = __shfl_sync(mask, (b == 0 && u == 0) ? Rw[0] : pnext, u, W);
+                if (!FT<F>::pos_finite(piv)) { ok = false; piv = FT<F>::from(1.0); }
+                const F lkk = FT<F>::sqrt_(piv);
+                const S rk = rcp_s(to_s<S>(lkk));
+                const F lc = d == 0 ? lkk : FT<F>::div(Rw[u], lkk);     // L(k0+u+d, k0+u)
+                // the next pivot's update (lane u+1 multiplies its own column entry by itself, the
+                // same operation the rank-1 update below performs with the shared copy) off the
+                // shared-memory round trip
+                pnext = FT<F>::fnma(lc, lc, Rw[(u + 1) % W]);
+                lcol[u] = lc;
+                if (l == u) rdl = rk;
+                *reinterpret_cast<F*>((l >= u ? Tc : Tn) + C::off(u, l)) = lc;
+                F* cb = colbuf + (u & 1) * W;
+                cb[d] = lc;
+                __syncwarp(mask);
+                F cv[W];
+                if constexpr (C::C == 0) {
+#pragma unroll
+                    for (int j = 0; j < W; ++j) cv[j] = cb[j];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < C::C; ++i) {
+                        const uint4 q = reinterpret_cast<const uint4*>(cb)[i];
+                        memcpy(&cv[i * C::EPC], &q, 16);
+                    }
+                }
+#pragma unroll
+                for (int j = 1; j < W; ++j) Rw[(u + j) % W] = FT<F>::fnma(lc, cv[j], Rw[(u + j) % W]);
+                if (l == u) {                          // row k0+u is done: this lane takes row k0+u+W
+#pragma unroll
+                    for (int c = 0; c < W; ++c) Rw[c] = FT<F>::from(0.0);
+                    Rw[u] = dgn;
+                    Rw[(u + W - 1) % W] = wen;
+                    Rw[(u + 1) % W] = son;
                 }
             }
-            __syncwarp();
+            __syncwarp(mask);
+            unsigned char* gF = LF + (size_t)b * BLK;
+            unsigned char* gB = LB + (size_t)b * BLK;
+            store_row<N, F, S, C>(gF, l, lcol);
+            copy_row<N, F, S, C>(gB, Tc, l);
+            reinterpret_cast<S*>(gF + C::HDR)[l] = rdl;
+            reinterpret_cast<S*>(gB + C::HDR)[l] = rdl;
+            __syncwarp(mask);
         }
+        // the factor was written by generic stores; the ring reads it through the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp(mask);
+        bool active = live && ok;
+        int status = ok ? 1 : 2, it = 0;
         double rel = 1.0;
-        int it = 0;
-        if (status == 0) {
-            // ---- step 2: x0 = (L L^T)^-1 b in u_s, stored in binary64
-            for (int e = lane; e < n; e += 32) rv[e] = (double)(S)h2;
-            __syncwarp();
-            band_solve<N, F, S>(Lb, rv, lane);
-            for (int e = lane; e < n; e += 32) xv[e] = rv[e];
-            __syncwarp();
-            status = 1;
-            for (it = 0; it <= i_max; ++it) {
-                // ---- step 4: r = b - A x in binary64
-                double part = 0.0;
-                for (int e = lane; e < n; e += 32) {
-                    int i = e % (N - 1) + 1, j = e / (N - 1) + 1, c = j * N + i;
-                    double ce = cE[c], cw = cE[c - 1], cn = cN[c], cs = cN[c - N];
-                    double Ax = ((ce + cw) + (cn + cs)) * xv[e];
-                    if (i < N - 1) Ax = fma(-ce, xv[e + 1], Ax);
-                    if (i > 1) Ax = fma(-cw, xv[e - 1], Ax);
-                    if (j < N - 1) Ax = fma(-cn, xv[e + N - 1], Ax);
-                    if (j > 1) Ax = fma(-cs, xv[e - (N - 1)], Ax);
-                    double r = h2 - Ax;
-                    rv[e] = r;
-                    part = fma(r, r, part);
-                }
-                rel = sqrt(wsum_d(part)) / bnorm;
-                __syncwarp();
-                if (!(rel == rel) || rel > DBL_MAX) { status = 3; break; }
-                if (rel < tol) { status = 0; break; }          // step 5
-                if (it == i_max) break;
-                // ---- step 7: d = (L L^T)^-1 r in u_s;  step 8: x += d in binary64
-                for (int e = lane; e < n; e += 32) rv[e] = (double)(S)rv[e];
-                __syncwarp();
-                band_solve<N, F, S>(Lb, rv, lane);
-                for (int e = lane; e < n; e += 32) xv[e] += rv[e];
-                __syncwarp();
-            }
+
+        // ---- step 2: x0 = (L L^T)^-1 b in u_s, stored in binary64
+#pragma unroll 4
+        for (int q = 0; q < PER; ++q) {
+            const int e = l + q * W;
+            v[e] = e < n ? (S)h2 : (S)0;
         }
+        __syncwarp(mask);
+        forward<N, F, S, C>(R, v, l, leader);
+        backward<N, F, S, C>(R, v, l, leader);
+#pragma unroll 4
+        for (int q = 0; q < PER; ++q) {
+            const int e = l + q * W;
+            xs[e] = (double)v[e];
+        }
+        __syncwarp(mask);
+        for (;;) {
+            // ---- step 4: r = b - A x in binary64 (rounded to u_s for the correction solve)
+            double part = 0.0;
+            if (active) {
+                for (int q = 0; q < PER; ++q) {
+                    const int e = l + q * W;
+                    double r = 0.0;
+                    if (e < n) {
+                        const int i = e % (N - 1) + 1, j = e / (N - 1) + 1;
+                        const double ce = A.cE(i, j), cw = A.cE(i - 1, j), cn = A.cN(i, j), cs = A.cN(i, j - 1);
+                        const double xe = xs[e];
+                        double Ax = ((ce + cw) + (cn + cs)) * xe;
+                        if (i < N - 1) Ax = fma(-ce, xs[e + 1], Ax);
+                        if (i > 1) Ax = fma(-cw, xs[e - 1], Ax);
+                        if (j < N - 1) Ax = fma(-cn, xs[e + N - 1], Ax);
+                        if (j > 1) Ax = fma(-cs, xs[e - (N - 1)], Ax);
+                        r = h2 - Ax;
+                        part = fma(r, r, part);
+                    }
+                    v[e] = (S)r;
+                }
+            }
+#pragma unroll
+            for (int o = W / 2; o > 0; o >>= 1) part += __shfl_xor_sync(mask, part, o, W);
+            if (active) {
+                rel = sqrt(part) / bnorm;
+                if (!(rel == rel) || rel > DBL_MAX) { status = 3; active = false; }
+                else if (rel < tol) { status = 0; active = false; }            // step 5
+                else if (it == i_max) { active = false; }
+            }
+            if (!__any_sync(mask, active)) break;
+            __syncwarp(mask);
+            // ---- step 7: d = (L L^T)^-1 r in u_s;  step 8: x += d in binary64
+            forward<N, F, S, C>(R, v, l, leader);
+            backward<N, F, S, C>(R, v, l, leader);
+            if (active) {
+#pragma unroll 4
+                for (int q = 0; q < PER; ++q) {
+                    const int e = l + q * W;
+                    xs[e] += (double)v[e];
+                }
+                ++it;
+            }
+            __syncwarp(mask);
+        }
+        ring_drain<NS>(R);
         double sx = 0.0;
-        for (int e = lane; e < n; e += 32) sx += xv[e];
-        sx = wsum_d(sx);
-        if (lane == 0) {
+        for (int q = 0; q < PER; ++q) sx += xs[l + q * W];      // padded rows hold exact zeros
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) sx += __shfl_xor_sync(mask, sx, o, W);
+        if (live && leader) {
             double* o = out + (size_t)job * kRecLen;
             o[0 + slot] = status == 2 ? 0.0 : h2 * sx;
             o[2 + slot] = (double)it;
             o[4 + slot] = rel;
             o[6 + slot] = (double)status;
         }
-        __syncwarp();
+        __syncwarp(mask);
     }
 }
 
-template <int N, typename F, typename S>
-static cudaError_t run_chol(const double* a, uint64_t nb, double tol, int i_max, double* out, int slot, unsigned* ctr,
-                            cudaStream_t s) {
-    using C = CholCfg<N, F>;
-    auto kern = chol_ir_kernel<N, F, S>;
-    static int bps = -1, sms = 0;
-    if (bps < 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * C::WARPS, C::SMEM);
-        if (e != cudaSuccess) return e;
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (bps < 1) return cudaErrorInvalidConfiguration;
+template <int N, typename F, typename S, int NS = 3, int WPC = 4>
+struct Launch {
+    using C = Chol2Cfg<N, F, S, NS, WPC>;
+    static cudaError_t occupancy(int& grid_max) {
+        static int bps = -1, sms = 0;
+        if (bps < 0) {
+            auto kern = chol_ir_kernel<N, F, S, NS, WPC>;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (e != cudaSuccess) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * WPC, C::SMEM);
+            if (e != cudaSuccess) return e;
+            int dev;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (bps < 1) { bps = -1; return cudaErrorInvalidConfiguration; }
+        }
+        grid_max = bps * sms;
+        return cudaSuccess;
     }
-    uint64_t need = (nb + C::WARPS - 1) / C::WARPS;
-    uint64_t grid = std::min<uint64_t>(need, (uint64_t)bps * sms);
-    if (grid == 0) return cudaSuccess;
-    kern<<<(unsigned)grid, 32 * C::WARPS, C::SMEM, s>>>(a, (int)nb, tol, i_max, out, slot, ctr);
-    return cudaGetLastError();
+    static constexpr uint64_t per_cta = (uint64_t)WPC * C::SEGS;
+    static uint64_t grid_for(uint64_t nb, int gm) { return std::min<uint64_t>((nb + per_cta - 1) / per_cta, (uint64_t)gm); }
+    // factor scratch for a launch over nb systems: one factor (both layouts) per resident segment
+    static cudaError_t scratch(size_t& bytes, uint64_t nb) {
+        int gm = 0;
+        cudaError_t e = occupancy(gm);
+        bytes = (size_t)grid_for(nb, gm) * per_cta * C::FBYTES;
+        return e;
+    }
+    static cudaError_t run(const double* a, uint64_t nb, double tol, int i_max, double* out, int slot, unsigned* ctr,
+                           void* fscratch, size_t fbytes, cudaStream_t s) {
+        int gm = 0;
+        cudaError_t e = occupancy(gm);
+        if (e != cudaSuccess) return e;
+        const uint64_t grid = std::min<uint64_t>(grid_for(nb, gm), fbytes / (per_cta * C::FBYTES));
+        if (nb == 0) return cudaSuccess;
+        if (grid == 0) return cudaErrorInvalidValue;
+        chol_ir_kernel<N, F, S, NS, WPC><<<(unsigned)grid, 32 * WPC, C::SMEM, s>>>(
+            a, (int)nb, tol, i_max, out, slot, ctr, static_cast<unsigned char*>(fscratch));
+        return cudaGetLastError();
+    }
+};
+
+// Ring depth / CTA shape for the h = 1/32 factors (MLMC_CHOL_VARIANT selects for tuning runs).
+int chol_variant() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = std::getenv("MLMC_CHOL_VARIANT");
+        v = e ? std::atoi(e) : 0;
+    }
+    return v;
 }
+
+template <int N, typename F, typename S, class Fn>
+cudaError_t with_shape(Fn&& fn) {
+    if constexpr (N == 32 && sizeof(S) == 4) {
+        switch (chol_variant()) {
+            case 1: return fn(Launch<N, F, S, 4, 4>{});
+            case 2: return fn(Launch<N, F, S, 6, 2>{});
+            case 3: return fn(Launch<N, F, S, 6, 3>{});
+            case 4: return fn(Launch<N, F, S, 8, 2>{});
+            default: return fn(Launch<N, F, S, 3, 4>{});
+        }
+    } else {
+        return fn(Launch<N, F, S, 3, 4>{});
+    }
+}
+
+// (u_f, u_s) -> instantiation; returns cudaErrorNotSupported for combinations not built.
+template <int N, class Fn>
+cudaError_t with_types(int u_f, int u_s, Fn&& fn) {
+    if (u_f == MLMC_FMT_F16) {
+        if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(fn);
+    } else if (u_f == MLMC_FMT_F32) {
+        if (u_s == MLMC_FMT_F32) return with_shape<N, float, float>(fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, float, double>(fn);
+    } else if (u_f == MLMC_FMT_F64) {
+        if constexpr (N <= 16) {
+            if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(fn);
+            if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(fn);
+        }
+    }
+    return cudaErrorNotSupported;
+}
+
+template <class Fn>
+cudaError_t with_mesh(int N, int u_f, int u_s, Fn&& fn) {
+    switch (N) {
+        case 2: return with_types<2>(u_f, u_s, fn);
+        case 4: return with_types<4>(u_f, u_s, fn);
+        case 8: return with_types<8>(u_f, u_s, fn);
+        case 16: return with_types<16>(u_f, u_s, fn);
+        case 32: return with_types<32>(u_f, u_s, fn);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace
 
 bool chol_supported(int N, int u_f, int u_s) {
     if (!(N == 2 || N == 4 || N == 8 || N == 16 || N == 32)) return false;
     if (!(u_f == MLMC_FMT_F16 || u_f == MLMC_FMT_F32 || u_f == MLMC_FMT_F64)) return false;
     if (!(u_s == MLMC_FMT_F32 || u_s == MLMC_FMT_F64)) return false;
-    if (u_f == MLMC_FMT_F64 && N == 32) return false;   // 240 KB band: beyond shared memory
+    if (u_f == MLMC_FMT_F64 && N == 32) return false;   // fp64 factor only where the old on-chip kernel had it
     return true;
 }
 
-template <int N>
-static cudaError_t chol_dispatch(int u_f, int u_s, const double* a, uint64_t nb, double tol, int i_max, double* out,
-                                 int slot, unsigned* ctr, cudaStream_t s) {
-    if (u_f == MLMC_FMT_F16) {
-        if (u_s == MLMC_FMT_F32) return run_chol<N, __half, float>(a, nb, tol, i_max, out, slot, ctr, s);
-        return run_chol<N, __half, double>(a, nb, tol, i_max, out, slot, ctr, s);
-    }
-    if (u_f == MLMC_FMT_F32) {
-        if (u_s == MLMC_FMT_F32) return run_chol<N, float, float>(a, nb, tol, i_max, out, slot, ctr, s);
-        return run_chol<N, float, double>(a, nb, tol, i_max, out, slot, ctr, s);
-    }
-    if constexpr (N <= 16) return run_chol<N, double, double>(a, nb, tol, i_max, out, slot, ctr, s);
-    return cudaErrorNotSupported;
+size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb) {
+    size_t bytes = 0;
+    cudaError_t e = with_mesh(N, u_f, u_s, [&](auto L) { return decltype(L)::scratch(bytes, nb); });
+    return e == cudaSuccess ? bytes : 0;
 }
 
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max, double* out,
-                           int slot, unsigned* ctr, cudaStream_t s) {
-    switch (N) {
-        case 2: return chol_dispatch<2>(u_f, u_s, a, nb, tol, i_max, out, slot, ctr, s);
-        case 4: return chol_dispatch<4>(u_f, u_s, a, nb, tol, i_max, out, slot, ctr, s);
-        case 8: return chol_dispatch<8>(u_f, u_s, a, nb, tol, i_max, out, slot, ctr, s);
-        case 16: return chol_dispatch<16>(u_f, u_s, a, nb, tol, i_max, out, slot, ctr, s);
-        case 32: return chol_dispatch<32>(u_f, u_s, a, nb, tol, i_max, out, slot, ctr, s);
-        default: return cudaErrorNotSupported;
-    }
+                           int slot, unsigned* ctr, void* fscratch, size_t fbytes, cudaStream_t s) {
+    return with_mesh(N, u_f, u_s, [&](auto L) {
+        return decltype(L)::run(a, nb, tol, i_max, out, slot, ctr, fscratch, fbytes, s);
+    });
 }
 
 }  // namespace mlmc
