@@ -1,4 +1,4 @@
-// k_chol.cu -- K4 v2: batched banded Cholesky in a low precision u_f + iterative refinement.
+// k_chol.cu -- K4: batched banded Cholesky in a low precision u_f + iterative refinement.
 //
 // Algorithm 1 for the P1 system A x = b of one sample:
 //   1. factorise A = L L^T in precision u_f
@@ -9,38 +9,38 @@
 //   7.   solve A d_i = r_i with the retained factor in u_s
 //   8.   x_{i+1} = x_i + d_i in u (binary64)
 // The matrix is the 5-point P1 operator (R10).  In natural ordering its band
-// width is bw = N - 1 and the factor fills the band, so L has W = N entries per
-// column: L(k+d, k), d = 0..W-1.
+// width is bw = N - 1 and the factor fills the band: W = N entries per row and
+// per column of L.  The system is padded to n_pad = N(N-1) = (N-1) W rows with
+// identity rows (zero right-hand side) so that every loop runs over whole
+// blocks of W rows.
 //
-// B200 mapping (K4).  One W-lane segment of a warp per
-// sample (W = N <= 32; 32/W samples share a warp and run in lockstep).
-//  * The factor never has to fit on chip: it is written once to a per-segment
-//    global scratch in "column-band" blocks, Lc[k][d] = L(k+d, k), W rows x W
-//    entries = one contiguous block per W columns, and streamed back into a
-//    3-slot shared-memory ring by TMA bulk copies (cp.async.bulk, mbarrier
-//    completion) for every substitution.  The factor format u_f sets the bytes
-//    each substitution moves -- the paper's memory-reference argument
-//    taken literally: fp16 halves them against fp32.
-//  * Factorisation (right-looking, band window in registers): lane l owns the
-//    rows r = l (mod W) currently in the W-row window [k, k+W); row r keeps
-//    A(r, c) for its W band columns in register c mod W, so every step k
-//    addresses the registers with the compile-time index k mod W (the k loop is
-//    unrolled by W).  Step k: pivot from lane k mod W by one shuffle, every lane
-//    divides its column entry by sqrt(pivot) in u_f, the column goes to the
-//    global factor (one coalesced W-entry row) and through shared memory to the
-//    rank-1 update of the window (W-1 FMAs per lane in u_f, no predication:
-//    entries right of a row's diagonal are dead registers).  The pivot lane
-//    then loads row k+W (3 nonzeros of A) into its registers.
-//  * Substitutions (column-oriented, rotating ownership): lane l holds the
-//    pending right-hand-side entry of the window row r = l (mod W); each row
-//    costs one shuffle, one multiply by the (off-chain) reciprocal pivot and one
-//    FMA per lane in u_s (R28); the finished entry is written in place to a
-//    shared-memory vector.  Forward reads Lc[k][*] (a block row), backward
-//    reads row k of L = Lc[k-d][d] (a block diagonal, bank-conflict free).
-//  * Residual and update in binary64 from the shared x and the triangle
-//    coefficients (conductances rebuilt on the fly, L1/L2).
-// The system is padded to n_pad = N(N-1) = (N-1) W rows with identity rows
-// (zero right-hand side), which keeps every loop a whole number of blocks.
+// B200 mapping (K4): two kernels per batch pass.
+//  K4a chol_factor_kernel -- one W-lane warp segment per sample (32/W samples
+//    per warp).  Right-looking factorisation with the W-row band window in
+//    registers: lane l owns the window row r = l (mod W) and keeps A(r, c) in
+//    register c mod W, so step k addresses registers with the compile-time
+//    index k mod W (k unrolled by W).  Step k: pivot by one shuffle (its update
+//    comes off the shared-memory round trip: lane k+1 squares its own entry),
+//    sqrt and reciprocal in u_f, column scaled by the reciprocal (R29), column
+//    through shared memory into the rank-1 update (W-1 FMAs per lane in u_f; the
+//    pivot lane then reloads its window row with row k+W).  The factor leaves
+//    in two lane-major layouts, one per substitution direction, W entries per
+//    lane and block plus the reciprocal pivots in u_s (R28):
+//      LF[b][l][u] = L(r_l(u), bW+u)   r_l(u) = the row = l (mod W) lane l
+//                                     holds at forward step u
+//      LB[b][l][u] = L(bW+u, c_l(u))   c_l(u) = the column = l (mod W) lane l
+//                                     holds at backward step u
+//    LB is assembled in shared-memory tiles (scattered per step, copied out per
+//    block).  The factor format u_f sets the bytes: the paper's memory-
+//    reference argument is literal here -- fp16 halves the factor.
+//  K4b chol_refine_kernel -- persistent, one segment per sample (job counter).
+//    Every substitution streams the sample's factor blocks back from HBM into
+//    an NS-slot shared-memory ring with TMA bulk copies (cp.async.bulk,
+//    mbarrier completion).  Column-oriented substitutions with rotating
+//    ownership: lane l holds the pending right-hand-side entry of its window
+//    row; per row one shuffle, one FMA, one multiply on the chain, all in u_s.
+//    Residual (binary64, conductances rebuilt from the triangle coefficients)
+//    and x (binary64, a per-segment global scratch, L1/L2 resident).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -58,33 +58,49 @@ template <typename T> struct FT;
 template <> struct FT<double> {
     static __device__ __forceinline__ double from(double v) { return v; }
     static __device__ __forceinline__ double fnma(double a, double b, double c) { return fma(-a, b, c); }
-    static __device__ __forceinline__ double div(double a, double b) { return a / b; }
     static __device__ __forceinline__ double sqrt_(double a) { return sqrt(a); }
     static __device__ __forceinline__ bool pos_finite(double a) { return a > 0.0 && a <= DBL_MAX; }
     static __device__ __forceinline__ float to_f(double v) { return (float)v; }
     static __device__ __forceinline__ double to_d(double v) { return v; }
+    static __device__ __forceinline__ double rcp(double v) { return __drcp_rn(v); }
+    static __device__ __forceinline__ double scale(double a, double inv) { return __dmul_rn(a, inv); }
 };
 template <> struct FT<float> {
     static __device__ __forceinline__ float from(double v) { return __double2float_rn(v); }
     static __device__ __forceinline__ float fnma(float a, float b, float c) { return __fmaf_rn(-a, b, c); }
-    static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
     static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
     static __device__ __forceinline__ bool pos_finite(float a) { return a > 0.0f && a <= FLT_MAX; }
     static __device__ __forceinline__ float to_f(float v) { return v; }
     static __device__ __forceinline__ double to_d(float v) { return (double)v; }
+    static __device__ __forceinline__ float rcp(float v) { return __frcp_rn(v); }
+    static __device__ __forceinline__ float scale(float a, float inv) { return __fmul_rn(a, inv); }
 };
 template <> struct FT<__half> {
     static __device__ __forceinline__ __half from(double v) { return __double2half(v); }
     static __device__ __forceinline__ __half fnma(__half a, __half b, __half c) { return __hfma(__hneg(a), b, c); }
-    static __device__ __forceinline__ __half div(__half a, __half b) { return __hdiv(a, b); }
-    static __device__ __forceinline__ __half sqrt_(__half a) { return __float2half_rn(sqrtf(__half2float(a))); }
+    static __device__ __forceinline__ __half sqrt_(__half a) { return __float2half_rn(__fsqrt_rn(__half2float(a))); }
     static __device__ __forceinline__ bool pos_finite(__half a) {
         const float f = __half2float(a);
         return f > 0.0f && f <= 65504.0f;
     }
     static __device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
     static __device__ __forceinline__ double to_d(__half v) { return (double)__half2float(v); }
+    static __device__ __forceinline__ float rcp(__half v) { return __frcp_rn(__half2float(v)); }
+    static __device__ __forceinline__ __half scale(__half a, float inv) { return __float2half_rn(__half2float(a) * inv); }
 };
+// type of the reciprocal pivot used to scale a column: max(F, binary32)
+template <typename F> struct Inv { using T = F; };
+template <> struct Inv<__half> { using T = float; };
+
+// correctly rounded reciprocal in the substitution precision (R28)
+__device__ __forceinline__ float rcp_s(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_s(double x) { return __drcp_rn(x); }
+// factor entry -> substitution precision S
+template <typename S, typename F> __device__ __forceinline__ S to_s(F v) {
+    if constexpr (sizeof(S) == 8) return FT<F>::to_d(v);
+    else return FT<F>::to_f(v);
+}
+
 // if (l == u) { cur = nxt; y = yk; } as one setp + two predicated moves, kept in place (volatile) so
 // the compiler does not materialise all W lane predicates of an unrolled block up front
 __device__ __forceinline__ void pivot_take(int l, int u, float& cur, float nxt, float& y, float yk) {
@@ -97,20 +113,11 @@ __device__ __forceinline__ void pivot_take(int l, int u, double& cur, double nxt
                  : "+d"(cur), "+d"(y)
                  : "r"(l), "r"(u), "d"(nxt), "d"(yk));
 }
-// correctly rounded reciprocal in the substitution precision (R28)
-__device__ __forceinline__ float rcp_s(float x) { return __frcp_rn(x); }
-__device__ __forceinline__ double rcp_s(double x) { return __drcp_rn(x); }
-// factor entry -> substitution precision S
-template <typename S, typename F> __device__ __forceinline__ S to_s(F v) {
-    if constexpr (sizeof(S) == 8) return FT<F>::to_d(v);
-    else return FT<F>::to_f(v);
-}
 
-template <int N, typename F, typename S, int NS_ = 3, int WPC_ = 4>
-struct Chol2Cfg {
-    static constexpr int NS = NS_;                     // ring slots (factor blocks in flight + in use)
-    static constexpr int WPC = WPC_;                   // warps per CTA
-    static constexpr int W = N;                        // band entries per column, segment width
+// ---- geometry of one mesh / format pair
+template <int N, typename F, typename S>
+struct Geo {
+    static constexpr int W = N;                        // band entries per row / column, segment width
     static constexpr int n = (N - 1) * (N - 1);
     static constexpr int NB = N - 1;                   // blocks of W rows / columns
     static constexpr int NPAD = NB * W;                // padded system size N(N-1) >= n
@@ -121,14 +128,7 @@ struct Chol2Cfg {
     static constexpr int LPR = C >= 8 ? 1 : (C > 0 ? 8 / C : 1);   // lane rows per 128-byte bank row
     static constexpr int HDR = W * FE;                 // reciprocal pivots (S) after the W lane rows
     static constexpr int BLK = ((HDR + W * (int)sizeof(S) + 127) / 128) * 128;   // block stride (bytes)
-    static constexpr size_t FBYTES = (size_t)2 * NB * BLK;   // forward + backward layouts per segment
-    // shared memory per segment: ring (NS blocks) | x (binary64) | v (u_s) | column buffer | mbarriers
-    static constexpr int OFF_X = NS * BLK;
-    static constexpr int OFF_V = OFF_X + NPAD * 8;
-    static constexpr int OFF_C = OFF_V + ((NPAD * (int)sizeof(S) + 15) / 16) * 16;
-    static constexpr int OFF_B = OFF_C + ((2 * W * (int)sizeof(F) + 15) / 16) * 16;
-    static constexpr int SEG_BYTES = ((OFF_B + NS * 8 + 127) / 128) * 128;
-    static constexpr int SMEM = SEG_BYTES * SEGS * WPC;
+    static constexpr size_t FBYTES = (size_t)2 * NB * BLK;   // LF + LB of one sample
     static_assert(W >= 2 && W <= 32 && (W & (W - 1)) == 0, "segment width must be a power of two <= 32");
     // byte offset of entry e of lane row r inside a block: 16-byte chunks rotated per lane row so that
     // a quarter-warp reading chunk i of 8 consecutive lane rows hits 8 distinct bank groups
@@ -138,64 +138,51 @@ struct Chol2Cfg {
     }
 };
 
-// ---- mbarrier / bulk-copy primitives (PTX)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint32_t bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-// (A slot is refilled only after every lane of the segment has consumed the values it read from it
-// and passed a __syncwarp, so no proxy fence is issued per fill.)
-__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-
-// FIFO ring of factor blocks for one segment (NS slots).  The blocks are consumed in a fixed
-// sequence -- forward pass LF[0..NB-1], backward pass LB[NB-1..0], forward, ... -- so fill
-// position p goes to slot p % NS and completes phase (p / NS) & 1 of that slot's mbarrier; the
-// producer (the segment's lane 0) keeps NS-1 positions ahead of the consumer.  Counters are
-// absolute across jobs (the mbarrier phases are); P0 is the first position of the current job.
-struct Ring {
-    unsigned char* buf;     // slot 0 (generic address)
-    uint32_t sbuf, bar;     // shared addresses of slot 0 and barrier 0
-    const unsigned char* lf;
-    const unsigned char* lb;
-    unsigned P0, iss, use;
-};
-
-template <int NB, int BLK, int NS>
-__device__ __forceinline__ const unsigned char* ring_acquire(Ring& R, bool leader) {
-    __syncwarp();                                   // all lanes are done with position use-1
-    while (R.iss < R.use + NS) {
-        const unsigned i = R.iss - R.P0, pass = i / NB, j = i % NB;
-        const unsigned char* src = (pass & 1) ? R.lb + (size_t)(NB - 1 - j) * BLK : R.lf + (size_t)j * BLK;
-        if (leader) bulk_load(R.sbuf + (R.iss % NS) * BLK, src, BLK, R.bar + 8 * (R.iss % NS));
-        ++R.iss;
+// lane row r of a block (shared memory) -> W values in precision S
+template <class G, typename F, typename S>
+__device__ __forceinline__ void load_row(const unsigned char* blk, int r, S (&lv)[G::W]) {
+    if constexpr (G::C == 0) {
+#pragma unroll
+        for (int e = 0; e < G::W; ++e) lv[e] = to_s<S>(*reinterpret_cast<const F*>(blk + G::off(r, e)));
+    } else {
+#pragma unroll
+        for (int i = 0; i < G::C; ++i) {
+            const uint4 q = *reinterpret_cast<const uint4*>(blk + G::off(r, i * G::EPC));
+            F t[G::EPC];
+            memcpy(t, &q, 16);
+#pragma unroll
+            for (int e = 0; e < G::EPC; ++e) lv[i * G::EPC + e] = to_s<S>(t[e]);
+        }
     }
-    mbar_wait(R.bar + 8 * (R.use % NS), (R.use / NS) & 1u);
-    const unsigned char* p = R.buf + (R.use % NS) * BLK;
-    ++R.use;
-    return p;
 }
-template <int NS>
-__device__ __forceinline__ void ring_drain(Ring& R) {
-    while (R.use < R.iss) {
-        mbar_wait(R.bar + 8 * (R.use % NS), (R.use / NS) & 1u);
-        ++R.use;
+// W factor values -> lane row r of a block (global)
+template <class G, typename F>
+__device__ __forceinline__ void store_row(unsigned char* blk, int r, const F (&vals)[G::W]) {
+    if constexpr (G::C == 0) {
+#pragma unroll
+        for (int e = 0; e < G::W; ++e) *reinterpret_cast<F*>(blk + G::off(r, e)) = vals[e];
+    } else {
+#pragma unroll
+        for (int i = 0; i < G::C; ++i) {
+            uint4 q;
+            memcpy(&q, &vals[i * G::EPC], 16);
+            *reinterpret_cast<uint4*>(blk + G::off(r, i * G::EPC)) = q;
+        }
     }
-    R.P0 = R.iss;
-    __syncwarp();
+}
+// raw copy of lane row r (shared -> global), same layout
+template <class G, typename F>
+__device__ __forceinline__ void copy_row(unsigned char* dst, const unsigned char* src, int r) {
+    if constexpr (G::C == 0) {
+#pragma unroll
+        for (int e = 0; e < G::W; ++e)
+            *reinterpret_cast<F*>(dst + G::off(r, e)) = *reinterpret_cast<const F*>(src + G::off(r, e));
+    } else {
+#pragma unroll
+        for (int i = 0; i < G::C; ++i)
+            *reinterpret_cast<uint4*>(dst + G::off(r, i * G::EPC)) =
+                *reinterpret_cast<const uint4*>(src + G::off(r, i * G::EPC));
+    }
 }
 
 // Entries of row r of A (interior node (i, j), r = (j-1)(N-1) + (i-1)) from the triangle
@@ -219,64 +206,241 @@ struct Coef {
     }
 };
 
-// lane row r of a block (shared memory) -> W values in precision S
-template <int N, typename F, typename S, class C = Chol2Cfg<N, F, S>>
-__device__ __forceinline__ void load_row(const unsigned char* blk, int r, S (&lv)[N]) {
-    if constexpr (C::C == 0) {
+// ======================================================================== K4a: factorisation
+constexpr int kFacWarps = 4;
+
+template <int N, typename F, typename S>
+struct FacCfg {
+    using G = Geo<N, F, S>;
+    // shared memory per segment: two LB tiles | column buffer (2 x W entries)
+    static constexpr int OFF_C = 2 * G::BLK;
+    static constexpr int SEG_BYTES = ((OFF_C + 2 * G::W * (int)sizeof(F) + 127) / 128) * 128;
+    static constexpr int SMEM = SEG_BYTES * G::SEGS * kFacWarps;
+};
+
+// Factorise samples [0, nb): factor of sample j at fac + j * FBYTES; status (0 ok, 2 breakdown) to
+// out[j*8 + 6 + slot].
+template <int N, typename F, typename S>
+__global__ void __launch_bounds__(32 * kFacWarps)
+chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __restrict__ fac,
+                   double* __restrict__ out, int slot) {
+    using G = Geo<N, F, S>;
+    using K = FacCfg<N, F, S>;
+    constexpr int W = G::W, NB = G::NB, SEGS = G::SEGS, BLK = G::BLK;
+    constexpr int P = 2 * N * N;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(16) uint4 zrow[8];          // 128 zero bytes (re-initialised window rows)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int seg = lane / W, l = lane % W;
+    const unsigned mask = 0xffffffffu;
+    if (threadIdx.x < 8) zrow[threadIdx.x] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int job = (blockIdx.x * kFacWarps + warp) * SEGS + seg;
+    const bool live = job < nb;
+    unsigned char* base = smem + (size_t)(warp * SEGS + seg) * K::SEG_BYTES;
+    F* colbuf = reinterpret_cast<F*>(base + K::OFF_C);
+    unsigned char* LF = fac + (size_t)(live ? job : 0) * G::FBYTES;
+    unsigned char* LB = LF + (size_t)NB * BLK;
+    const Coef<N> A{a_all + (size_t)(live ? job : 0) * P};
+
+    // the tile of block 0 keeps zeros where no column exists (c < 0)
+    for (int e = l; e < BLK / 16; e += W) reinterpret_cast<uint4*>(base)[e] = make_uint4(0, 0, 0, 0);
+    F Rw[W];
 #pragma unroll
-        for (int e = 0; e < N; ++e) lv[e] = to_s<S>(*reinterpret_cast<const F*>(blk + C::off(r, e)));
-    } else {
+    for (int c = 0; c < W; ++c) Rw[c] = FT<F>::from(0.0);
+    {
+        // row l: diagonal in slot l, west (column l-1) in slot l-1, south (column l-(N-1), only
+        // for l = W-1) in slot (l+1) mod W
+        double dg, we, so;
+        A.row(l, dg, we, so);
 #pragma unroll
-        for (int i = 0; i < C::C; ++i) {
-            const uint4 q = *reinterpret_cast<const uint4*>(blk + C::off(r, i * C::EPC));
-            F t[C::EPC];
-            memcpy(t, &q, 16);
-#pragma unroll
-            for (int e = 0; e < C::EPC; ++e) lv[i * C::EPC + e] = to_s<S>(t[e]);
+        for (int u = 0; u < W; ++u) {
+            if (u == ((l + 1) & (W - 1))) Rw[u] = FT<F>::from(so);
+            if (u == ((l + W - 1) & (W - 1))) Rw[u] = FT<F>::from(we);
+            if (u == l) Rw[u] = FT<F>::from(dg);
         }
     }
-}
-// W factor values -> lane row r of a block in global memory
-template <int N, typename F, typename S, class C = Chol2Cfg<N, F, S>>
-__device__ __forceinline__ void store_row(unsigned char* blk, int r, const F (&vals)[N]) {
-    if constexpr (C::C == 0) {
-#pragma unroll
-        for (int e = 0; e < N; ++e) *reinterpret_cast<F*>(blk + C::off(r, e)) = vals[e];
-    } else {
-#pragma unroll
-        for (int i = 0; i < C::C; ++i) {
-            uint4 q;
-            memcpy(&q, &vals[i * C::EPC], 16);
-            *reinterpret_cast<uint4*>(blk + C::off(r, i * C::EPC)) = q;
+    __syncwarp(mask);
+    bool ok = true;
+    F pnext = FT<F>::from(0.0);
+    for (int b = 0; b < NB; ++b) {
+        const int k0 = b * W;
+        unsigned char* Tc = base + (b & 1) * BLK;          // LB tile of block b (rows k0 .. k0+W-1)
+        unsigned char* Tn = base + ((b + 1) & 1) * BLK;    // LB tile of block b+1
+        // the row each lane takes after its pivot step in this block: k0 + W + l (loads issued early)
+        F dgn = FT<F>::from(0.0), wen = FT<F>::from(0.0), son = FT<F>::from(0.0);
+        if (b + 1 < NB) {
+            double dg, we, so;
+            A.row(k0 + W + l, dg, we, so);
+            dgn = FT<F>::from(dg);
+            wen = FT<F>::from(we);
+            son = FT<F>::from(so);
         }
-    }
-}
-// raw copy of lane row r (shared -> global), same layout
-template <int N, typename F, typename S, class C = Chol2Cfg<N, F, S>>
-__device__ __forceinline__ void copy_row(unsigned char* dst, const unsigned char* src, int r) {
-    if constexpr (C::C == 0) {
+        F lcol[W];
+        S rdl = (S)0;
 #pragma unroll
-        for (int e = 0; e < N; ++e) *reinterpret_cast<F*>(dst + C::off(r, e)) = *reinterpret_cast<const F*>(src + C::off(r, e));
-    } else {
+        for (int u = 0; u < W; ++u) {
+            const int d = (l - u) & (W - 1);          // this lane holds row k0 + u + d
+            // pivot: lane u's diagonal, from the fast path of the previous step (k > 0)
+            F piv = __shfl_sync(mask, (b == 0 && u == 0) ? Rw[0] : pnext, u, W);
+            if (!FT<F>::pos_finite(piv)) { ok = false; piv = FT<F>::from(1.0); }
+            const F lkk = FT<F>::sqrt_(piv);
+            const typename Inv<F>::T inv = FT<F>::rcp(lkk);
+            S rk;                                      // 1 / L(k,k) in u_s for the substitutions (R28)
+            if constexpr (sizeof(S) == sizeof(inv)) rk = inv;
+            else rk = rcp_s(to_s<S>(lkk));
+            const F lc = d == 0 ? lkk : FT<F>::scale(Rw[u], inv);   // L(k0+u+d, k0+u)
+            // the next pivot's update: lane u+1 squares its own column entry (the same operation the
+            // rank-1 update below performs with the shared copy), off the shared-memory round trip
+            pnext = FT<F>::fnma(lc, lc, Rw[(u + 1) % W]);
+            lcol[u] = lc;
+            if (l == u) rdl = rk;
+            *reinterpret_cast<F*>((l >= u ? Tc : Tn) + G::off(u, l)) = lc;
+            F* cb = colbuf + (u & 1) * W;
+            cb[d] = lc;
+            __syncwarp(mask);
+            F cv[W];
+            if constexpr (G::C == 0) {
 #pragma unroll
-        for (int i = 0; i < C::C; ++i)
-            *reinterpret_cast<uint4*>(dst + C::off(r, i * C::EPC)) = *reinterpret_cast<const uint4*>(src + C::off(r, i * C::EPC));
+                for (int j = 0; j < W; ++j) cv[j] = cb[j];
+            } else {
+#pragma unroll
+                for (int i = 0; i < G::C; ++i) {
+                    const uint4 q = reinterpret_cast<const uint4*>(cb)[i];
+                    memcpy(&cv[i * G::EPC], &q, 16);
+                }
+            }
+#pragma unroll
+            for (int j = 1; j < W; ++j) Rw[(u + j) % W] = FT<F>::fnma(lc, cv[j], Rw[(u + j) % W]);
+            if (l == u) {                              // row k0+u is done: this lane takes row k0+u+W
+                if constexpr (G::C == 0) {
+#pragma unroll
+                    for (int c = 0; c < W; ++c) Rw[c] = FT<F>::from(0.0);
+                } else {                               // zero the window row with vector loads
+#pragma unroll
+                    for (int i = 0; i < G::C; ++i) {
+                        const uint4 q = zrow[i];
+                        memcpy(&Rw[i * G::EPC], &q, 16);
+                    }
+                }
+                Rw[u] = dgn;
+                Rw[(u + W - 1) % W] = wen;
+                Rw[(u + 1) % W] = son;
+            }
+        }
+        __syncwarp(mask);
+        if (live) {
+            unsigned char* gF = LF + (size_t)b * BLK;
+            unsigned char* gB = LB + (size_t)b * BLK;
+            store_row<G, F>(gF, l, lcol);
+            copy_row<G, F>(gB, Tc, l);
+            reinterpret_cast<S*>(gF + G::HDR)[l] = rdl;
+            reinterpret_cast<S*>(gB + G::HDR)[l] = rdl;
+        }
+        __syncwarp(mask);
     }
+    if (live && l == 0) out[(size_t)job * kRecLen + 6 + slot] = ok ? 0.0 : 2.0;
 }
 
-// Forward substitution L y = v in place (u_s).  Block b of LF holds, for lane l, the entries
-// L(r_l(u), bW+u), u = 0..W-1, of the row r_l(u) = l (mod W) that lane owns at step u, and the
-// reciprocal pivot 1/L(bW+l, bW+l) in the header (R28).  Per row: one multiply, one shuffle and
-// one FMA on the chain; the pivot lane then takes the row W further on.
-template <int N, typename F, typename S, class C>
-__device__ __noinline__ void forward(Ring& R, S* v, int l, bool leader) {
-    constexpr int W = C::W, NB = C::NB;
+// ======================================================================== K4b: refinement
+// ---- mbarrier / bulk-copy primitives (PTX)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// (A slot is refilled only after every lane of the segment has consumed the values it read from it
+// and passed a __syncwarp, so no proxy fence is issued per fill.)
+// The factor is streamed once per substitution and evicted first from L2, which keeps the small,
+// re-read working set (x, the coefficients) resident.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+template <int N, typename F, typename S, int NS_, int WPC_>
+struct RefCfg {
+    using G = Geo<N, F, S>;
+    static constexpr int NS = NS_;                     // ring slots
+    static constexpr int WPC = WPC_;                   // warps per CTA
+    // shared memory per segment: ring (NS blocks) | v (u_s) | mbarriers
+    static constexpr int OFF_V = NS * G::BLK;
+    static constexpr int OFF_B = OFF_V + ((G::NPAD * (int)sizeof(S) + 15) / 16) * 16;
+    static constexpr int SEG_BYTES = ((OFF_B + NS * 8 + 127) / 128) * 128;
+    static constexpr int SMEM = SEG_BYTES * G::SEGS * WPC;
+    static constexpr size_t XBYTES = (size_t)G::NPAD * 8;   // global x scratch per resident segment
+};
+
+// FIFO ring of factor blocks for one segment (NS slots).  The blocks are consumed in a fixed
+// sequence -- forward pass LF[0..NB-1], backward pass LB[NB-1..0], forward, ... -- so fill
+// position p goes to slot p % NS and completes phase (p / NS) & 1 of that slot's mbarrier; the
+// producer (the segment's lane 0) keeps NS-1 positions ahead of the consumer.  Counters are
+// absolute across jobs (the mbarrier phases are).
+template <int NB, int BLK, int NS>
+struct Ring {
+    unsigned char* buf;     // slot 0 (generic address)
+    uint32_t sbuf, bar;     // shared addresses of slot 0 and barrier 0
+    const unsigned char* lf;
+    const unsigned char* lb;
+    unsigned iss, use, pass, j;   // next fill: pass index and block position within the pass
+    uint64_t pol;                 // L2 policy of the fills
+
+    __device__ __forceinline__ const unsigned char* acquire(bool leader) {
+        __syncwarp();                                   // all lanes are done with position use-1
+        while (iss < use + NS) {
+            const unsigned char* src = (pass & 1) ? lb + (size_t)(NB - 1 - j) * BLK : lf + (size_t)j * BLK;
+            if (leader) bulk_load(sbuf + (iss % NS) * BLK, src, BLK, bar + 8 * (iss % NS), pol);
+            ++iss;
+            if (++j == NB) { j = 0; ++pass; }
+        }
+        mbar_wait(bar + 8 * (use % NS), (use / NS) & 1u);
+        const unsigned char* p = buf + (use % NS) * BLK;
+        ++use;
+        return p;
+    }
+    __device__ __forceinline__ void start(const unsigned char* f_lf, const unsigned char* f_lb) {
+        lf = f_lf;
+        lb = f_lb;
+        pass = 0;
+        j = 0;
+    }
+    __device__ __forceinline__ void drain() {
+        while (use < iss) {
+            mbar_wait(bar + 8 * (use % NS), (use / NS) & 1u);
+            ++use;
+        }
+        __syncwarp();
+    }
+};
+
+// Forward substitution L y = v in place (u_s).  LF block b gives lane l the entries L(r_l(u), bW+u)
+// of the row it owns at step u and 1/L(bW+l, bW+l).  Per row: a shuffle, an FMA and a multiply on
+// the chain; the pivot lane then takes the row W further on.
+template <class G, typename F, typename S, class R>
+__device__ __forceinline__ void forward(R& ring, S* v, int l, bool leader) {
+    constexpr int W = G::W, NB = G::NB;
     S cur = v[l];
     for (int b = 0; b < NB; ++b) {
-        const unsigned char* blk = ring_acquire<NB, C::BLK, C::NS>(R, leader);
+        const unsigned char* blk = ring.acquire(leader);
         S lv[W];
-        load_row<N, F, S, C>(blk, l, lv);
-        const S rd = reinterpret_cast<const S*>(blk + C::HDR)[l];
+        load_row<G, F, S>(blk, l, lv);
+        const S rd = reinterpret_cast<const S*>(blk + G::HDR)[l];
         const int k0 = b * W;
         const S nxt = b + 1 < NB ? v[k0 + W + l] : (S)0;
         S yv = (S)0;
@@ -285,7 +449,7 @@ __device__ __noinline__ void forward(Ring& R, S* v, int l, bool leader) {
         for (int u = 0; u < W; ++u) {
             const S yk = __shfl_sync(0xffffffffu, t, u, W);
             const S c2 = fma(-lv[u], yk, cur);
-            t = c2 * rd;                             // chain: shuffle -> FMA -> multiply (lane u+1)
+            t = c2 * rd;
             cur = c2;
             pivot_take(l, u, cur, nxt, yv, yk);
         }
@@ -294,17 +458,17 @@ __device__ __noinline__ void forward(Ring& R, S* v, int l, bool leader) {
     __syncwarp();
 }
 
-// Backward substitution L^T x = v in place (u_s).  Block b of LB holds, for lane l, the entries
-// L(bW+u, r_l(u)) of row bW+u at the column r_l(u) = l (mod W) that lane owns at step u.
-template <int N, typename F, typename S, class C>
-__device__ __noinline__ void backward(Ring& R, S* v, int l, bool leader) {
-    constexpr int W = C::W, NB = C::NB;
+// Backward substitution L^T x = v in place (u_s).  LB block b gives lane l the entries
+// L(bW+u, c_l(u)) of row bW+u at the column it owns at step u.
+template <class G, typename F, typename S, class R>
+__device__ __forceinline__ void backward(R& ring, S* v, int l, bool leader) {
+    constexpr int W = G::W, NB = G::NB;
     S cur = v[(NB - 1) * W + l];
     for (int b = NB - 1; b >= 0; --b) {
-        const unsigned char* blk = ring_acquire<NB, C::BLK, C::NS>(R, leader);
+        const unsigned char* blk = ring.acquire(leader);
         S lv[W];
-        load_row<N, F, S, C>(blk, l, lv);
-        const S rd = reinterpret_cast<const S*>(blk + C::HDR)[l];
+        load_row<G, F, S>(blk, l, lv);
+        const S rd = reinterpret_cast<const S*>(blk + G::HDR)[l];
         const int k0 = b * W;
         const S nxt = b > 0 ? v[k0 - W + l] : (S)0;
         S xv = (S)0;
@@ -324,34 +488,30 @@ __device__ __noinline__ void backward(Ring& R, S* v, int l, bool leader) {
 
 template <int N, typename F, typename S, int NS, int WPC>
 __global__ void __launch_bounds__(32 * WPC)
-chol_ir_kernel(const double* __restrict__ a_all, int nb, double tol, int i_max, double* __restrict__ out, int slot,
-               unsigned* __restrict__ job_counter, unsigned char* __restrict__ fscratch) {
-    using C = Chol2Cfg<N, F, S, NS, WPC>;
-    constexpr int W = C::W, n = C::n, NB = C::NB, NPAD = C::NPAD, SEGS = C::SEGS, BLK = C::BLK;
+chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_max, double* __restrict__ out,
+                   int slot, unsigned* __restrict__ job_counter, const unsigned char* __restrict__ fac,
+                   double* __restrict__ xscratch) {
+    using G = Geo<N, F, S>;
+    using K = RefCfg<N, F, S, NS, WPC>;
+    constexpr int W = G::W, n = G::n, NB = G::NB, NPAD = G::NPAD, SEGS = G::SEGS, BLK = G::BLK;
     constexpr int P = 2 * N * N, PER = NPAD / W;     // vector entries per lane (= NB)
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int seg = lane / W, l = lane % W;
     const unsigned mask = 0xffffffffu;
     const bool leader = l == 0;
-    unsigned char* base = smem + (size_t)(warp * SEGS + seg) * C::SEG_BYTES;
-    unsigned char* ring = base;
-    double* xs = reinterpret_cast<double*>(base + C::OFF_X);
-    S* v = reinterpret_cast<S*>(base + C::OFF_V);
-    F* colbuf = reinterpret_cast<F*>(base + C::OFF_C);
-    const size_t gseg = ((size_t)blockIdx.x * WPC + warp) * SEGS + seg;
-    unsigned char* LF = fscratch + gseg * C::FBYTES;
-    unsigned char* LB = LF + (size_t)NB * BLK;
-    Ring R;
-    R.buf = ring;
-    R.sbuf = smem_u32(ring);
-    R.bar = smem_u32(base + C::OFF_B);
-    R.lf = LF;
-    R.lb = LB;
-    R.P0 = R.iss = R.use = 0;
+    unsigned char* base = smem + (size_t)(warp * SEGS + seg) * K::SEG_BYTES;
+    S* v = reinterpret_cast<S*>(base + K::OFF_V);
+    double* xs = xscratch + (((size_t)blockIdx.x * WPC + warp) * SEGS + seg) * NPAD;
+    Ring<NB, BLK, NS> ring;
+    ring.buf = base;
+    ring.sbuf = smem_u32(base);
+    ring.bar = smem_u32(base + K::OFF_B);
+    ring.iss = ring.use = 0;
+    ring.pol = policy_evict_first();
     if (leader) {
 #pragma unroll
-        for (int q = 0; q < NS; ++q) mbar_init(R.bar + 8 * q);
+        for (int q = 0; q < NS; ++q) mbar_init(ring.bar + 8 * q);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -365,186 +525,100 @@ chol_ir_kernel(const double* __restrict__ a_all, int nb, double tol, int i_max, 
         if (jb >= nb) break;
         const int job = jb + seg;
         const bool live = job < nb;
-        const Coef<N> A{a_all + (size_t)(live ? job : nb - 1) * P};
-
-        // ---- step 1: right-looking banded Cholesky in F, window rows [k, k+W) in registers
-        // (ring slots 0 / 1 serve as the tiles in which the backward layout LB is assembled)
-        for (int e = l; e < BLK / 16; e += W) reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
-        F Rw[W];
-#pragma unroll
-        for (int c = 0; c < W; ++c) Rw[c] = FT<F>::from(0.0);
-        {
-            // row l: diagonal in slot l, west (column l-1) in slot l-1, south (column l-(N-1), only
-            // for l = W-1) in slot (l+1) mod W
-            double dg, we, so;
-            A.row(l, dg, we, so);
-#pragma unroll
-            for (int u = 0; u < W; ++u) {
-                if (u == ((l + 1) & (W - 1))) Rw[u] = FT<F>::from(so);
-                if (u == ((l + W - 1) & (W - 1))) Rw[u] = FT<F>::from(we);
-                if (u == l) Rw[u] = FT<F>::from(dg);
-            }
-        }
-        __syncwarp(mask);
-        bool ok = true;
-        F pnext = FT<F>::from(0.0);
-        for (int b = 0; b < NB; ++b) {
-            const int k0 = b * W;
-            unsigned char* Tc = ring + (b & 1) * BLK;          // tile of block b (rows k0 .. k0+W-1)
-            unsigned char* Tn = ring + ((b + 1) & 1) * BLK;    // tile of block b+1
-            // the row each lane takes after its pivot step in this block: k0 + W + l (loads issued early)
-            F dgn = FT<F>::from(0.0), wen = FT<F>::from(0.0), son = FT<F>::from(0.0);
-            if (b + 1 < NB) {
-                double dg, we, so;
-                A.row(k0 + W + l, dg, we, so);
-                dgn = FT<F>::from(dg);
-                wen = FT<F>::from(we);
-                son = FT<F>::from(so);
-            }
-            F lcol[W];
-            S rdl = (S)0;
-#pragma unroll
-            for (int u = 0; u < W; ++u) {
-                const int d = (l - u) & (W - 1);      // this lane holds row k0 + u + d
-                // pivot: lane u's diagonal, from the fast path of the previous step (k > 0)
-                F piv = __shfl_sync(mask, (b == 0 && u == 0) ? Rw[0] : pnext, u, W);
-                if (!FT<F>::pos_finite(piv)) { ok = false; piv = FT<F>::from(1.0); }
-                const F lkk = FT<F>::sqrt_(piv);
-                const S rk = rcp_s(to_s<S>(lkk));
-                const F lc = d == 0 ? lkk : FT<F>::div(Rw[u], lkk);     // L(k0+u+d, k0+u)
-                // the next pivot's update (lane u+1 multiplies its own column entry by itself, the
-                // same operation the rank-1 update below performs with the shared copy) off the
-                // shared-memory round trip
-                pnext = FT<F>::fnma(lc, lc, Rw[(u + 1) % W]);
-                lcol[u] = lc;
-                if (l == u) rdl = rk;
-                *reinterpret_cast<F*>((l >= u ? Tc : Tn) + C::off(u, l)) = lc;
-                F* cb = colbuf + (u & 1) * W;
-                cb[d] = lc;
-                __syncwarp(mask);
-                F cv[W];
-                if constexpr (C::C == 0) {
-#pragma unroll
-                    for (int j = 0; j < W; ++j) cv[j] = cb[j];
-                } else {
-#pragma unroll
-                    for (int i = 0; i < C::C; ++i) {
-                        const uint4 q = reinterpret_cast<const uint4*>(cb)[i];
-                        memcpy(&cv[i * C::EPC], &q, 16);
-                    }
-                }
-#pragma unroll
-                for (int j = 1; j < W; ++j) Rw[(u + j) % W] = FT<F>::fnma(lc, cv[j], Rw[(u + j) % W]);
-                if (l == u) {                          // row k0+u is done: this lane takes row k0+u+W
-#pragma unroll
-                    for (int c = 0; c < W; ++c) Rw[c] = FT<F>::from(0.0);
-                    Rw[u] = dgn;
-                    Rw[(u + W - 1) % W] = wen;
-                    Rw[(u + 1) % W] = son;
-                }
-            }
-            __syncwarp(mask);
-            unsigned char* gF = LF + (size_t)b * BLK;
-            unsigned char* gB = LB + (size_t)b * BLK;
-            store_row<N, F, S, C>(gF, l, lcol);
-            copy_row<N, F, S, C>(gB, Tc, l);
-            reinterpret_cast<S*>(gF + C::HDR)[l] = rdl;
-            reinterpret_cast<S*>(gB + C::HDR)[l] = rdl;
-            __syncwarp(mask);
-        }
-        // the factor was written by generic stores; the ring reads it through the async proxy
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp(mask);
+        const int jj = live ? job : nb - 1;
+        const Coef<N> A{a_all + (size_t)jj * P};
+        const unsigned char* LF = fac + (size_t)jj * G::FBYTES;
+        ring.start(LF, LF + (size_t)NB * BLK);
+        double* orec = out + (size_t)jj * kRecLen;
+        const bool ok = orec[6 + slot] == 0.0;        // factorisation status from K4a
         bool active = live && ok;
-        int status = ok ? 1 : 2, it = 0;
+        int status = ok ? 1 : 2, it = -1;
         double rel = 1.0;
-
-        // ---- step 2: x0 = (L L^T)^-1 b in u_s, stored in binary64
 #pragma unroll 4
         for (int q = 0; q < PER; ++q) {
             const int e = l + q * W;
-            v[e] = e < n ? (S)h2 : (S)0;
+            v[e] = e < n ? (S)h2 : (S)0;               // b in u_s
         }
         __syncwarp(mask);
-        forward<N, F, S, C>(R, v, l, leader);
-        backward<N, F, S, C>(R, v, l, leader);
-#pragma unroll 4
-        for (int q = 0; q < PER; ++q) {
-            const int e = l + q * W;
-            xs[e] = (double)v[e];
-        }
-        __syncwarp(mask);
+        // it = -1: step 2, x0 = (L L^T)^-1 b;  it >= 0: steps 4-8
         for (;;) {
-            // ---- step 4: r = b - A x in binary64 (rounded to u_s for the correction solve)
-            double part = 0.0;
-            if (active) {
-                for (int q = 0; q < PER; ++q) {
-                    const int e = l + q * W;
-                    double r = 0.0;
-                    if (e < n) {
-                        const int i = e % (N - 1) + 1, j = e / (N - 1) + 1;
-                        const double ce = A.cE(i, j), cw = A.cE(i - 1, j), cn = A.cN(i, j), cs = A.cN(i, j - 1);
-                        const double xe = xs[e];
-                        double Ax = ((ce + cw) + (cn + cs)) * xe;
-                        if (i < N - 1) Ax = fma(-ce, xs[e + 1], Ax);
-                        if (i > 1) Ax = fma(-cw, xs[e - 1], Ax);
-                        if (j < N - 1) Ax = fma(-cn, xs[e + N - 1], Ax);
-                        if (j > 1) Ax = fma(-cs, xs[e - (N - 1)], Ax);
-                        r = h2 - Ax;
-                        part = fma(r, r, part);
+            if (it >= 0) {
+                // ---- step 4: r = b - A x in binary64 (rounded to u_s for the correction solve)
+                double part = 0.0;
+                if (active) {
+#pragma unroll 1
+                    for (int q = 0; q < PER; ++q) {
+                        const int e = l + q * W;
+                        double r = 0.0;
+                        if (e < n) {
+                            const int i = e % (N - 1) + 1, j = e / (N - 1) + 1;
+                            const double ce = A.cE(i, j), cw = A.cE(i - 1, j), cn = A.cN(i, j), cs = A.cN(i, j - 1);
+                            double Ax = ((ce + cw) + (cn + cs)) * xs[e];
+                            if (i < N - 1) Ax = fma(-ce, xs[e + 1], Ax);
+                            if (i > 1) Ax = fma(-cw, xs[e - 1], Ax);
+                            if (j < N - 1) Ax = fma(-cn, xs[e + N - 1], Ax);
+                            if (j > 1) Ax = fma(-cs, xs[e - (N - 1)], Ax);
+                            r = h2 - Ax;
+                            part = fma(r, r, part);
+                        }
+                        v[e] = (S)r;
                     }
-                    v[e] = (S)r;
                 }
-            }
 #pragma unroll
-            for (int o = W / 2; o > 0; o >>= 1) part += __shfl_xor_sync(mask, part, o, W);
-            if (active) {
-                rel = sqrt(part) / bnorm;
-                if (!(rel == rel) || rel > DBL_MAX) { status = 3; active = false; }
-                else if (rel < tol) { status = 0; active = false; }            // step 5
-                else if (it == i_max) { active = false; }
-            }
-            if (!__any_sync(mask, active)) break;
-            __syncwarp(mask);
-            // ---- step 7: d = (L L^T)^-1 r in u_s;  step 8: x += d in binary64
-            forward<N, F, S, C>(R, v, l, leader);
-            backward<N, F, S, C>(R, v, l, leader);
-            if (active) {
-#pragma unroll 4
-                for (int q = 0; q < PER; ++q) {
-                    const int e = l + q * W;
-                    xs[e] += (double)v[e];
+                for (int o = W / 2; o > 0; o >>= 1) part += __shfl_xor_sync(mask, part, o, W);
+                if (active) {
+                    rel = sqrt(part) / bnorm;
+                    if (!(rel == rel) || rel > DBL_MAX) { status = 3; active = false; }
+                    else if (rel < tol) { status = 0; active = false; }        // step 5
+                    else if (it == i_max) { active = false; }
                 }
-                ++it;
+                if (!__any_sync(mask, active)) break;
+                __syncwarp(mask);
             }
+            // ---- steps 2 / 7: (L L^T)^-1 v in u_s;  step 8: x += d in binary64
+            forward<G, F, S>(ring, v, l, leader);
+            backward<G, F, S>(ring, v, l, leader);
+            if (it < 0) {
+#pragma unroll 4
+                for (int q = 0; q < PER; ++q) xs[l + q * W] = (double)v[l + q * W];
+            } else if (active) {
+#pragma unroll 4
+                for (int q = 0; q < PER; ++q) xs[l + q * W] += (double)v[l + q * W];
+            }
+            if (it < 0 || active) ++it;
             __syncwarp(mask);
         }
-        ring_drain<NS>(R);
+        ring.drain();
         double sx = 0.0;
         for (int q = 0; q < PER; ++q) sx += xs[l + q * W];      // padded rows hold exact zeros
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) sx += __shfl_xor_sync(mask, sx, o, W);
         if (live && leader) {
-            double* o = out + (size_t)job * kRecLen;
-            o[0 + slot] = status == 2 ? 0.0 : h2 * sx;
-            o[2 + slot] = (double)it;
-            o[4 + slot] = rel;
-            o[6 + slot] = (double)status;
+            orec[0 + slot] = status == 2 ? 0.0 : h2 * sx;
+            orec[2 + slot] = (double)(it < 0 ? 0 : it);
+            orec[4 + slot] = rel;
+            orec[6 + slot] = (double)status;
         }
         __syncwarp(mask);
     }
 }
 
+// ======================================================================== launch
 template <int N, typename F, typename S, int NS = 3, int WPC = 4>
 struct Launch {
-    using C = Chol2Cfg<N, F, S, NS, WPC>;
-    static cudaError_t occupancy(int& grid_max) {
+    using G = Geo<N, F, S>;
+    using KF = FacCfg<N, F, S>;
+    using KR = RefCfg<N, F, S, NS, WPC>;
+    static cudaError_t setup(int& grid_max) {
         static int bps = -1, sms = 0;
         if (bps < 0) {
-            auto kern = chol_ir_kernel<N, F, S, NS, WPC>;
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel<N, F, S>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, KF::SMEM);
             if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * WPC, C::SMEM);
+            auto kern = chol_refine_kernel<N, F, S, NS, WPC>;
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, KR::SMEM);
+            if (e != cudaSuccess) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * WPC, KR::SMEM);
             if (e != cudaSuccess) return e;
             int dev;
             cudaGetDevice(&dev);
@@ -554,30 +628,39 @@ struct Launch {
         grid_max = bps * sms;
         return cudaSuccess;
     }
-    static constexpr uint64_t per_cta = (uint64_t)WPC * C::SEGS;
-    static uint64_t grid_for(uint64_t nb, int gm) { return std::min<uint64_t>((nb + per_cta - 1) / per_cta, (uint64_t)gm); }
-    // factor scratch for a launch over nb systems: one factor (both layouts) per resident segment
+    static constexpr uint64_t per_cta = (uint64_t)WPC * G::SEGS;
+    static size_t fac_bytes(uint64_t nb) { return (nb * G::FBYTES + 255) & ~(size_t)255; }
+    // scratch of a launch over nb systems: every factor (LF + LB) + x of every resident refine segment
     static cudaError_t scratch(size_t& bytes, uint64_t nb) {
         int gm = 0;
-        cudaError_t e = occupancy(gm);
-        bytes = (size_t)grid_for(nb, gm) * per_cta * C::FBYTES;
+        cudaError_t e = setup(gm);
+        const uint64_t grid = std::min<uint64_t>((nb + per_cta - 1) / per_cta, (uint64_t)gm);
+        bytes = fac_bytes(nb) + (size_t)grid * per_cta * KR::XBYTES;
         return e;
     }
     static cudaError_t run(const double* a, uint64_t nb, double tol, int i_max, double* out, int slot, unsigned* ctr,
-                           void* fscratch, size_t fbytes, cudaStream_t s) {
-        int gm = 0;
-        cudaError_t e = occupancy(gm);
-        if (e != cudaSuccess) return e;
-        const uint64_t grid = std::min<uint64_t>(grid_for(nb, gm), fbytes / (per_cta * C::FBYTES));
+                           void* scr, size_t bytes, cudaStream_t s) {
         if (nb == 0) return cudaSuccess;
-        if (grid == 0) return cudaErrorInvalidValue;
-        chol_ir_kernel<N, F, S, NS, WPC><<<(unsigned)grid, 32 * WPC, C::SMEM, s>>>(
-            a, (int)nb, tol, i_max, out, slot, ctr, static_cast<unsigned char*>(fscratch));
+        int gm = 0;
+        cudaError_t e = setup(gm);
+        if (e != cudaSuccess) return e;
+        size_t need = 0;
+        scratch(need, nb);
+        if (need > bytes) return cudaErrorInvalidValue;
+        unsigned char* fac = static_cast<unsigned char*>(scr);
+        double* xs = reinterpret_cast<double*>(fac + fac_bytes(nb));
+        const uint64_t fgrid = (nb + kFacWarps * G::SEGS - 1) / (kFacWarps * G::SEGS);
+        chol_factor_kernel<N, F, S><<<(unsigned)fgrid, 32 * kFacWarps, KF::SMEM, s>>>(a, (int)nb, fac, out, slot);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        const uint64_t grid = std::min<uint64_t>((nb + per_cta - 1) / per_cta, (uint64_t)gm);
+        chol_refine_kernel<N, F, S, NS, WPC><<<(unsigned)grid, 32 * WPC, KR::SMEM, s>>>(a, (int)nb, tol, i_max, out,
+                                                                                     slot, ctr, fac, xs);
         return cudaGetLastError();
     }
 };
 
-// Ring depth / CTA shape for the h = 1/32 factors (MLMC_CHOL_VARIANT selects for tuning runs).
+// Ring depth / CTA shape of the refinement kernel for the h = 1/32 factors (MLMC_CHOL_VARIANT
+// selects for tuning runs).
 int chol_variant() {
     static int v = -2;
     if (v == -2) {
@@ -592,9 +675,9 @@ cudaError_t with_shape(Fn&& fn) {
     if constexpr (N == 32 && sizeof(S) == 4) {
         switch (chol_variant()) {
             case 1: return fn(Launch<N, F, S, 4, 4>{});
-            case 2: return fn(Launch<N, F, S, 6, 2>{});
-            case 3: return fn(Launch<N, F, S, 6, 3>{});
-            case 4: return fn(Launch<N, F, S, 8, 2>{});
+            case 2: return fn(Launch<N, F, S, 3, 2>{});
+            case 3: return fn(Launch<N, F, S, 4, 2>{});
+            case 4: return fn(Launch<N, F, S, 6, 2>{});
             default: return fn(Launch<N, F, S, 3, 4>{});
         }
     } else {
@@ -638,7 +721,7 @@ bool chol_supported(int N, int u_f, int u_s) {
     if (!(N == 2 || N == 4 || N == 8 || N == 16 || N == 32)) return false;
     if (!(u_f == MLMC_FMT_F16 || u_f == MLMC_FMT_F32 || u_f == MLMC_FMT_F64)) return false;
     if (!(u_s == MLMC_FMT_F32 || u_s == MLMC_FMT_F64)) return false;
-    if (u_f == MLMC_FMT_F64 && N == 32) return false;   // fp64 factor only where the old on-chip kernel had it
+    if (u_f == MLMC_FMT_F64 && N == 32) return false;   // no binary64 factor on the h = 1/32 mesh
     return true;
 }
 
@@ -649,9 +732,9 @@ size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb) {
 }
 
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max, double* out,
-                           int slot, unsigned* ctr, void* fscratch, size_t fbytes, cudaStream_t s) {
+                           int slot, unsigned* ctr, void* scratch, size_t bytes, cudaStream_t s) {
     return with_mesh(N, u_f, u_s, [&](auto L) {
-        return decltype(L)::run(a, nb, tol, i_max, out, slot, ctr, fscratch, fbytes, s);
+        return decltype(L)::run(a, nb, tol, i_max, out, slot, ctr, scratch, bytes, s);
     });
 }
 
