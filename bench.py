@@ -35,6 +35,17 @@ METRIC = "coupled level samples/sec per level and time-to-eps at 1/2/4/8 B200; H
 UNIT = "coupled samples/s"
 FLOPS_PER_NODE_ITER = 25.0       # algorithmic fp64 flops of one MINRES iteration per unknown
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+
+
+def _measured_hbm_gbs() -> float:
+    """MEASURED_PEAKS.json (driver-written, copy bandwidth); else the profiling guide's B200 fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0                    # B200_PROFILING.md fallback (6.65 TB/s), used only without the file
+
+
+HBM_PEAK_GBS = _measured_hbm_gbs()
 CPU_SAMPLE = {0: 2048, 1: 384, 2: 96, 3: 24}       # cpu_baseline: bounded oracle sample per level
 REF_SAMPLE = {0: 256, 1: 64, 2: 16, 3: 8}          # --impl reference: per-step oracle sample per level
 
@@ -342,7 +353,10 @@ def e2e_leg(ctx, cfg, args, world, rank, torch, np, dist):
 
 def c3_leg(local, torch):
     """configs[2]: 100000 coupled samples per level, h = 1/8, 1/16, 1/32, banded Cholesky in fp16 / fp32
-    with fp64 iterative refinement to 1e-10 (substitutions in fp32); device-timed per level."""
+    with fp64 iterative refinement to 1e-10 (substitutions in fp32); device-timed per level.  K4 is HBM-bound:
+    its roofline line counts the algorithmic factor bytes -- the band factor
+    n(bw+1) b_f written once and read by every substitution (2 per solve: x0 and each correction) -- plus the
+    coefficient read, over the library's per-launch CUDA-event time of the Cholesky-IR kernels."""
     from paper_2503_05533_b200 import Context, precision
     cfg = W.CONFIGS["C3"]
     ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
@@ -352,18 +366,33 @@ def c3_leg(local, torch):
     out = {}
     for uf in ("h", "s"):
         prec = precision("chol_ir", uf, "s")
+        bf = 2 if uf == "h" else 4
         for l, n in enumerate(cfg["N"]):
             ctx.sample_level_async(l, 2000, cfg["seed"], 10**7, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
+            ctx.profile_enable(True)
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             ctx.sample_level_async(l, n, cfg["seed"], 0, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
             a1.record(stream)
             torch.cuda.synchronize()
+            prof = ctx.profile_read()
+            ctx.profile_enable(False)
             s = sums.cpu().numpy()
             ms = a0.elapsed_time(a1)
+            Nf, Nc = cfg["h0_inv"] << l, (cfg["h0_inv"] << (l - 1)) if l else 0
+            k_ms = sum(r[3] for r in prof if r[0] == "chol_ir")
+
+            def solve_bytes(N, steps_sum):
+                fac = (N - 1) ** 2 * N * bf                      # band factor n (bw + 1) b_f
+                return n * fac * 3 + fac * 2 * steps_sum + n * 16 * N * N
+
+            alg = solve_bytes(Nf, s[7]) + (solve_bytes(Nc, s[8]) if l else 0.0)
+            gbs = alg / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
             out[f"l{l}_{'fp16' if uf == 'h' else 'fp32'}"] = {
-                "h": f"1/{cfg['h0_inv'] << l}", "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
-                "mean_ir_steps_fine": s[7] / n, "max_ir_steps_fine": s[9], "failures": s[6]}
+                "h": f"1/{Nf}", "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
+                "mean_ir_steps_fine": s[7] / n, "max_ir_steps_fine": s[9], "failures": s[6],
+                "k4_ms": k_ms, "k4_algorithmic_GB": alg / 1e9, "k4_achieved_GBs": gbs,
+                "k4_hbm_frac": gbs / HBM_PEAK_GBS}
     ctx.close()
     return out
 
