@@ -57,7 +57,7 @@ class KernelStat(C.Structure):
     _fields_ = [("kind", C.c_int32), ("N", C.c_int32), ("launches", C.c_uint64), ("ms", C.c_double)]
 
 
-KERNEL_KINDS = {0: "rng", 1: "field", 2: "minres", 3: "chol_ir", 4: "sums"}
+KERNEL_KINDS = {0: "rng", 1: "field", 2: "minres", 3: "chol_ir", 4: "sums", 5: "order"}
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_void_p)
 LEVEL_SAMPLER_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(Precision),

@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -103,7 +104,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Workspace layout for one pass of `batch` samples of `level`.
 struct WsLayout {
-    size_t xi, a_f, a_c, rec, chunks, ctr, gm, ch_f, ch_c, ch_f_bytes, ch_c_bytes, total;
+    size_t xi, a_f, a_c, rec, chunks, ctr, keys_f, keys_c, ord_f, ord_c, gm, ch_f, ch_c, ch_f_bytes, ch_c_bytes, total;
     int gm_ctas;
 };
 // Cholesky factor scratch of one solve (0 for MINRES / unsupported combinations)
@@ -122,6 +123,11 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.rec = off;    off += align256(sizeof(double) * batch * kRecLen);
     L.chunks = off; off += align256(sizeof(double) * kSumsLen * ((batch + kChunk - 1) / kChunk + 1));
     L.ctr = off;    off += align256(sizeof(unsigned) * 16);
+    // contrast keys and longest-first orders of the fine / coarse MINRES solves (order_kernel)
+    L.keys_f = off; off += align256(sizeof(unsigned long long) * 2 * batch);
+    L.keys_c = off; off += align256(sizeof(unsigned long long) * 2 * batch);
+    L.ord_f = off;  off += align256(sizeof(int) * batch);
+    L.ord_c = off;  off += align256(sizeof(int) * batch);
     L.gm = off;
     L.gm_ctas = 0;
     if (Nf >= kGmMinN) {   // per-CTA vector scratch of the global-memory MINRES (fine and coarse share it)
@@ -202,20 +208,34 @@ void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
     else { fixed = n * bw * bw * fmt_bits(p->u_f) / 64.0; step = 4.0 * n * bw; }
 }
 
+// Longest-first job order for a MINRES solve (LPT scheduling of the persistent CTAs): worth it where
+// a launch is a few waves of long solves (h >= 1/32: the tile kernel, nb <= kOrderMax).  MLMC_ORDER=0
+// switches it off (A/B runs).
+bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("MLMC_ORDER");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return env && p->solver == MLMC_SOLVER_MINRES && N >= 32 && N < kGmMinN && nb >= 2 && nb <= (uint64_t)kOrderMax &&
+           minres_tile_variant(N) >= 0;
+}
+
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
                double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas, void* ch_scratch,
-               size_t ch_bytes) {
+               size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
         bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
+        if (keys && order) CU(counted(ctx, ex.st, MLMC_K_ORDER, N, [&] { return launch_order(keys, (int)nb, order, ex.st); }));
         if (N >= kGmMinN)
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
                 return launch_minres_gm(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st);
             }));
         else
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
-                       [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, ex.st); }));
+                       [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, keys ? order : nullptr, ex.st); }));
     } else {
         int mi = p->max_iter > 0 ? p->max_iter : 50;
         CU(counted(ctx, ex.st, MLMC_K_CHOL_IR, N,
@@ -274,11 +294,18 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
             CU(counted(ctx, st, MLMC_K_RNG, 0,
                        [&] { return launch_rng(xi, m, nb, seed, level, first_index + done, st); }));
         }
+        const bool ord_f = use_order(pf, Nf, nb), ord_c = level > 0 && use_order(pc, Nc, nb);
+        unsigned long long* kf = ord_f ? reinterpret_cast<unsigned long long*>(ex.ws + L.keys_f) : nullptr;
+        unsigned long long* kc = ord_c ? reinterpret_cast<unsigned long long*>(ex.ws + L.keys_c) : nullptr;
+        if (kf) CU(cudaMemsetAsync(kf, 0, sizeof(unsigned long long) * 2 * nb, st));
+        if (kc) CU(cudaMemsetAsync(kc, 0, sizeof(unsigned long long) * 2 * nb, st));
         CU(counted(ctx, st, MLMC_K_FIELD, Nf,
-                   [&] { return launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, st); }));
+                   [&] { return launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, kf, st); }));
         if (level > 0)
             CU(counted(ctx, st, MLMC_K_FIELD, Nc,
-                       [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, st); }));
+                       [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, kc, st); }));
+        int* of = reinterpret_cast<int*>(ex.ws + L.ord_f);
+        int* oc = reinterpret_cast<int*>(ex.ws + L.ord_c);
         if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, st));
         const bool sched = sch && nb == n;               // single pass only
         if (sched && sch->prep) CU(cudaEventRecord(sch->prep, st));
@@ -291,15 +318,17 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         }
         void* chf = ex.ws + L.ch_f;
         void* chc = ex.ws + L.ch_c;
-        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes))) return rc;
+        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes, kf, of)))
+            return rc;
         if (fork) {
             const Exec exc{ex.ws, ex.bytes, sch->st_c};
-            if ((rc = solve_mesh(ctx, exc, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc, L.ch_c_bytes)))
+            if ((rc = solve_mesh(ctx, exc, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc, L.ch_c_bytes, kc,
+                                 oc)))
                 return rc;
             CU(cudaEventRecord(sch->join, sch->st_c));
             CU(cudaStreamWaitEvent(st, sch->join, 0));
         } else if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc,
-                                                 L.ch_c_bytes))) {
+                                                 L.ch_c_bytes, kc, oc))) {
             return rc;
         }
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
@@ -597,7 +626,7 @@ int mlmc_debug_field(mlmc_ctx* ctx, int level, int mesh_level, uint64_t n, uint6
     if (!xi) CU(cudaMalloc(&xi, sizeof(double) * std::max<uint64_t>(n, 1) * ctx->pr.m));
     CU(launch_rng(xi, ctx->pr.m, n, seed, level, first_index, ctx->stream));
     int N = level_N(ctx, mesh_level);
-    if (a_dev) CU(launch_field(ctx->phi_dev[mesh_level], xi, a_dev, 2 * N * N, ctx->pr.m, n, ctx->stream));
+    if (a_dev) CU(launch_field(ctx->phi_dev[mesh_level], xi, a_dev, 2 * N * N, ctx->pr.m, n, nullptr, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (!xi_dev) cudaFree(xi);
     return MLMC_OK;

@@ -26,17 +26,25 @@ void build_phi(const mlmc_problem& pr, const KLModes& kl, int N, std::vector<dou
 // K0: xi[b*m + k] ~ N(0,1), b < nb, for global index first_index + b.
 cudaError_t launch_rng(double* xi, int m, uint64_t nb, uint64_t seed, int level, uint64_t first_index,
                        cudaStream_t s);
-// K1+K2: a[b*P + p] = exp(sum_k xi[b*m+k] * phi[p*m+k]).
+// K1+K2: a[b*P + p] = exp(sum_k xi[b*m+k] * phi[p*m+k]).  keys (optional, device, 2*nb u64, zeroed
+// by the caller): keys[2b] = max_p a (bits), keys[2b+1] = ~min_p a (bits), the coefficient contrast.
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
-                         cudaStream_t s);
-// K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].
+                         unsigned long long* keys, cudaStream_t s);
+// Longest-first order of nb <= kOrderMax systems by descending contrast max a / min a (a single-CTA
+// bitonic sort of the field keys): order[i] = system index.  The contrast predicts the MINRES
+// iteration count (correlation 0.83 on configs[1] level 3), so the job counter hands out the long
+// solves first (LPT scheduling of the persistent CTAs).
+constexpr int kOrderMax = 4096;
+cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cudaStream_t s);
+// K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].  order (optional,
+// device, nb ints): the sequence in which the systems are taken (order_kernel: longest first).
 cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                          int slot, unsigned* job_counter, bool verify, cudaStream_t s);
+                          int slot, unsigned* job_counter, bool verify, const int* order, cudaStream_t s);
 bool minres_supported(int N);
 // K3 v2 (k_minres_tile.cu): 2-column register tiles for N = 8, 16, 32, 64; variant < 0 = not used for N.
 int minres_tile_variant(int N);
 cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                               int slot, unsigned* job_counter, bool verify, cudaStream_t s);
+                               int slot, unsigned* job_counter, bool verify, const int* order, cudaStream_t s);
 // K3 for N >= 128: vectors in a per-CTA global scratch (nctas CTAs, minres_gm_scratch_per_cta(N) bytes each).
 constexpr int kGmMinN = 128;
 size_t minres_gm_scratch_per_cta(int N);

@@ -11,6 +11,7 @@
 //     Register-tiled FFMA64: a 64(b) x 64(p) output tile per 256-thread CTA,
 //     4x4 outputs per thread, k staged through shared memory in chunks of 16.
 #include <cuda_runtime.h>
+#include <cfloat>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -72,8 +73,16 @@ cudaError_t launch_rng(double* xi, int m, uint64_t nb, uint64_t seed, int level,
 // ---------------------------------------------------------------------------- K1 + K2
 constexpr int FT_B = 64, FT_P = 64, FT_K = 16;
 
+// Per-sample contrast keys (optional): keys[2b] = max a, keys[2b+1] = ~min a as u64 bit patterns
+// (order-preserving for positive doubles), combined with atomicMax.
+__device__ __forceinline__ void key_update(unsigned long long* keys, int b, double mx, double mn) {
+    atomicMax(keys + 2 * b, (unsigned long long)__double_as_longlong(mx));
+    atomicMax(keys + 2 * b + 1, ~(unsigned long long)__double_as_longlong(mn));
+}
+
 __global__ void __launch_bounds__(256) field_kernel(const double* __restrict__ phi, const double* __restrict__ xi,
-                                                    double* __restrict__ a, int P, int m, int nb) {
+                                                    double* __restrict__ a, int P, int m, int nb,
+                                                    unsigned long long* __restrict__ keys) {
     __shared__ double sX[FT_K][FT_B + 1];
     __shared__ double sP[FT_K][FT_P + 1];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // tx -> p, ty -> b
@@ -109,11 +118,18 @@ __global__ void __launch_bounds__(256) field_kernel(const double* __restrict__ p
     for (int i = 0; i < 4; ++i) {
         int b = b0 + ty + 16 * i;
         if (b >= nb) continue;
+        double mx = 0.0, mn = DBL_MAX;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             int p = p0 + tx + 16 * j;
-            if (p < P) a[(size_t)b * P + p] = exp(acc[i][j]);
+            if (p < P) {
+                const double v = exp(acc[i][j]);
+                a[(size_t)b * P + p] = v;
+                mx = fmax(mx, v);
+                mn = fmin(mn, v);
+            }
         }
+        if (keys) key_update(keys, b, mx, mn);
     }
 }
 
@@ -131,9 +147,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 __global__ void __launch_bounds__(256) field_dmma_kernel(const double* __restrict__ phi, const double* __restrict__ xi,
-                                                         double* __restrict__ a, int P, int m, int nb) {
+                                                         double* __restrict__ a, int P, int m, int nb,
+                                                         unsigned long long* __restrict__ keys) {
     __shared__ double sX[FD_K][FD_PITCH];
     __shared__ double sP[FD_K][FD_PITCH];
+    __shared__ double kmx[4][FD_B], kmn[4][FD_B];      // per-warp-column contrast partials
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wb = warp >> 2, wp = warp & 3;            // warp tile: samples 32*wb.., centroids 16*wp..
     const int gq = lane >> 2, tq = lane & 3;            // fragment row group / thread in group
@@ -168,18 +186,91 @@ __global__ void __launch_bounds__(256) field_dmma_kernel(const double* __restric
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const int b = b0 + 32 * wb + 8 * t + gq;
-        if (b >= nb) continue;
+        double mx = 0.0, mn = DBL_MAX;
+        if (b < nb) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int p = p0 + 16 * wp + 8 * u + 2 * tq;
-            double* dst = a + (size_t)b * P + p;
-            if (p + 1 < P) {
-                *reinterpret_cast<double2*>(dst) = make_double2(exp(acc[t][u][0]), exp(acc[t][u][1]));
-            } else if (p < P) {
-                dst[0] = exp(acc[t][u][0]);
+            for (int u = 0; u < 2; ++u) {
+                const int p = p0 + 16 * wp + 8 * u + 2 * tq;
+                double* dst = a + (size_t)b * P + p;
+                if (p + 1 < P) {
+                    const double v0 = exp(acc[t][u][0]), v1 = exp(acc[t][u][1]);
+                    *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+                    mx = fmax(mx, fmax(v0, v1));
+                    mn = fmin(mn, fmin(v0, v1));
+                } else if (p < P) {
+                    const double v0 = exp(acc[t][u][0]);
+                    dst[0] = v0;
+                    mx = fmax(mx, v0);
+                    mn = fmin(mn, v0);
+                }
+            }
+        }
+        if (keys) {                                   // reduce over the 4 lanes of the row group
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
+            if (tq == 0) {
+                kmx[wp][32 * wb + 8 * t + gq] = mx;
+                kmn[wp][32 * wb + 8 * t + gq] = mn;
             }
         }
     }
+    if (keys) {                                       // one atomic pair per sample and CTA
+        __syncthreads();
+        if (threadIdx.x < FD_B && b0 + threadIdx.x < nb) {
+            const int r = threadIdx.x;
+            const double mx = fmax(fmax(kmx[0][r], kmx[1][r]), fmax(kmx[2][r], kmx[3][r]));
+            const double mn = fmin(fmin(kmn[0][r], kmn[1][r]), fmin(kmn[2][r], kmn[3][r]));
+            key_update(keys, b0 + r, mx, mn);
+        }
+    }
+}
+
+// Longest-first order: one CTA of 1024 threads sorts (contrast, index) pairs of nb <= kOrderMax
+// systems by descending contrast (bitonic network in shared memory; ties by ascending index).
+__global__ void __launch_bounds__(1024) order_kernel(const unsigned long long* __restrict__ keys, int nb,
+                                                     int* __restrict__ order) {
+    __shared__ double sk[kOrderMax];
+    __shared__ int si[kOrderMax];
+    int n2 = 1;
+    while (n2 < nb) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < nb) {
+            const double mx = __longlong_as_double((long long)keys[2 * i]);
+            const double mn = __longlong_as_double((long long)~keys[2 * i + 1]);
+            sk[i] = mn > 0.0 ? mx / mn : DBL_MAX;
+        } else {
+            sk[i] = -1.0;                             // padding sorts last
+        }
+        si[i] = i;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    // descending by key inside blocks with (i & k) == 0, ascending otherwise
+                    const bool before = sk[i] > sk[ixj] || (sk[i] == sk[ixj] && si[i] < si[ixj]);
+                    const bool desc = (i & k) == 0;
+                    if (desc != before) {
+                        const double tk = sk[i]; sk[i] = sk[ixj]; sk[ixj] = tk;
+                        const int ti = si[i]; si[i] = si[ixj]; si[ixj] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) order[i] = si[i];
+}
+
+cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cudaStream_t s) {
+    if (nb <= 0) return cudaSuccess;
+    if (nb > kOrderMax) return cudaErrorInvalidValue;
+    order_kernel<<<1, 1024, 0, s>>>(keys, nb, order);
+    return cudaGetLastError();
 }
 
 static bool field_use_ffma() {
@@ -192,14 +283,14 @@ static bool field_use_ffma() {
 }
 
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
-                         cudaStream_t s) {
+                         unsigned long long* keys, cudaStream_t s) {
     if (nb == 0) return cudaSuccess;
     if (field_use_ffma() || (P & 1)) {
         dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nb + FT_B - 1) / FT_B));
-        field_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb);
+        field_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb, keys);
     } else {
         dim3 grid((P + FD_P - 1) / FD_P, (unsigned)((nb + FD_B - 1) / FD_B));
-        field_dmma_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb);
+        field_dmma_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb, keys);
     }
     return cudaGetLastError();
 }

@@ -127,7 +127,7 @@ __device__ __forceinline__ double4 tsum3(double a, double b, double c, double* b
 template <int N, int R, int MINB, int CM, bool VERIFY>
 __global__ void __launch_bounds__(TileCfg<N, R, MINB, CM>::BLOCK, MINB)
 minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
-                   int slot, unsigned* __restrict__ job_counter) {
+                   int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order) {
     using K = TileCfg<N, R, MINB, CM>;
     constexpr int PAIRS = K::PAIRS, PW = K::PW, RP = K::RP, TPS = K::TPS, GROUPS = K::GROUPS;
     constexpr bool DS = K::DS, WS = K::WS;
@@ -159,7 +159,8 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
         const int job = *jobslot;
         tsync<TPS, GROUPS>(g);
         if (job >= nb) break;
-        const double* a = a_all + (size_t)job * P;
+        const int sj = order ? __ldg(order + job) : job;     // longest-first order (order_kernel) if given
+        const double* a = a_all + (size_t)sj * P;
         auto aL = [&](int ii, int jj) { return __ldg(a + 2 * (jj * N + ii)); };
         auto aU = [&](int ii, int jj) { return __ldg(a + 2 * (jj * N + ii) + 1); };
         // cE(i,j): edge (i,j)-(i+1,j), lower triangle of cell (i,j) + upper of cell (i,j-1)
@@ -370,7 +371,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
             relres = sqrt(rr) * inv_beta1;
         }
         if (tg == 0) {
-            double* o = out + (size_t)job * kRecLen;
+            double* o = out + (size_t)sj * kRecLen;
             o[0 + slot] = h2 * Xq;
             o[2 + slot] = (double)k;
             o[4 + slot] = relres;
@@ -382,7 +383,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
 
 template <int N, int R, int MINB, int CM, bool VERIFY>
 cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
-                     cudaStream_t s) {
+                     const int* order, cudaStream_t s) {
     using K = TileCfg<N, R, MINB, CM>;
     auto kern = minres_tile_kernel<N, R, MINB, CM, VERIFY>;
     static int blocks_per_sm = -1, sms = 0;
@@ -399,7 +400,7 @@ cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, dou
     const uint64_t need = (nb + K::GROUPS - 1) / K::GROUPS;
     const uint64_t grid = std::min<uint64_t>(need, (uint64_t)blocks_per_sm * sms);
     if (grid == 0) return cudaSuccess;
-    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr);
+    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order);
     return cudaGetLastError();
 }
 
@@ -423,35 +424,35 @@ int minres_tile_variant(int N) {
 // Variant table (index = MLMC_MINRES_TILE_N<N>): <N, R, MINB, CM>; measured with tools/tune_minres.py.
 template <bool V>
 static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                                 int slot, unsigned* ctr, cudaStream_t s) {
+                                 int slot, unsigned* ctr, const int* order, cudaStream_t s) {
     switch (N) {
         case 8:   // two systems per warp (16 threads each)
-            if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 16:
-            if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_tile<16, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            return run_tile<16, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 32:
-            if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_tile<32, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            return run_tile<32, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 64:
             // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67
-            if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, s);
-            return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+            if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         default: return cudaErrorNotSupported;
     }
 }
 
 cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                               unsigned* ctr, bool verify, cudaStream_t s) {
+                               unsigned* ctr, bool verify, const int* order, cudaStream_t s) {
     const int var = minres_tile_variant(N);
-    return verify ? tile_dispatch<true>(N, var, a, nb, tol, max_iter, out, slot, ctr, s)
-                  : tile_dispatch<false>(N, var, a, nb, tol, max_iter, out, slot, ctr, s);
+    return verify ? tile_dispatch<true>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, s)
+                  : tile_dispatch<false>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, s);
 }
 
 }  // namespace mlmc
