@@ -299,6 +299,7 @@ def run_ours(args):
         line["e2e"] = e2e_leg(ctx, cfg, args, world, rank, torch, np, dist)
         line["time_to_eps"] = adaptive_leg(args, world, rank, local, torch, dist)
         line["c3_cholesky_ir"] = c3_leg(local, torch)
+        line["k3c_fine_meshes"] = fine_leg(local, torch)
         if rank == 0 and world == 1:
             from oracle import core as oc
             oc.build()
@@ -393,6 +394,38 @@ def c3_leg(local, torch):
                 "mean_ir_steps_fine": s[7] / n, "max_ir_steps_fine": s[9], "failures": s[6],
                 "k4_ms": k_ms, "k4_algorithmic_GB": alg / 1e9, "k4_achieved_GBs": gbs,
                 "k4_hbm_frac": gbs / HBM_PEAK_GBS}
+    ctx.close()
+    return out
+
+
+def fine_leg(local, torch):
+    """K3c, the streamed MINRES of the fine meshes (configs[4] field, h = 1/256 and 1/512): one batch of
+    148 systems (one per SM) per mesh, 300 MINRES steps each (max_iter; the finest levels of configs[4]
+    need thousands -- the rate per step is what the roofline measures).  K3c moves p_j, p_{j-1}, cE, cN
+    in and p_{j+1} out once per step: 40 algorithmic bytes per unknown and step (DESIGN.md section 6);
+    the kernel time is the library's per-launch CUDA-event time."""
+    from paper_2503_05533_b200 import Context, precision
+    cfg = W.CONFIGS["C5"]
+    ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
+                  L_max=cfg["L_max"], device=local, workspace_bytes=4 << 30)
+    sums = torch.zeros(12, dtype=torch.float64, device=torch.device("cuda", local))
+    nb, steps = 148, 300
+    prec = precision("minres", max_iter=steps)
+    out = {}
+    for level in (5, 6):
+        N = cfg["h0_inv"] << level
+        ctx.sample_level_async(level, 2, cfg["seed"], 10**6, prec, prec, 1e-14, 1e-14, sums_out=sums)
+        ctx.profile_enable(True)
+        ctx.sample_level_async(level, nb, cfg["seed"], 0, prec, prec, 1e-14, 1e-14, sums_out=sums)
+        prof = ctx.profile_read()
+        ctx.profile_enable(False)
+        s = sums.cpu().numpy()
+        k_ms = sum(r[3] for r in prof if r[0] == "minres" and r[1] == N)
+        node_steps = s[7] * (N - 1) ** 2
+        gbs = 40.0 * node_steps / (k_ms / 1e3) / 1e9
+        out[f"h=1/{N}"] = {"systems": nb, "minres_steps_each": s[7] / nb, "kernel_ms": k_ms,
+                           "unknown_steps_per_s": node_steps / (k_ms / 1e3), "achieved_GBs_40B": gbs,
+                           "hbm_frac": gbs / HBM_PEAK_GBS, "bound": "hbm"}
     ctx.close()
     return out
 

@@ -132,7 +132,7 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.gm_ctas = 0;
     if (Nf >= kGmMinN) {   // per-CTA vector scratch of the global-memory MINRES (fine and coarse share it)
         L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1));
-        off += align256(minres_gm_scratch_per_cta(Nf) * L.gm_ctas);
+        off += align256(std::max(minres_gm_scratch_per_cta(Nf), minres_stream_scratch_per_cta(Nf)) * L.gm_ctas);
     }
     // factor scratch of the Cholesky-IR solves (fine and coarse may run concurrently: two regions)
     L.ch_f_bytes = chol_bytes(pf, Nf, batch);
@@ -221,6 +221,16 @@ bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
            minres_tile_variant(N) >= 0;
 }
 
+// MLMC_MINRES_GM=1 selects the three-phase global-memory MINRES instead of the streamed one (A/B).
+bool use_gm_kernel() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("MLMC_MINRES_GM");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
                double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas, void* ch_scratch,
                size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr) {
@@ -229,7 +239,11 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
         int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
         bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
         if (keys && order) CU(counted(ctx, ex.st, MLMC_K_ORDER, N, [&] { return launch_order(keys, (int)nb, order, ex.st); }));
-        if (N >= kGmMinN)
+        if (N >= kGmMinN && minres_stream_supported(N) && !use_gm_kernel())
+            CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
+                return launch_minres_stream(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st);
+            }));
+        else if (N >= kGmMinN)
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
                 return launch_minres_gm(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st);
             }));

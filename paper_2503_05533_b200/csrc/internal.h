@@ -50,6 +50,12 @@ constexpr int kGmMinN = 128;
 size_t minres_gm_scratch_per_cta(int N);
 cudaError_t launch_minres_gm(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                              unsigned* job_counter, double* scratch, int nctas, cudaStream_t s);
+// K3c for N = 128, 256, 512: one pass per MINRES step streamed through HBM with TMA-tiled planes
+// (k_minres_stream.cu); same scratch convention (nctas CTAs x minres_stream_scratch_per_cta(N) bytes).
+bool minres_stream_supported(int N);
+size_t minres_stream_scratch_per_cta(int N);
+cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                                 unsigned* job_counter, double* scratch, int nctas, cudaStream_t s);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of
 // chol_scratch_bytes(N, u_f, u_s, nb) bytes for a launch over nb systems (one factor per resident
 // warp segment; a smaller scratch shrinks the grid; 0 = unsupported).

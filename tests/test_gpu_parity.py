@@ -320,3 +320,27 @@ def test_adaptive_C4_matches_oracle_controller():
         assert abs(o.estimate - g["estimate"]) < 0.1 * cfg["eps"]
     assert 0.030 < g["estimate"] < 0.038
     ctx.close()
+
+
+# ============================================================================ K3c: streamed fine meshes
+def test_streamed_minres_fine_mesh_parity():
+    """K3c (h = 1/128 fine, 1/64 coarse; configs[4] field): per-sample Q within the rigorous residual
+    bound of the oracle's direct banded Cholesky solve, at a tight and a loose tolerance."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    P = _oracle(cfg)
+    n = 4
+    for tol in (1e-11, 1e-6):
+        r = ctx.sample_level(4, n, seed=11, prec_fine=precision("minres"), tol_fine=tol, tol_coarse=tol,
+                             per_sample=True)
+        ps = r.per_sample
+        assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
+        assert np.all(ps[:, 4] <= tol)
+        exs = _pmap(lambda k: (_exact(P, 128, oc.normals(11, 4, k, cfg["m"])),
+                               _exact(P, 64, oc.normals(11, 4, k, cfg["m"]))), list(range(n)))
+        for k, ((qf, bf, xf), (qc, bc, xc)) in enumerate(exs):
+            assert abs(ps[k, 0] - qf) <= tol * bf * xf * (1 + 1e-6) + 1e-14 * qf, (tol, k, ps[k, 0], qf)
+            assert abs(ps[k, 1] - qc) <= tol * bc * xc * (1 + 1e-6) + 1e-14 * qc
+        if tol < 1e-10:
+            assert np.max(np.abs(ps[:, 0] / np.array([e[0][0] for e in exs]) - 1)) < 1e-9
+    ctx.close()
