@@ -300,6 +300,8 @@ def run_ours(args):
         line["time_to_eps"] = adaptive_leg(args, world, rank, local, torch, dist)
         line["c3_cholesky_ir"] = c3_leg(local, torch)
         line["k3c_fine_meshes"] = fine_leg(local, torch)
+        if rank == 0:
+            line["paper_mpml_vs_mlmc"] = paper_leg(local)
         if rank == 0 and world == 1:
             from oracle import core as oc
             oc.build()
@@ -427,6 +429,23 @@ def fine_leg(local, torch):
                            "unknown_steps_per_s": node_steps / (k_ms / 1e3), "achieved_GBs_40B": gbs,
                            "hbm_frac": gbs / HBM_PEAK_GBS, "bound": "hbm"}
     ctx.close()
+    return out
+
+
+def paper_leg(local):
+    """The paper's own experiment (Section 5.1): adaptive MPML vs standard adaptive MLMC (fixed
+    MINRES tolerance 1e-6) on the Eq. (20) field, R = 100 replicate runs per method and TOL^2 (the paper:
+    1000; tools/paper_experiment.py runs those, profiles/r01e_paper_experiment.md).  Reports the modelled
+    cost ratio (the paper's FLOP count analogue, ~1.5 there), the GPU solve-time ratio and both MSEs."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import paper_experiment
+    t0 = time.perf_counter()
+    res = paper_experiment.run(R=100, device=local)
+    out = {"R": res["R"], "reference_Q": res["reference"]["estimate"], "seconds": time.perf_counter() - t0}
+    for k, e in res["tol2"].items():
+        out[f"TOL2={k}"] = {"cost_ratio_mlmc_over_mpml": e["cost_ratio_mlmc_over_mpml"],
+                            "gpu_time_ratio_mlmc_over_mpml": e["gpu_time_ratio_mlmc_over_mpml"],
+                            "mse_mpml": e["mpml"]["mse"], "mse_mlmc": e["mlmc"]["mse"]}
     return out
 
 

@@ -80,7 +80,8 @@ typedef struct {
  *   u_f (MLMC_FMT_F16 / F32 / F64), initial and correction substitutions in
  *   u_s (F32 or F64, R24), residual in u_r and x in u (both F64), stop when
  *   ||r||/||b|| < tol, at most max_iter refinement steps.
- * max_iter = 0 selects the default (MINRES: 4n+100, IR: 50).
+ * max_iter = 0 selects the default (MINRES: 16n+1000 -- loss of orthogonality
+ * at coefficient contrasts ~1e7 takes well over n steps; IR: 50).
  * MINRES reports phibar_k/||b|| (the stopping quantity) as the residual and
  * computes Q from the scalar recurrence of 1^T x_k (R26); with
  * MLMC_FLAG_VERIFY it also carries x_k and reports ||b - A x_k||/||b||, with
@@ -232,12 +233,16 @@ typedef struct {
     int32_t rank, world; /* this process's slice of every level's new indices */
     int32_t max_rounds;  /* safety cap (default 100) */
     uint64_t seed;
+    int32_t on_fail;     /* a solve that misses its tolerance (max_iter, breakdown; R15): 0 = stop with
+                            MLMC_ESOLVER, 1 = keep the sample (Q of the last iterate) and count it in
+                            mlmc_result.n_fail -- never resampled either way */
+    int32_t reserved0;
 } mlmc_adaptive_opts;
 
 typedef struct {
     double   estimate;                   /* Eq. (3): sum_l hat Y_l */
     int32_t  L, rounds, code;            /* code: MLMC_OK or MLMC_ELMAX */
-    int32_t  reserved;
+    int32_t  n_fail;                     /* solves that missed their tolerance (kept under on_fail = 1) */
     uint64_t N[MLMC_MAX_LEVELS];         /* samples drawn per level (all ranks) */
     double   eps[MLMC_MAX_LEVELS];       /* eps_l of the last round */
     double   mean[MLMC_MAX_LEVELS];      /* hat Y_l */

@@ -43,12 +43,12 @@ class LevelInfo(C.Structure):
 class AdaptiveOpts(C.Structure):
     _fields_ = [("k_p", C.c_double), ("fixed_tol", C.c_double), ("r_bias", C.c_double), ("N_init", C.c_int32),
                 ("policy", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("max_rounds", C.c_int32),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("on_fail", C.c_int32), ("reserved0", C.c_int32)]
 
 
 class Result(C.Structure):
     _fields_ = [("estimate", C.c_double), ("L", C.c_int32), ("rounds", C.c_int32), ("code", C.c_int32),
-                ("reserved", C.c_int32), ("N", C.c_uint64 * MLMC_MAX_LEVELS), ("eps", C.c_double * MLMC_MAX_LEVELS),
+                ("n_fail", C.c_int32), ("N", C.c_uint64 * MLMC_MAX_LEVELS), ("eps", C.c_double * MLMC_MAX_LEVELS),
                 ("mean", C.c_double * MLMC_MAX_LEVELS), ("var", C.c_double * MLMC_MAX_LEVELS),
                 ("cost", C.c_double * MLMC_MAX_LEVELS), ("solve_seconds", C.c_double)]
 

@@ -190,11 +190,12 @@ class Context:
         return xi[:n], a[:n]
 
     def adaptive_run(self, eps: float, k_p: float = 0.05, N_init: int = 100, policy: int = 0, seed: int = 0,
-                     fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None) -> dict:
+                     fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None,
+                     on_fail: int = 0) -> dict:
         """mlmc_adaptive_run (Algorithm 2).  With a torch.distributed group the per-round level sums are
         all-reduced through it (NCCL on GPU tensors, gloo on CPU tensors)."""
         rank, world, cb = _allreduce_callback(group, self.device)
-        opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed)
+        opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed, on_fail, 0)
         res = K.Result()
         rc = K.lib().mlmc_adaptive_run(self.ctx, eps, C.byref(opts), cb, None, C.byref(res))
         if rc not in (K.MLMC_OK, K.MLMC_ELMAX):
@@ -204,7 +205,7 @@ class Context:
 
 def _result_dict(res) -> dict:
     L = res.L
-    return {"estimate": res.estimate, "L": L, "rounds": res.rounds, "code": res.code,
+    return {"estimate": res.estimate, "L": L, "rounds": res.rounds, "code": res.code, "n_fail": res.n_fail,
             "N": list(res.N[:L + 1]), "eps": list(res.eps[:L + 1]), "mean": list(res.mean[:L + 1]),
             "var": list(res.var[:L + 1]), "cost": list(res.cost[:L + 1]), "solve_seconds": res.solve_seconds}
 
@@ -234,7 +235,7 @@ def _allreduce_callback(group, device):
 
 def mlmc_adaptive_run_host(h0_inv: int, L_max: int, eps: float, sampler, k_p: float = 0.05, N_init: int = 100,
                            policy: int = 0, seed: int = 0, fixed_tol: float = 1e-10, r_bias: float = 1.0,
-                           max_rounds: int = 100, group=None) -> dict:
+                           max_rounds: int = 100, group=None, on_fail: int = 0) -> dict:
     """The library's Algorithm 2 over a host sampler (no GPU): ``sampler(level, n, first_index, prec_fine,
     prec_coarse, tol_fine, tol_coarse) -> 12 level sums``.  Used by the CPU tests of the controller and
     of the multi-rank exchange (gloo)."""
@@ -252,7 +253,7 @@ def mlmc_adaptive_run_host(h0_inv: int, L_max: int, eps: float, sampler, k_p: fl
             return 1
 
     scb = K.LEVEL_SAMPLER_FN(_cb)
-    opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed)
+    opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed, on_fail, 0)
     res = K.Result()
     rc = K.lib().mlmc_adaptive_run_host(h0_inv, L_max, eps, C.byref(opts), scb, None, cb, None, C.byref(res))
     if rc not in (K.MLMC_OK, K.MLMC_ELMAX):

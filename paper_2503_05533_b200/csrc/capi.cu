@@ -236,7 +236,7 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
                size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
-        int mi = p->max_iter > 0 ? p->max_iter : 4 * n + 100;
+        int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;   // finite-precision Lanczos at contrast ~1e7 (Eq. (20), sigma = 2) needs > n
         bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
         if (keys && order) CU(counted(ctx, ex.st, MLMC_K_ORDER, N, [&] { return launch_order(keys, (int)nb, order, ex.st); }));
         if (N >= kGmMinN && minres_stream_supported(N) && !use_gm_kernel())

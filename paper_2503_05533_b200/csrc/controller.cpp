@@ -15,6 +15,7 @@
 // multi-rank exchange).
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -70,6 +71,7 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
     std::vector<double> epsl;
     int L = 1, rounds = 0, code = MLMC_OK;
     double solve_s = 0.0;
+    int64_t n_fail = 0;
 
     auto stats = [&](int l, double& mean, double& var, double& cost) {
         const double n = acc[l].s[5];
@@ -137,8 +139,10 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
                 acc[l].s[k] = (k == 9 || k == 10) ? std::max(acc[l].s[k], rs[k]) : acc[l].s[k] + rs[k];
             acc[l].drawn += dN[l];
             if (rs[6] > 0) failed = true;
+            n_fail += (int64_t)rs[6];
         }
-        if (failed) { code = MLMC_ESOLVER; break; }   // a failed solve is never resampled (R15)
+        // a failed solve is never resampled (R15): stop, or keep it and count it (on_fail = 1)
+        if (failed && o.on_fail != 1) { code = MLMC_ESOLVER; break; }
         // steps 5-7
         std::vector<double> mean(L + 1), V(L + 1), C(L + 1), Nopt(L + 1);
         for (int l = 0; l <= L; ++l) stats(l, mean[l], V[l], C[l]);
@@ -165,6 +169,7 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
     out->L = L;
     out->rounds = rounds;
     out->code = code;
+    out->n_fail = (int32_t)std::min<int64_t>(n_fail, INT32_MAX);
     out->solve_seconds = solve_s;
     double est = 0.0;
     for (int l = 0; l <= L && l < MLMC_MAX_LEVELS; ++l) {

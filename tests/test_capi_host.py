@@ -83,3 +83,30 @@ def test_invalid_problems_rejected():
     for p in bad:
         ctx = C.c_void_p()
         assert K.lib().mlmc_plan_levels(C.byref(p), C.byref(ctx)) == K.MLMC_EINVAL
+
+
+def test_controller_failed_solves_abort_or_are_counted():
+    """R15: a sample whose solve missed its tolerance is never resampled; Algorithm 2 either stops with
+    MLMC_ESOLVER (on_fail = 0) or keeps it and reports the count (on_fail = 1).  Host sampler: level sums
+    with a variance that decays 4x per level, one failed solve flagged on level 0 of the first round."""
+    import numpy as np
+    from paper_2503_05533_b200 import _capi as K
+    from paper_2503_05533_b200.api import mlmc_adaptive_run_host
+
+    calls = {"n": 0}
+
+    def sampler(level, n, first, pf, pc, tf, tc):
+        rng = np.random.default_rng(1000 * level + first)
+        y = rng.normal(0.03 * 4.0 ** -level, 0.01 * 4.0 ** -level, n)
+        s = np.zeros(12)
+        s[0], s[1], s[4], s[5] = y.sum(), (y * y).sum(), n * 4.0 ** level, n
+        if level == 0 and calls["n"] == 0:
+            s[6] = 1.0
+        calls["n"] += 1
+        return s
+
+    with pytest.raises(RuntimeError, match="solver failure"):
+        mlmc_adaptive_run_host(8, 4, 2e-3, sampler, N_init=50)
+    calls["n"] = 0
+    r = mlmc_adaptive_run_host(8, 4, 2e-3, sampler, N_init=50, on_fail=1)
+    assert r["n_fail"] == 1 and r["code"] in (K.MLMC_OK, K.MLMC_ELMAX) and r["L"] >= 1

@@ -344,3 +344,21 @@ def test_streamed_minres_fine_mesh_parity():
         if tol < 1e-10:
             assert np.max(np.abs(ps[:, 0] / np.array([e[0][0] for e in exs]) - 1)) < 1e-9
     ctx.close()
+
+
+# ============================================================================ the paper's experiment
+def test_paper_experiment_mpml_cost_gain_without_accuracy_loss():
+    """Section 5.1: adaptive MPML vs standard adaptive MLMC (fixed MINRES tol 1e-6) on the
+    Eq. (20) field at TOL^2 = 2e-6, 200 replicate runs each: both MSEs within TOL^2 and equal up to
+    their statistical error, and MPML cheaper (the paper: ~1.5x fewer FLOPs)."""
+    import sys as _sys
+    import os as _os
+    _sys.path.insert(0, _os.path.join(_os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))), "tools"))
+    import paper_experiment
+    res = paper_experiment.run(R=200, tol2s=(2e-6,))
+    e = res["tol2"]["2e-06"]
+    for m in ("mpml", "mlmc"):                   # MSE <= TOL^2 up to its own 95% sampling error
+        assert e[m]["mse"] - e[m]["mse_ci95"] < 2e-6, (m, e[m])
+    diff = abs(e["mpml"]["mse"] - e["mlmc"]["mse"])
+    assert diff < 3.0 * math.hypot(e["mpml"]["mse_ci95"], e["mlmc"]["mse_ci95"]) / 1.96, e
+    assert e["cost_ratio_mlmc_over_mpml"] > 1.25, e
