@@ -331,9 +331,12 @@ def e2e_leg(ctx, cfg, args, world, rank, torch, np, dist):
     from paper_2503_05533_b200 import precision
     mr = precision("minres")
 
+    L = len(Nl)
+    tol_c = [tols[l - 1] if l else tols[0] for l in range(L)]
+
     def step():
-        for l in range(len(Nl)):
-            ctx.sample_level_xi(l, xs[l], mr, mr, tols[l], tols[l - 1] if l else tols[0], per_sample=outs[l])
+        # one call: every level's host xi copied in and records copied out on the level's own stream
+        ctx.sample_levels_xi(list(range(L)), xs, [mr] * L, [mr] * L, tols, tol_c, per_sample=outs)
     for _ in range(max(1, args.warmup)):
         step()
     if world > 1:
@@ -350,7 +353,8 @@ def e2e_leg(ctx, cfg, args, world, rank, torch, np, dist):
         el = float(t.item())
     return {"value": world * sum(Nl) * args.steps / el, "unit": UNIT,
             "h2d_bytes_per_step": int(sum(Nl) * m * 8), "d2h_bytes_per_step": int(sum(Nl) * 8 * 8 + len(Nl) * 96),
-            "api": "mlmc_sample_level_xi (host pinned xi in, host per-sample records + level sums out)",
+            "api": "mlmc_sample_levels_xi (all levels concurrently; host pinned xi in, host per-sample records + "
+                   "level sums out)",
             "clock": "host wall clock around the synchronous calls, max over ranks"}
 
 

@@ -196,6 +196,16 @@ int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const u
                              const mlmc_precision* prec_coarse, const double* tol_fine,
                              const double* tol_coarse, double* sums_dev);
 
+/* Several levels with caller-supplied random inputs, concurrently (the host-buffer path of one fixed-N
+ * MLMC step): entry q processes n[q] samples of levels[q] from xi[q] (n[q]*m doubles, host -- pinned
+ * makes the copy asynchronous -- or dev) exactly as mlmc_sample_level_xi would; out_sums (host) gets
+ * nlev records, per_sample (optional array of nlev pointers, each NULL, host or dev, n[q] *
+ * MLMC_SAMPLE_LEN doubles) the per-sample records.  All copies and kernels run on internal streams
+ * forked from the bound one; synchronises it once before returning.  Errors as mlmc_sample_level. */
+int mlmc_sample_levels_xi(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, const double* const* xi,
+                          const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse, const double* tol_fine,
+                          const double* tol_coarse, mlmc_level_sums* out_sums, double* const* per_sample);
+
 /* Caller-supplied random inputs (the SPEC's coupled_sample(l, omega)): exactly
  * mlmc_sample_level, except that xi (n*m doubles, sample-major, host or dev;
  * standard normals, the field's omega = sqrt(sigma2) xi) replaces the Philox

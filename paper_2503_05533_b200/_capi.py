@@ -108,6 +108,9 @@ def lib():
     L.mlmc_debug_field.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]
     L.mlmc_sample_level_xi.argtypes = [vp, C.c_int, C.c_uint64, vp, C.POINTER(Precision), C.POINTER(Precision),
                                        C.c_double, C.c_double, C.POINTER(LevelSums), vp]
+    L.mlmc_sample_levels_xi.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.POINTER(vp),
+                                        C.POINTER(Precision), C.POINTER(Precision), dp, dp, C.POINTER(LevelSums),
+                                        C.POINTER(vp)]
     L.mlmc_sample_levels_async.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.c_uint64,
                                            C.POINTER(C.c_uint64), C.POINTER(Precision), C.POINTER(Precision), dp, dp,
                                            vp]

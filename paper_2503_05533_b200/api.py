@@ -169,6 +169,23 @@ class Context:
                 self.ctx)
         return LevelResult({f: getattr(sums, f) for f in SUM_FIELDS}, per_sample)
 
+    def sample_levels_xi(self, levels, xis, prec_fine, prec_coarse, tol_fine, tol_coarse, per_sample=None) -> list:
+        """mlmc_sample_levels_xi: all listed levels concurrently from caller-supplied normals xis[q] [n_q, m]
+        (host numpy / pinned tensors or device tensors); per_sample: None or a list of host / device
+        [n_q, 8] float64 buffers filled in place.  Returns one sums dict per entry."""
+        k = len(levels)
+        ptr = lambda a: a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+        xs = (C.c_void_p * k)(*[ptr(x) for x in xis])
+        ps = (C.c_void_p * k)(*[ptr(p) if p is not None else None for p in (per_sample or [None] * k)])
+        pf = (K.Precision * k)(*[_as_prec(p) for p in prec_fine])
+        pc = (K.Precision * k)(*[_as_prec(p) for p in prec_coarse])
+        sums = (K.LevelSums * k)()
+        rc = K.lib().mlmc_sample_levels_xi(self.ctx, k, (C.c_int * k)(*levels),
+                                           (C.c_uint64 * k)(*[int(x.shape[0]) for x in xis]), xs, pf, pc,
+                                           (C.c_double * k)(*tol_fine), (C.c_double * k)(*tol_coarse), sums, ps)
+        K.check(rc, self.ctx)
+        return [{f: getattr(sums[q], f) for f in SUM_FIELDS} for q in range(k)]
+
     def profile_enable(self, on: bool = True):
         K.check(K.lib().mlmc_profile_enable(self.ctx, 1 if on else 0), self.ctx)
 

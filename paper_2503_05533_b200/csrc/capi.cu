@@ -513,10 +513,17 @@ int mlmc_sample_level(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
     return MLMC_OK;
 }
 
-int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, uint64_t seed,
-                             const uint64_t* first_index, const mlmc_precision* prec_fine,
-                             const mlmc_precision* prec_coarse, const double* tol_fine, const double* tol_coarse,
-                             double* sums_dev) {
+}  // extern "C"
+
+namespace {
+
+// Several levels concurrently (shared by mlmc_sample_levels_async and mlmc_sample_levels_xi): xi_in[q]
+// (optional, host or device) replaces the Philox draw of entry q, per_sample[q] (optional, host or
+// device) receives its records.
+int sample_levels_impl(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, uint64_t seed,
+                       const uint64_t* first_index, const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse,
+                       const double* tol_fine, const double* tol_coarse, double* sums_dev,
+                       const double* const* xi_in = nullptr, double* const* per_sample = nullptr) {
     if (!ctx || nlev < 1 || nlev > MLMC_MAX_LEVELS || !levels || !n || !first_index || !prec_fine || !prec_coarse ||
         !tol_fine || !tol_coarse || !sums_dev)
         return fail(ctx, MLMC_EINVAL, "NULL / bad argument");
@@ -585,13 +592,42 @@ int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const u
         const bool top_single =
             max_batch(ctx, levels[order[0]], slice[order[0]], &prec_fine[order[0]], &prec_coarse[order[0]]) >= n[order[0]];
         if (!top_single) sch.prep = sch.gate = nullptr;   // the largest level runs in passes: no gate
+        const double* xq = xi_in ? xi_in[q] : nullptr;
+        double* pq = per_sample ? per_sample[q] : nullptr;
         int rc = run_level(ctx, Exec{ctx->ws + offs[q], slice[q], st}, levels[q], n[q], seed, first_index[q],
                            &prec_fine[q], &prec_coarse[q], tol_fine[q], tol_coarse[q], sums_dev + (size_t)q * kSumsLen,
-                           nullptr, false, nullptr, false, &sch);
+                           pq, pq && is_device_ptr(pq), xq, xq && is_device_ptr(xq), &sch);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->join_ev[k], st));
     }
     for (int k = 0; k < nlev; ++k) CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[k], 0));
+    return MLMC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mlmc_sample_levels_async(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, uint64_t seed,
+                             const uint64_t* first_index, const mlmc_precision* prec_fine,
+                             const mlmc_precision* prec_coarse, const double* tol_fine, const double* tol_coarse,
+                             double* sums_dev) {
+    return sample_levels_impl(ctx, nlev, levels, n, seed, first_index, prec_fine, prec_coarse, tol_fine, tol_coarse,
+                              sums_dev);
+}
+
+int mlmc_sample_levels_xi(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_t* n, const double* const* xi,
+                          const mlmc_precision* prec_fine, const mlmc_precision* prec_coarse, const double* tol_fine,
+                          const double* tol_coarse, mlmc_level_sums* out_sums, double* const* per_sample) {
+    if (!ctx || !xi || !out_sums || nlev < 1 || nlev > MLMC_MAX_LEVELS) return fail(ctx, MLMC_EINVAL, "NULL / bad argument");
+    for (int q = 0; q < nlev; ++q)
+        if (!xi[q] && n && n[q] > 0) return fail(ctx, MLMC_EINVAL, "xi[q] is NULL");
+    std::vector<uint64_t> first(nlev, 0);
+    int rc = sample_levels_impl(ctx, nlev, levels, n, 0, first.data(), prec_fine, prec_coarse, tol_fine, tol_coarse,
+                                ctx->sums_dev, xi, per_sample);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(out_sums, ctx->sums_dev, sizeof(double) * kSumsLen * nlev, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return MLMC_OK;
 }
 

@@ -362,3 +362,23 @@ def test_paper_experiment_mpml_cost_gain_without_accuracy_loss():
     diff = abs(e["mpml"]["mse"] - e["mlmc"]["mse"])
     assert diff < 3.0 * math.hypot(e["mpml"]["mse_ci95"], e["mlmc"]["mse_ci95"]) / 1.96, e
     assert e["cost_ratio_mlmc_over_mpml"] > 1.25, e
+
+
+def test_levels_xi_concurrent_equals_single_level_calls():
+    """mlmc_sample_levels_xi (all levels at once, host xi in, host records out) reproduces the per-level
+    mlmc_sample_level_xi results bit for bit (same xi, same kernels, different streams)."""
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    rng = np.random.default_rng(7)
+    ns = [700, 300, 90, 12]
+    xs = [rng.standard_normal((n, cfg["m"])) for n in ns]
+    tf = cfg["tols"]
+    tc = [tf[l - 1] if l else tf[0] for l in range(4)]
+    outs = [np.zeros((n, 8)) for n in ns]
+    sums = ctx.sample_levels_xi([0, 1, 2, 3], xs, ["minres"] * 4, ["minres"] * 4, tf, tc, per_sample=outs)
+    for l in range(4):
+        ref = np.zeros((ns[l], 8))
+        r = ctx.sample_level_xi(l, xs[l], "minres", "minres", tf[l], tc[l], per_sample=ref)
+        assert np.array_equal(ref, outs[l]), l
+        assert sums[l]["n"] == ns[l] and abs(sums[l]["sum_y"] - r.sums["sum_y"]) <= 1e-15 * abs(r.sums["sum_y"])
+    ctx.close()
