@@ -546,7 +546,7 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
                 // ---- step 4: r = b - A x in binary64 (rounded to u_s for the correction solve)
                 double part = 0.0;
                 if (active) {
-#pragma unroll 1
+#pragma unroll 4
                     for (int q = 0; q < PER; ++q) {
                         const int e = l + q * W;
                         double r = 0.0;
