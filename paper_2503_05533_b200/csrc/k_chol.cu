@@ -42,12 +42,14 @@
 //    Residual (binary64, conductances rebuilt from the triangle coefficients)
 //    and x (binary64, a per-segment global scratch, L1/L2 resident).
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -88,9 +90,40 @@ template <> struct FT<__half> {
     static __device__ __forceinline__ float rcp(__half v) { return __frcp_rn(__half2float(v)); }
     static __device__ __forceinline__ __half scale(__half a, float inv) { return __float2half_rn(__half2float(a) * inv); }
 };
+// quarter precision (NEXT-2, the paper's q43 of P:86 / R17): OCP E4M3 storage, every operation computed
+// in binary32 and rounded once to E4M3 (round to nearest even, saturating at +-448: the hardware format;
+// the SPEC's q43 saturates at 240 -- same grid below it)
+using fp8 = __nv_fp8_e4m3;
+template <> struct FT<fp8> {
+    static __device__ __forceinline__ float f(fp8 v) { return (float)v; }
+    static __device__ __forceinline__ fp8 from(double v) { return fp8((float)v); }
+    static __device__ __forceinline__ fp8 fnma(fp8 a, fp8 b, fp8 c) { return fp8(__fmaf_rn(-f(a), f(b), f(c))); }
+    static __device__ __forceinline__ fp8 sqrt_(fp8 a) { return fp8(__fsqrt_rn(f(a))); }
+    static __device__ __forceinline__ bool pos_finite(fp8 a) {
+        const float x = f(a);
+        return x > 0.0f && x < 448.0f;                 // 448 = saturated
+    }
+    static __device__ __forceinline__ float to_f(fp8 v) { return f(v); }
+    static __device__ __forceinline__ double to_d(fp8 v) { return (double)f(v); }
+    static __device__ __forceinline__ float rcp(fp8 v) { return __frcp_rn(f(v)); }
+    static __device__ __forceinline__ fp8 scale(fp8 a, float inv) { return fp8(f(a) * inv); }
+};
 // type of the reciprocal pivot used to scale a column: max(F, binary32)
 template <typename F> struct Inv { using T = F; };
 template <> struct Inv<__half> { using T = float; };
+template <> struct Inv<fp8> { using T = float; };
+
+// shuffle of a factor-format value (E4M3 through its byte)
+template <typename F>
+__device__ __forceinline__ F shfl_f(unsigned mask, F v, int src, int w) {
+    if constexpr (std::is_same_v<F, fp8>) {
+        fp8 r;
+        r.__x = (__nv_fp8_storage_t)__shfl_sync(mask, (unsigned)v.__x, src, w);
+        return r;
+    } else {
+        return __shfl_sync(mask, v, src, w);
+    }
+}
 
 // correctly rounded reciprocal in the substitution precision (R28)
 __device__ __forceinline__ float rcp_s(float x) { return __frcp_rn(x); }
@@ -212,8 +245,12 @@ constexpr int kFacWarps = 4;
 template <int N, typename F, typename S>
 struct FacCfg {
     using G = Geo<N, F, S>;
-    // shared memory per segment: two LB tiles | column buffer (2 x W entries)
-    static constexpr int OFF_C = 2 * G::BLK;
+    // binary64 factors at W = 32 keep neither the finished column entries nor the broadcast column in
+    // registers (the window alone is 64 registers): the forward layout goes through a third tile
+    static constexpr bool LIGHT = sizeof(F) == 8 && N == 32;
+    // shared memory per segment: two LB tiles | [LF tile] | column buffer (2 x W entries)
+    static constexpr int OFF_F = 2 * G::BLK;
+    static constexpr int OFF_C = (LIGHT ? 3 : 2) * G::BLK;
     static constexpr int SEG_BYTES = ((OFF_C + 2 * G::W * (int)sizeof(F) + 127) / 128) * 128;
     static constexpr int SMEM = SEG_BYTES * G::SEGS * kFacWarps;
 };
@@ -229,11 +266,12 @@ chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __re
     constexpr int W = G::W, NB = G::NB, SEGS = G::SEGS, BLK = G::BLK;
     constexpr int P = 2 * N * N;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(16) uint4 zrow[8];          // 128 zero bytes (re-initialised window rows)
+    __shared__ __align__(16) uint4 zrow[16];         // 256 zero bytes (re-initialised window rows)
+    static_assert(G::C <= 16, "zero row too short");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int seg = lane / W, l = lane % W;
     const unsigned mask = 0xffffffffu;
-    if (threadIdx.x < 8) zrow[threadIdx.x] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < 16) zrow[threadIdx.x] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     const int job = (blockIdx.x * kFacWarps + warp) * SEGS + seg;
     const bool live = job < nb;
@@ -276,13 +314,14 @@ chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __re
             wen = FT<F>::from(we);
             son = FT<F>::from(so);
         }
-        F lcol[W];
+        F lcol[K::LIGHT ? 1 : W];
+        unsigned char* TF = base + K::OFF_F;            // LF tile (LIGHT)
         S rdl = (S)0;
 #pragma unroll
         for (int u = 0; u < W; ++u) {
             const int d = (l - u) & (W - 1);          // this lane holds row k0 + u + d
             // pivot: lane u's diagonal, from the fast path of the previous step (k > 0)
-            F piv = __shfl_sync(mask, (b == 0 && u == 0) ? Rw[0] : pnext, u, W);
+            F piv = shfl_f<F>(mask, (b == 0 && u == 0) ? Rw[0] : pnext, u, W);
             if (!FT<F>::pos_finite(piv)) { ok = false; piv = FT<F>::from(1.0); }
             const F lkk = FT<F>::sqrt_(piv);
             const typename Inv<F>::T inv = FT<F>::rcp(lkk);
@@ -293,25 +332,31 @@ chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __re
             // the next pivot's update: lane u+1 squares its own column entry (the same operation the
             // rank-1 update below performs with the shared copy), off the shared-memory round trip
             pnext = FT<F>::fnma(lc, lc, Rw[(u + 1) % W]);
-            lcol[u] = lc;
+            if constexpr (K::LIGHT) *reinterpret_cast<F*>(TF + G::off(l, u)) = lc;
+            else lcol[K::LIGHT ? 0 : u] = lc;
             if (l == u) rdl = rk;
             *reinterpret_cast<F*>((l >= u ? Tc : Tn) + G::off(u, l)) = lc;
             F* cb = colbuf + (u & 1) * W;
             cb[d] = lc;
             __syncwarp(mask);
-            F cv[W];
-            if constexpr (G::C == 0) {
+            if constexpr (K::LIGHT) {
 #pragma unroll
-                for (int j = 0; j < W; ++j) cv[j] = cb[j];
+                for (int j = 1; j < W; ++j) Rw[(u + j) % W] = FT<F>::fnma(lc, cb[j], Rw[(u + j) % W]);
             } else {
+                F cv[W];
+                if constexpr (G::C == 0) {
 #pragma unroll
-                for (int i = 0; i < G::C; ++i) {
-                    const uint4 q = reinterpret_cast<const uint4*>(cb)[i];
-                    memcpy(&cv[i * G::EPC], &q, 16);
+                    for (int j = 0; j < W; ++j) cv[j] = cb[j];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < G::C; ++i) {
+                        const uint4 q = reinterpret_cast<const uint4*>(cb)[i];
+                        memcpy(&cv[i * G::EPC], &q, 16);
+                    }
                 }
-            }
 #pragma unroll
-            for (int j = 1; j < W; ++j) Rw[(u + j) % W] = FT<F>::fnma(lc, cv[j], Rw[(u + j) % W]);
+                for (int j = 1; j < W; ++j) Rw[(u + j) % W] = FT<F>::fnma(lc, cv[j], Rw[(u + j) % W]);
+            }
             if (l == u) {                              // row k0+u is done: this lane takes row k0+u+W
                 if constexpr (G::C == 0) {
 #pragma unroll
@@ -332,7 +377,8 @@ chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __re
         if (live) {
             unsigned char* gF = LF + (size_t)b * BLK;
             unsigned char* gB = LB + (size_t)b * BLK;
-            store_row<G, F>(gF, l, lcol);
+            if constexpr (K::LIGHT) copy_row<G, F>(gF, TF, l);
+            else store_row<G, F>(gF, l, lcol);
             copy_row<G, F>(gB, Tc, l);
             reinterpret_cast<S*>(gF + G::HDR)[l] = rdl;
             reinterpret_cast<S*>(gB + G::HDR)[l] = rdl;
@@ -688,17 +734,18 @@ cudaError_t with_shape(Fn&& fn) {
 // (u_f, u_s) -> instantiation; returns cudaErrorNotSupported for combinations not built.
 template <int N, class Fn>
 cudaError_t with_types(int u_f, int u_s, Fn&& fn) {
-    if (u_f == MLMC_FMT_F16) {
+    if (u_f == MLMC_FMT_E4M3) {
+        if (u_s == MLMC_FMT_F32) return with_shape<N, fp8, float>(fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, fp8, double>(fn);
+    } else if (u_f == MLMC_FMT_F16) {
         if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(fn);
         if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(fn);
     } else if (u_f == MLMC_FMT_F32) {
         if (u_s == MLMC_FMT_F32) return with_shape<N, float, float>(fn);
         if (u_s == MLMC_FMT_F64) return with_shape<N, float, double>(fn);
     } else if (u_f == MLMC_FMT_F64) {
-        if constexpr (N <= 16) {
-            if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(fn);
-            if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(fn);
-        }
+        if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(fn);
     }
     return cudaErrorNotSupported;
 }
@@ -719,9 +766,8 @@ cudaError_t with_mesh(int N, int u_f, int u_s, Fn&& fn) {
 
 bool chol_supported(int N, int u_f, int u_s) {
     if (!(N == 2 || N == 4 || N == 8 || N == 16 || N == 32)) return false;
-    if (!(u_f == MLMC_FMT_F16 || u_f == MLMC_FMT_F32 || u_f == MLMC_FMT_F64)) return false;
+    if (!(u_f == MLMC_FMT_E4M3 || u_f == MLMC_FMT_F16 || u_f == MLMC_FMT_F32 || u_f == MLMC_FMT_F64)) return false;
     if (!(u_s == MLMC_FMT_F32 || u_s == MLMC_FMT_F64)) return false;
-    if (u_f == MLMC_FMT_F64 && N == 32) return false;   // no binary64 factor on the h = 1/32 mesh
     return true;
 }
 

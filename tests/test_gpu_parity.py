@@ -382,3 +382,47 @@ def test_levels_xi_concurrent_equals_single_level_calls():
         assert np.array_equal(ref, outs[l]), l
         assert sums[l]["n"] == ns[l] and abs(sums[l]["sum_y"] - r.sums["sum_y"]) <= 1e-15 * abs(r.sums["sum_y"])
     ctx.close()
+
+
+# ============================================================================ NEXT-2: quarter / binary64 factors
+def test_quarter_precision_factor_level0_h0_quarter():
+    """The paper's last example: s = 1, sigma = 1, h0 = 1/4, quarter-precision (q43 ~ E4M3)
+    factor on level 0 with iterative refinement (here u_s = binary32, u = u_r = binary64, R14/R17).
+    IR converges to 1e-10 on every sample, Q within the residual bound of the oracle's direct solve,
+    and the oracle's emulated Algorithm 1 with a q43 factor converges on the same systems."""
+    cfg = dict(field="eq20", field_code=1, m=1, sigma2=1.0, corr_len=0.0, q_decay=2.0, h0_inv=4, L_max=3)
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    for lev, quad in ((0, "qsdd"), (1, "hsdd")):
+        prec = precision("chol_ir", quad[0], quad[1], max_iter=200)
+        r = ctx.sample_level(lev, 400, seed=21, prec_fine=prec, prec_coarse=precision("chol_ir", "q", "s", max_iter=200),
+                             tol_fine=1e-10, tol_coarse=1e-10, per_sample=True)
+        ps = r.per_sample
+        assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0), (lev, ps[:, 6:8].max())
+        assert np.all(ps[:, 4] < 1e-10)
+        Nf = 4 << lev
+        idx = list(range(0, 400, 40))
+        exs = _pmap(lambda k: _exact(P, Nf, oc.normals(21, lev, k, 1)), idx)
+        for k, (q, bn, xn) in zip(idx, exs):
+            assert abs(ps[k, 0] - q) <= 1e-10 * bn * xn * (1 + 1e-6) + 1e-14 * q
+        for k in idx[:3]:
+            o = P.solve_mesh(Nf, oc.normals(21, lev, k, 1), oc.SOLVER_IR, tol=1e-10, quad=quad, max_iter=200)
+            assert o["status"] == 0
+    ctx.close()
+
+
+def test_binary64_factor_on_the_h32_mesh():
+    """Binary64 band factor at h = 1/32 (the standard-MLMC direct solver of P:694): one refinement step
+    at most to 1e-13, Q equal to the oracle's direct solve to 1e-11 relative."""
+    cfg = W.CONFIGS["C3"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    P = _oracle(cfg)
+    prec = precision("chol_ir", "d", "d")
+    r = ctx.sample_level(2, 60, seed=4, prec_fine=prec, prec_coarse=prec, tol_fine=1e-13, tol_coarse=1e-13,
+                         per_sample=True)
+    ps = r.per_sample
+    assert r.sums["n_fail"] == 0 and ps[:, 2].max() <= 2
+    exs = _pmap(lambda k: _exact(P, 32, oc.normals(4, 2, k, cfg["m"])), list(range(0, 60, 6)))
+    for k, (q, _, _) in zip(range(0, 60, 6), exs):
+        assert abs(ps[k, 0] / q - 1) < 1e-11
+    ctx.close()
