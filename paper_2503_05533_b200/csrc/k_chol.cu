@@ -241,6 +241,9 @@ struct Coef {
 
 // ======================================================================== K4a: factorisation
 constexpr int kFacWarps = 4;
+#ifndef FAC_MINB_DEFAULT
+#define FAC_MINB_DEFAULT 4
+#endif
 
 template <int N, typename F, typename S>
 struct FacCfg {
@@ -253,12 +256,14 @@ struct FacCfg {
     static constexpr int OFF_C = (LIGHT ? 3 : 2) * G::BLK;
     static constexpr int SEG_BYTES = ((OFF_C + 2 * G::W * (int)sizeof(F) + 127) / 128) * 128;
     static constexpr int SMEM = SEG_BYTES * G::SEGS * kFacWarps;
+    // resident CTAs the register allocation is bounded for (MLMC_CHOL_FAC_MINB overrides for tuning)
+    static constexpr int MINB = sizeof(F) == 8 ? 2 : FAC_MINB_DEFAULT;
 };
 
 // Factorise samples [0, nb): factor of sample j at fac + j * FBYTES; status (0 ok, 2 breakdown) to
 // out[j*8 + 6 + slot].
 template <int N, typename F, typename S>
-__global__ void __launch_bounds__(32 * kFacWarps)
+__global__ void __launch_bounds__(32 * kFacWarps, FacCfg<N, F, S>::MINB)
 chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __restrict__ fac,
                    double* __restrict__ out, int slot) {
     using G = Geo<N, F, S>;
