@@ -62,38 +62,69 @@ def parse():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled every ~2 ms by NVML on a background thread between
+    start() and stop() -- the timed region is tens of milliseconds, far below nvidia-smi's polling
+    period.  Falls back to one nvidia-smi reading if NVML is unavailable."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.index = index
+        self.rows = []
+        self.ev = threading.Event()
+        self.th = None
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                                      stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            get = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.get_reasons = lambda: get(self.h)
         except Exception:
-            self.p = None
-        t0 = time.time()
-        while self.p and time.time() - t0 < 5 and os.path.getsize(self.f.name) == 0:
-            time.sleep(0.05)
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        while not self.ev.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), self.get_reasons()))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.nv:
+            self.rows = []
+            self.ev.clear()
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
 
     def stop(self) -> dict:
-        if self.p:
-            self.p.terminate()
-            self.p.wait()
-        rows = []
-        for ln in open(self.f.name):
-            v = [x.strip() for x in ln.split(",")]
-            if len(v) >= 7 and v[0].isdigit():
-                rows.append(v)
-        os.unlink(self.f.name)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = sorted(int(r[0]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons, "samples": len(rows)}
+        if not self.nv:
+            return self._smi_once()
+        self.ev.set()
+        if self.th:
+            self.th.join()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "source": "nvml"}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({name for _, mask in self.rows for name, const in self.REASONS
+                          if mask & getattr(self.nv, const, 0)})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml, every 2 ms during the timed steps"}
+
+    def _smi_once(self) -> dict:
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True).stdout
+            a, b = [int(x) for x in out.strip().split(",")[:2]]
+            return {"sm_mhz": a, "sm_max_mhz": b, "reasons": [], "samples": 1, "source": "nvidia-smi (no NVML)"}
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"], "samples": 0}
 
 
 # ----------------------------------------------------------------------------- oracle timing
@@ -200,6 +231,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     ctx.profile_enable(False)             # reset the per-kernel table: launch counts only (no event overhead)
+    clocks.start()
     total_ms = 0.0
     iters_f = [0.0] * L
     iters_c = [0.0] * L
@@ -217,6 +249,7 @@ def run_ours(args):
             iters_f[l] += s[l, 7] / world
             iters_c[l] += s[l, 8] / world
     torch.cuda.synchronize()
+    clk = clocks.stop()
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -224,7 +257,6 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     gpu_launches = int(sum(r[2] for r in ctx.profile_read()))
-    clk = clocks.stop()
 
     # per-level throughput: each level alone (same launch path), CUDA events, L2 flushed before each;
     # the library brackets every kernel with events here (serialised kernels: clean per-kernel times)
