@@ -227,43 +227,59 @@ __global__ void __launch_bounds__(256) field_dmma_kernel(const double* __restric
     }
 }
 
-// Longest-first order: one CTA of 1024 threads sorts (contrast, index) pairs of nb <= kOrderMax
-// systems by descending contrast (bitonic network in shared memory; ties by ascending index).
+// Longest-first order: one CTA of 1024 threads buckets the nb <= kOrderMax systems by log contrast
+// (256 buckets between the batch's extremes, highest contrast first) -- a counting sort, four barriers,
+// instead of a comparison sort: the schedule only needs the long solves early, and the order within
+// a bucket (atomic placement) does not change any result (every system is solved independently).
 __global__ void __launch_bounds__(1024) order_kernel(const unsigned long long* __restrict__ keys, int nb,
                                                      int* __restrict__ order) {
-    __shared__ double sk[kOrderMax];
-    __shared__ int si[kOrderMax];
-    int n2 = 1;
-    while (n2 < nb) n2 <<= 1;
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        if (i < nb) {
-            const double mx = __longlong_as_double((long long)keys[2 * i]);
-            const double mn = __longlong_as_double((long long)~keys[2 * i + 1]);
-            sk[i] = mn > 0.0 ? mx / mn : DBL_MAX;
-        } else {
-            sk[i] = -1.0;                             // padding sorts last
-        }
-        si[i] = i;
+    constexpr int NBK = 256;
+    __shared__ float lk[kOrderMax];
+    __shared__ int cnt[NBK], pos[NBK];
+    __shared__ float red_lo[32], red_hi[32];
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const double mx = __longlong_as_double((long long)keys[2 * i]);
+        const double mn = __longlong_as_double((long long)~keys[2 * i + 1]);
+        const float v = (mn > 0.0 && mx >= mn) ? (float)log(mx / mn) : 1e30f;
+        lk[i] = v;
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+    if (threadIdx.x < NBK) cnt[threadIdx.x] = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) { red_lo[threadIdx.x >> 5] = lo; red_hi[threadIdx.x >> 5] = hi; }
+    __syncthreads();
+    lo = red_lo[0];
+    hi = red_hi[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fminf(lo, red_lo[w]); hi = fmaxf(hi, red_hi[w]); }
+    const float scale = hi > lo ? (NBK - 1) / (hi - lo) : 0.0f;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int bk = (NBK - 1) - min(NBK - 1, max(0, (int)((lk[i] - lo) * scale)));   // 0 = highest contrast
+        lk[i] = __int_as_float(bk);
+        atomicAdd(&cnt[bk], 1);
     }
     __syncthreads();
-    for (int k = 2; k <= n2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    // descending by key inside blocks with (i & k) == 0, ascending otherwise
-                    const bool before = sk[i] > sk[ixj] || (sk[i] == sk[ixj] && si[i] < si[ixj]);
-                    const bool desc = (i & k) == 0;
-                    if (desc != before) {
-                        const double tk = sk[i]; sk[i] = sk[ixj]; sk[ixj] = tk;
-                        const int ti = si[i]; si[i] = si[ixj]; si[ixj] = ti;
-                    }
-                }
-            }
-            __syncthreads();
+    if (threadIdx.x < 32) {                            // exclusive prefix sum of the 256 counts (one warp)
+        int v[NBK / 32], run = 0;
+#pragma unroll
+        for (int j = 0; j < NBK / 32; ++j) { v[j] = cnt[threadIdx.x * (NBK / 32) + j]; run += v[j]; }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)threadIdx.x >= o) incl += t;
         }
+        int base = incl - run;
+#pragma unroll
+        for (int j = 0; j < NBK / 32; ++j) { pos[threadIdx.x * (NBK / 32) + j] = base; base += v[j]; }
     }
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) order[i] = si[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) order[atomicAdd(&pos[__float_as_int(lk[i])], 1)] = i;
 }
 
 cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cudaStream_t s) {
