@@ -440,3 +440,44 @@ def test_paper_direct_solver_experiment_same_samples():
     for k, e in res["tol2"].items():
         assert e["mse_rel_diff"] < 1e-3, (k, e["mse_rel_diff"])
         assert e["memory_gain_total"] > 1.5 and e["k4_hbm_gain_total"] > 1.5, (k, e)
+
+
+def test_streamed_minres_edge_cases_and_order_invariance():
+    """K3c with fewer systems than SMs, one system, and a batch just over one wave; the longest-first
+    job order (C2 level 3, the tile kernel) changes no per-sample result: the same samples drawn one
+    at a time (no ordering: a single system) and in a batch agree bit for bit."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=2 << 30)
+    mr = precision("minres", max_iter=400)
+    for n in (0, 1, 3, 150):
+        r = ctx.sample_level(4, n, seed=2, prec_fine=mr, prec_coarse=mr, tol_fine=1e-6, tol_coarse=1e-6,
+                             per_sample=True)
+        assert r.sums["n"] == n
+        if n:
+            one = ctx.sample_level(4, 1, seed=2, first_index=n - 1, prec_fine=mr, prec_coarse=mr, tol_fine=1e-6,
+                                   tol_coarse=1e-6, per_sample=True).per_sample
+            assert np.array_equal(one[0], r.per_sample[n - 1])
+    ctx.close()
+    c2 = W.CONFIGS["C2"]
+    ctx = _ctx(c2, ws=1 << 30)
+    batch = ctx.sample_level(3, 40, seed=9, prec_fine=mr, prec_coarse=mr, tol_fine=1e-7, tol_coarse=1e-6,
+                             per_sample=True).per_sample
+    for k in (0, 17, 39):
+        one = ctx.sample_level(3, 1, seed=9, first_index=k, prec_fine=mr, prec_coarse=mr, tol_fine=1e-7,
+                               tol_coarse=1e-6, per_sample=True).per_sample
+        assert np.array_equal(one[0], batch[k]), k
+    ctx.close()
+
+
+def test_adaptive_run_counts_failed_solves_on_gpu():
+    """R15 on the GPU path: Cholesky-IR with an fp16 factor (policy 1, Table 1) cannot reach 1e-15
+    (limiting accuracy, Corollary 3.3); on_fail = 0 stops with a solver error, on_fail = 1 finishes
+    and reports the failures."""
+    cfg = W.CONFIGS["C4"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    with pytest.raises(RuntimeError, match="solver failure"):
+        ctx.adaptive_run(cfg["eps"], k_p=0.0, fixed_tol=1e-15, N_init=20, seed=3, max_rounds=3, policy=1)
+    r = ctx.adaptive_run(cfg["eps"], k_p=0.0, fixed_tol=1e-15, N_init=20, seed=3, max_rounds=3, policy=1,
+                       on_fail=1)
+    assert r["n_fail"] > 0
+    ctx.close()
