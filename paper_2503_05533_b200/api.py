@@ -27,7 +27,7 @@ def precision(solver: str = "minres", u_f: str = "s", u_s: str = "s", u: str = "
               max_iter: int = 0, verify: bool = False) -> K.Precision:
     """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad.
     verify=True (MINRES): also carry x_k and report the true residual."""
-    s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR}[solver]
+    s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR, "mgcg": K.SOLVER_MGCG}[solver]
     return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter, K.FLAG_VERIFY if verify else 0)
 
 
@@ -37,8 +37,8 @@ def _as_prec(p) -> K.Precision:
     if isinstance(p, K.Precision):
         return p
     if isinstance(p, str):
-        if p == "minres":
-            return precision("minres")
+        if p in ("minres", "mgcg"):
+            return precision(p)
         # quad string like "hsdd": Cholesky-IR (u_f, u_s, u, u_r)
         return precision("chol_ir", p[0], p[1], p[2], p[3])
     raise TypeError(p)

@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["host_kl.cpp", "capi.cu", "controller.cpp", "k_field.cu", "k_minres.cu", "k_minres_tile.cu", "k_minres_gm.cu", "k_minres_stream.cu", "k_chol.cu",
+SOURCES = ["host_kl.cpp", "capi.cu", "controller.cpp", "k_field.cu", "k_minres.cu", "k_minres_tile.cu", "k_minres_gm.cu", "k_minres_stream.cu", "k_mgcg.cu", "k_chol.cu",
            "k_reduce.cu"]
 
 

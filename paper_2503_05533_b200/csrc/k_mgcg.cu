@@ -1,0 +1,458 @@
+// k_mgcg.cu -- K3m: multigrid-preconditioned conjugate gradients for the on-chip meshes (NEXT-4).
+//
+// SURVEY section 8(f) NEXT-4 ("multigrid-preconditioned Krylov, the optimal solver, gamma = 2",
+// P:439): the same P1 system A x = b (R10) and the same accuracy contract as the paper's
+// MINRES -- stop at the first k with ||r_k||_2 / ||b||_2 <= tol (the relative residual of Eq. (2),
+// P:70-73, R9; r_k the CG recurrence residual) -- solved by preconditioned CG in binary64 with one
+// symmetric V(1,1) cycle in binary32 as the preconditioner.  The QoI is carried as
+// 1^T x_k = sum_i alpha_i 1^T p_i (a scalar, no x vector; cf. R26).
+//
+// Hierarchy: the P1 meshes are nested (h, 2h, ..., 1/2).  P = P1 interpolation on the coarse
+// triangles (a fine node on a coarse horizontal, vertical or SW-NE diagonal edge takes the mean of its
+// two endpoints), restriction = P^T, and the coarse operators are Galerkin-exact: for piecewise-
+// constant coefficients P^T A_h P is the P1 stiffness of the coarse mesh whose triangle coefficients
+// are the means of the four fine triangles inside each coarse triangle (the coarse basis functions
+// are linear on the coarse triangle), so every level is again R10's 5-point conductance operator.
+// Smoother: red-black Gauss-Seidel, red then black before the coarse correction, black then red
+// after (symmetric: M^-1 is SPD, CG applies); the single unknown of the h = 1/2 level is solved
+// exactly.
+//
+// B200 mapping: a group of T threads per system (persistent CTAs, job counter), every grid of the
+// system in shared memory (binary64: p and the fine conductances; binary32: u, f, residual and the
+// conductances of every level), r and A p in registers (thread-strided nodes); two fused reductions
+// per CG step.
+#include <cuda_runtime.h>
+#include <cfloat>
+#include <cstdint>
+#include <cstdio>
+
+#include "internal.h"
+
+namespace mlmc {
+namespace {
+
+template <int N, int T, int GROUPS_>
+struct MgCfg {
+    static constexpr int GROUPS = GROUPS_;
+    static constexpr int BLOCK = T * GROUPS;
+    static constexpr int C = N - 1;
+    static constexpr int n = C * C;
+    static constexpr int PER = (n + T - 1) / T;                // fine nodes per thread
+    static constexpr int G = N + 1;                            // grid side, Dirichlet ring included
+    static constexpr int LV = __builtin_ctz(N);                // levels N, N/2, ..., 2
+    static constexpr int D_P = 0, D_CE = G * G, D_CN = 2 * G * G, D_END = 3 * G * G;   // binary64 grids
+    static __host__ __device__ constexpr int gl(int l) { return (N >> l) + 1; }
+    // binary32 grids per level l: u, f, t, cE, cN (gl(l)^2 floats each)
+    static __host__ __device__ constexpr int foff(int l) {
+        int o = 0;
+        for (int k = 0; k < l; ++k) o += 5 * gl(k) * gl(k);
+        return o;
+    }
+    static constexpr int F_END = (foff(LV) + 3) / 4 * 4;       // keeps what follows 16-byte aligned
+    static constexpr int NW = T >= 32 ? T / 32 : 1;
+    static constexpr size_t SYS = (((size_t)D_END * 8 + (size_t)F_END * 4 + (size_t)2 * NW * 8 + 16) + 127) / 128 * 128;
+    static constexpr size_t SMEM = SYS * GROUPS;
+    static_assert((N & (N - 1)) == 0 && N >= 4, "power-of-two mesh");
+};
+
+template <int T, int GROUPS>
+__device__ __forceinline__ void gsync(int g) {
+    if constexpr (T < 32) __syncwarp(0xffffu << (threadIdx.x & 16));
+    else if constexpr (T == 32) __syncwarp();
+    else if constexpr (GROUPS == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(T) : "memory");
+}
+
+// sums of (a, b) over the group's threads, identical in every thread (fixed order)
+template <int T, int GROUPS>
+__device__ __forceinline__ double2 gsum2(double a, double b, double* red, int tg, int g) {
+    constexpr int W = T >= 32 ? 32 : T;
+    const unsigned msk = T >= 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(msk, a, o, W);
+        b += __shfl_xor_sync(msk, b, o, W);
+    }
+    if constexpr (T <= 32) {
+        return make_double2(a, b);
+    } else {
+        constexpr int NW = T / 32;
+        gsync<T, GROUPS>(g);                                   // previous readers of red are done
+        if ((tg & 31) == 0) { red[2 * (tg >> 5)] = a; red[2 * (tg >> 5) + 1] = b; }
+        gsync<T, GROUPS>(g);
+        double sa = red[0], sb = red[1];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) { sa += red[2 * w]; sb += red[2 * w + 1]; }
+        return make_double2(sa, sb);
+    }
+}
+
+struct Lvl {             // one level's binary32 grids (side Gl = Nl + 1, node (i, j) at j * Gl + i)
+    float *u, *f, *t, *ce, *cn;
+    int Nl, Gl;
+};
+
+// red-black Gauss-Seidel sweep over the interior nodes of colour `col` ((i + j) % 2 == col):
+// rows come in pairs holding C nodes of each colour (C = Nl - 1 is odd)
+template <int T, int GROUPS>
+__device__ __forceinline__ void rbgs(const Lvl& L, int col, int tg, int g) {
+    const int C = L.Nl - 1;
+    for (int q = tg; q < ((C + 1) / 2) * C; q += T) {
+        const int pr = q / C, w = q % C;
+        int j = 2 * pr + 1;
+        int i0 = ((1 + j) & 1) == col ? 1 : 2;
+        const int n1 = (C - i0) / 2 + 1;
+        int i = i0 + 2 * w;
+        if (w >= n1) {
+            ++j;
+            if (j > C) continue;
+            i0 = ((1 + j) & 1) == col ? 1 : 2;
+            i = i0 + 2 * (w - n1);
+        }
+        const int c = j * L.Gl + i;
+        const float ce = L.ce[c], cw = L.ce[c - 1], cn = L.cn[c], cs = L.cn[c - L.Gl];
+        float s = L.f[c];
+        s = fmaf(ce, L.u[c + 1], s);
+        s = fmaf(cw, L.u[c - 1], s);
+        s = fmaf(cn, L.u[c + L.Gl], s);
+        s = fmaf(cs, L.u[c - L.Gl], s);
+        L.u[c] = s / ((ce + cw) + (cn + cs));
+    }
+    gsync<T, GROUPS>(g);
+}
+
+// conductances of a level from its triangle coefficients (aL at t[c], aU at f[c] for cell (i, j),
+// c = j * Gl + i): cE(i,j) = (aL(i,j) + aU(i,j-1))/2, cN(i,j) = (aU(i,j) + aL(i-1,j))/2 (R10)
+template <int T, int GROUPS>
+__device__ __forceinline__ void level_conductances(const Lvl& L, int tg, int g) {
+    const int Nl = L.Nl, Gl = L.Gl;
+    for (int c = tg; c < Gl * Gl; c += T) {
+        const int i = c % Gl, j = c / Gl;
+        L.ce[c] = (i < Nl && j >= 1 && j < Nl) ? 0.5f * (L.t[c] + L.f[c - Gl]) : 0.0f;
+        L.cn[c] = (i >= 1 && i < Nl && j < Nl) ? 0.5f * (L.f[c] + L.t[c - 1]) : 0.0f;
+    }
+    gsync<T, GROUPS>(g);
+}
+
+#ifndef MG_SMALL
+#define MG_SMALL 8    // levels of side < MG_SMALL run on one warp
+#endif
+// ---- compile-time level operations.  A level of side NL is processed by NT threads (the whole group
+// on the big levels; one warp once NL <= 16, synchronised by __syncwarp) -- every loop bound and
+// index division is a compile-time constant.
+template <int NT, int T, int GROUPS>
+__device__ __forceinline__ void lsync(int g) {
+    if constexpr (NT == T) gsync<T, GROUPS>(g);
+    else __syncwarp();
+}
+
+template <int NL, int NT, int T, int GROUPS>
+__device__ __forceinline__ void l_rbgs(const Lvl& L, int col, int tg, int g) {
+    constexpr int C = NL - 1, GL = NL + 1;
+    for (int q = tg; q < ((C + 1) / 2) * C; q += NT) {
+        const int pr = q / C, w = q % C;
+        int j = 2 * pr + 1;
+        int i0 = ((1 + j) & 1) == col ? 1 : 2;
+        const int n1 = (C - i0) / 2 + 1;
+        int i = i0 + 2 * w;
+        if (w >= n1) {
+            ++j;
+            if (j > C) continue;
+            i0 = ((1 + j) & 1) == col ? 1 : 2;
+            i = i0 + 2 * (w - n1);
+        }
+        const int c = j * GL + i;
+        const float ce = L.ce[c], cw = L.ce[c - 1], cn = L.cn[c], cs = L.cn[c - GL];
+        float s = L.f[c];
+        s = fmaf(ce, L.u[c + 1], s);
+        s = fmaf(cw, L.u[c - 1], s);
+        s = fmaf(cn, L.u[c + GL], s);
+        s = fmaf(cs, L.u[c - GL], s);
+        L.u[c] = __fdividef(s, (ce + cw) + (cn + cs));
+    }
+    lsync<NT, T, GROUPS>(g);
+}
+
+// levels of side NL: [u | f | t | cE | cN] at fb + offset, offsets of the halving sequence N, N/2, ...
+template <int N, int NL>
+__device__ __forceinline__ Lvl lvl_at(float* fb) {
+    int off = 0;
+#pragma unroll
+    for (int k = N; k > NL; k >>= 1) off += 5 * (k + 1) * (k + 1);
+    constexpr int sz = (NL + 1) * (NL + 1);
+    float* b0 = fb + off;
+    return Lvl{b0, b0 + sz, b0 + 2 * sz, b0 + 3 * sz, b0 + 4 * sz, NL, NL + 1};
+}
+
+// V(1,1) cycle from level NL down (u_NL = M^-1 f_NL; u starts at 0)
+template <int N, int NL, int T, int GROUPS>
+__device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
+    constexpr int NT = NL >= MG_SMALL ? T : (T >= 32 ? 32 : T);
+    constexpr int GL = NL + 1, C = NL - 1;
+    const Lvl L = lvl_at<N, NL>(fb);
+    if (NT != T && tg >= NT) return;                    // small levels: one warp
+    for (int c = tg; c < GL * GL; c += NT) L.u[c] = 0.0f;
+    lsync<NT, T, GROUPS>(g);
+    if constexpr (NL == 2) {                            // one unknown: exact
+        if (tg == 0) {
+            constexpr int c = GL + 1;
+            L.u[c] = L.f[c] / ((L.ce[c] + L.ce[c - 1]) + (L.cn[c] + L.cn[c - GL]));
+        }
+        lsync<NT, T, GROUPS>(g);
+    } else {
+        l_rbgs<NL, NT, T, GROUPS>(L, 0, tg, g);
+        l_rbgs<NL, NT, T, GROUPS>(L, 1, tg, g);
+        for (int e = tg; e < C * C; e += NT) {         // t = f - A u
+            const int c = (e / C + 1) * GL + (e % C + 1);
+            const float ce = L.ce[c], cw = L.ce[c - 1], cn = L.cn[c], cs = L.cn[c - GL];
+            float Au = ((ce + cw) + (cn + cs)) * L.u[c];
+            Au = fmaf(-ce, L.u[c + 1], Au);
+            Au = fmaf(-cw, L.u[c - 1], Au);
+            Au = fmaf(-cn, L.u[c + GL], Au);
+            Au = fmaf(-cs, L.u[c - GL], Au);
+            L.t[c] = L.f[c] - Au;
+        }
+        lsync<NT, T, GROUPS>(g);
+        // f_{NL/2} = P^T t: coarse (I, J) gathers fine (2I, 2J) with weight 1 and its E, W, N, S, NE, SW
+        // neighbours with weight 1/2 (P1 prolongation on SW-NE triangles)
+        constexpr int NC = NL / 2, GC = NC + 1, CC = NC - 1;
+        const Lvl Cv = lvl_at<N, NC>(fb);
+        for (int e = tg; e < GC * GC; e += NT) {
+            const int I = e % GC, J = e / GC;
+            float v = 0.0f;
+            if (I >= 1 && I <= CC && J >= 1 && J <= CC) {
+                const int c = (2 * J) * GL + 2 * I;
+                v = L.t[c] + 0.5f * ((L.t[c + 1] + L.t[c - 1]) + (L.t[c + GL] + L.t[c - GL]) +
+                                     (L.t[c + GL + 1] + L.t[c - GL - 1]));
+            }
+            Cv.f[e] = v;
+        }
+        lsync<NT, T, GROUPS>(g);
+        vcyc<N, NC, T, GROUPS>(fb, tg, g);
+        if constexpr (NT == T && NC < MG_SMALL && T > 32) gsync<T, GROUPS>(g);   // the warp's small levels are done
+        for (int e = tg; e < C * C; e += NT) {         // u += P u_{NL/2}
+            const int i = e % C + 1, j = e / C + 1, c = j * GL + i;
+            const int I = i >> 1, J = j >> 1;
+            const float* U = Cv.u;
+            float v;
+            if (!(i & 1) && !(j & 1)) v = U[J * GC + I];
+            else if ((i & 1) && !(j & 1)) v = 0.5f * (U[J * GC + I] + U[J * GC + I + 1]);
+            else if (!(i & 1) && (j & 1)) v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I]);
+            else v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I + 1]);                // SW-NE diagonal
+            L.u[c] += v;
+        }
+        lsync<NT, T, GROUPS>(g);
+        l_rbgs<NL, NT, T, GROUPS>(L, 1, tg, g);
+        l_rbgs<NL, NT, T, GROUPS>(L, 0, tg, g);
+    }
+}
+
+template <int N, int T, int GROUPS>
+__global__ void __launch_bounds__(MgCfg<N, T, GROUPS>::BLOCK)
+mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
+            unsigned* __restrict__ job_counter, const int* __restrict__ order) {
+    using K = MgCfg<N, T, GROUPS>;
+    constexpr int G = K::G, C = K::C, n = K::n, PER = K::PER, LV = K::LV, P = 2 * N * N;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int g = threadIdx.x / T, tg = threadIdx.x % T;
+    unsigned char* base = smem + (size_t)g * K::SYS;
+    double* dg = reinterpret_cast<double*>(base);
+    double* pg = dg + K::D_P;
+    double* cE = dg + K::D_CE;
+    double* cN = dg + K::D_CN;
+    float* fb = reinterpret_cast<float*>(dg + K::D_END);
+    double* red = reinterpret_cast<double*>(fb + K::F_END);
+    int* jobslot = reinterpret_cast<int*>(red + 2 * K::NW);
+    const double h = 1.0 / N, h2 = h * h;
+
+    // the thread's fine interior nodes: e = tg + k T, (i, j) = (e % C + 1, e / C + 1)
+    auto cidx = [&](int k) {
+        const int e = tg + k * T;
+        return (e / C + 1) * G + (e % C + 1);
+    };
+    auto live = [&](int k) { return tg + k * T < n; };
+
+    // level l's grids (runtime l)
+    auto level = [&](int l) {
+        int off = 0;
+        for (int k = 0; k < l; ++k) off += 5 * K::gl(k) * K::gl(k);
+        const int gl = K::gl(l), sz = gl * gl;
+        float* b0 = fb + off;
+        return Lvl{b0, b0 + sz, b0 + 2 * sz, b0 + 3 * sz, b0 + 4 * sz, N >> l, gl};
+    };
+
+    auto vcycle = [&]() {
+        vcyc<N, N, T, GROUPS>(fb, tg, g);
+        if constexpr (N < MG_SMALL && T > 32) gsync<T, GROUPS>(g);
+    };
+
+    for (;;) {
+        if (tg == 0) jobslot[0] = (int)atomicAdd(job_counter, 1u);
+        gsync<T, GROUPS>(g);
+        const int job = jobslot[0];
+        gsync<T, GROUPS>(g);
+        if (job >= nb) break;
+        const int sj = order ? __ldg(order + job) : job;
+        const double* a = a_all + (size_t)sj * P;
+
+        // ---- set-up: binary64 fine conductances, binary32 triangle coefficients of every level
+        const Lvl L0 = level(0);
+        for (int c = tg; c < G * G; c += T) {
+            const int i = c % G, j = c / G;
+            cE[c] = (i < N && j >= 1 && j < N) ? 0.5 * (__ldg(a + 2 * (j * N + i)) + __ldg(a + 2 * ((j - 1) * N + i) + 1)) : 0.0;
+            cN[c] = (i >= 1 && i < N && j < N) ? 0.5 * (__ldg(a + 2 * (j * N + i) + 1) + __ldg(a + 2 * (j * N + i - 1))) : 0.0;
+            pg[c] = 0.0;
+            const bool cell = i < N && j < N;
+            L0.t[c] = cell ? (float)__ldg(a + 2 * (j * N + i)) : 0.0f;          // aL of cell (i, j)
+            L0.f[c] = cell ? (float)__ldg(a + 2 * (j * N + i) + 1) : 0.0f;      // aU
+            L0.ce[c] = (float)cE[c];
+            L0.cn[c] = (float)cN[c];
+        }
+        gsync<T, GROUPS>(g);
+        for (int l = 1; l < LV; ++l) {
+            // coarse lower triangle of cell (I, J) = mean of fine L(2I,2J), L(2I+1,2J), U(2I+1,2J),
+            // L(2I+1,2J+1); upper = mean of U(2I,2J), L(2I,2J+1), U(2I,2J+1), U(2I+1,2J+1)
+            const Lvl F = level(l - 1);
+            const Lvl Cv = level(l);
+            const int Gf = F.Gl, Gc = Cv.Gl, Nc = Cv.Nl;
+            for (int e = tg; e < Gc * Gc; e += T) {
+                const int I = e % Gc, J = e / Gc;
+                float aL = 0.0f, aU = 0.0f;
+                if (I < Nc && J < Nc) {
+                    const int c = (2 * J) * Gf + 2 * I;
+                    aL = 0.25f * ((F.t[c] + F.t[c + 1]) + (F.f[c + 1] + F.t[c + Gf + 1]));
+                    aU = 0.25f * ((F.f[c] + F.t[c + Gf]) + (F.f[c + Gf] + F.f[c + Gf + 1]));
+                }
+                Cv.t[e] = aL;
+                Cv.f[e] = aU;
+            }
+            gsync<T, GROUPS>(g);
+            level_conductances<T, GROUPS>(Cv, tg, g);
+        }
+
+        // ---- PCG from x0 = 0: r = b, z = M^-1 r, p = z
+        double r[PER], q[PER];
+        double rr = 0.0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            r[k] = live(k) ? h2 : 0.0;
+            if (live(k)) L0.f[cidx(k)] = (float)h2;
+            rr = fma(r[k], r[k], rr);
+        }
+        gsync<T, GROUPS>(g);
+        vcycle();
+        double rz = 0.0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            if (live(k)) {
+                const double z = (double)L0.u[cidx(k)];
+                pg[cidx(k)] = z;
+                rz = fma(r[k], z, rz);
+            }
+        double2 S = gsum2<T, GROUPS>(rz, rr, red, tg, g);
+        rz = S.x;
+        const double bnorm = sqrt(S.y);
+        const double tol_b = tol * bnorm;
+        double Xq = 0.0, rnorm = bnorm;
+        int it = 0, status = 1;
+        if (bnorm == 0.0) status = 0;
+        while (status == 1 && it < max_iter) {
+            // q = A p (binary64), p.q and 1^T p
+            double pq = 0.0, sp = 0.0;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                q[k] = 0.0;
+                if (live(k)) {
+                    const int c = cidx(k);
+                    const double ce = cE[c], cw = cE[c - 1], cn = cN[c], cs = cN[c - G];
+                    const double pv = pg[c];
+                    double Ap = ((ce + cw) + (cn + cs)) * pv;
+                    Ap = fma(-ce, pg[c + 1], Ap);
+                    Ap = fma(-cw, pg[c - 1], Ap);
+                    Ap = fma(-cn, pg[c + G], Ap);
+                    Ap = fma(-cs, pg[c - G], Ap);
+                    q[k] = Ap;
+                    pq = fma(pv, Ap, pq);
+                    sp += pv;
+                }
+            }
+            S = gsum2<T, GROUPS>(pq, sp, red, tg, g);
+            const double alpha = rz / S.x;
+            Xq = fma(alpha, S.y, Xq);                          // 1^T x += alpha 1^T p
+            rr = 0.0;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                r[k] = fma(-alpha, q[k], r[k]);
+                if (live(k)) L0.f[cidx(k)] = (float)r[k];
+                rr = fma(r[k], r[k], rr);
+            }
+            ++it;
+            gsync<T, GROUPS>(g);
+            vcycle();
+            double rz_new = 0.0;
+            double zk[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                zk[k] = live(k) ? (double)L0.u[cidx(k)] : 0.0;
+                rz_new = fma(r[k], zk[k], rz_new);
+            }
+            S = gsum2<T, GROUPS>(rz_new, rr, red, tg, g);
+            rnorm = sqrt(S.y);
+            if (!(rnorm == rnorm)) { status = 3; break; }
+            if (rnorm <= tol_b) { status = 0; break; }         // ||r_k|| / ||b|| <= tol
+            const double beta = S.x / rz;
+            rz = S.x;
+#pragma unroll
+            for (int k = 0; k < PER; ++k)
+                if (live(k)) pg[cidx(k)] = fma(beta, pg[cidx(k)], zk[k]);
+            gsync<T, GROUPS>(g);
+        }
+        if (tg == 0) {
+            double* o = out + (size_t)sj * kRecLen;
+            o[0 + slot] = h2 * Xq;
+            o[2 + slot] = (double)it;
+            o[4 + slot] = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+            o[6 + slot] = (double)status;
+        }
+        gsync<T, GROUPS>(g);
+    }
+}
+
+template <int N, int T, int GROUPS>
+cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
+                   const int* order, cudaStream_t s) {
+    using K = MgCfg<N, T, GROUPS>;
+    auto kern = mgcg_kernel<N, T, GROUPS>;
+    static int bps = -1, sms = 0;
+    if (bps < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, K::BLOCK, K::SMEM);
+        if (e != cudaSuccess) return e;
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (bps < 1) { bps = -1; return cudaErrorInvalidConfiguration; }
+    }
+    const uint64_t grid = std::min<uint64_t>((nb + GROUPS - 1) / GROUPS, (uint64_t)bps * sms);
+    if (grid == 0) return cudaSuccess;
+    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool mgcg_supported(int N) { return N == 8 || N == 16 || N == 32 || N == 64; }
+
+cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                        unsigned* ctr, const int* order, cudaStream_t s) {
+    switch (N) {
+        case 8: return run_mg<8, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        case 16: return run_mg<16, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        case 32: return run_mg<32, 128, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        case 64: return run_mg<64, 256, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace mlmc

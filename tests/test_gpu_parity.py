@@ -481,3 +481,29 @@ def test_adaptive_run_counts_failed_solves_on_gpu():
                        on_fail=1)
     assert r["n_fail"] > 0
     ctx.close()
+
+
+# ============================================================================ NEXT-4: MG-PCG
+@pytest.mark.parametrize("level,tol", [(0, 1e-10), (1, 1e-8), (2, 1e-6), (3, 1e-10)])
+def test_mgcg_within_residual_bound(level, tol):
+    """K3m (multigrid-preconditioned CG, same stopping rule ||r||/||b|| <= tol): per-sample Q within the
+    rigorous bound of the oracle's direct solve, fine and coarse halves; iteration counts mesh-
+    independent (<= 20 at every level, MINRES needs 25..600)."""
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    n = {0: 200, 1: 100, 2: 40, 3: 12}[level]
+    r = ctx.sample_level(level, n, seed=13, prec_fine=precision("mgcg"), prec_coarse=precision("mgcg"),
+                         tol_fine=tol, tol_coarse=tol, per_sample=True)
+    ps = r.per_sample
+    assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
+    assert ps[:, 2].max() <= 20 and np.all(ps[:, 4] <= tol)
+    Nf = 8 << level
+    idx = list(range(0, n, max(1, n // 6)))
+    exs = _pmap(lambda k: (_exact(P, Nf, oc.normals(13, level, k, cfg["m"])),
+                           _exact(P, Nf // 2, oc.normals(13, level, k, cfg["m"])) if level else None), idx)
+    for k, (f, c) in zip(idx, exs):
+        assert abs(ps[k, 0] - f[0]) <= tol * f[1] * f[2] * (1 + 1e-6) + 1e-14 * f[0], (level, k)
+        if c is not None:
+            assert abs(ps[k, 1] - c[0]) <= tol * c[1] * c[2] * (1 + 1e-6) + 1e-14 * c[0]
+    ctx.close()

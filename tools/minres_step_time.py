@@ -12,10 +12,11 @@ import workloads as W  # noqa: E402
 from paper_2503_05533_b200 import Context, precision  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 400
+solver = sys.argv[2] if len(sys.argv) > 2 else "minres"
 cfg = W.CONFIGS["C2"]
 ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=8, L_max=3,
               device=0, workspace_bytes=2 << 30)
-pr = precision("minres", max_iter=steps)
+pr = precision(solver, max_iter=steps)
 sums = torch.zeros(12, dtype=torch.float64, device="cuda")
 for level, nb in ((0, 148 * 32), (1, 148 * 4 * 3), (2, 148 * 3), (3, 148)):
     N = 8 << level
@@ -26,6 +27,6 @@ for level, nb in ((0, 148 * 32), (1, 148 * 4 * 3), (2, 148 * 3), (3, 148)):
     ctx.profile_enable(False)
     ms = sum(r[3] for r in prof if r[0] == "minres" and r[1] == N)
     n = (N - 1) ** 2
-    print(json.dumps({"N": N, "systems": nb, "steps": steps, "us_per_step": ms * 1e3 / steps,
+    print(json.dumps({"solver": solver, "N": N, "systems": nb, "steps": steps, "us_per_step": ms * 1e3 / steps,
                       "alg_tflops": 25.0 * n * nb * steps / (ms / 1e3) / 1e12}), flush=True)
 ctx.close()
