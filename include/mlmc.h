@@ -80,10 +80,11 @@ typedef struct {
  *   u_f (MLMC_FMT_F16 / F32 / F64), initial and correction substitutions in
  *   u_s (F32 or F64, R24), residual in u_r and x in u (both F64), stop when
  *   ||r||/||b|| < tol, at most max_iter refinement steps.
- * solver = MLMC_SOLVER_MGCG (NEXT-4 of SURVEY section 8(f), h >= 1/64): conjugate gradients in
+ * solver = MLMC_SOLVER_MGCG (NEXT-4 of SURVEY section 8(f), h = 1/8 .. 1/512): conjugate gradients in
  *   binary64 preconditioned by one symmetric multigrid V(1,1) cycle in binary32 (nested P1 meshes,
  *   Galerkin-exact coarse operators, red-black Gauss-Seidel), the same stopping rule ||r_k||/||b|| <=
  *   tol (r_k the CG recurrence residual) and the same records; iterations are CG steps.  u_* ignored.
+ *   h >= 1/64: every grid on chip; h <= 1/128: one CTA per system over workspace scratch.
  * max_iter = 0 selects the default (MINRES: 16n+1000 -- loss of orthogonality
  * at coefficient contrasts ~1e7 takes well over n steps; IR: 50).
  * MINRES reports phibar_k/||b|| (the stopping quantity) as the residual and
@@ -244,7 +245,7 @@ typedef struct {
     double  r_bias;      /* the "r" of the bias test, R1: default 1 */
     int32_t N_init;      /* R6: default 100 */
     int32_t policy;      /* 0 = MINRES everywhere (paper-minres), 1 = Table 1 IR quads (paper-ir),
-                            2 = MG-PCG on h = 1/32, 1/64 and MINRES elsewhere (NEXT-4) */
+                            2 = MG-PCG on h <= 1/32 and MINRES on h = 1/8, 1/16 (NEXT-4) */
     int32_t rank, world; /* this process's slice of every level's new indices */
     int32_t max_rounds;  /* safety cap (default 100) */
     uint64_t seed;

@@ -132,7 +132,8 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.gm_ctas = 0;
     if (Nf >= kGmMinN) {   // per-CTA vector scratch of the global-memory MINRES (fine and coarse share it)
         L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1));
-        off += align256(std::max(minres_gm_scratch_per_cta(Nf), minres_stream_scratch_per_cta(Nf)) * L.gm_ctas);
+        off += align256(std::max({minres_gm_scratch_per_cta(Nf), minres_stream_scratch_per_cta(Nf), mgcg_scratch_per_cta(Nf)}) *
+                        L.gm_ctas);
     }
     // factor scratch of the Cholesky-IR solves (fine and coarse may run concurrently: two regions)
     L.ch_f_bytes = chol_bytes(pf, Nf, batch);
@@ -258,7 +259,7 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
     } else if (p->solver == MLMC_SOLVER_MGCG) {
         int mi = p->max_iter > 0 ? p->max_iter : 1000;
         CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
-                   [&] { return launch_mgcg(N, a, nb, tol, mi, rec, slot, ctr, nullptr, ex.st); }));
+                   [&] { return launch_mgcg(N, a, nb, tol, mi, rec, slot, ctr, nullptr, gm_scratch, gm_ctas, ex.st); }));
     } else {
         int mi = p->max_iter > 0 ? p->max_iter : 50;
         CU(counted(ctx, ex.st, MLMC_K_CHOL_IR, N,

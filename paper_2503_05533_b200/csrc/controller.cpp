@@ -38,7 +38,7 @@ mlmc_precision minres_prec() {
 // banded factor exists (N <= 32); u = u_r = binary64 here (the paper's level
 // 0/1 working precisions h/s are not implemented), MINRES beyond (R14).
 mlmc_precision policy_prec(int policy, int level, int N) {
-    if (policy == 2 && N >= 32 && N <= 64)   // NEXT-4: MG-PCG where it beats MINRES
+    if (policy == 2 && N >= 32)   // NEXT-4: MG-PCG where it beats MINRES, h <= 1/32
         return mlmc_precision{MLMC_SOLVER_MGCG, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
     if (policy == 1 && N <= 32) {
         if (level == 0)

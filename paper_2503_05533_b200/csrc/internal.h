@@ -56,10 +56,12 @@ bool minres_stream_supported(int N);
 size_t minres_stream_scratch_per_cta(int N);
 cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                                  unsigned* job_counter, double* scratch, int nctas, cudaStream_t s);
-// K3m (NEXT-4): multigrid-preconditioned CG for N = 8..64 (k_mgcg.cu), same record convention.
+// K3m (NEXT-4): multigrid-preconditioned CG (k_mgcg.cu), same record convention.  N = 8..64 on chip;
+// N = 128..512 one CTA per system over nctas x mgcg_scratch_per_cta(N) bytes of global scratch.
 bool mgcg_supported(int N);
+size_t mgcg_scratch_per_cta(int N);
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                        unsigned* job_counter, const int* order, cudaStream_t s);
+                        unsigned* job_counter, const int* order, void* scratch, int nctas, cudaStream_t s);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of
 // chol_scratch_bytes(N, u_f, u_s, nb) bytes for a launch over nb systems (one factor per resident
 // warp segment; a smaller scratch shrinks the grid; 0 = unsupported).

@@ -11,6 +11,7 @@
 //     Register-tiled FFMA64: a 64(b) x 64(p) output tile per 256-thread CTA,
 //     4x4 outputs per thread, k staged through shared memory in chunks of 16.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
@@ -301,14 +302,25 @@ static bool field_use_ffma() {
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
                          unsigned long long* keys, cudaStream_t s) {
     if (nb == 0) return cudaSuccess;
-    if (field_use_ffma() || (P & 1)) {
-        dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nb + FT_B - 1) / FT_B));
-        field_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb, keys);
-    } else {
-        dim3 grid((P + FD_P - 1) / FD_P, (unsigned)((nb + FD_B - 1) / FD_B));
-        field_dmma_kernel<<<grid, 256, 0, s>>>(phi, xi, a, P, m, (int)nb, keys);
+    // grid.y (sample blocks) is capped at 65535: larger batches go in slices of whole sample blocks
+    const bool ffma = field_use_ffma() || (P & 1);
+    const uint64_t per = 65535ull * (ffma ? FT_B : FD_B);
+    for (uint64_t b0 = 0; b0 < nb; b0 += per) {
+        const uint64_t nbs = std::min<uint64_t>(per, nb - b0);
+        const double* xs = xi + b0 * m;
+        double* as = a + b0 * (uint64_t)P;
+        unsigned long long* ks = keys ? keys + 2 * b0 : nullptr;
+        if (ffma) {
+            dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nbs + FT_B - 1) / FT_B));
+            field_kernel<<<grid, 256, 0, s>>>(phi, xs, as, P, m, (int)nbs, ks);
+        } else {
+            dim3 grid((P + FD_P - 1) / FD_P, (unsigned)((nbs + FD_B - 1) / FD_B));
+            field_dmma_kernel<<<grid, 256, 0, s>>>(phi, xs, as, P, m, (int)nbs, ks);
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
 }  // namespace mlmc

@@ -191,8 +191,6 @@ __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
     constexpr int GL = NL + 1, C = NL - 1;
     const Lvl L = lvl_at<N, NL>(fb);
     if (NT != T && tg >= NT) return;                    // small levels: one warp
-    for (int c = tg; c < GL * GL; c += NT) L.u[c] = 0.0f;
-    lsync<NT, T, GROUPS>(g);
     if constexpr (NL == 2) {                            // one unknown: exact
         if (tg == 0) {
             constexpr int c = GL + 1;
@@ -200,7 +198,15 @@ __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
         }
         lsync<NT, T, GROUPS>(g);
     } else {
-        l_rbgs<NL, NT, T, GROUPS>(L, 0, tg, g);
+        // first red sweep from u = 0 (the Dirichlet ring of u is zeroed once per system in mg_setup):
+        // red nodes u = f / diag, black nodes u = 0 -- one pass instead of a zero fill plus a sweep
+        for (int e = tg; e < C * C; e += NT) {
+            const int i = e % C + 1, j = e / C + 1, c = j * GL + i;
+            float v = 0.0f;
+            if (!((i + j) & 1)) v = __fdividef(L.f[c], (L.ce[c] + L.ce[c - 1]) + (L.cn[c] + L.cn[c - GL]));
+            L.u[c] = v;
+        }
+        lsync<NT, T, GROUPS>(g);
         l_rbgs<NL, NT, T, GROUPS>(L, 1, tg, g);
         for (int e = tg; e < C * C; e += NT) {         // t = f - A u
             const int c = (e / C + 1) * GL + (e % C + 1);
@@ -247,12 +253,69 @@ __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
     }
 }
 
+// level l's grids (runtime l)
+template <int N>
+__device__ __forceinline__ Lvl level_rt(float* fb, int l) {
+    int off = 0;
+    for (int k = 0; k < l; ++k) off += 5 * ((N >> k) + 1) * ((N >> k) + 1);
+    const int gl = (N >> l) + 1, sz = gl * gl;
+    float* b0 = fb + off;
+    return Lvl{b0, b0 + sz, b0 + 2 * sz, b0 + 3 * sz, b0 + 4 * sz, N >> l, gl};
+}
+
+// Per-system set-up: binary64 fine conductances cE, cN and p = 0; binary32 triangle coefficients,
+// conductances and zero u (Dirichlet rings included) on every level.
+template <int N, int T, int GROUPS>
+__device__ __forceinline__ void mg_setup(const double* __restrict__ a, double* cE, double* cN, double* pg, float* fb,
+                                         int tg, int g) {
+    constexpr int G = N + 1, LV = __builtin_ctz(N);
+    const Lvl L0 = level_rt<N>(fb, 0);
+    for (int c = tg; c < G * G; c += T) {
+        const int i = c % G, j = c / G;
+        const bool cell = i < N && j >= 0 && j < N;
+        const double aL = cell ? __ldg(a + 2 * (j * N + i)) : 0.0;          // aL of cell (i, j)
+        const double aU = cell ? __ldg(a + 2 * (j * N + i) + 1) : 0.0;      // aU
+        const double ce = (i < N && j >= 1 && j < N) ? 0.5 * (aL + __ldg(a + 2 * ((j - 1) * N + i) + 1)) : 0.0;
+        const double cn = (i >= 1 && i < N && j < N) ? 0.5 * (aU + __ldg(a + 2 * (j * N + i - 1))) : 0.0;
+        cE[c] = ce;
+        cN[c] = cn;
+        pg[c] = 0.0;
+        L0.t[c] = (float)aL;
+        L0.f[c] = (float)aU;
+        L0.ce[c] = (float)ce;
+        L0.cn[c] = (float)cn;
+        L0.u[c] = 0.0f;
+    }
+    gsync<T, GROUPS>(g);
+    for (int l = 1; l < LV; ++l) {
+        // coarse lower triangle of cell (I, J) = mean of fine L(2I,2J), L(2I+1,2J), U(2I+1,2J),
+        // L(2I+1,2J+1); upper = mean of U(2I,2J), L(2I,2J+1), U(2I,2J+1), U(2I+1,2J+1)
+        const Lvl F = level_rt<N>(fb, l - 1);
+        const Lvl Cv = level_rt<N>(fb, l);
+        const int Gf = F.Gl, Gc = Cv.Gl, Nc = Cv.Nl;
+        for (int e = tg; e < Gc * Gc; e += T) {
+            const int I = e % Gc, J = e / Gc;
+            float aL = 0.0f, aU = 0.0f;
+            if (I < Nc && J < Nc) {
+                const int c = (2 * J) * Gf + 2 * I;
+                aL = 0.25f * ((F.t[c] + F.t[c + 1]) + (F.f[c + 1] + F.t[c + Gf + 1]));
+                aU = 0.25f * ((F.f[c] + F.t[c + Gf]) + (F.f[c + Gf] + F.f[c + Gf + 1]));
+            }
+            Cv.t[e] = aL;
+            Cv.f[e] = aU;
+            Cv.u[e] = 0.0f;
+        }
+        gsync<T, GROUPS>(g);
+        level_conductances<T, GROUPS>(Cv, tg, g);
+    }
+}
+
 template <int N, int T, int GROUPS>
 __global__ void __launch_bounds__(MgCfg<N, T, GROUPS>::BLOCK)
 mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
             unsigned* __restrict__ job_counter, const int* __restrict__ order) {
     using K = MgCfg<N, T, GROUPS>;
-    constexpr int G = K::G, C = K::C, n = K::n, PER = K::PER, LV = K::LV, P = 2 * N * N;
+    constexpr int G = K::G, C = K::C, n = K::n, PER = K::PER, P = 2 * N * N;
     extern __shared__ __align__(128) unsigned char smem[];
     const int g = threadIdx.x / T, tg = threadIdx.x % T;
     unsigned char* base = smem + (size_t)g * K::SYS;
@@ -272,15 +335,6 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
     };
     auto live = [&](int k) { return tg + k * T < n; };
 
-    // level l's grids (runtime l)
-    auto level = [&](int l) {
-        int off = 0;
-        for (int k = 0; k < l; ++k) off += 5 * K::gl(k) * K::gl(k);
-        const int gl = K::gl(l), sz = gl * gl;
-        float* b0 = fb + off;
-        return Lvl{b0, b0 + sz, b0 + 2 * sz, b0 + 3 * sz, b0 + 4 * sz, N >> l, gl};
-    };
-
     auto vcycle = [&]() {
         vcyc<N, N, T, GROUPS>(fb, tg, g);
         if constexpr (N < MG_SMALL && T > 32) gsync<T, GROUPS>(g);
@@ -294,41 +348,8 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
         if (job >= nb) break;
         const int sj = order ? __ldg(order + job) : job;
         const double* a = a_all + (size_t)sj * P;
-
-        // ---- set-up: binary64 fine conductances, binary32 triangle coefficients of every level
-        const Lvl L0 = level(0);
-        for (int c = tg; c < G * G; c += T) {
-            const int i = c % G, j = c / G;
-            cE[c] = (i < N && j >= 1 && j < N) ? 0.5 * (__ldg(a + 2 * (j * N + i)) + __ldg(a + 2 * ((j - 1) * N + i) + 1)) : 0.0;
-            cN[c] = (i >= 1 && i < N && j < N) ? 0.5 * (__ldg(a + 2 * (j * N + i) + 1) + __ldg(a + 2 * (j * N + i - 1))) : 0.0;
-            pg[c] = 0.0;
-            const bool cell = i < N && j < N;
-            L0.t[c] = cell ? (float)__ldg(a + 2 * (j * N + i)) : 0.0f;          // aL of cell (i, j)
-            L0.f[c] = cell ? (float)__ldg(a + 2 * (j * N + i) + 1) : 0.0f;      // aU
-            L0.ce[c] = (float)cE[c];
-            L0.cn[c] = (float)cN[c];
-        }
-        gsync<T, GROUPS>(g);
-        for (int l = 1; l < LV; ++l) {
-            // coarse lower triangle of cell (I, J) = mean of fine L(2I,2J), L(2I+1,2J), U(2I+1,2J),
-            // L(2I+1,2J+1); upper = mean of U(2I,2J), L(2I,2J+1), U(2I,2J+1), U(2I+1,2J+1)
-            const Lvl F = level(l - 1);
-            const Lvl Cv = level(l);
-            const int Gf = F.Gl, Gc = Cv.Gl, Nc = Cv.Nl;
-            for (int e = tg; e < Gc * Gc; e += T) {
-                const int I = e % Gc, J = e / Gc;
-                float aL = 0.0f, aU = 0.0f;
-                if (I < Nc && J < Nc) {
-                    const int c = (2 * J) * Gf + 2 * I;
-                    aL = 0.25f * ((F.t[c] + F.t[c + 1]) + (F.f[c + 1] + F.t[c + Gf + 1]));
-                    aU = 0.25f * ((F.f[c] + F.t[c + Gf]) + (F.f[c + Gf] + F.f[c + Gf + 1]));
-                }
-                Cv.t[e] = aL;
-                Cv.f[e] = aU;
-            }
-            gsync<T, GROUPS>(g);
-            level_conductances<T, GROUPS>(Cv, tg, g);
-        }
+        mg_setup<N, T, GROUPS>(a, cE, cN, pg, fb, tg, g);
+        const Lvl L0 = level_rt<N>(fb, 0);
 
         // ---- PCG from x0 = 0: r = b, z = M^-1 r, p = z
         double r[PER], q[PER];
@@ -418,6 +439,138 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
     }
 }
 
+// ---- K3m-g: the same MG-PCG for the streamed meshes (h = 1/128 .. 1/512).  One CTA (MG_GM_T threads) per
+// system, every grid of the system in a per-CTA slice of global scratch: binary64 [p | cE | cN | r | q],
+// then the binary32 levels exactly as on chip.  The passes are the on-chip ones (same arithmetic, same
+// order per node), each a coalesced sweep over the grid through L1/L2; __syncthreads orders them.
+#ifndef MG_GM_T
+#define MG_GM_T 512
+#endif
+template <int N>
+struct MgGm {
+    static constexpr int T = MG_GM_T;
+    static constexpr int G = N + 1;
+    static constexpr size_t GG = (size_t)G * G;
+    static constexpr size_t D_END = 5 * GG;                                          // doubles
+    static constexpr size_t F_END = (MgCfg<N, 32, 1>::F_END + 31) / 32 * 32;           // floats
+    static constexpr size_t SYS = ((D_END * 8 + F_END * 4) + 255) / 256 * 256;       // bytes per CTA
+};
+
+template <int N>
+__global__ void __launch_bounds__(MG_GM_T, 1)
+mgcg_gm_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
+               unsigned* __restrict__ job_counter, const int* __restrict__ order, unsigned char* __restrict__ scratch) {
+    using K = MgGm<N>;
+    constexpr int T = K::T, G = K::G, C = N - 1, n = C * C, P = 2 * N * N;
+    __shared__ double red[2 * (T / 32)];
+    __shared__ int jobslot;
+    const int tg = threadIdx.x;
+    double* dg = reinterpret_cast<double*>(scratch + (size_t)blockIdx.x * K::SYS);
+    double* pg = dg;
+    double* cE = dg + K::GG;
+    double* cN = dg + 2 * K::GG;
+    double* rg = dg + 3 * K::GG;
+    double* qg = dg + 4 * K::GG;
+    float* fb = reinterpret_cast<float*>(dg + K::D_END);
+    const double h = 1.0 / N, h2 = h * h;
+    auto cix = [](int e) { return (e / C + 1) * G + (e % C + 1); };
+
+    for (;;) {
+        if (tg == 0) jobslot = (int)atomicAdd(job_counter, 1u);
+        __syncthreads();
+        const int job = jobslot;
+        __syncthreads();
+        if (job >= nb) break;
+        const int sj = order ? __ldg(order + job) : job;
+        const double* a = a_all + (size_t)sj * P;
+        mg_setup<N, T, 1>(a, cE, cN, pg, fb, tg, 0);
+        const Lvl L0 = level_rt<N>(fb, 0);
+
+        double rr = 0.0;
+        for (int e = tg; e < n; e += T) {
+            const int c = cix(e);
+            rg[c] = h2;
+            L0.f[c] = (float)h2;
+            rr = fma(h2, h2, rr);
+        }
+        __syncthreads();
+        vcyc<N, N, T, 1>(fb, tg, 0);
+        double rz = 0.0;
+#pragma unroll 4
+        for (int e = tg; e < n; e += T) {
+            const int c = cix(e);
+            const double z = (double)L0.u[c];
+            pg[c] = z;
+            rz = fma(rg[c], z, rz);
+        }
+        double2 S = gsum2<T, 1>(rz, rr, red, tg, 0);
+        rz = S.x;
+        const double bnorm = sqrt(S.y);
+        const double tol_b = tol * bnorm;
+        double Xq = 0.0, rnorm = bnorm;
+        int it = 0, status = 1;
+        if (bnorm == 0.0) status = 0;
+        while (status == 1 && it < max_iter) {
+            double pq = 0.0, sp = 0.0;
+#pragma unroll 4
+            for (int e = tg; e < n; e += T) {
+                const int c = cix(e);
+                const double ce = cE[c], cw = cE[c - 1], cn = cN[c], cs = cN[c - G];
+                const double pv = pg[c];
+                double Ap = ((ce + cw) + (cn + cs)) * pv;
+                Ap = fma(-ce, pg[c + 1], Ap);
+                Ap = fma(-cw, pg[c - 1], Ap);
+                Ap = fma(-cn, pg[c + G], Ap);
+                Ap = fma(-cs, pg[c - G], Ap);
+                qg[c] = Ap;
+                pq = fma(pv, Ap, pq);
+                sp += pv;
+            }
+            S = gsum2<T, 1>(pq, sp, red, tg, 0);
+            const double alpha = rz / S.x;
+            Xq = fma(alpha, S.y, Xq);
+            rr = 0.0;
+#pragma unroll 4
+            for (int e = tg; e < n; e += T) {                  // own nodes only: no barrier needed on q
+                const int c = cix(e);
+                const double rv = fma(-alpha, qg[c], rg[c]);
+                rg[c] = rv;
+                L0.f[c] = (float)rv;
+                rr = fma(rv, rv, rr);
+            }
+            ++it;
+            __syncthreads();
+            vcyc<N, N, T, 1>(fb, tg, 0);
+            double rz_new = 0.0;
+#pragma unroll 4
+            for (int e = tg; e < n; e += T) {
+                const int c = cix(e);
+                rz_new = fma(rg[c], (double)L0.u[c], rz_new);
+            }
+            S = gsum2<T, 1>(rz_new, rr, red, tg, 0);
+            rnorm = sqrt(S.y);
+            if (!(rnorm == rnorm)) { status = 3; break; }
+            if (rnorm <= tol_b) { status = 0; break; }
+            const double beta = S.x / rz;
+            rz = S.x;
+#pragma unroll 4
+            for (int e = tg; e < n; e += T) {
+                const int c = cix(e);
+                pg[c] = fma(beta, pg[c], (double)L0.u[c]);
+            }
+            __syncthreads();
+        }
+        if (tg == 0) {
+            double* o = out + (size_t)sj * kRecLen;
+            o[0 + slot] = h2 * Xq;
+            o[2 + slot] = (double)it;
+            o[4 + slot] = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+            o[6 + slot] = (double)status;
+        }
+        __syncthreads();
+    }
+}
+
 template <int N, int T, int GROUPS>
 cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
                    const int* order, cudaStream_t s) {
@@ -440,17 +593,40 @@ cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, doubl
     return cudaGetLastError();
 }
 
+template <int N>
+cudaError_t run_mg_gm(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
+                      const int* order, void* scratch, int nctas, cudaStream_t s) {
+    if (!scratch || nctas < 1) return cudaErrorInvalidValue;
+    const uint64_t grid = std::min<uint64_t>(nb, (uint64_t)nctas);
+    if (grid == 0) return cudaSuccess;
+    mgcg_gm_kernel<N><<<(unsigned)grid, MgGm<N>::T, 0, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order,
+                                                           static_cast<unsigned char*>(scratch));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
-bool mgcg_supported(int N) { return N == 8 || N == 16 || N == 32 || N == 64; }
+bool mgcg_supported(int N) { return N == 8 || N == 16 || N == 32 || N == 64 || N == 128 || N == 256 || N == 512; }
+
+size_t mgcg_scratch_per_cta(int N) {
+    switch (N) {
+        case 128: return MgGm<128>::SYS;
+        case 256: return MgGm<256>::SYS;
+        case 512: return MgGm<512>::SYS;
+        default: return 0;
+    }
+}
 
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                        unsigned* ctr, const int* order, cudaStream_t s) {
+                        unsigned* ctr, const int* order, void* scratch, int nctas, cudaStream_t s) {
     switch (N) {
         case 8: return run_mg<8, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 16: return run_mg<16, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 32: return run_mg<32, 128, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 64: return run_mg<64, 256, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        case 128: return run_mg_gm<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+        case 256: return run_mg_gm<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+        case 512: return run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
         default: return cudaErrorNotSupported;
     }
 }

@@ -507,3 +507,47 @@ def test_mgcg_within_residual_bound(level, tol):
         if c is not None:
             assert abs(ps[k, 1] - c[0]) <= tol * c[1] * c[2] * (1 + 1e-6) + 1e-14 * c[0]
     ctx.close()
+
+
+@pytest.mark.parametrize("level,n,tol", [(4, 4, 1e-10), (4, 150, 1e-6), (5, 2, 1e-8)])
+def test_mgcg_streamed_meshes_within_residual_bound(level, n, tol):
+    """K3m-g (MG-PCG with every grid in global scratch, h = 1/128 and 1/256; configs[4] field): per-
+    sample Q within the rigorous bound of the oracle's direct solve on sampled systems, iteration
+    counts mesh-independent; a batch over one wave of CTAs (n = 150 > 148) and single systems agree
+    bit for bit (one CTA per system, no cross-system state)."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=8 << 30)
+    P = _oracle(cfg)
+    mg = precision("mgcg")
+    r = ctx.sample_level(level, n, seed=21, prec_fine=mg, prec_coarse=mg, tol_fine=tol, tol_coarse=tol,
+                         per_sample=True)
+    ps = r.per_sample
+    assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
+    assert ps[:, 2].max() <= 25 and np.all(ps[:, 4] <= tol)
+    Nf = 8 << level
+    idx = [0, n - 1] if n > 1 else [0]
+    exs = _pmap(lambda k: (_exact(P, Nf, oc.normals(21, level, k, cfg["m"])),
+                           _exact(P, Nf // 2, oc.normals(21, level, k, cfg["m"]))), idx)
+    for k, ((qf, bf, xf), (qc, bc, xc)) in zip(idx, exs):
+        assert abs(ps[k, 0] - qf) <= tol * bf * xf * (1 + 1e-6) + 1e-14 * qf, (level, k, ps[k, 0], qf)
+        assert abs(ps[k, 1] - qc) <= tol * bc * xc * (1 + 1e-6) + 1e-14 * qc
+    if n > 1:
+        one = ctx.sample_level(level, 1, seed=21, first_index=n - 1, prec_fine=mg, prec_coarse=mg, tol_fine=tol,
+                               tol_coarse=tol, per_sample=True).per_sample
+        assert np.array_equal(one[0], ps[n - 1])
+    ctx.close()
+
+
+def test_level_pass_over_field_grid_limit():
+    """One pass of more than 65535 x 64 samples (the field kernel's grid.y limit, sliced in launch_field):
+    the last sample of a 4.3M-sample level-0 pass equals the same sample drawn alone, bit for bit."""
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg, ws=12 << 30)
+    mr = precision("minres")
+    n = 65535 * 64 + 1000
+    r = ctx.sample_level(0, n, seed=5, prec_fine=mr, tol_fine=1e-4, per_sample=True)
+    assert r.sums["n"] == n and r.sums["n_fail"] == 0
+    for k in (0, 65535 * 64 - 1, 65535 * 64, n - 1):
+        one = ctx.sample_level(0, 1, seed=5, first_index=k, prec_fine=mr, tol_fine=1e-4, per_sample=True).per_sample
+        assert np.array_equal(one[0], r.per_sample[k]), k
+    ctx.close()

@@ -10,7 +10,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workloads as W  # noqa: E402
-from paper_2503_05533_b200 import Context  # noqa: E402
+from paper_2503_05533_b200 import Context, precision  # noqa: E402
 
 eps = float(sys.argv[1]) if len(sys.argv) > 1 else 2e-5
 policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
@@ -18,6 +18,9 @@ cfg = W.CONFIGS["C5"]
 ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
               L_max=cfg["L_max"], device=0, workspace_bytes=16 << 30)
 ctx.adaptive_run(1e-3, k_p=cfg["k_p"], seed=99, policy=policy)          # warm-up (plan, kernels)
+for l in range(cfg["L_max"] + 1):                                        # KL tables of every level on HBM
+    p = precision("mgcg" if policy == 2 and (cfg["h0_inv"] << l) >= 32 else "minres")
+    ctx.sample_level(l, 1, seed=98, prec_fine=p, prec_coarse=p, tol_fine=1e-6, tol_coarse=1e-6)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 r = ctx.adaptive_run(eps, k_p=cfg["k_p"], N_init=100, seed=cfg["seed"], policy=policy, on_fail=1)
