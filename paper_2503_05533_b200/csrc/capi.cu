@@ -130,10 +130,13 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.ord_c = off;  off += align256(sizeof(int) * batch);
     L.gm = off;
     L.gm_ctas = 0;
-    if (Nf >= kGmMinN) {   // per-CTA vector scratch of the global-memory MINRES (fine and coarse share it)
-        L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1));
-        off += align256(std::max({minres_gm_scratch_per_cta(Nf), minres_stream_scratch_per_cta(Nf), mgcg_scratch_per_cta(Nf)}) *
-                        L.gm_ctas);
+    if (Nf >= kGmMinN) {   // per-CTA scratch of the streamed-mesh solvers (fine and coarse share it)
+        const bool mg = (pf && pf->solver == MLMC_SOLVER_MGCG) || (pc && pc->solver == MLMC_SOLVER_MGCG);
+        const int per_sm = mg ? mgcg_ctas_per_sm(Nf) : 1;
+        L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1) * per_sm);
+        size_t per_cta = std::max(minres_gm_scratch_per_cta(Nf), minres_stream_scratch_per_cta(Nf));
+        if (mg) per_cta = std::max(per_cta, mgcg_scratch_per_cta(Nf));
+        off += align256(per_cta * L.gm_ctas);
     }
     // factor scratch of the Cholesky-IR solves (fine and coarse may run concurrently: two regions)
     L.ch_f_bytes = chol_bytes(pf, Nf, batch);

@@ -60,6 +60,7 @@ cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol
 // N = 128..512 one CTA per system over nctas x mgcg_scratch_per_cta(N) bytes of global scratch.
 bool mgcg_supported(int N);
 size_t mgcg_scratch_per_cta(int N);
+int mgcg_ctas_per_sm(int N);   // resident systems per SM of the streamed-mesh MG-PCG
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                         unsigned* job_counter, const int* order, void* scratch, int nctas, cudaStream_t s);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of

@@ -25,6 +25,8 @@
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -571,6 +573,342 @@ mgcg_gm_kernel(const double* __restrict__ a_all, int nb, double tol, int max_ite
     }
 }
 
+// ---- K3m-t: the streamed-mesh MG-PCG with temporal blocking (default for h = 1/128 .. 1/512).
+// The fine level's ten grid passes per CG step become three:
+//   A (tiles): r_k = r_{k-1} - alpha q, f = r_k in binary32, first red sweep, black sweep, residual
+//      t = f - A u and restriction P^T t -- on a 128 x 32 tile with a 4-node halo held in shared
+//      memory (the halo is recomputed, never exchanged); stores r_k, u and the coarse right-hand side;
+//   B (tiles): u += P u_c, black sweep, red sweep -> z, r^T z -- 2-node halo; stores z;
+//   C (plain): p_{k+1} = z + beta p_k and q = A p_{k+1} formed together (p_{k+1} at the four
+//      neighbours recomputed from p_k and z), p^T q, 1^T p.
+// r and p are ping-pong buffers (a tile's halo must read the previous iterate even where the
+// neighbouring tile has already written the new one); z has its own grid.  Per node and step
+// every value is the on-chip kernel's, with the same operations in the same order; only the
+// partial-sum order of the dot products differs.  Coarser levels: vcyc from h = 2/N as above.
+#ifndef MG_TL_T
+#define MG_TL_T 512
+#endif
+#ifndef MG_TL_MINB
+#define MG_TL_MINB 1
+#endif
+template <int N>
+struct MgTl {
+    static constexpr int T = MG_TL_T;
+    static constexpr int G = N + 1;
+    static constexpr size_t GG = (size_t)G * G;
+    static constexpr int TX = N >= 128 ? 128 : N, TY = 32, H = 4;
+    static constexpr int RX = TX + 2 * H, RY = TY + 2 * H, RN = RX * RY;
+    static constexpr int NTX = (N - 1 + TX - 1) / TX, NTY = (N - 1 + TY - 1) / TY;
+    static constexpr size_t D_END = 7 * GG;                                  // p0 p1 cE cN r0 r1 q
+    static constexpr size_t F_END = (MgCfg<N, 32, 1>::F_END + 31) / 32 * 32;
+    static constexpr size_t SYS = ((D_END * 8 + F_END * 4) + 255) / 256 * 256;
+    static constexpr size_t SMEM = (size_t)4 * RN * 4 + 2 * (T / 32) * 8 + 16;
+};
+
+template <int N>
+__global__ void __launch_bounds__(MG_TL_T, MG_TL_MINB)
+mgcg_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
+                 int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order,
+                 unsigned char* __restrict__ scratch) {
+    using K = MgTl<N>;
+    constexpr int T = K::T, G = K::G, C = N - 1, n = C * C, P = 2 * N * N;
+    constexpr int RX = K::RX, RN = K::RN, H = K::H, TX = K::TX, TY = K::TY;
+    constexpr int NC = N / 2, GC = NC + 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* sf = reinterpret_cast<float*>(smem);       // f, then t (pass A)
+    float* sce = sf + RN;
+    float* scn = sce + RN;
+    float* su = scn + RN;
+    double* red = reinterpret_cast<double*>(su + RN);
+    int* jobslot = reinterpret_cast<int*>(red + 2 * (T / 32));
+    const int tg = threadIdx.x;
+    double* dg = reinterpret_cast<double*>(scratch + (size_t)blockIdx.x * K::SYS);
+    double* pb[2] = {dg, dg + K::GG};
+    double* cE = dg + 2 * K::GG;
+    double* cN = dg + 3 * K::GG;
+    double* rb[2] = {dg + 4 * K::GG, dg + 5 * K::GG};
+    double* qg = dg + 6 * K::GG;
+    float* fb = reinterpret_cast<float*>(dg + K::D_END);
+    const double h = 1.0 / N, h2 = h * h;
+    auto cix = [](int e) { return (e / C + 1) * G + (e % C + 1); };
+    auto interior = [](int i, int j) { return i >= 1 && i <= C && j >= 1 && j <= C; };
+
+    for (;;) {
+        if (tg == 0) *jobslot = (int)atomicAdd(job_counter, 1u);
+        __syncthreads();
+        const int job = *jobslot;
+        __syncthreads();
+        if (job >= nb) break;
+        const int sj = order ? __ldg(order + job) : job;
+        const double* a = a_all + (size_t)sj * P;
+        mg_setup<N, T, 1>(a, cE, cN, pb[0], fb, tg, 0);
+        const Lvl L0 = level_rt<N>(fb, 0);     // u = pre-smoothed u, f = z; t unused
+        const Lvl L1 = level_rt<N>(fb, 1);
+        float* zg = L0.f;
+        for (int c = tg; c < (int)K::GG; c += T) {
+            const int i = c % G, j = c / G;
+            pb[1][c] = 0.0;
+            rb[0][c] = interior(i, j) ? h2 : 0.0;
+            rb[1][c] = 0.0;
+            qg[c] = 0.0;
+            zg[c] = 0.0f;
+        }
+        __syncthreads();
+        int cr = 0, cp = 0;            // current r / p buffers
+
+        // ---- pass A: r_new = r_old - alpha q, pre-smoothing, residual, restriction
+        auto pass_a = [&](double alpha) {
+            const double* ro = rb[cr];
+            double* rn = rb[cr ^ 1];
+            double rr = 0.0;
+            for (int ty = 0; ty < K::NTY; ++ty)
+                for (int tx = 0; tx < K::NTX; ++tx) {
+                    const int x0 = 1 + tx * TX, y0 = 1 + ty * TY;
+                    const int xe = min(x0 + TX, N), ye = min(y0 + TY, N);       // owned: [x0, xe) x [y0, ye)
+                    auto inreg = [&](int i, int j, int hh) {
+                        return i >= x0 - hh && i < xe + hh && j >= y0 - hh && j < ye + hh;
+                    };
+#pragma unroll 4
+                    for (int k = tg; k < RN; k += T) {
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        float f = 0.0f, ce = 0.0f, cn = 0.0f;
+                        if (i >= 0 && i <= N && j >= 0 && j <= N && inreg(i, j, H)) {
+                            const int c = j * G + i;
+                            ce = L0.ce[c];
+                            cn = L0.cn[c];
+                            if (interior(i, j)) {
+                                const double r = fma(-alpha, qg[c], ro[c]);
+                                f = (float)r;
+                                if (inreg(i, j, 0)) {
+                                    rn[c] = r;
+                                    rr = fma(r, r, rr);
+                                }
+                            }
+                        }
+                        sf[k] = f;
+                        sce[k] = ce;
+                        scn[k] = cn;
+                    }
+                    __syncthreads();
+                    for (int k = tg; k < RN; k += T) {       // first red sweep from u = 0
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        float u = 0.0f;
+                        if (interior(i, j) && inreg(i, j, H - 1) && !((i + j) & 1))
+                            u = __fdividef(sf[k], (sce[k] + sce[k - 1]) + (scn[k] + scn[k - RX]));
+                        su[k] = u;
+                    }
+                    __syncthreads();
+                    for (int k = tg; k < RN; k += T) {       // black sweep
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        if (interior(i, j) && inreg(i, j, H - 2) && ((i + j) & 1)) {
+                            const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
+                            float s = sf[k];
+                            s = fmaf(ce, su[k + 1], s);
+                            s = fmaf(cw, su[k - 1], s);
+                            s = fmaf(cn, su[k + RX], s);
+                            s = fmaf(cs, su[k - RX], s);
+                            su[k] = __fdividef(s, (ce + cw) + (cn + cs));
+                        }
+                    }
+                    __syncthreads();
+                    for (int k = tg; k < RN; k += T) {       // t = f - A u (in place of f); store u
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        if (interior(i, j) && inreg(i, j, 1)) {
+                            const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
+                            float Au = ((ce + cw) + (cn + cs)) * su[k];
+                            Au = fmaf(-ce, su[k + 1], Au);
+                            Au = fmaf(-cw, su[k - 1], Au);
+                            Au = fmaf(-cn, su[k + RX], Au);
+                            Au = fmaf(-cs, su[k - RX], Au);
+                            sf[k] = sf[k] - Au;
+                            if (inreg(i, j, 0)) L0.u[j * G + i] = su[k];
+                        }
+                    }
+                    __syncthreads();
+                    // f_c = P^T t for the coarse nodes whose centre (2I, 2J) this tile owns
+                    const int Ilo = max(1, (x0 + 1) / 2), Ihi = min(NC - 1, (xe - 1) / 2);
+                    const int Jlo = max(1, (y0 + 1) / 2), Jhi = min(NC - 1, (ye - 1) / 2);
+                    const int nI = Ihi - Ilo + 1, nJ = Jhi - Jlo + 1;
+                    if (nI > 0 && nJ > 0)
+                        for (int e = tg; e < nI * nJ; e += T) {
+                            const int I = Ilo + e % nI, J = Jlo + e / nI;
+                            const int k = (2 * J - y0 + H) * RX + (2 * I - x0 + H);
+                            L1.f[J * GC + I] = sf[k] + 0.5f * ((sf[k + 1] + sf[k - 1]) + (sf[k + RX] + sf[k - RX]) +
+                                                               (sf[k + RX + 1] + sf[k - RX - 1]));
+                        }
+                    __syncthreads();
+                }
+            cr ^= 1;
+            return rr;
+        };
+
+        // ---- pass B: u += P u_c, post-smoothing (black, red) -> z, r^T z
+        auto pass_b = [&]() {
+            const double* rn = rb[cr];
+            const float* U = L1.u;
+            double rz = 0.0;
+            for (int ty = 0; ty < K::NTY; ++ty)
+                for (int tx = 0; tx < K::NTX; ++tx) {
+                    const int x0 = 1 + tx * TX, y0 = 1 + ty * TY;
+                    const int xe = min(x0 + TX, N), ye = min(y0 + TY, N);
+                    auto inreg = [&](int i, int j, int hh) {
+                        return i >= x0 - hh && i < xe + hh && j >= y0 - hh && j < ye + hh;
+                    };
+#pragma unroll 4
+                    for (int k = tg; k < RN; k += T) {
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        float f = 0.0f, ce = 0.0f, cn = 0.0f, u = 0.0f;
+                        if (i >= 0 && i <= N && j >= 0 && j <= N && inreg(i, j, 2)) {
+                            const int c = j * G + i;
+                            ce = L0.ce[c];
+                            cn = L0.cn[c];
+                            if (interior(i, j)) {
+                                f = (float)rn[c];
+                                const int I = i >> 1, J = j >> 1;
+                                float v;
+                                if (!(i & 1) && !(j & 1)) v = U[J * GC + I];
+                                else if ((i & 1) && !(j & 1)) v = 0.5f * (U[J * GC + I] + U[J * GC + I + 1]);
+                                else if (!(i & 1) && (j & 1)) v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I]);
+                                else v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I + 1]);
+                                u = L0.u[c] + v;
+                            }
+                        }
+                        sf[k] = f;
+                        sce[k] = ce;
+                        scn[k] = cn;
+                        su[k] = u;
+                    }
+                    __syncthreads();
+                    for (int k = tg; k < RN; k += T) {       // black sweep
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        if (interior(i, j) && inreg(i, j, 1) && ((i + j) & 1)) {
+                            const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
+                            float s = sf[k];
+                            s = fmaf(ce, su[k + 1], s);
+                            s = fmaf(cw, su[k - 1], s);
+                            s = fmaf(cn, su[k + RX], s);
+                            s = fmaf(cs, su[k - RX], s);
+                            su[k] = __fdividef(s, (ce + cw) + (cn + cs));
+                        }
+                    }
+                    __syncthreads();
+                    for (int k = tg; k < RN; k += T) {       // red sweep on the owned nodes; z out
+                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                        if (interior(i, j) && inreg(i, j, 0)) {
+                            float z = su[k];
+                            if (!((i + j) & 1)) {
+                                const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
+                                float s = sf[k];
+                                s = fmaf(ce, su[k + 1], s);
+                                s = fmaf(cw, su[k - 1], s);
+                                s = fmaf(cn, su[k + RX], s);
+                                s = fmaf(cs, su[k - RX], s);
+                                z = __fdividef(s, (ce + cw) + (cn + cs));
+                            }
+                            const int c = j * G + i;
+                            zg[c] = z;
+                            rz = fma(rn[c], (double)z, rz);
+                        }
+                    }
+                    __syncthreads();
+                }
+            return rz;
+        };
+
+        // ---- pass C: p_new = z + beta p_old and q = A p_new; p^T q, 1^T p
+        auto pass_c = [&](double beta, double& pq, double& sp) {
+            const double* po = pb[cp];
+            double* pn = pb[cp ^ 1];
+            pq = 0.0;
+            sp = 0.0;
+#pragma unroll 2
+            for (int e = tg; e < n; e += T) {
+                const int c = cix(e);
+                auto pnew = [&](int cc) { return fma(beta, po[cc], (double)zg[cc]); };
+                const double ce = cE[c], cw = cE[c - 1], cn = cN[c], cs = cN[c - G];
+                const double pv = pnew(c);
+                double Ap = ((ce + cw) + (cn + cs)) * pv;
+                Ap = fma(-ce, pnew(c + 1), Ap);
+                Ap = fma(-cw, pnew(c - 1), Ap);
+                Ap = fma(-cn, pnew(c + G), Ap);
+                Ap = fma(-cs, pnew(c - G), Ap);
+                qg[c] = Ap;
+                pn[c] = pv;
+                pq = fma(pv, Ap, pq);
+                sp += pv;
+            }
+            cp ^= 1;
+        };
+
+        // ---- PCG from x0 = 0 (r_0 = b, q = 0, p = 0, alpha = beta = 0 for the first passes)
+        double rr = pass_a(0.0);
+        __syncthreads();
+        vcyc<N, NC, T, 1>(fb, tg, 0);
+        double rz = pass_b();
+        double2 S = gsum2<T, 1>(rz, rr, red, tg, 0);
+        rz = S.x;
+        const double bnorm = sqrt(S.y);
+        const double tol_b = tol * bnorm;
+        double Xq = 0.0, rnorm = bnorm, beta = 0.0;
+        int it = 0, status = 1;
+        if (bnorm == 0.0) status = 0;
+        while (status == 1 && it < max_iter) {
+            double pq, sp;
+            pass_c(beta, pq, sp);
+            S = gsum2<T, 1>(pq, sp, red, tg, 0);
+            const double alpha = rz / S.x;
+            Xq = fma(alpha, S.y, Xq);
+            rr = pass_a(alpha);
+            ++it;
+            __syncthreads();
+            vcyc<N, NC, T, 1>(fb, tg, 0);
+            const double rz_new = pass_b();
+            S = gsum2<T, 1>(rz_new, rr, red, tg, 0);
+            rnorm = sqrt(S.y);
+            if (!(rnorm == rnorm)) { status = 3; break; }
+            if (rnorm <= tol_b) { status = 0; break; }
+            beta = S.x / rz;
+            rz = S.x;
+        }
+        if (tg == 0) {
+            double* o = out + (size_t)sj * kRecLen;
+            o[0 + slot] = h2 * Xq;
+            o[2 + slot] = (double)it;
+            o[4 + slot] = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+            o[6 + slot] = (double)status;
+        }
+        __syncthreads();
+    }
+}
+
+template <int N>
+cudaError_t run_mg_tile(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
+                        const int* order, void* scratch, int nctas, cudaStream_t s) {
+    if (!scratch || nctas < 1) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(mgcg_tile_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)MgTl<N>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const uint64_t grid = std::min<uint64_t>(nb, (uint64_t)nctas);
+    if (grid == 0) return cudaSuccess;
+    mgcg_tile_kernel<N><<<(unsigned)grid, MgTl<N>::T, MgTl<N>::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr,
+                                                                          order, static_cast<unsigned char*>(scratch));
+    return cudaGetLastError();
+}
+
+// MLMC_MG_GM=plain selects the ten-pass global-memory kernel (A/B runs).
+bool use_mg_plain() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("MLMC_MG_GM");
+        v = (e && std::strcmp(e, "plain") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 template <int N, int T, int GROUPS>
 cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
                    const int* order, cudaStream_t s) {
@@ -609,24 +947,34 @@ cudaError_t run_mg_gm(const double* a, uint64_t nb, double tol, int max_iter, do
 bool mgcg_supported(int N) { return N == 8 || N == 16 || N == 32 || N == 64 || N == 128 || N == 256 || N == 512; }
 
 size_t mgcg_scratch_per_cta(int N) {
+    const bool plain = use_mg_plain();
     switch (N) {
-        case 128: return MgGm<128>::SYS;
-        case 256: return MgGm<256>::SYS;
-        case 512: return MgGm<512>::SYS;
+        case 128: return plain ? MgGm<128>::SYS : MgTl<128>::SYS;
+        case 256: return plain ? MgGm<256>::SYS : MgTl<256>::SYS;
+        case 512: return plain ? MgGm<512>::SYS : MgTl<512>::SYS;
         default: return 0;
     }
 }
 
+int mgcg_ctas_per_sm(int N) { return N >= 128 && !use_mg_plain() ? MG_TL_MINB : 1; }
+
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                         unsigned* ctr, const int* order, void* scratch, int nctas, cudaStream_t s) {
+    const bool plain = use_mg_plain();
     switch (N) {
         case 8: return run_mg<8, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 16: return run_mg<16, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 32: return run_mg<32, 128, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 64: return run_mg<64, 256, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-        case 128: return run_mg_gm<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
-        case 256: return run_mg_gm<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
-        case 512: return run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+        case 128:
+            return plain ? run_mg_gm<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s)
+                         : run_mg_tile<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+        case 256:
+            return plain ? run_mg_gm<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s)
+                         : run_mg_tile<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+        case 512:
+            return plain ? run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s)
+                         : run_mg_tile<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
         default: return cudaErrorNotSupported;
     }
 }

@@ -26,7 +26,14 @@ t0 = time.perf_counter()
 r = ctx.adaptive_run(eps, k_p=cfg["k_p"], N_init=100, seed=cfg["seed"], policy=policy, on_fail=1)
 torch.cuda.synchronize()
 el = time.perf_counter() - t0
+prof = None
+if len(sys.argv) > 3 and sys.argv[3] == "prof":       # per kernel class device time (events: a second run)
+    ctx.profile_enable(True)
+    ctx.adaptive_run(eps, k_p=cfg["k_p"], N_init=100, seed=cfg["seed"], policy=policy, on_fail=1)
+    prof = [(k, n, c, round(ms, 2)) for k, n, c, ms in ctx.profile_read() if ms > 0.5]
+    ctx.profile_enable(False)
 print(json.dumps({"eps": eps, "policy": policy, "seconds": el, "solve_seconds": r["solve_seconds"], "L": r["L"],
                   "N": r["N"], "eps_l": r["eps"], "mean": r["mean"], "var": r["var"], "cost": r["cost"],
-                  "estimate": r["estimate"], "rounds": r["rounds"], "code": r["code"], "n_fail": r["n_fail"]}))
+                  "estimate": r["estimate"], "rounds": r["rounds"], "code": r["code"], "n_fail": r["n_fail"],
+                  "profile_ms": prof}))
 ctx.close()
