@@ -10,6 +10,8 @@ Tolerances:
     + 1e-14 Q, the rigorous per-sample bound of DESIGN.md section 4 (w = b, A SPD).
 """
 import math
+import os
+import sys
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -551,3 +553,14 @@ def test_level_pass_over_field_grid_limit():
         one = ctx.sample_level(0, 1, seed=5, first_index=k, prec_fine=mr, tol_fine=1e-4, per_sample=True).per_sample
         assert np.array_equal(one[0], r.per_sample[k]), k
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_replicate_rmse_within_eps(name):
+    """The estimator pin of SURVEY section 8(c): over R = 50 seeds, RMSE(Q_hat - Q_ref) <= eps, with
+    Q_ref the same GPU path at eps / 5 (its samples are the ones the per-sample parity tests pin)."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import replicates
+    r = replicates.run(name, R=50)
+    assert r["rmse"] <= r["eps"], r
+    assert 0.030 < r["mean_estimate"] < 0.038
