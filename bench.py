@@ -397,6 +397,7 @@ def c3_leg(local, torch):
     its roofline line counts the algorithmic factor bytes -- the band factor
     n(bw+1) b_f written once and read by every substitution (2 per solve: x0 and each correction) -- plus the
     coefficient read, over the library's per-launch CUDA-event time of the Cholesky-IR kernels."""
+    import numpy as np
     from paper_2503_05533_b200 import Context, precision
     cfg = W.CONFIGS["C3"]
     ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
@@ -428,9 +429,14 @@ def c3_leg(local, torch):
 
             alg = solve_bytes(Nf, s[7]) + (solve_bytes(Nc, s[8]) if l else 0.0)
             gbs = alg / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+            # IR-step histogram of the fine solves: a separate untimed pass over
+            # the same samples with per-sample records
+            ps = ctx.sample_level(l, n, cfg["seed"], 0, prec, prec, cfg["tol"], cfg["tol"], per_sample=True).per_sample
+            steps, counts = np.unique(ps[:, 2].astype(int), return_counts=True)
             out[f"l{l}_{'fp16' if uf == 'h' else 'fp32'}"] = {
                 "h": f"1/{Nf}", "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
                 "mean_ir_steps_fine": s[7] / n, "max_ir_steps_fine": s[9], "failures": s[6],
+                "ir_steps_histogram_fine": {str(int(a)): int(b) for a, b in zip(steps, counts)},
                 "k4_ms": k_ms, "k4_algorithmic_GB": alg / 1e9, "k4_achieved_GBs": gbs,
                 "k4_hbm_frac": gbs / HBM_PEAK_GBS}
     ctx.close()
@@ -465,6 +471,24 @@ def fine_leg(local, torch):
         out[f"h=1/{N}"] = {"systems": nb, "minres_steps_each": s[7] / nb, "kernel_ms": k_ms,
                            "unknown_steps_per_s": node_steps / (k_ms / 1e3), "achieved_GBs_40B": gbs,
                            "hbm_frac": gbs / HBM_PEAK_GBS, "bound": "hbm"}
+    # K3m-t, the temporally blocked MG-PCG on the same meshes (NEXT-4): a real solve to 1e-6, 148 systems.
+    # Algorithmic bytes per fine unknown and CG step: 106 on the fine level (passes C 44, A 37, B 25) + 37
+    # for the coarser levels' plain V-cycle passes = 143 B (ncu measured 147).
+    mg = precision("mgcg")
+    for level in (5, 6):
+        N = cfg["h0_inv"] << level
+        ctx.sample_level_async(level, 2, cfg["seed"], 10**6, mg, mg, 1e-6, 1e-6, sums_out=sums)
+        ctx.profile_enable(True)
+        ctx.sample_level_async(level, nb, cfg["seed"], 0, mg, mg, 1e-6, 1e-6, sums_out=sums)
+        prof = ctx.profile_read()
+        ctx.profile_enable(False)
+        s = sums.cpu().numpy()
+        k_ms = sum(r[3] for r in prof if r[0] == "minres" and r[1] == N)
+        node_steps = s[7] * (N - 1) ** 2
+        gbs = 143.0 * node_steps / (k_ms / 1e3) / 1e9
+        out[f"mgpcg h=1/{N}"] = {"systems": nb, "cg_steps_mean": s[7] / nb, "kernel_ms": k_ms,
+                                 "unknown_steps_per_s": node_steps / (k_ms / 1e3), "achieved_GBs_143B": gbs,
+                                 "hbm_frac": gbs / HBM_PEAK_GBS, "bound": "hbm"}
     ctx.close()
     return out
 

@@ -21,6 +21,7 @@
 // system in shared memory (binary64: p and the fine conductances; binary32: u, f, residual and the
 // conductances of every level), r and A p in registers (thread-strided nodes); two fused reductions
 // per CG step.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cfloat>
 #include <cstdint>
@@ -150,7 +151,8 @@ __device__ __forceinline__ void lsync(int g) {
 
 template <int NL, int NT, int T, int GROUPS>
 __device__ __forceinline__ void l_rbgs(const Lvl& L, int col, int tg, int g) {
-    constexpr int C = NL - 1, GL = NL + 1;
+    constexpr int C = NL - 1, GL = NL + 1, UR = NL >= 128 ? 4 : 1;   // big (global-memory) levels: more loads in flight
+#pragma unroll (UR)
     for (int q = tg; q < ((C + 1) / 2) * C; q += NT) {
         const int pr = q / C, w = q % C;
         int j = 2 * pr + 1;
@@ -190,7 +192,7 @@ __device__ __forceinline__ Lvl lvl_at(float* fb) {
 template <int N, int NL, int T, int GROUPS>
 __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
     constexpr int NT = NL >= MG_SMALL ? T : (T >= 32 ? 32 : T);
-    constexpr int GL = NL + 1, C = NL - 1;
+    constexpr int GL = NL + 1, C = NL - 1, UR = NL >= 128 ? 4 : 1;
     const Lvl L = lvl_at<N, NL>(fb);
     if (NT != T && tg >= NT) return;                    // small levels: one warp
     if constexpr (NL == 2) {                            // one unknown: exact
@@ -202,6 +204,7 @@ __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
     } else {
         // first red sweep from u = 0 (the Dirichlet ring of u is zeroed once per system in mg_setup):
         // red nodes u = f / diag, black nodes u = 0 -- one pass instead of a zero fill plus a sweep
+#pragma unroll (UR)
         for (int e = tg; e < C * C; e += NT) {
             const int i = e % C + 1, j = e / C + 1, c = j * GL + i;
             float v = 0.0f;
@@ -210,6 +213,7 @@ __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
         }
         lsync<NT, T, GROUPS>(g);
         l_rbgs<NL, NT, T, GROUPS>(L, 1, tg, g);
+#pragma unroll (UR)
         for (int e = tg; e < C * C; e += NT) {         // t = f - A u
             const int c = (e / C + 1) * GL + (e % C + 1);
             const float ce = L.ce[c], cw = L.ce[c - 1], cn = L.cn[c], cs = L.cn[c - GL];
@@ -238,6 +242,7 @@ __device__ __forceinline__ void vcyc(float* fb, int tg, int g) {
         lsync<NT, T, GROUPS>(g);
         vcyc<N, NC, T, GROUPS>(fb, tg, g);
         if constexpr (NT == T && NC < MG_SMALL && T > 32) gsync<T, GROUPS>(g);   // the warp's small levels are done
+#pragma unroll (UR)
         for (int e = tg; e < C * C; e += NT) {         // u += P u_{NL/2}
             const int i = e % C + 1, j = e / C + 1, c = j * GL + i;
             const int I = i >> 1, J = j >> 1;
@@ -576,61 +581,127 @@ mgcg_gm_kernel(const double* __restrict__ a_all, int nb, double tol, int max_ite
 // ---- K3m-t: the streamed-mesh MG-PCG with temporal blocking (default for h = 1/128 .. 1/512).
 // The fine level's ten grid passes per CG step become three:
 //   A (tiles): r_k = r_{k-1} - alpha q, f = r_k in binary32, first red sweep, black sweep, residual
-//      t = f - A u and restriction P^T t -- on a 128 x 32 tile with a 4-node halo held in shared
-//      memory (the halo is recomputed, never exchanged); stores r_k, u and the coarse right-hand side;
+//      t = f - A u and restriction P^T t -- on a 64 x 32 tile with a 4-node halo (recomputed, never
+//      exchanged); stores r_k, u and the coarse right-hand side;
 //   B (tiles): u += P u_c, black sweep, red sweep -> z, r^T z -- 2-node halo; stores z;
-//   C (plain): p_{k+1} = z + beta p_k and q = A p_{k+1} formed together (p_{k+1} at the four
+//   C (tiles): p_{k+1} = z + beta p_k and q = A p_{k+1} formed together (p_{k+1} at the four
 //      neighbours recomputed from p_k and z), p^T q, 1^T p.
-// r and p are ping-pong buffers (a tile's halo must read the previous iterate even where the
-// neighbouring tile has already written the new one); z has its own grid.  Per node and step
-// every value is the on-chip kernel's, with the same operations in the same order; only the
-// partial-sum order of the dot products differs.  Coarser levels: vcyc from h = 2/N as above.
-#ifndef MG_TL_T
-#define MG_TL_T 512
-#endif
-#ifndef MG_TL_MINB
-#define MG_TL_MINB 1
-#endif
-template <int N>
-struct MgTl {
-    static constexpr int T = MG_TL_T;
-    static constexpr int G = N + 1;
-    static constexpr size_t GG = (size_t)G * G;
-    static constexpr int TX = N >= 128 ? 128 : N, TY = 32, H = 4;
-    static constexpr int RX = TX + 2 * H, RY = TY + 2 * H, RN = RX * RY;
-    static constexpr int NTX = (N - 1 + TX - 1) / TX, NTY = (N - 1 + TY - 1) / TY;
-    static constexpr size_t D_END = 7 * GG;                                  // p0 p1 cE cN r0 r1 q
-    static constexpr size_t F_END = (MgCfg<N, 32, 1>::F_END + 31) / 32 * 32;
-    static constexpr size_t SYS = ((D_END * 8 + F_END * 4) + 255) / 256 * 256;
-    static constexpr size_t SMEM = (size_t)4 * RN * 4 + 2 * (T / 32) * 8 + 16;
-};
+// The tiles' inputs arrive as TMA boxes (72 x 40, zero-filled outside the grid) in two shared-memory
+// stages, so the next tile streams in while this one is computed (as K3c).  r and p are ping-pong
+// planes (a tile's halo must read the previous iterate where the neighbouring tile has already
+// written the new one); z has its own plane.  Per node and step every value is the on-chip kernel's,
+// with the same operations in the same order; only the partial-sum order of the dot products
+// differs.  Coarser levels: vcyc from h = 2/N in the on-chip layout.
+//
+// Per-CTA scratch: binary64 planes [7][N+1][GP] (p0 p1 cE cN r0 r1 q), binary32 planes [4][N+1][GP]
+// (ce cn u z), GP = N + 4 with grid column i stored at i + 3 (so every box starts 16-byte aligned),
+// then the on-chip level layout (level 0 only as set-up temporaries).
+namespace tl {
+constexpr int T = 512;
+constexpr int TX = 64, TY = 32, H = 4;
+constexpr int BX = TX + 2 * H, BY = TY + 2 * H, BN = BX * BY;          // 72 x 40 box
+constexpr int B64 = BN * 8, B32 = BN * 4;                               // box bytes (multiples of 128)
+constexpr int STAGE = 2 * B64 + 3 * B32;     // A: R, Q | CE, CN; B: R | CE, CN, U; C: P, CE64, CN64 | Z
+static_assert(3 * B64 + B32 == STAGE, "pass C's boxes fill the same stage");
+constexpr size_t SMEM = 2 * (size_t)STAGE + 2 * (size_t)B32 + 2 * (T / 32) * 8 + 2 * 8 + 16;
+enum { P0, P1, DCE, DCN, R0, R1, DQ, ND };                               // binary64 planes
+enum { FCE, FCN, FU, FZ, NF };                                           // binary32 planes
+__host__ __device__ constexpr int gp(int N) { return N + 4; }
+}  // namespace tl
 
 template <int N>
-__global__ void __launch_bounds__(MG_TL_T, MG_TL_MINB)
-mgcg_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
+struct MgTl {
+    static constexpr int GP = tl::gp(N);
+    static constexpr size_t PL = (size_t)GP * (N + 1);                   // elements per plane
+    static constexpr size_t D_BYTES = tl::ND * PL * 8;
+    static constexpr size_t F_BYTES = tl::NF * PL * 4;
+    static constexpr size_t F_END = (MgCfg<N, 32, 1>::F_END + 31) / 32 * 32;   // on-chip level layout
+    static constexpr size_t SYS = (D_BYTES + F_BYTES + F_END * 4 + 255) / 256 * 256;
+    static constexpr int NTX = (N - 1 + tl::TX - 1) / tl::TX, NTY = (N - 1 + tl::TY - 1) / tl::TY;
+    static constexpr int NT = NTX * NTY;
+};
+
+__device__ __forceinline__ uint32_t mg_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mg_mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mg_tma(uint32_t dst, const CUtensorMap* map, int x, int y, int plane, int cta,
+                                       uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+            "r"(dst), "l"(map), "r"(x), "r"(y), "r"(plane), "r"(cta), "r"(bar)
+        : "memory");
+}
+
+// issue tile t of pass A (mode 0: r_old = plane v, q | ce, cn), B (mode 1: r_new = plane v | ce, cn, u) or
+// C (mode 2: p_old = plane v, cE, cN | z) into stage s
+template <int N>
+__device__ __forceinline__ void mg_issue(const CUtensorMap* m64, const CUtensorMap* m32, unsigned char* stage0,
+                                         uint32_t bar0, int cta, int t, int s, int mode, int v) {
+    using K = MgTl<N>;
+    const int x = (t % K::NTX) * tl::TX;                          // stored column of node x0 - H
+    const int y = 1 + (t / K::NTX) * tl::TY - tl::H;
+    const uint32_t dst = mg_smem_u32(stage0 + (size_t)s * tl::STAGE), bar = bar0 + 8 * s;
+    const uint32_t bytes = mode == 0 ? 2 * tl::B64 + 2 * tl::B32 : mode == 1 ? tl::B64 + 3 * tl::B32 : 3 * tl::B64 + tl::B32;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    mg_tma(dst, m64, x, y, v, cta, bar);
+    if (mode == 2) {
+        mg_tma(dst + tl::B64, m64, x, y, tl::DCE, cta, bar);
+        mg_tma(dst + 2 * tl::B64, m64, x, y, tl::DCN, cta, bar);
+        mg_tma(dst + 3 * tl::B64, m32, x, y, tl::FZ, cta, bar);
+        return;
+    }
+    if (mode == 0) mg_tma(dst + tl::B64, m64, x, y, tl::DQ, cta, bar);
+    mg_tma(dst + 2 * tl::B64, m32, x, y, tl::FCE, cta, bar);
+    mg_tma(dst + 2 * tl::B64 + tl::B32, m32, x, y, tl::FCN, cta, bar);
+    if (mode == 1) mg_tma(dst + 2 * tl::B64 + 2 * tl::B32, m32, x, y, tl::FU, cta, bar);
+}
+
+template <int N>
+__global__ void __launch_bounds__(tl::T, 1)
+mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant__ CUtensorMap m32,
+                 const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
                  int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order,
                  unsigned char* __restrict__ scratch) {
     using K = MgTl<N>;
-    constexpr int T = K::T, G = K::G, C = N - 1, n = C * C, P = 2 * N * N;
-    constexpr int RX = K::RX, RN = K::RN, H = K::H, TX = K::TX, TY = K::TY;
+    constexpr int T = tl::T, GP = K::GP, C = N - 1, n = C * C, P = 2 * N * N;
+    constexpr int BX = tl::BX, BN = tl::BN, H = tl::H, TX = tl::TX, TY = tl::TY, NT = K::NT;
     constexpr int NC = N / 2, GC = NC + 1;
-    extern __shared__ __align__(16) unsigned char smem[];
-    float* sf = reinterpret_cast<float*>(smem);       // f, then t (pass A)
-    float* sce = sf + RN;
-    float* scn = sce + RN;
-    float* su = scn + RN;
-    double* red = reinterpret_cast<double*>(su + RN);
-    int* jobslot = reinterpret_cast<int*>(red + 2 * (T / 32));
-    const int tg = threadIdx.x;
-    double* dg = reinterpret_cast<double*>(scratch + (size_t)blockIdx.x * K::SYS);
-    double* pb[2] = {dg, dg + K::GG};
-    double* cE = dg + 2 * K::GG;
-    double* cN = dg + 3 * K::GG;
-    double* rb[2] = {dg + 4 * K::GG, dg + 5 * K::GG};
-    double* qg = dg + 6 * K::GG;
-    float* fb = reinterpret_cast<float*>(dg + K::D_END);
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* stage0 = smem;
+    float* sf = reinterpret_cast<float*>(smem + 2 * tl::STAGE);     // f, then t (pass A)
+    float* su = sf + BN;
+    double* red = reinterpret_cast<double*>(su + BN);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * (T / 32));
+    int* jobslot = reinterpret_cast<int*>(bars + 2);
+    const int tg = threadIdx.x, cta = blockIdx.x;
+    unsigned char* base = scratch + (size_t)cta * K::SYS;
+    double* D = reinterpret_cast<double*>(base);
+    float* F = reinterpret_cast<float*>(base + K::D_BYTES);
+    float* fb = reinterpret_cast<float*>(base + K::D_BYTES + K::F_BYTES);    // on-chip level layout
+    auto dpl = [&](int pl) { return D + (size_t)pl * K::PL; };
+    auto fpl = [&](int pl) { return F + (size_t)pl * K::PL; };
+    double* cE = dpl(tl::DCE);
+    double* cN = dpl(tl::DCN);
+    double* qg = dpl(tl::DQ);
+    float* ug = fpl(tl::FU);
+    float* zg = fpl(tl::FZ);
     const double h = 1.0 / N, h2 = h * h;
-    auto cix = [](int e) { return (e / C + 1) * G + (e % C + 1); };
+    const uint32_t bar0 = mg_smem_u32(&bars[0]);
+    if (tg == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    auto gix = [](int i, int j) { return j * GP + i + 3; };
     auto interior = [](int i, int j) { return i >= 1 && i <= C && j >= 1 && j <= C; };
 
     for (;;) {
@@ -641,210 +712,195 @@ mgcg_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_i
         if (job >= nb) break;
         const int sj = order ? __ldg(order + job) : job;
         const double* a = a_all + (size_t)sj * P;
-        mg_setup<N, T, 1>(a, cE, cN, pb[0], fb, tg, 0);
-        const Lvl L0 = level_rt<N>(fb, 0);     // u = pre-smoothed u, f = z; t unused
-        const Lvl L1 = level_rt<N>(fb, 1);
-        float* zg = L0.f;
-        for (int c = tg; c < (int)K::GG; c += T) {
-            const int i = c % G, j = c / G;
-            pb[1][c] = 0.0;
-            rb[0][c] = interior(i, j) ? h2 : 0.0;
-            rb[1][c] = 0.0;
-            qg[c] = 0.0;
-            zg[c] = 0.0f;
+        // on-chip-layout levels (coarse levels; level 0 as temporaries); its binary64 outputs go to
+        // planes that are re-initialised below
+        mg_setup<N, T, 1>(a, dpl(tl::R1), dpl(tl::DQ), dpl(tl::P1), fb, tg, 0);
+        for (int e = tg; e < (int)K::PL; e += T) {
+            const int i = e % GP - 3, j = e / GP;
+            double ce = 0.0, cn = 0.0;
+            if (i >= 0 && i < N && j >= 1 && j < N)
+                ce = 0.5 * (__ldg(a + 2 * (j * N + i)) + __ldg(a + 2 * ((j - 1) * N + i) + 1));
+            if (i >= 1 && i < N && j < N) cn = 0.5 * (__ldg(a + 2 * (j * N + i) + 1) + __ldg(a + 2 * (j * N + i - 1)));
+            D[e] = 0.0;                                     // p0
+            D[K::PL + e] = 0.0;                             // p1
+            cE[e] = ce;
+            cN[e] = cn;
+            D[tl::R0 * K::PL + e] = interior(i, j) ? h2 : 0.0;
+            D[tl::R1 * K::PL + e] = 0.0;
+            qg[e] = 0.0;
+            F[e] = (float)ce;
+            F[K::PL + e] = (float)cn;
+            ug[e] = 0.0f;
+            zg[e] = 0.0f;
         }
-        __syncthreads();
-        int cr = 0, cp = 0;            // current r / p buffers
+        const Lvl L1 = level_rt<N>(fb, 1);
+        int cr = 0, cp = 0;            // current r / p planes (R0 + cr, P0 + cp)
 
-        // ---- pass A: r_new = r_old - alpha q, pre-smoothing, residual, restriction
-        auto pass_a = [&](double alpha) {
-            const double* ro = rb[cr];
-            double* rn = rb[cr ^ 1];
-            double rr = 0.0;
-            for (int ty = 0; ty < K::NTY; ++ty)
-                for (int tx = 0; tx < K::NTX; ++tx) {
-                    const int x0 = 1 + tx * TX, y0 = 1 + ty * TY;
-                    const int xe = min(x0 + TX, N), ye = min(y0 + TY, N);       // owned: [x0, xe) x [y0, ye)
-                    auto inreg = [&](int i, int j, int hh) {
-                        return i >= x0 - hh && i < xe + hh && j >= y0 - hh && j < ye + hh;
-                    };
-#pragma unroll 4
-                    for (int k = tg; k < RN; k += T) {
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
-                        float f = 0.0f, ce = 0.0f, cn = 0.0f;
-                        if (i >= 0 && i <= N && j >= 0 && j <= N && inreg(i, j, H)) {
-                            const int c = j * G + i;
-                            ce = L0.ce[c];
-                            cn = L0.cn[c];
-                            if (interior(i, j)) {
-                                const double r = fma(-alpha, qg[c], ro[c]);
-                                f = (float)r;
-                                if (inreg(i, j, 0)) {
-                                    rn[c] = r;
-                                    rr = fma(r, r, rr);
-                                }
+        // ---- tile loop of pass A or B (TMA double buffer; first two tiles issued here)
+        // mode 0 = pass A (coef = alpha, acc = r^T r), 1 = pass B (acc = r^T z), 2 = pass C (coef = beta,
+        // acc = p^T q, acc2 = 1^T p)
+        auto run_pass = [&](int mode, double coef, double& acc, double& acc2) {
+            const bool pass_a = mode == 0;
+            const int ro = mode == 2 ? tl::P0 + cp : tl::R0 + cr;      // A: r_old; B: r_new; C: p_old
+            double* rn = dpl(tl::R0 + (cr ^ 1));
+            double* pn = dpl(tl::P0 + (cp ^ 1));
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // generic stores -> TMA reads
+            __syncthreads();
+            if (tg == 0) {
+                mg_issue<N>(&m64, &m32, stage0, bar0, cta, 0, 0, mode, ro);
+                if (NT > 1) mg_issue<N>(&m64, &m32, stage0, bar0, cta, 1, 1, mode, ro);
+            }
+            const float* U = L1.u;
+            for (int t = 0; t < NT; ++t) {
+                const int s = t & 1;
+                mg_mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
+                phase ^= 1u << s;
+                const unsigned char* st = stage0 + (size_t)s * tl::STAGE;
+                const double* R = reinterpret_cast<const double*>(st);
+                const double* Q = reinterpret_cast<const double*>(st + tl::B64);
+                const float* CE = reinterpret_cast<const float*>(st + 2 * tl::B64);
+                const float* CN = CE + BN;
+                const float* UU = CN + BN;
+                const int x0 = 1 + (t % K::NTX) * TX, y0 = 1 + (t / K::NTX) * TY;
+                const int xe = min(x0 + TX, N), ye = min(y0 + TY, N);
+                auto inreg = [&](int i, int j, int hh) {
+                    return i >= x0 - hh && i < xe + hh && j >= y0 - hh && j < ye + hh;
+                };
+                auto black = [&](int hh) {
+                    for (int k = tg; k < BN; k += T) {
+                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
+                        if (interior(i, j) && inreg(i, j, hh) && ((i + j) & 1)) {
+                            const float ce = CE[k], cw = CE[k - 1], cn = CN[k], cs = CN[k - BX];
+                            float sv = sf[k];
+                            sv = fmaf(ce, su[k + 1], sv);
+                            sv = fmaf(cw, su[k - 1], sv);
+                            sv = fmaf(cn, su[k + BX], sv);
+                            sv = fmaf(cs, su[k - BX], sv);
+                            su[k] = __fdividef(sv, (ce + cw) + (cn + cs));
+                        }
+                    }
+                };
+                if (mode == 2) {
+                    // p_new = z + beta p_old and q = A p_new on the owned nodes (p_new at the neighbours
+                    // recomputed from the box)
+                    const double* PB = R;
+                    const double* E64 = PB + BN;
+                    const double* N64 = E64 + BN;
+                    const float* ZB = reinterpret_cast<const float*>(N64 + BN);
+                    auto pnew = [&](int kk) { return fma(coef, PB[kk], (double)ZB[kk]); };
+                    for (int k = tg; k < BN; k += T) {
+                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
+                        if (interior(i, j) && inreg(i, j, 0)) {
+                            const double ce = E64[k], cw = E64[k - 1], cn = N64[k], cs = N64[k - BX];
+                            const double pv = pnew(k);
+                            double Ap = ((ce + cw) + (cn + cs)) * pv;
+                            Ap = fma(-ce, pnew(k + 1), Ap);
+                            Ap = fma(-cw, pnew(k - 1), Ap);
+                            Ap = fma(-cn, pnew(k + BX), Ap);
+                            Ap = fma(-cs, pnew(k - BX), Ap);
+                            const int c = gix(i, j);
+                            qg[c] = Ap;
+                            pn[c] = pv;
+                            acc = fma(pv, Ap, acc);
+                            acc2 += pv;
+                        }
+                    }
+                } else if (pass_a) {
+                    for (int k = tg; k < BN; k += T) {       // r_k, f = (float) r_k; first red sweep
+                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
+                        float f = 0.0f;
+                        if (interior(i, j) && inreg(i, j, H)) {
+                            const double r = fma(-coef, Q[k], R[k]);
+                            f = (float)r;
+                            if (inreg(i, j, 0)) {
+                                rn[gix(i, j)] = r;
+                                acc = fma(r, r, acc);
                             }
                         }
                         sf[k] = f;
-                        sce[k] = ce;
-                        scn[k] = cn;
-                    }
-                    __syncthreads();
-                    for (int k = tg; k < RN; k += T) {       // first red sweep from u = 0
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
                         float u = 0.0f;
                         if (interior(i, j) && inreg(i, j, H - 1) && !((i + j) & 1))
-                            u = __fdividef(sf[k], (sce[k] + sce[k - 1]) + (scn[k] + scn[k - RX]));
+                            u = __fdividef(f, (CE[k] + CE[k - 1]) + (CN[k] + CN[k - BX]));
                         su[k] = u;
                     }
                     __syncthreads();
-                    for (int k = tg; k < RN; k += T) {       // black sweep
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
-                        if (interior(i, j) && inreg(i, j, H - 2) && ((i + j) & 1)) {
-                            const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
-                            float s = sf[k];
-                            s = fmaf(ce, su[k + 1], s);
-                            s = fmaf(cw, su[k - 1], s);
-                            s = fmaf(cn, su[k + RX], s);
-                            s = fmaf(cs, su[k - RX], s);
-                            su[k] = __fdividef(s, (ce + cw) + (cn + cs));
-                        }
-                    }
+                    black(H - 2);
                     __syncthreads();
-                    for (int k = tg; k < RN; k += T) {       // t = f - A u (in place of f); store u
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                    for (int k = tg; k < BN; k += T) {       // t = f - A u (in place of f); store u
+                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
                         if (interior(i, j) && inreg(i, j, 1)) {
-                            const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
+                            const float ce = CE[k], cw = CE[k - 1], cn = CN[k], cs = CN[k - BX];
                             float Au = ((ce + cw) + (cn + cs)) * su[k];
                             Au = fmaf(-ce, su[k + 1], Au);
                             Au = fmaf(-cw, su[k - 1], Au);
-                            Au = fmaf(-cn, su[k + RX], Au);
-                            Au = fmaf(-cs, su[k - RX], Au);
+                            Au = fmaf(-cn, su[k + BX], Au);
+                            Au = fmaf(-cs, su[k - BX], Au);
                             sf[k] = sf[k] - Au;
-                            if (inreg(i, j, 0)) L0.u[j * G + i] = su[k];
+                            if (inreg(i, j, 0)) ug[gix(i, j)] = su[k];
                         }
                     }
                     __syncthreads();
-                    // f_c = P^T t for the coarse nodes whose centre (2I, 2J) this tile owns
                     const int Ilo = max(1, (x0 + 1) / 2), Ihi = min(NC - 1, (xe - 1) / 2);
                     const int Jlo = max(1, (y0 + 1) / 2), Jhi = min(NC - 1, (ye - 1) / 2);
                     const int nI = Ihi - Ilo + 1, nJ = Jhi - Jlo + 1;
                     if (nI > 0 && nJ > 0)
                         for (int e = tg; e < nI * nJ; e += T) {
                             const int I = Ilo + e % nI, J = Jlo + e / nI;
-                            const int k = (2 * J - y0 + H) * RX + (2 * I - x0 + H);
-                            L1.f[J * GC + I] = sf[k] + 0.5f * ((sf[k + 1] + sf[k - 1]) + (sf[k + RX] + sf[k - RX]) +
-                                                               (sf[k + RX + 1] + sf[k - RX - 1]));
+                            const int k = (2 * J - y0 + H) * BX + (2 * I - x0 + H);
+                            L1.f[J * GC + I] = sf[k] + 0.5f * ((sf[k + 1] + sf[k - 1]) + (sf[k + BX] + sf[k - BX]) +
+                                                               (sf[k + BX + 1] + sf[k - BX - 1]));
                         }
-                    __syncthreads();
-                }
-            cr ^= 1;
-            return rr;
-        };
-
-        // ---- pass B: u += P u_c, post-smoothing (black, red) -> z, r^T z
-        auto pass_b = [&]() {
-            const double* rn = rb[cr];
-            const float* U = L1.u;
-            double rz = 0.0;
-            for (int ty = 0; ty < K::NTY; ++ty)
-                for (int tx = 0; tx < K::NTX; ++tx) {
-                    const int x0 = 1 + tx * TX, y0 = 1 + ty * TY;
-                    const int xe = min(x0 + TX, N), ye = min(y0 + TY, N);
-                    auto inreg = [&](int i, int j, int hh) {
-                        return i >= x0 - hh && i < xe + hh && j >= y0 - hh && j < ye + hh;
-                    };
-#pragma unroll 4
-                    for (int k = tg; k < RN; k += T) {
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
-                        float f = 0.0f, ce = 0.0f, cn = 0.0f, u = 0.0f;
-                        if (i >= 0 && i <= N && j >= 0 && j <= N && inreg(i, j, 2)) {
-                            const int c = j * G + i;
-                            ce = L0.ce[c];
-                            cn = L0.cn[c];
-                            if (interior(i, j)) {
-                                f = (float)rn[c];
-                                const int I = i >> 1, J = j >> 1;
-                                float v;
-                                if (!(i & 1) && !(j & 1)) v = U[J * GC + I];
-                                else if ((i & 1) && !(j & 1)) v = 0.5f * (U[J * GC + I] + U[J * GC + I + 1]);
-                                else if (!(i & 1) && (j & 1)) v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I]);
-                                else v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I + 1]);
-                                u = L0.u[c] + v;
-                            }
+                } else {
+                    for (int k = tg; k < BN; k += T) {       // f = (float) r_k, u = u_pre + P u_c
+                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
+                        float f = 0.0f, u = 0.0f;
+                        if (interior(i, j) && inreg(i, j, 2)) {
+                            f = (float)R[k];
+                            const int I = i >> 1, J = j >> 1;
+                            float v;
+                            if (!(i & 1) && !(j & 1)) v = U[J * GC + I];
+                            else if ((i & 1) && !(j & 1)) v = 0.5f * (U[J * GC + I] + U[J * GC + I + 1]);
+                            else if (!(i & 1) && (j & 1)) v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I]);
+                            else v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I + 1]);
+                            u = UU[k] + v;
                         }
                         sf[k] = f;
-                        sce[k] = ce;
-                        scn[k] = cn;
                         su[k] = u;
                     }
                     __syncthreads();
-                    for (int k = tg; k < RN; k += T) {       // black sweep
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
-                        if (interior(i, j) && inreg(i, j, 1) && ((i + j) & 1)) {
-                            const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
-                            float s = sf[k];
-                            s = fmaf(ce, su[k + 1], s);
-                            s = fmaf(cw, su[k - 1], s);
-                            s = fmaf(cn, su[k + RX], s);
-                            s = fmaf(cs, su[k - RX], s);
-                            su[k] = __fdividef(s, (ce + cw) + (cn + cs));
-                        }
-                    }
+                    black(1);
                     __syncthreads();
-                    for (int k = tg; k < RN; k += T) {       // red sweep on the owned nodes; z out
-                        const int i = x0 - H + k % RX, j = y0 - H + k / RX;
+                    for (int k = tg; k < BN; k += T) {       // red sweep on the owned nodes; z out
+                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
                         if (interior(i, j) && inreg(i, j, 0)) {
                             float z = su[k];
                             if (!((i + j) & 1)) {
-                                const float ce = sce[k], cw = sce[k - 1], cn = scn[k], cs = scn[k - RX];
-                                float s = sf[k];
-                                s = fmaf(ce, su[k + 1], s);
-                                s = fmaf(cw, su[k - 1], s);
-                                s = fmaf(cn, su[k + RX], s);
-                                s = fmaf(cs, su[k - RX], s);
-                                z = __fdividef(s, (ce + cw) + (cn + cs));
+                                const float ce = CE[k], cw = CE[k - 1], cn = CN[k], cs = CN[k - BX];
+                                float sv = sf[k];
+                                sv = fmaf(ce, su[k + 1], sv);
+                                sv = fmaf(cw, su[k - 1], sv);
+                                sv = fmaf(cn, su[k + BX], sv);
+                                sv = fmaf(cs, su[k - BX], sv);
+                                z = __fdividef(sv, (ce + cw) + (cn + cs));
                             }
-                            const int c = j * G + i;
-                            zg[c] = z;
-                            rz = fma(rn[c], (double)z, rz);
+                            zg[gix(i, j)] = z;
+                            acc = fma(R[k], (double)z, acc);
                         }
                     }
-                    __syncthreads();
                 }
-            return rz;
-        };
-
-        // ---- pass C: p_new = z + beta p_old and q = A p_new; p^T q, 1^T p
-        auto pass_c = [&](double beta, double& pq, double& sp) {
-            const double* po = pb[cp];
-            double* pn = pb[cp ^ 1];
-            pq = 0.0;
-            sp = 0.0;
-#pragma unroll 2
-            for (int e = tg; e < n; e += T) {
-                const int c = cix(e);
-                auto pnew = [&](int cc) { return fma(beta, po[cc], (double)zg[cc]); };
-                const double ce = cE[c], cw = cE[c - 1], cn = cN[c], cs = cN[c - G];
-                const double pv = pnew(c);
-                double Ap = ((ce + cw) + (cn + cs)) * pv;
-                Ap = fma(-ce, pnew(c + 1), Ap);
-                Ap = fma(-cw, pnew(c - 1), Ap);
-                Ap = fma(-cn, pnew(c + G), Ap);
-                Ap = fma(-cs, pnew(c - G), Ap);
-                qg[c] = Ap;
-                pn[c] = pv;
-                pq = fma(pv, Ap, pq);
-                sp += pv;
+                __syncthreads();                            // stage s, sf, su free
+                if (tg == 0 && t + 2 < NT) mg_issue<N>(&m64, &m32, stage0, bar0, cta, t + 2, s, mode, ro);
             }
-            cp ^= 1;
+            if (mode == 0) cr ^= 1;
+            if (mode == 2) cp ^= 1;
         };
 
         // ---- PCG from x0 = 0 (r_0 = b, q = 0, p = 0, alpha = beta = 0 for the first passes)
-        double rr = pass_a(0.0);
+        double rr = 0.0, rz = 0.0, dummy = 0.0;
+        run_pass(0, 0.0, rr, dummy);
         __syncthreads();
         vcyc<N, NC, T, 1>(fb, tg, 0);
-        double rz = pass_b();
+        run_pass(1, 0.0, rz, dummy);
         double2 S = gsum2<T, 1>(rz, rr, red, tg, 0);
         rz = S.x;
         const double bnorm = sqrt(S.y);
@@ -853,16 +909,18 @@ mgcg_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_i
         int it = 0, status = 1;
         if (bnorm == 0.0) status = 0;
         while (status == 1 && it < max_iter) {
-            double pq, sp;
-            pass_c(beta, pq, sp);
+            double pq = 0.0, sp = 0.0;
+            run_pass(2, beta, pq, sp);
             S = gsum2<T, 1>(pq, sp, red, tg, 0);
             const double alpha = rz / S.x;
             Xq = fma(alpha, S.y, Xq);
-            rr = pass_a(alpha);
+            rr = 0.0;
+            run_pass(0, alpha, rr, dummy);
             ++it;
             __syncthreads();
             vcyc<N, NC, T, 1>(fb, tg, 0);
-            const double rz_new = pass_b();
+            double rz_new = 0.0;
+            run_pass(1, 0.0, rz_new, dummy);
             S = gsum2<T, 1>(rz_new, rr, red, tg, 0);
             rnorm = sqrt(S.y);
             if (!(rnorm == rnorm)) { status = 3; break; }
@@ -884,18 +942,29 @@ mgcg_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_i
 template <int N>
 cudaError_t run_mg_tile(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
                         const int* order, void* scratch, int nctas, cudaStream_t s) {
+    using K = MgTl<N>;
     if (!scratch || nctas < 1) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(mgcg_tile_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)MgTl<N>::SMEM);
+                                             (int)tl::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const uint64_t grid = std::min<uint64_t>(nb, (uint64_t)nctas);
     if (grid == 0) return cudaSuccess;
-    mgcg_tile_kernel<N><<<(unsigned)grid, MgTl<N>::T, MgTl<N>::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr,
-                                                                          order, static_cast<unsigned char*>(scratch));
+    CUtensorMap m64, m32;
+    const uint64_t d64[4] = {(uint64_t)K::GP, (uint64_t)N + 1, (uint64_t)tl::ND, grid};
+    const uint64_t s64[3] = {(uint64_t)K::GP * 8, K::PL * 8, K::SYS};
+    const uint64_t d32[4] = {(uint64_t)K::GP, (uint64_t)N + 1, (uint64_t)tl::NF, grid};
+    const uint64_t s32[3] = {(uint64_t)K::GP * 4, K::PL * 4, K::SYS};
+    const uint32_t box[4] = {(uint32_t)tl::BX, (uint32_t)tl::BY, 1, 1};
+    unsigned char* sc = static_cast<unsigned char*>(scratch);
+    if (!encode_tensor_map(&m64, true, 4, sc, d64, s64, box) ||
+        !encode_tensor_map(&m32, false, 4, sc + K::D_BYTES, d32, s32, box))
+        return cudaErrorInvalidValue;
+    mgcg_tile_kernel<N><<<(unsigned)grid, tl::T, tl::SMEM, s>>>(m64, m32, a, (int)nb, tol, max_iter, out, slot, ctr,
+                                                               order, sc);
     return cudaGetLastError();
 }
 
@@ -956,7 +1025,7 @@ size_t mgcg_scratch_per_cta(int N) {
     }
 }
 
-int mgcg_ctas_per_sm(int N) { return N >= 128 && !use_mg_plain() ? MG_TL_MINB : 1; }
+int mgcg_ctas_per_sm(int N) { (void)N; return 1; }
 
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                         unsigned* ctr, const int* order, void* scratch, int nctas, cudaStream_t s) {

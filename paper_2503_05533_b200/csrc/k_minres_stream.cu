@@ -314,6 +314,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
+bool encode_tensor_map(void* map, bool f64, int rank, void* base, const uint64_t* dims, const uint64_t* strides,
+                       const uint32_t* box) {
+    auto enc = encode_fn();
+    if (!enc || rank < 1 || rank > 5) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], e[5];
+    for (int k = 0; k < rank; ++k) { d[k] = dims[k]; b[k] = box[k]; e[k] = 1; }
+    for (int k = 0; k + 1 < rank; ++k) st[k] = strides[k];
+    return enc(static_cast<CUtensorMap*>(map), f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+               (cuuint32_t)rank, base, d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool minres_stream_supported(int N) { return N == 128 || N == 256 || N == 512; }
 
 size_t minres_stream_scratch_per_cta(int N) { return sizeof(double) * NPLANE * (size_t)(N + 1) * pitch(N); }
