@@ -603,7 +603,8 @@ constexpr int BX = TX + 2 * H, BY = TY + 2 * H, BN = BX * BY;          // 72 x 4
 constexpr int B64 = BN * 8, B32 = BN * 4;                               // box bytes (multiples of 128)
 constexpr int STAGE = 2 * B64 + 3 * B32;     // A: R, Q | CE, CN; B: R | CE, CN, U; C: P, CE64, CN64 | Z
 static_assert(3 * B64 + B32 == STAGE, "pass C's boxes fill the same stage");
-constexpr size_t SMEM = 2 * (size_t)STAGE + 2 * (size_t)B32 + 2 * (T / 32) * 8 + 2 * 8 + 16;
+constexpr int CWX = TX / 2 + 4, CWY = TY / 2 + 4;                       // coarse window of a tile
+constexpr size_t SMEM = 2 * (size_t)STAGE + 2 * (size_t)B32 + (CWX * CWY * 4 + 7) / 8 * 8 + 2 * (T / 32) * 8 + 2 * 8 + 16;
 enum { P0, P1, DCE, DCN, R0, R1, DQ, ND };                               // binary64 planes
 enum { FCE, FCN, FU, FZ, NF };                                           // binary32 planes
 __host__ __device__ constexpr int gp(int N) { return N + 4; }
@@ -677,7 +678,8 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
     unsigned char* stage0 = smem;
     float* sf = reinterpret_cast<float*>(smem + 2 * tl::STAGE);     // f, then t (pass A)
     float* su = sf + BN;
-    double* red = reinterpret_cast<double*>(su + BN);
+    float* scu = su + BN;                                          // coarse u of the tile (pass B)
+    double* red = reinterpret_cast<double*>(scu + tl::CWX * tl::CWY);
     uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * (T / 32));
     int* jobslot = reinterpret_cast<int*>(bars + 2);
     const int tg = threadIdx.x, cta = blockIdx.x;
@@ -701,6 +703,13 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
     }
     __syncthreads();
     uint32_t phase = 0;
+    constexpr int MS = (BN + T - 1) / T;
+    int kxy[MS];                                                   // box coordinates of this thread's slots
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+        const int k = tg + m * T;
+        kxy[m] = (k % BX) | ((k / BX) << 16);
+    }
     auto gix = [](int i, int j) { return j * GP + i + 3; };
     auto interior = [](int i, int j) { return i >= 1 && i <= C && j >= 1 && j <= C; };
 
@@ -736,11 +745,11 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
         const Lvl L1 = level_rt<N>(fb, 1);
         int cr = 0, cp = 0;            // current r / p planes (R0 + cr, P0 + cp)
 
-        // ---- tile loop of pass A or B (TMA double buffer; first two tiles issued here)
+        // ---- tile loop of one pass (TMA double buffer; the first two tiles are issued here).
         // mode 0 = pass A (coef = alpha, acc = r^T r), 1 = pass B (acc = r^T z), 2 = pass C (coef = beta,
-        // acc = p^T q, acc2 = 1^T p)
+        // acc = p^T q, acc2 = 1^T p).  Thread tg owns box slots k = tg + m T (coordinates in kxy[m]); a
+        // stage touches the slots whose box coordinates fall in a per-tile window (span()).
         auto run_pass = [&](int mode, double coef, double& acc, double& acc2) {
-            const bool pass_a = mode == 0;
             const int ro = mode == 2 ? tl::P0 + cp : tl::R0 + cr;      // A: r_old; B: r_new; C: p_old
             double* rn = dpl(tl::R0 + (cr ^ 1));
             double* pn = dpl(tl::P0 + (cp ^ 1));
@@ -753,6 +762,23 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
             const float* U = L1.u;
             for (int t = 0; t < NT; ++t) {
                 const int s = t & 1;
+                const int x0 = 1 + (t % K::NTX) * TX, y0 = 1 + (t / K::NTX) * TY;
+                const int ox = x0 - H, oy = y0 - H;                     // grid node of box slot (0, 0)
+                const int wx = min(x0 + TX, N) - x0, wy = min(y0 + TY, N) - y0;   // owned extent
+                const int par = (ox + oy) & 1;                          // colour of slot (lx, ly): (lx + ly + par) & 1
+                // window of the interior nodes within hh of the owned region, in box coordinates
+                auto span = [&](int hh) {
+                    return make_int4(max(H - hh, 1 - ox), min(wx + H + hh - 1, C - ox), max(H - hh, 1 - oy),
+                                     min(wy + H + hh - 1, C - oy));
+                };
+                auto in = [](int4 w, int lx, int ly) { return lx >= w.x && lx <= w.y && ly >= w.z && ly <= w.w; };
+                const int cx0 = max(0, (x0 - 2) >> 1), cy0 = max(0, (y0 - 2) >> 1);
+                if (mode == 1) {                                        // coarse u of the tile -> smem
+                    for (int e = tg; e < tl::CWX * tl::CWY; e += T) {
+                        const int I = cx0 + e % tl::CWX, J = cy0 + e / tl::CWX;
+                        scu[e] = (I <= NC && J <= NC) ? U[J * GC + I] : 0.0f;
+                    }
+                }
                 mg_mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
                 phase ^= 1u << s;
                 const unsigned char* st = stage0 + (size_t)s * tl::STAGE;
@@ -761,15 +787,11 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
                 const float* CE = reinterpret_cast<const float*>(st + 2 * tl::B64);
                 const float* CN = CE + BN;
                 const float* UU = CN + BN;
-                const int x0 = 1 + (t % K::NTX) * TX, y0 = 1 + (t / K::NTX) * TY;
-                const int xe = min(x0 + TX, N), ye = min(y0 + TY, N);
-                auto inreg = [&](int i, int j, int hh) {
-                    return i >= x0 - hh && i < xe + hh && j >= y0 - hh && j < ye + hh;
-                };
-                auto black = [&](int hh) {
-                    for (int k = tg; k < BN; k += T) {
-                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
-                        if (interior(i, j) && inreg(i, j, hh) && ((i + j) & 1)) {
+                auto sweep = [&](int4 w, int colour) {                  // Gauss-Seidel on one colour
+#pragma unroll
+                    for (int m = 0; m < MS; ++m) {
+                        const int k = tg + m * T, lx = kxy[m] & 0xffff, ly = kxy[m] >> 16;
+                        if (k < BN && in(w, lx, ly) && ((lx + ly + par) & 1) == colour) {
                             const float ce = CE[k], cw = CE[k - 1], cn = CN[k], cs = CN[k - BX];
                             float sv = sf[k];
                             sv = fmaf(ce, su[k + 1], sv);
@@ -788,9 +810,11 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
                     const double* N64 = E64 + BN;
                     const float* ZB = reinterpret_cast<const float*>(N64 + BN);
                     auto pnew = [&](int kk) { return fma(coef, PB[kk], (double)ZB[kk]); };
-                    for (int k = tg; k < BN; k += T) {
-                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
-                        if (interior(i, j) && inreg(i, j, 0)) {
+                    const int4 w0 = span(0);
+#pragma unroll
+                    for (int m = 0; m < MS; ++m) {
+                        const int k = tg + m * T, lx = kxy[m] & 0xffff, ly = kxy[m] >> 16;
+                        if (k < BN && in(w0, lx, ly)) {
                             const double ce = E64[k], cw = E64[k - 1], cn = N64[k], cs = N64[k - BX];
                             const double pv = pnew(k);
                             double Ap = ((ce + cw) + (cn + cs)) * pv;
@@ -798,37 +822,40 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
                             Ap = fma(-cw, pnew(k - 1), Ap);
                             Ap = fma(-cn, pnew(k + BX), Ap);
                             Ap = fma(-cs, pnew(k - BX), Ap);
-                            const int c = gix(i, j);
+                            const int c = gix(ox + lx, oy + ly);
                             qg[c] = Ap;
                             pn[c] = pv;
                             acc = fma(pv, Ap, acc);
                             acc2 += pv;
                         }
                     }
-                } else if (pass_a) {
-                    for (int k = tg; k < BN; k += T) {       // r_k, f = (float) r_k; first red sweep
-                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
-                        float f = 0.0f;
-                        if (interior(i, j) && inreg(i, j, H)) {
+                } else if (mode == 0) {
+                    const int4 wH = span(H), w3 = span(H - 1), w0 = span(0), w1 = span(1);
+#pragma unroll
+                    for (int m = 0; m < MS; ++m) {                      // r_k, f = (float) r_k; first red sweep
+                        const int k = tg + m * T, lx = kxy[m] & 0xffff, ly = kxy[m] >> 16;
+                        if (k >= BN) continue;
+                        float f = 0.0f, u = 0.0f;
+                        if (in(wH, lx, ly)) {
                             const double r = fma(-coef, Q[k], R[k]);
                             f = (float)r;
-                            if (inreg(i, j, 0)) {
-                                rn[gix(i, j)] = r;
+                            if (in(w0, lx, ly)) {
+                                rn[gix(ox + lx, oy + ly)] = r;
                                 acc = fma(r, r, acc);
                             }
+                            if (in(w3, lx, ly) && !((lx + ly + par) & 1))
+                                u = __fdividef(f, (CE[k] + CE[k - 1]) + (CN[k] + CN[k - BX]));
                         }
                         sf[k] = f;
-                        float u = 0.0f;
-                        if (interior(i, j) && inreg(i, j, H - 1) && !((i + j) & 1))
-                            u = __fdividef(f, (CE[k] + CE[k - 1]) + (CN[k] + CN[k - BX]));
                         su[k] = u;
                     }
                     __syncthreads();
-                    black(H - 2);
+                    sweep(span(H - 2), 1);
                     __syncthreads();
-                    for (int k = tg; k < BN; k += T) {       // t = f - A u (in place of f); store u
-                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
-                        if (interior(i, j) && inreg(i, j, 1)) {
+#pragma unroll
+                    for (int m = 0; m < MS; ++m) {                      // t = f - A u (in place of f); store u
+                        const int k = tg + m * T, lx = kxy[m] & 0xffff, ly = kxy[m] >> 16;
+                        if (k < BN && in(w1, lx, ly)) {
                             const float ce = CE[k], cw = CE[k - 1], cn = CN[k], cs = CN[k - BX];
                             float Au = ((ce + cw) + (cn + cs)) * su[k];
                             Au = fmaf(-ce, su[k + 1], Au);
@@ -836,45 +863,53 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
                             Au = fmaf(-cn, su[k + BX], Au);
                             Au = fmaf(-cs, su[k - BX], Au);
                             sf[k] = sf[k] - Au;
-                            if (inreg(i, j, 0)) ug[gix(i, j)] = su[k];
+                            if (in(w0, lx, ly)) ug[gix(ox + lx, oy + ly)] = su[k];
                         }
                     }
                     __syncthreads();
-                    const int Ilo = max(1, (x0 + 1) / 2), Ihi = min(NC - 1, (xe - 1) / 2);
-                    const int Jlo = max(1, (y0 + 1) / 2), Jhi = min(NC - 1, (ye - 1) / 2);
+                    // f_c = P^T t for the coarse nodes whose centre (2I, 2J) this tile owns
+                    const int Ilo = max(1, (x0 + 1) / 2), Ihi = min(NC - 1, (x0 + wx - 1) / 2);
+                    const int Jlo = max(1, (y0 + 1) / 2), Jhi = min(NC - 1, (y0 + wy - 1) / 2);
                     const int nI = Ihi - Ilo + 1, nJ = Jhi - Jlo + 1;
                     if (nI > 0 && nJ > 0)
                         for (int e = tg; e < nI * nJ; e += T) {
                             const int I = Ilo + e % nI, J = Jlo + e / nI;
-                            const int k = (2 * J - y0 + H) * BX + (2 * I - x0 + H);
+                            const int k = (2 * J - oy) * BX + (2 * I - ox);
                             L1.f[J * GC + I] = sf[k] + 0.5f * ((sf[k + 1] + sf[k - 1]) + (sf[k + BX] + sf[k - BX]) +
                                                                (sf[k + BX + 1] + sf[k - BX - 1]));
                         }
                 } else {
-                    for (int k = tg; k < BN; k += T) {       // f = (float) r_k, u = u_pre + P u_c
-                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
+                    __syncthreads();                                    // scu written
+                    const int4 w2 = span(2), w0 = span(0);
+#pragma unroll
+                    for (int m = 0; m < MS; ++m) {                      // f = (float) r_k, u = u_pre + P u_c
+                        const int k = tg + m * T, lx = kxy[m] & 0xffff, ly = kxy[m] >> 16;
+                        if (k >= BN) continue;
                         float f = 0.0f, u = 0.0f;
-                        if (interior(i, j) && inreg(i, j, 2)) {
+                        if (in(w2, lx, ly)) {
+                            const int i = ox + lx, j = oy + ly;
                             f = (float)R[k];
-                            const int I = i >> 1, J = j >> 1;
+                            const int I = (i >> 1) - cx0, J = (j >> 1) - cy0;
+                            const float* Uc = scu + J * tl::CWX + I;
                             float v;
-                            if (!(i & 1) && !(j & 1)) v = U[J * GC + I];
-                            else if ((i & 1) && !(j & 1)) v = 0.5f * (U[J * GC + I] + U[J * GC + I + 1]);
-                            else if (!(i & 1) && (j & 1)) v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I]);
-                            else v = 0.5f * (U[J * GC + I] + U[(J + 1) * GC + I + 1]);
+                            if (!(i & 1) && !(j & 1)) v = Uc[0];
+                            else if ((i & 1) && !(j & 1)) v = 0.5f * (Uc[0] + Uc[1]);
+                            else if (!(i & 1) && (j & 1)) v = 0.5f * (Uc[0] + Uc[tl::CWX]);
+                            else v = 0.5f * (Uc[0] + Uc[tl::CWX + 1]);
                             u = UU[k] + v;
                         }
                         sf[k] = f;
                         su[k] = u;
                     }
                     __syncthreads();
-                    black(1);
+                    sweep(span(1), 1);
                     __syncthreads();
-                    for (int k = tg; k < BN; k += T) {       // red sweep on the owned nodes; z out
-                        const int i = x0 - H + k % BX, j = y0 - H + k / BX;
-                        if (interior(i, j) && inreg(i, j, 0)) {
+#pragma unroll
+                    for (int m = 0; m < MS; ++m) {                      // red sweep on the owned nodes; z out
+                        const int k = tg + m * T, lx = kxy[m] & 0xffff, ly = kxy[m] >> 16;
+                        if (k < BN && in(w0, lx, ly)) {
                             float z = su[k];
-                            if (!((i + j) & 1)) {
+                            if (!((lx + ly + par) & 1)) {
                                 const float ce = CE[k], cw = CE[k - 1], cn = CN[k], cs = CN[k - BX];
                                 float sv = sf[k];
                                 sv = fmaf(ce, su[k + 1], sv);
@@ -883,12 +918,12 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
                                 sv = fmaf(cs, su[k - BX], sv);
                                 z = __fdividef(sv, (ce + cw) + (cn + cs));
                             }
-                            zg[gix(i, j)] = z;
+                            zg[gix(ox + lx, oy + ly)] = z;
                             acc = fma(R[k], (double)z, acc);
                         }
                     }
                 }
-                __syncthreads();                            // stage s, sf, su free
+                __syncthreads();                            // stage s, sf, su, scu free
                 if (tg == 0 && t + 2 < NT) mg_issue<N>(&m64, &m32, stage0, bar0, cta, t + 2, s, mode, ro);
             }
             if (mode == 0) cr ^= 1;
