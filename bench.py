@@ -452,7 +452,7 @@ def fine_leg(local, torch):
     from paper_2503_05533_b200 import Context, precision
     cfg = W.CONFIGS["C5"]
     ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
-                  L_max=cfg["L_max"], device=local, workspace_bytes=4 << 30)
+                  L_max=cfg["L_max"], device=local, workspace_bytes=8 << 30)
     sums = torch.zeros(12, dtype=torch.float64, device=torch.device("cuda", local))
     nb, steps = 148, 300
     prec = precision("minres", max_iter=steps)
