@@ -39,7 +39,8 @@ namespace {
 template <int N, int R, int MINB_, int CM_>
 struct TileCfg {
     static constexpr int CM = CM_;
-    static constexpr bool DS = CM & 1, WS = CM & 2;
+    static constexpr bool DS = CM & 1, WS = CM & 2, CS = CM & 4;
+    static_assert(!(CS && (DS || WS)), "CS keeps every conductance in shared memory");
     static constexpr int C = N - 1;                       // interior columns / rows
     static constexpr int PAIRS = N / 2;                   // pair p: columns 2p+1, 2p+2 (column N is a phantom)
     static constexpr int S = (C + R - 1) / R;             // row strips
@@ -56,8 +57,13 @@ struct TileCfg {
     static constexpr int GRID = ROWS * RP;
     static constexpr int DGRID = DS ? S * R * 2 * PAIRS : 0;   // d at [(row-1) * 2 * PAIRS + parity * PAIRS + pair]
     static constexpr int WGRID = WS ? S * R * PAIRS : 0;       // -cW of column 0 at [(row-1) * PAIRS + pair]
+    // CS: cE(i, j) at [(j - 1) * 2 PE + (i & 1) * PE + (i >> 1)] for rows 1 .. S*R, cN(i, j) at
+    // [j * 2 PE + (i & 1) * PE + (i >> 1)] for rows 0 .. S*R (phantom rows / columns hold zeros)
+    static constexpr int PE = PAIRS + 1;
+    static constexpr int CEG = CS ? S * R * 2 * PE : 0;
+    static constexpr int CNG = CS ? (S * R + 1) * 2 * PE : 0;
     static constexpr int RED = 4 * NW;                         // reduction buffer: NW x (3 partials + pad)
-    static constexpr int SMEM_PER_GROUP = GRID + DGRID + WGRID + RED;
+    static constexpr int SMEM_PER_GROUP = GRID + DGRID + WGRID + CEG + CNG + RED;
     static constexpr size_t SMEM = sizeof(double) * SMEM_PER_GROUP * GROUPS + 16 * GROUPS;
 };
 
@@ -142,14 +148,16 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                    int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order) {
     using K = TileCfg<N, R, MINB, CM>;
     constexpr int PAIRS = K::PAIRS, PW = K::PW, RP = K::RP, TPS = K::TPS, GROUPS = K::GROUPS;
-    constexpr bool DS = K::DS, WS = K::WS;
-    constexpr int P = 2 * N * N;
+    constexpr bool DS = K::DS, WS = K::WS, CS = K::CS;
+    constexpr int P = 2 * N * N, PE = K::PE;
     extern __shared__ double smem[];
     const int g = threadIdx.x / TPS, tg = threadIdx.x % TPS;
     double* Sg = smem + g * K::SMEM_PER_GROUP;           // exchange grid [row * RP + parity * PW + pair + 1]
     double* Dg = Sg + K::GRID;
     double* Wg = Dg + K::DGRID;
-    double* red = Wg + K::WGRID;                          // NW x 4 doubles (3 partials + pad)
+    double* CEg = Wg + K::WGRID;
+    double* CNg = CEg + K::CEG;
+    double* red = CNg + K::CNG;                           // NW x 4 doubles (3 partials + pad)
     int* jobslot = reinterpret_cast<int*>(smem + K::SMEM_PER_GROUP * GROUPS) + 4 * g;
 
     const int p = tg % PAIRS, s = tg / PAIRS;
@@ -182,10 +190,21 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
 
         // ---- conductances (negated) and diagonal of the tile; phantom nodes get zeros.  Column 1's
         // west conductance is column 0's east one (same edge).
-        double nE0[R], nE1[R], nN0[R], nN1[R], nW0[WS ? 1 : R], dg0[DS ? 1 : R], dg1[DS ? 1 : R];
+        constexpr int RR = CS ? 1 : R;
+        double nE0[RR], nE1[RR], nN0[RR], nN1[RR], nW0[WS || CS ? 1 : R], dg0[DS || CS ? 1 : R], dg1[DS || CS ? 1 : R];
         double nS0 = 0.0, nS1 = 0.0;                    // south conductances of the tile's first row
+        if constexpr (CS) {
+            for (int e = tg; e < K::CEG; e += TPS) {
+                const int j = e / (2 * PE) + 1, i = 2 * (e % PE) + (e / PE) % 2;
+                CEg[e] = (j <= K::C && i <= K::C) ? cEf(i, j) : 0.0;
+            }
+            for (int e = tg; e < K::CNG; e += TPS) {
+                const int j = e / (2 * PE), i = 2 * (e % PE) + (e / PE) % 2;
+                CNg[e] = (j <= K::C && i >= 1 && i <= K::C) ? cNf(i, j) : 0.0;
+            }
+        }
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < (CS ? 0 : R); ++r) {
             const int j = j0 + r;
             const bool rl = j <= K::C;
             const double e0 = rl ? cEf(i0, j) : 0.0;
@@ -234,6 +253,38 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
             t1 = fma(sS1, vS1, t1);
         };
 
+        // CS: the same stencil (same operations, same order) with the conductances from shared memory;
+        // sc0 / sc1 carry the previous row's north conductances as this row's south ones
+        auto stencil_cs = [&](const double (&VA)[R], const double (&VB)[R], int r, double& t0, double& t1,
+                              double& sc0, double& sc1) {
+            const int j = j0 + r;
+            const double* ce = CEg + (j - 1) * 2 * PE;
+            const double* cn = CNg + j * 2 * PE;
+            const double w0 = ce[p], e0 = ce[PE + p], e1 = ce[p + 1];
+            const double n0 = cn[PE + p], n1 = cn[p + 1];
+            if (r == 0) { sc0 = cn[-2 * PE + PE + p]; sc1 = cn[-2 * PE + p + 1]; }
+            const double s0 = sc0, s1 = sc1;
+            const double vW = westp[r * RP], vE = eastp[r * RP];
+            const double vN0 = (r + 1 < R) ? VA[r + 1 < R ? r + 1 : r] : own[R * RP];
+            const double vN1 = (r + 1 < R) ? VB[r + 1 < R ? r + 1 : r] : own[R * RP + PW];
+            const double vS0 = (r > 0) ? VA[r > 0 ? r - 1 : 0] : own[-RP];
+            const double vS1 = (r > 0) ? VB[r > 0 ? r - 1 : 0] : own[-RP + PW];
+            const double d0 = (e0 + w0) + (n0 + s0);
+            const double d1 = (e1 + e0) + (n1 + s1);
+            t0 = d0 * VA[r];
+            t1 = d1 * VB[r];
+            t0 = fma(-e0, VB[r], t0);
+            t1 = fma(-e0, VA[r], t1);
+            t0 = fma(-w0, vW, t0);
+            t1 = fma(-e1, vE, t1);
+            t0 = fma(-n0, vN0, t0);
+            t1 = fma(-n1, vN1, t1);
+            t0 = fma(-s0, vS0, t0);
+            t1 = fma(-s1, vS1, t1);
+            sc0 = n0;
+            sc1 = n1;
+        };
+
         // ---- state: X = p_{j-1}, Y = p_j, T = A p_j
         double X0[R], X1[R], Y0[R], Y1[R], T0[R], T1[R];
         double Wa0[VERIFY ? R : 1], Wa1[VERIFY ? R : 1], Wb0[VERIFY ? R : 1], Wb1[VERIFY ? R : 1];
@@ -261,10 +312,12 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
         // one step j with roles (XA/XB = p_{j-1}, YA/YB = p_j, grid = p_j); false when done
         auto step = [&](double (&XA)[R], double (&XB)[R], double (&YA)[R], double (&YB)[R]) -> bool {
             double pa0 = 0.0, pa1 = 0.0, pb0 = 0.0, pb1 = 0.0, pc0 = 0.0, pc1 = 0.0;
+            double sc0 = 0.0, sc1 = 0.0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 double t0, t1;
-                stencil(YA, YB, r, westp, eastp, own, t0, t1);
+                if constexpr (CS) stencil_cs(YA, YB, r, t0, t1, sc0, sc1);
+                else stencil(YA, YB, r, westp, eastp, own, t0, t1);
                 T0[r] = t0;
                 T1[r] = t1;
                 pa0 = fma(YA[r], t0, pa0);
@@ -369,12 +422,13 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 own[r * RP + PW] = x1[VERIFY ? r : 0];
             }
             tsync<TPS, GROUPS>(g);
-            double rr = 0.0;
+            double rr = 0.0, sc0 = 0.0, sc1 = 0.0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const bool rl = (r < R - 1) || top_live;
                 double t0, t1;
-                stencil(x0, x1, r, westp, eastp, own, t0, t1);
+                if constexpr (CS) stencil_cs(x0, x1, r, t0, t1, sc0, sc1);
+                else stencil(x0, x1, r, westp, eastp, own, t0, t1);
                 const double res0 = rl ? h2 - t0 : 0.0;
                 const double res1 = rl && col1_live ? h2 - t1 : 0.0;
                 rr = fma(res0, res0, fma(res1, res1, rr));
@@ -449,12 +503,19 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            // v4 / v5 (conductances in shared memory, 5 / 4 systems per SM): 0.80 / 0.81 ms vs v0 0.74 ms
+            // on configs[1] level 2, bit-identical records
+            if (var == 4) return run_tile<32, 4, 5, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 5) return run_tile<32, 4, 4, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             return run_tile<32, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 64:
-            // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67
+            // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67, v4 2.97
+            // (v4: every conductance in shared memory, two systems per SM; bit-identical records, but the
+            // ~60 shared loads per thread and step outweigh the second resident system)
             if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 4) return run_tile<64, 8, 2, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         default: return cudaErrorNotSupported;
     }
