@@ -564,3 +564,31 @@ def test_replicate_rmse_within_eps(name):
     r = replicates.run(name, R=50)
     assert r["rmse"] <= r["eps"], r
     assert 0.030 < r["mean_estimate"] < 0.038
+
+
+def test_mgcg_edge_cases_and_finest_mesh():
+    """MG-PCG edge cases: empty and single-system passes on every kernel (on chip h = 1/8 .. 1/64, tiled
+    h = 1/128 .. 1/512), a single system equals the same sample inside a batch bit for bit; at h = 1/512
+    (no oracle solve in test time) MG-PCG and the streamed MINRES agree to the tolerance they were
+    both solved to (same per-sample residual contract)."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=8 << 30)
+    mg, mr = precision("mgcg"), precision("minres")
+    for level in range(cfg["L_max"] + 1):
+        assert ctx.sample_level(level, 0, seed=3, prec_fine=mg, prec_coarse=mg, tol_fine=1e-6,
+                                tol_coarse=1e-6).sums["n"] == 0
+        n = 3 if level >= 5 else 37
+        batch = ctx.sample_level(level, n, seed=3, prec_fine=mg, prec_coarse=mg, tol_fine=1e-7, tol_coarse=1e-7,
+                                 per_sample=True).per_sample
+        assert np.all(batch[:, 6:8] == 0) and np.all(batch[:, 4] <= 1e-7)
+        one = ctx.sample_level(level, 1, seed=3, first_index=n - 1, prec_fine=mg, prec_coarse=mg, tol_fine=1e-7,
+                               tol_coarse=1e-7, per_sample=True).per_sample
+        assert np.array_equal(one[0], batch[n - 1]), level
+    a = ctx.sample_level(6, 2, seed=4, prec_fine=mg, prec_coarse=mg, tol_fine=1e-9, tol_coarse=1e-9,
+                         per_sample=True).per_sample
+    b = ctx.sample_level(6, 2, seed=4, prec_fine=mr, prec_coarse=mr, tol_fine=1e-9, tol_coarse=1e-9,
+                         per_sample=True).per_sample
+    assert np.all(a[:, 6:8] == 0) and np.all(b[:, 6:8] == 0)
+    # |Q_mg - Q_exact| and |Q_minres - Q_exact| are each <= tol ||b|| ||x|| <= 1.5 tol Q (DESIGN.md section 4)
+    assert np.all(np.abs(a[:, :2] - b[:, :2]) <= 2 * 1.5e-9 * np.abs(b[:, :2]) + 1e-15)
+    ctx.close()
