@@ -14,6 +14,9 @@ Modules
                             textbook MINRES, Algorithm 1 with emulated rounding.
 ``mlmc.py``                 estimators Eq. (3)/(4), the eps_l schedule
                             Eqs. (14)-(16), the N_l update and Algorithm 2.
+``mg.py``                   NEXT-4: multigrid-preconditioned CG by the textbook
+                            definitions (P1 prolongation, Galerkin P^T A P,
+                            red-black Gauss-Seidel V(1,1)), numpy / scipy.sparse.
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` (see DESIGN.md section 4 for the pin list).

@@ -592,3 +592,24 @@ def test_mgcg_edge_cases_and_finest_mesh():
     # |Q_mg - Q_exact| and |Q_minres - Q_exact| are each <= tol ||b|| ||x|| <= 1.5 tol Q
     assert np.all(np.abs(a[:, :2] - b[:, :2]) <= 2 * 1.5e-9 * np.abs(b[:, :2]) + 1e-15)
     ctx.close()
+
+
+@pytest.mark.parametrize("level", [1, 2, 3])
+def test_mgcg_iterations_track_oracle_pcg(level):
+    """K3m against the oracle's textbook MG-PCG (oracle/mg.py: Galerkin products P^T A P, binary64
+    V-cycle) on the same fields: CG step counts within +-1 (the kernel's V-cycle runs in binary32)
+    and both QoIs within the residual bound of each other."""
+    from oracle import mg as omg
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    tol = 1e-8
+    n = 6
+    r = ctx.sample_level(level, n, seed=17, prec_fine=precision("mgcg"), prec_coarse=precision("mgcg"),
+                         tol_fine=tol, tol_coarse=tol, per_sample=True).per_sample
+    Nf = 8 << level
+    outs = _pmap(lambda k: omg.pcg(Nf, P.field_triangles(Nf, oc.normals(17, level, k, cfg["m"])), tol), range(n))
+    for k, o in enumerate(outs):
+        assert o["status"] == 0 and abs(int(r[k, 2]) - o["iters"]) <= 1, (level, k, r[k, 2], o["iters"])
+        assert abs(r[k, 0] - o["Q"]) <= 2 * 1.5 * tol * o["Q"], (level, k)
+    ctx.close()
