@@ -12,6 +12,7 @@
 // Paper field Eq. (20): Phi[p][j-1] = sqrt(sigma2) j^-q sin(2 pi j x1) cos(2 pi j x2).
 #include <algorithm>
 #include <cmath>
+#include <thread>
 
 #include "internal.h"
 
@@ -76,31 +77,48 @@ void build_phi(const mlmc_problem& pr, const KLModes& kl, int N, std::vector<dou
     int Kused = 0;
     if (pr.field == MLMC_FIELD_EXPCOV_KL)
         for (int k = 0; k < m; ++k) Kused = std::max(Kused, std::max(kl.ik[k], kl.jk[k]));
-    std::vector<double> e1(Kused + 1), e2(Kused + 1), sq(m);
+    std::vector<double> sq(m);
     if (pr.field == MLMC_FIELD_EXPCOV_KL)
         for (int k = 0; k < m; ++k) sq[k] = std::sqrt(kl.lam[k]);
-    for (int j = 0; j < N; ++j)
-        for (int i = 0; i < N; ++i)
-            for (int up = 0; up < 2; ++up) {
-                // lower triangle {(i,j),(i+1,j),(i+1,j+1)}: centroid (i+2/3, j+1/3) h
-                // upper triangle {(i,j),(i+1,j+1),(i,j+1)}: centroid (i+1/3, j+2/3) h
-                double x1 = (i + (up ? 1.0 : 2.0) / 3.0) * h;
-                double x2 = (j + (up ? 2.0 : 1.0) / 3.0) * h;
-                double* row = &phi[((size_t)2 * (j * N + i) + up) * m];
-                if (pr.field == MLMC_FIELD_EXPCOV_KL) {
-                    for (int q = 1; q <= Kused; ++q) {
-                        double w = kl.w[q - 1], r = kl.c / w;
-                        e1[q] = kl.nrm[q - 1] * (std::cos(w * x1) + r * std::sin(w * x1));
-                        e2[q] = kl.nrm[q - 1] * (std::cos(w * x2) + r * std::sin(w * x2));
+    // rows j of the mesh in parallel (the h = 1/512 table at m = 256 is 1.07 GB); each entry is
+    // computed by the same expression whichever thread writes it
+    auto rows = [&](int j_begin, int j_end) {
+        std::vector<double> e1(Kused + 1), e2(Kused + 1);
+        for (int j = j_begin; j < j_end; ++j)
+            for (int i = 0; i < N; ++i)
+                for (int up = 0; up < 2; ++up) {
+                    // lower triangle {(i,j),(i+1,j),(i+1,j+1)}: centroid (i+2/3, j+1/3) h
+                    // upper triangle {(i,j),(i+1,j+1),(i,j+1)}: centroid (i+1/3, j+2/3) h
+                    double x1 = (i + (up ? 1.0 : 2.0) / 3.0) * h;
+                    double x2 = (j + (up ? 2.0 : 1.0) / 3.0) * h;
+                    double* row = &phi[((size_t)2 * (j * N + i) + up) * m];
+                    if (pr.field == MLMC_FIELD_EXPCOV_KL) {
+                        for (int q = 1; q <= Kused; ++q) {
+                            double w = kl.w[q - 1], r = kl.c / w;
+                            e1[q] = kl.nrm[q - 1] * (std::cos(w * x1) + r * std::sin(w * x1));
+                            e2[q] = kl.nrm[q - 1] * (std::cos(w * x2) + r * std::sin(w * x2));
+                        }
+                        for (int k = 0; k < m; ++k) row[k] = sq[k] * e1[kl.ik[k]] * e2[kl.jk[k]];
+                    } else {
+                        double sd = std::sqrt(pr.sigma2);
+                        for (int jj = 1; jj <= m; ++jj)
+                            row[jj - 1] = sd * std::pow((double)jj, -pr.q_decay) * std::sin(2.0 * pi * jj * x1) *
+                                          std::cos(2.0 * pi * jj * x2);
                     }
-                    for (int k = 0; k < m; ++k) row[k] = sq[k] * e1[kl.ik[k]] * e2[kl.jk[k]];
-                } else {
-                    double sd = std::sqrt(pr.sigma2);
-                    for (int jj = 1; jj <= m; ++jj)
-                        row[jj - 1] = sd * std::pow((double)jj, -pr.q_decay) * std::sin(2.0 * pi * jj * x1) *
-                                      std::cos(2.0 * pi * jj * x2);
                 }
-            }
+    };
+    const size_t work = (size_t)P * m;
+    const int nt = work < (1u << 20) ? 1 : (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+    if (nt == 1) {
+        rows(0, N);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) {
+        const int jb = (int)((long long)N * t / nt), je = (int)((long long)N * (t + 1) / nt);
+        if (jb < je) pool.emplace_back(rows, jb, je);
+    }
+    for (auto& th : pool) th.join();
 }
 
 }  // namespace mlmc
