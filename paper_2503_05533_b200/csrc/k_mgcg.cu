@@ -671,7 +671,7 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
                  int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order,
                  unsigned char* __restrict__ scratch) {
     using K = MgTl<N>;
-    constexpr int T = tl::T, GP = K::GP, C = N - 1, n = C * C, P = 2 * N * N;
+    constexpr int T = tl::T, GP = K::GP, C = N - 1, P = 2 * N * N;
     constexpr int BX = tl::BX, BN = tl::BN, H = tl::H, TX = tl::TX, TY = tl::TY, NT = K::NT;
     constexpr int NC = N / 2, GC = NC + 1;
     extern __shared__ __align__(128) unsigned char smem[];

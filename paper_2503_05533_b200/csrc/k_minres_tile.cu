@@ -193,7 +193,10 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
         constexpr int RR = CS ? 1 : R;
         double nE0[RR], nE1[RR], nN0[RR], nN1[RR], nW0[WS || CS ? 1 : R], dg0[DS || CS ? 1 : R], dg1[DS || CS ? 1 : R];
         double nS0 = 0.0, nS1 = 0.0;                    // south conductances of the tile's first row
+        if constexpr (DS || CS) dg0[0] = dg1[0] = 0.0;   // placeholders of the shared-memory paths
+        if constexpr (WS || CS) nW0[0] = 0.0;
         if constexpr (CS) {
+            nE0[0] = nE1[0] = nN0[0] = nN1[0] = 0.0;
             for (int e = tg; e < K::CEG; e += TPS) {
                 const int j = e / (2 * PE) + 1, i = 2 * (e % PE) + (e / PE) % 2;
                 CEg[e] = (j <= K::C && i <= K::C) ? cEf(i, j) : 0.0;
