@@ -217,19 +217,6 @@ void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
     else { fixed = n * bw * bw * fmt_bits(p->u_f) / 64.0; step = 4.0 * n * bw; }
 }
 
-// Longest-first job order for a MINRES solve (LPT scheduling of the persistent CTAs): worth it where
-// a launch is a few waves of long solves (h >= 1/32: the tile kernel, nb <= kOrderMax).  MLMC_ORDER=0
-// switches it off (A/B runs).
-bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = std::getenv("MLMC_ORDER");
-        env = (e && e[0] == '0') ? 0 : 1;
-    }
-    return env && p->solver == MLMC_SOLVER_MINRES && N >= 32 && N < kGmMinN && nb >= 2 && nb <= (uint64_t)kOrderMax &&
-           minres_tile_variant(N) >= 0;
-}
-
 // MLMC_MINRES_GM=1 selects the three-phase global-memory MINRES instead of the streamed one (A/B).
 bool use_gm_kernel() {
     static int v = -1;
@@ -239,6 +226,21 @@ bool use_gm_kernel() {
     }
     return v == 1;
 }
+
+// Longest-first job order for a MINRES solve (LPT scheduling of the persistent CTAs): worth it where
+// a launch is a few waves of long solves (h >= 1/32: the tile and streamed kernels, nb <= kOrderMax).  MLMC_ORDER=0
+// switches it off (A/B runs).
+bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("MLMC_ORDER");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (!env || p->solver != MLMC_SOLVER_MINRES || N < 32 || nb < 2 || nb > (uint64_t)kOrderMax) return false;
+    if (N >= kGmMinN) return minres_stream_supported(N) && !use_gm_kernel();   // streamed kernel (K3c)
+    return minres_tile_variant(N) >= 0;
+}
+
 
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
                double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas, void* ch_scratch,
@@ -250,7 +252,8 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
         if (keys && order) CU(counted(ctx, ex.st, MLMC_K_ORDER, N, [&] { return launch_order(keys, (int)nb, order, ex.st); }));
         if (N >= kGmMinN && minres_stream_supported(N) && !use_gm_kernel())
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
-                return launch_minres_stream(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st);
+                return launch_minres_stream(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st,
+                                            keys ? order : nullptr);
             }));
         else if (N >= kGmMinN)
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {

@@ -59,7 +59,9 @@ bool encode_tensor_map(void* map, bool f64, int rank, void* base, const uint64_t
                        const uint32_t* box);
 size_t minres_stream_scratch_per_cta(int N);
 cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                                 unsigned* job_counter, double* scratch, int nctas, cudaStream_t s);
+                                 unsigned* job_counter, double* scratch, int nctas, cudaStream_t s,
+                                 const int* order = nullptr);
+int minres_stream_cluster(uint64_t nb, int sms);   // CTAs per system of a streamed MINRES launch
 // K3m (NEXT-4): multigrid-preconditioned CG (k_mgcg.cu), same record convention.  N = 8..64 on chip;
 // N = 128..512 one CTA per system over nctas x mgcg_scratch_per_cta(N) bytes of global scratch.
 bool mgcg_supported(int N);

@@ -26,13 +26,17 @@
 #include <cudaTypedefs.h>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+
+#include <cooperative_groups.h>
 
 #include "internal.h"
 
 namespace mlmc {
 namespace {
+namespace cg = cooperative_groups;
 
 constexpr int ST = 512;                  // threads per CTA
 constexpr int TW = 64, TH = 32;          // tile of interior nodes
@@ -43,7 +47,7 @@ constexpr int PL_CE = 3, PL_CN = 4;
 constexpr int BOX = BW * BH;             // doubles per plane box
 constexpr int BOX_BYTES = BOX * 8;       // 19584 = 153 * 128
 constexpr int STAGE = 4 * BOX;           // doubles per stage (p_j, p_{j-1}, cE, cN)
-constexpr size_t SMEM = (size_t)(2 * STAGE + PW * PH + 3 * (ST / 32)) * 8 + 2 * 8 + 16;
+constexpr size_t SMEM = (size_t)(2 * STAGE + PW * PH + 3 * (ST / 32) + 8) * 8 + 2 * 8 + 16;
 
 // row pitch: grid columns 0..N stored at 1..N+1 (column 0 = padding), N + 2 doubles (16-byte multiple)
 __host__ __device__ constexpr int pitch(int N) { return N + 2; }
@@ -117,23 +121,33 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, double* stage
     tma_box(dst + 3 * BOX_BYTES, map, x, y, PL_CN, cta, bar);
 }
 
+// CS > 1: one system per thread-block cluster of CS CTAs (the tiles of a pass dealt round-robin to the
+// CTAs, every CTA reading the halos from the shared planes in HBM/L2); the block partials are summed
+// across the cluster through distributed shared memory in rank order (identical in every CTA), and
+// the cluster barrier of that exchange also publishes each pass's p_{j+1} to the whole cluster.  For
+// fewer systems than SMs and long, uneven solves (the finest levels) -- a lone system gets CS SMs.
+template <int CS>
 __global__ void __launch_bounds__(ST, 1)
 minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const double* __restrict__ a_all, int nb,
                      double tol, int max_iter, double* __restrict__ out, int slot, unsigned* __restrict__ job_counter,
-                     double* __restrict__ scratch) {
+                     double* __restrict__ scratch, const int* __restrict__ order) {
     // all shared memory is dynamic so that the TMA boxes start 128-byte aligned:
-    // [stage 0 | stage 1 | p_{j+1} tile | block partials | mbarriers | job slot]
+    // [stage 0 | stage 1 | p_{j+1} tile | block partials | cluster partials | mbarriers | job slots]
     extern __shared__ __align__(128) double sm[];
     double* stage0 = sm;
     double* PN = sm + 2 * STAGE;                       // p_{j+1} on the tile + halo, [PH][PW]
     double* red = PN + PW * PH;                        // 3 x 16 warp partials
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 3 * (ST / 32));
+    double* part = red + 3 * (ST / 32);                // [2][4]: this CTA's block sums, by step parity
+    uint64_t* bars = reinterpret_cast<uint64_t*>(part + 8);
     int& jobslot = *reinterpret_cast<int*>(bars + 2);
+    int& jobmine = *(reinterpret_cast<int*>(bars + 2) + 1);
     const int G = N + 1, GP = pitch(N), C = N - 1;
     const size_t PLANE = (size_t)G * GP;
     const int tiles_x = (C + TW - 1) / TW, tiles_y = (C + TH - 1) / TH, T = tiles_x * tiles_y;
     const int P = 2 * N * N, tid = threadIdx.x;
-    const int cta = blockIdx.x;
+    const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int cta = blockIdx.x / CS;                   // system slot: scratch planes + tensor-map coordinate
+    const int Tr = (T - rank + CS - 1) / CS;           // this CTA's tiles: rank, rank + CS, ...
     double* base = scratch + (size_t)cta * NPLANE * PLANE;
     const double h = 1.0 / N, h2 = h * h;
     const uint32_t bar0 = smem_u32(&bars[0]);
@@ -147,14 +161,25 @@ minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const doubl
 
     const CUtensorMap* mp = &map;                      // the __grid_constant__ parameter itself (param space)
     for (;;) {
-        if (tid == 0) jobslot = (int)atomicAdd(job_counter, 1u);
-        __syncthreads();
-        const int job = jobslot;
-        __syncthreads();
+        int job;
+        if constexpr (CS > 1) {
+            auto cl = cg::this_cluster();
+            if (rank == 0 && tid == 0) jobslot = (int)atomicAdd(job_counter, 1u);
+            cl.sync();
+            if (tid == 0) jobmine = *cl.map_shared_rank(&jobslot, 0);
+            __syncthreads();
+            job = jobmine;
+        } else {
+            if (tid == 0) jobslot = (int)atomicAdd(job_counter, 1u);
+            __syncthreads();
+            job = jobslot;
+            __syncthreads();
+        }
         if (job >= nb) break;
-        const double* a = a_all + (size_t)job * P;
+        const int sj = order ? __ldg(order + job) : job;
+        const double* a = a_all + (size_t)sj * P;
         // ---- planes: cE, cN from the coefficients (R10); p_0 = 0, p_1 = b, third vector's ring = 0
-        for (size_t e = tid; e < PLANE; e += ST) {
+        for (size_t e = (size_t)rank * ST + tid; e < PLANE; e += (size_t)CS * ST) {
             const int i = (int)(e % GP) - 1, j = (int)(e / GP);   // column 0 is padding (i = -1)
             const bool in = i >= 1 && i <= C && j >= 1 && j <= C;
             base[e] = 0.0;                                                  // P0 = p_0
@@ -167,13 +192,14 @@ minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const doubl
             base[PL_CN * PLANE + e] = cn;
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");        // generic writes -> TMA reads
-        __syncthreads();
+        if constexpr (CS > 1) cg::this_cluster().sync();
+        else __syncthreads();
         int pprev = 0, pcur = 1, pnext = 2;             // plane roles: p_{j-1}, p_j, p_{j+1}
         // pass coefficients: p_{j+1} = ct t_j + c1 p_j + c0 p_{j-1}; the first pass copies p_1
         double ct = 0.0, c1 = 1.0, c0 = 0.0;
         if (tid == 0) {
-            issue_tile(mp, stage0, bar0, tiles_x, cta, 0, 0, pcur, pprev);
-            if (T > 1) issue_tile(mp, stage0, bar0, tiles_x, cta, 1, 1, pcur, pprev);
+            if (Tr > 0) issue_tile(mp, stage0, bar0, tiles_x, cta, rank, 0, pcur, pprev);
+            if (Tr > 1) issue_tile(mp, stage0, bar0, tiles_x, cta, rank + CS, 1, pcur, pprev);
         }
         double beta1 = 0.0, tol_b = 0.0, inv_beta1 = 0.0, invb_prev = 0.0, alpha_prev = 0.0, sigma_prev = 0.0;
         double dbar = 0.0, epsln = 0.0, phibar = 0.0, cs = -1.0, sn = 0.0, s1q = 0.0, s2q = 0.0, Xq = 0.0;
@@ -181,8 +207,8 @@ minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const doubl
         for (int pass = 0;; ++pass) {
             double sa = 0.0, sb = 0.0, sc = 0.0;
             double* gnext = base + (size_t)pnext * PLANE;
-            for (int t = 0; t < T; ++t) {
-                const int s = t & 1;
+            for (int u = 0; u < Tr; ++u) {
+                const int s = u & 1, t = rank + u * CS;
                 mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
                 phase ^= 1u << s;
                 const double* Pj = stage0 + s * STAGE;
@@ -228,9 +254,26 @@ minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const doubl
                     gnext[(size_t)gj * GP + gi + 1] = pv;
                 }
                 __syncthreads();                        // stage s and PN are free
-                if (tid == 0 && t + 2 < T) issue_tile(mp, stage0, bar0, tiles_x, cta, t + 2, s, pcur, pprev);
+                if (tid == 0 && u + 2 < Tr) issue_tile(mp, stage0, bar0, tiles_x, cta, t + 2 * CS, s, pcur, pprev);
             }
-            const double3 S = bsum3(sa, sb, sc, red);
+            double3 S = bsum3(sa, sb, sc, red);
+            if constexpr (CS > 1) {
+                // cluster sum in rank order; the barrier also publishes this pass's p_{j+1} stores
+                auto cl = cg::this_cluster();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                double* mine = part + 4 * (k & 1);
+                if (tid == 0) { mine[0] = S.x; mine[1] = S.y; mine[2] = S.z; }
+                cl.sync();
+                double3 T3 = make_double3(0.0, 0.0, 0.0);
+#pragma unroll
+                for (int r = 0; r < CS; ++r) {
+                    const double* pr = cl.map_shared_rank(mine, r);
+                    T3.x += pr[0];
+                    T3.y += pr[1];
+                    T3.z += pr[2];
+                }
+                S = T3;
+            }
             // ---- scalars of Lanczos step j+1 (p_{j+1} = the vector just formed), as in the tile kernel
             const double bb = S.y;
             const double invb = bb > 0.0 ? rsqrt(bb) : 0.0;
@@ -280,15 +323,17 @@ minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const doubl
             pprev = pcur;
             pcur = pnext;
             pnext = old;
-            asm volatile("fence.proxy.async.global;" ::: "memory");    // this pass's stores -> next TMA reads
-            __syncthreads();
+            if constexpr (CS == 1) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");    // this pass's stores -> next TMA reads
+                __syncthreads();
+            }
             if (tid == 0) {
-                issue_tile(mp, stage0, bar0, tiles_x, cta, 0, 0, pcur, pprev);
-                if (T > 1) issue_tile(mp, stage0, bar0, tiles_x, cta, 1, 1, pcur, pprev);
+                if (Tr > 0) issue_tile(mp, stage0, bar0, tiles_x, cta, rank, 0, pcur, pprev);
+                if (Tr > 1) issue_tile(mp, stage0, bar0, tiles_x, cta, rank + CS, 1, pcur, pprev);
             }
         }
-        if (tid == 0) {
-            double* o = out + (size_t)job * kRecLen;
+        if (tid == 0 && rank == 0) {
+            double* o = out + (size_t)sj * kRecLen;
             o[0 + slot] = h2 * Xq;
             o[2 + slot] = (double)k;
             o[4 + slot] = phibar * inv_beta1;
@@ -296,6 +341,7 @@ minres_stream_kernel(const __grid_constant__ CUtensorMap map, int N, const doubl
         }
         __syncthreads();
     }
+    if constexpr (CS > 1) cg::this_cluster().sync();   // no CTA leaves while another may read its shared memory
 }
 
 // ---- tensor map over the scratch: [slot][plane][row][col] binary64, boxes of BW x BH x 1 x 1
@@ -331,30 +377,88 @@ bool minres_stream_supported(int N) { return N == 128 || N == 256 || N == 512; }
 
 size_t minres_stream_scratch_per_cta(int N) { return sizeof(double) * NPLANE * (size_t)(N + 1) * pitch(N); }
 
+namespace {
+template <int CS>
+cudaError_t run_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                       unsigned* ctr, double* scratch, int nctas, const int* order, cudaStream_t s) {
+    auto kern = minres_stream_kernel<CS>;
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        if (e != cudaSuccess) return e;
+        if (CS > 1) {
+            cudaLaunchConfig_t qc = {};
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = CS;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.gridDim = dim3(CS * 16);
+            qc.blockDim = dim3(ST);
+            qc.dynamicSmemBytes = SMEM;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &qc);
+            if (e != cudaSuccess) return e;
+            if (max_clusters < 1) { max_clusters = -1; return cudaErrorInvalidConfiguration; }
+        } else {
+            max_clusters = 1 << 30;
+        }
+    }
+    const int systems = (int)std::min<uint64_t>(std::min<uint64_t>(nb, (uint64_t)nctas), (uint64_t)max_clusters);
+    if (systems <= 0) return cudaSuccess;
+    CUtensorMap map;
+    const uint64_t dims[4] = {(uint64_t)pitch(N), (uint64_t)(N + 1), (uint64_t)NPLANE, (uint64_t)systems};
+    const uint64_t strides[3] = {(uint64_t)pitch(N) * 8, (uint64_t)pitch(N) * (N + 1) * 8,
+                                 (uint64_t)pitch(N) * (N + 1) * 8 * NPLANE};
+    const uint32_t box[4] = {BW, BH, 1, 1};
+    if (!encode_tensor_map(&map, true, 4, scratch, dims, strides, box)) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3(systems * CS);
+    cfg.blockDim = dim3(ST);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = s;
+    if (CS > 1) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, map, N, a, (int)nb, tol, max_iter, out, slot, ctr, scratch, order);
+}
+}  // namespace
+
+// CTAs per system: MLMC_STREAM_CLUSTER=1|2|4|8 overrides; by default a cluster of 4 when the launch has
+// at most one system per SM (the finest levels: few, long and uneven solves), else 1.  Measured on
+// configs[4] (tools/k3c_cluster.py, 100 systems): h = 1/512 8.61 / 3.62 / 3.75 s at 1 / 4 / 8 CTAs,
+// h = 1/256 821 / 456 / 385 / 486 ms at 1 / 2 / 4 / 8, h = 1/128 78 / 47 / 48 / 75 ms; with 300 or 441
+// systems one CTA per system is as fast or faster.
+int minres_stream_cluster(uint64_t nb, int sms) {
+    static int env = -2;
+    if (env == -2) {
+        const char* e = std::getenv("MLMC_STREAM_CLUSTER");
+        env = e ? std::atoi(e) : -1;
+    }
+    if (env == 1 || env == 2 || env == 4 || env == 8) return env;
+    return nb <= (uint64_t)sms ? 4 : 1;
+}
+
 cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                                 unsigned* ctr, double* scratch, int nctas, cudaStream_t s) {
+                                 unsigned* ctr, double* scratch, int nctas, cudaStream_t s, const int* order) {
     if (nb == 0) return cudaSuccess;
     if (!minres_stream_supported(N)) return cudaErrorNotSupported;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(minres_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    switch (minres_stream_cluster(nb, sms)) {
+        case 8: return run_stream<8>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
+        case 4: return run_stream<4>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
+        case 2: return run_stream<2>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
+        default: return run_stream<1>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
     }
-    const int grid = (int)std::min<uint64_t>(nb, (uint64_t)nctas);
-    auto enc = encode_fn();
-    if (!enc) return cudaErrorNotSupported;
-    CUtensorMap map;
-    const cuuint64_t dims[4] = {(cuuint64_t)pitch(N), (cuuint64_t)(N + 1), (cuuint64_t)NPLANE, (cuuint64_t)grid};
-    const cuuint64_t strides[3] = {(cuuint64_t)pitch(N) * 8, (cuuint64_t)pitch(N) * (N + 1) * 8,
-                                   (cuuint64_t)pitch(N) * (N + 1) * 8 * NPLANE};
-    const cuuint32_t box[4] = {BW, BH, 1, 1}, estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, scratch, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    minres_stream_kernel<<<grid, ST, SMEM, s>>>(map, N, a, (int)nb, tol, max_iter, out, slot, ctr, scratch);
-    return cudaGetLastError();
 }
 
 }  // namespace mlmc
