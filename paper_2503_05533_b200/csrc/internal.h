@@ -61,7 +61,7 @@ size_t minres_stream_scratch_per_cta(int N);
 cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                                  unsigned* job_counter, double* scratch, int nctas, cudaStream_t s,
                                  const int* order = nullptr);
-int minres_stream_cluster(uint64_t nb, int sms);   // CTAs per system of a streamed MINRES launch
+int minres_stream_cluster(int N);   // CTAs per system of a streamed MINRES launch (a function of the mesh)
 // K3m (NEXT-4): multigrid-preconditioned CG (k_mgcg.cu), same record convention.  N = 8..64 on chip;
 // N = 128..512 one CTA per system over nctas x mgcg_scratch_per_cta(N) bytes of global scratch.
 bool mgcg_supported(int N);

@@ -431,29 +431,29 @@ cudaError_t run_stream(int N, const double* a, uint64_t nb, double tol, int max_
 }
 }  // namespace
 
-// CTAs per system: MLMC_STREAM_CLUSTER=1|2|4|8 overrides; by default a cluster of 4 when the launch has
-// at most one system per SM (the finest levels: few, long and uneven solves), else 1.  Measured on
-// configs[4] (tools/k3c_cluster.py, 100 systems): h = 1/512 8.61 / 3.62 / 3.75 s at 1 / 4 / 8 CTAs,
-// h = 1/256 821 / 456 / 385 / 486 ms at 1 / 2 / 4 / 8, h = 1/128 78 / 47 / 48 / 75 ms; with 300 or 441
-// systems one CTA per system is as fast or faster.
-int minres_stream_cluster(uint64_t nb, int sms) {
+// CTAs per system: MLMC_STREAM_CLUSTER=1|2|4|8 overrides; by default 2 on every streamed mesh -- fixed
+// per mesh, so that a sample's result does not depend on the batch it is drawn in (the cluster size
+// fixes the partial-sum order).  Measured on configs[4] (tools/k3c_cluster.py, tools/gpu_k3c_cs2.sh):
+// 100 systems at h = 1/512 8.61 / 4.67 / 3.62 / 3.75 s at 1 / 2 / 4 / 8 CTAs, at h = 1/256 821 / 456 /
+// 385 / 486 ms, at h = 1/128 78 / 47 / 48 / 75 ms; 148 equal-length systems (bench.py k3c_fine_meshes)
+// 0.80 / 0.76 of HBM at h = 1/256 and 0.78 / 0.78 at 1/512 for 1 / 2 CTAs, but 0.57 / 0.63 for 4 (clusters
+// of 4 leave SMs of every GPC idle); 441 systems at h = 1/128: 122 / 135 ms for 1 / 2.
+int minres_stream_cluster(int N) {
     static int env = -2;
     if (env == -2) {
         const char* e = std::getenv("MLMC_STREAM_CLUSTER");
         env = e ? std::atoi(e) : -1;
     }
+    (void)N;
     if (env == 1 || env == 2 || env == 4 || env == 8) return env;
-    return nb <= (uint64_t)sms ? 4 : 1;
+    return 2;
 }
 
 cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                                  unsigned* ctr, double* scratch, int nctas, cudaStream_t s, const int* order) {
     if (nb == 0) return cudaSuccess;
     if (!minres_stream_supported(N)) return cudaErrorNotSupported;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    switch (minres_stream_cluster(nb, sms)) {
+    switch (minres_stream_cluster(N)) {
         case 8: return run_stream<8>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
         case 4: return run_stream<4>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
         case 2: return run_stream<2>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
