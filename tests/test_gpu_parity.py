@@ -613,3 +613,19 @@ def test_mgcg_iterations_track_oracle_pcg(level):
         assert o["status"] == 0 and abs(int(r[k, 2]) - o["iters"]) <= 1, (level, k, r[k, 2], o["iters"])
         assert abs(r[k, 0] - o["Q"]) <= 2 * 1.5 * tol * o["Q"], (level, k)
     ctx.close()
+
+
+def test_c_quickstart(tmp_path):
+    """The C ABI from plain C (examples/quickstart.c): plan, workspace from cudaMalloc, one coupled pass of
+    every configs[1] level, Algorithm 2 on configs[3]; estimates in the survey's sanity range."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "quickstart")
+    pkg = os.path.join(root, "paper_2503_05533_b200")
+    subprocess.check_call(["gcc", "-std=c99", "-O2", os.path.join(root, "examples", "quickstart.c"),
+                           "-I" + os.path.join(root, "include"), "-I/usr/local/cuda/include", "-L" + pkg, "-lmlmc",
+                           "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + pkg, "-o", exe])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("ok")
+    assert "level 3:" in r.stdout and "adaptive MPML" in r.stdout
