@@ -21,7 +21,11 @@ struct mlmc_ctx {
     int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
-    std::vector<double*> phi_dev;        // per level, lazily built
+    std::vector<double*> phi_dev;        // per level, lazily built (P x m synthesis, MLMC_FIELD_KERNEL=dense)
+    SepModes sep;                        // separable synthesis (default): modes by x-function ...
+    int* sep_i = nullptr;                // ... on the device: aoff [K+1] | mk [m] | mb [m]
+    double* sep_c = nullptr;             //     c_k [m]
+    std::vector<double*> tab_dev;        // per level: the four 1D tables [4][N][K], lazily built
     unsigned char* ws = nullptr;         // borrowed workspace
     size_t ws_bytes = 0;
     double* sums_dev = nullptr;          // owned: MLMC_MAX_LEVELS * kSumsLen
@@ -174,9 +178,45 @@ struct LevelSched {
     cudaEvent_t fork = nullptr, join = nullptr, prep = nullptr, gate = nullptr;
 };
 
+// Which synthesis a mesh uses (a function of N, m and K only, so results never depend on the batch):
+// the separable one (K1s) where it needs several times fewer flops than the P x m contraction -- 4 m N +
+// 4 K N^2 against 4 m N^2, weighted 5x for the CUDA-core kernel against the DMMA one (measured: at N = 8
+// the DMMA kernel wins even at m = 256) -- or where Phi would not be small (> 256 MB); the P x m one
+// (K1, DMMA) otherwise.  MLMC_FIELD_KERNEL=dense|ffma forces the P x m one.
+bool field_sep(const mlmc_ctx* ctx, int N) {
+    if (field_use_dense()) return false;
+    const double m = ctx->pr.m, K = ctx->sep.K > 0 ? ctx->sep.K : m;
+    const double phi_bytes = 8.0 * 2.0 * N * N * m;
+    return 5.0 * (m + K * N) < N * m || phi_bytes > 256.0 * (1 << 20);
+}
+
+// Plan data of a level's field synthesis, built on first use: the separable tables (a few KB per level)
+// or the P x m matrix Phi (1.07 GB at h = 1/512, m = 256).
 int ensure_phi(mlmc_ctx* ctx, int level) {
+    const int N = level_N(ctx, level);
+    if (!field_use_dense() && !ctx->sep_i) build_sep_modes(ctx->pr, ctx->kl, ctx->sep);
+    if (field_sep(ctx, N)) {
+        if (!ctx->sep_i) {
+            const int m = ctx->pr.m, K = ctx->sep.K;
+            std::vector<int32_t> ints(ctx->sep.aoff);
+            ints.insert(ints.end(), ctx->sep.mk.begin(), ctx->sep.mk.end());
+            ints.insert(ints.end(), ctx->sep.mb.begin(), ctx->sep.mb.end());
+            CU(cudaMalloc(&ctx->sep_i, sizeof(int32_t) * ints.size()));
+            CU(cudaMemcpy(ctx->sep_i, ints.data(), sizeof(int32_t) * ints.size(), cudaMemcpyHostToDevice));
+            CU(cudaMalloc(&ctx->sep_c, sizeof(double) * m));
+            CU(cudaMemcpy(ctx->sep_c, ctx->sep.mc.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
+            (void)K;
+        }
+        if (ctx->tab_dev[level]) return MLMC_OK;
+        std::vector<double> tab;
+        build_sep_tables(ctx->pr, ctx->kl, ctx->sep, N, tab);
+        double* d = nullptr;
+        CU(cudaMalloc(&d, tab.size() * sizeof(double)));
+        CU(cudaMemcpy(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+        ctx->tab_dev[level] = d;
+        return MLMC_OK;
+    }
     if (ctx->phi_dev[level]) return MLMC_OK;
-    int N = level_N(ctx, level);
     std::vector<double> phi;
     build_phi(ctx->pr, ctx->kl, N, phi);
     double* d = nullptr;
@@ -184,6 +224,17 @@ int ensure_phi(mlmc_ctx* ctx, int level) {
     CU(cudaMemcpy(d, phi.data(), phi.size() * sizeof(double), cudaMemcpyHostToDevice));
     ctx->phi_dev[level] = d;
     return MLMC_OK;
+}
+
+// K1 + K2 of mesh level `mesh` for nb samples (xi -> a), on stream st
+cudaError_t field(const mlmc_ctx* ctx, int mesh, const double* xi, double* a, uint64_t nb, unsigned long long* keys,
+                  cudaStream_t st) {
+    const int N = level_N(ctx, mesh), m = ctx->pr.m;
+    if (!field_sep(ctx, N)) return launch_field(ctx->phi_dev[mesh], xi, a, 2 * N * N, m, nb, keys, st);
+    const int K = ctx->sep.K;
+    const int* aoff = ctx->sep_i;
+    return launch_field_sep(ctx->tab_dev[mesh], aoff, aoff + K + 1, aoff + K + 1 + m, ctx->sep_c, K, xi, a, N, m, nb,
+                            keys, st);
 }
 
 int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
@@ -330,10 +381,10 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         if (kf) CU(cudaMemsetAsync(kf, 0, sizeof(unsigned long long) * 2 * nb, st));
         if (kc) CU(cudaMemsetAsync(kc, 0, sizeof(unsigned long long) * 2 * nb, st));
         CU(counted(ctx, st, MLMC_K_FIELD, Nf,
-                   [&] { return launch_field(ctx->phi_dev[level], xi, af, 2 * Nf * Nf, m, nb, kf, st); }));
+                   [&] { return field(ctx, level, xi, af, nb, kf, st); }));
         if (level > 0)
             CU(counted(ctx, st, MLMC_K_FIELD, Nc,
-                       [&] { return launch_field(ctx->phi_dev[level - 1], xi, ac, 2 * Nc * Nc, m, nb, kc, st); }));
+                       [&] { return field(ctx, level - 1, xi, ac, nb, kc, st); }));
         int* of = reinterpret_cast<int*>(ex.ws + L.ord_f);
         int* oc = reinterpret_cast<int*>(ex.ws + L.ord_c);
         if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, st));
@@ -445,6 +496,7 @@ int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
         if (rc) { delete ctx; return fail(nullptr, rc, "KL eigenpairs failed"); }
     }
     ctx->phi_dev.assign(p.L_max + 1, nullptr);
+    ctx->tab_dev.assign(p.L_max + 1, nullptr);
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, p.device);
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
@@ -471,6 +523,9 @@ void mlmc_destroy(mlmc_ctx* ctx) {
     drain_pending(ctx);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (double* d : ctx->phi_dev) if (d) cudaFree(d);
+    for (double* d : ctx->tab_dev) if (d) cudaFree(d);
+    if (ctx->sep_i) cudaFree(ctx->sep_i);
+    if (ctx->sep_c) cudaFree(ctx->sep_c);
     if (ctx->sums_dev) cudaFree(ctx->sums_dev);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -692,7 +747,8 @@ int mlmc_debug_field(mlmc_ctx* ctx, int level, int mesh_level, uint64_t n, uint6
     if (!xi) CU(cudaMalloc(&xi, sizeof(double) * std::max<uint64_t>(n, 1) * ctx->pr.m));
     CU(launch_rng(xi, ctx->pr.m, n, seed, level, first_index, ctx->stream));
     int N = level_N(ctx, mesh_level);
-    if (a_dev) CU(launch_field(ctx->phi_dev[mesh_level], xi, a_dev, 2 * N * N, ctx->pr.m, n, nullptr, ctx->stream));
+    (void)N;
+    if (a_dev) CU(field(ctx, mesh_level, xi, a_dev, n, nullptr, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (!xi_dev) cudaFree(xi);
     return MLMC_OK;

@@ -121,4 +121,59 @@ void build_phi(const mlmc_problem& pr, const KLModes& kl, int N, std::vector<dou
     for (auto& th : pool) th.join();
 }
 
+void build_sep_modes(const mlmc_problem& pr, const KLModes& kl, SepModes& out) {
+    const int m = pr.m;
+    std::vector<int32_t> a(m), b(m);
+    std::vector<double> c(m);
+    int K = 0;
+    for (int k = 0; k < m; ++k) {
+        if (pr.field == MLMC_FIELD_EXPCOV_KL) {     // sqrt(lambda_k) e_{ik}(x1) e_{jk}(x2)
+            a[k] = kl.ik[k] - 1;
+            b[k] = kl.jk[k] - 1;
+            c[k] = std::sqrt(kl.lam[k]);
+        } else {                                    // sqrt(sigma2) j^-q sin(2 pi j x1) cos(2 pi j x2), j = k + 1
+            a[k] = b[k] = k;
+            c[k] = std::sqrt(pr.sigma2) * std::pow((double)(k + 1), -pr.q_decay);
+        }
+        K = std::max(K, std::max(a[k], b[k]) + 1);
+    }
+    out.K = K;
+    out.aoff.assign(K + 1, 0);
+    for (int k = 0; k < m; ++k) ++out.aoff[a[k] + 1];
+    for (int i = 0; i < K; ++i) out.aoff[i + 1] += out.aoff[i];
+    std::vector<int32_t> pos(out.aoff.begin(), out.aoff.end() - 1);
+    out.mk.assign(m, 0);
+    out.mb.assign(m, 0);
+    out.mc.assign(m, 0.0);
+    for (int k = 0; k < m; ++k) {                   // stable: modes of one a keep their KL order
+        const int e = pos[a[k]]++;
+        out.mk[e] = k;
+        out.mb[e] = b[k];
+        out.mc[e] = c[k];
+    }
+}
+
+void build_sep_tables(const mlmc_problem& pr, const KLModes& kl, const SepModes& sm, int N, std::vector<double>& tab) {
+    const int K = sm.K;
+    const double h = 1.0 / N;
+    const double pi = 3.141592653589793238462643383279502884;
+    tab.assign((size_t)4 * N * K, 0.0);
+    for (int i = 0; i < N; ++i)
+        for (int t = 0; t < 2; ++t) {
+            const double x = (i + (t ? 2.0 : 1.0) / 3.0) * h;
+            for (int q = 0; q < K; ++q) {
+                double f, g;
+                if (pr.field == MLMC_FIELD_EXPCOV_KL) {   // the same 1D function in both directions
+                    const double w = kl.w[q], r = kl.c / w;
+                    f = g = kl.nrm[q] * (std::cos(w * x) + r * std::sin(w * x));
+                } else {
+                    f = std::sin(2.0 * pi * (q + 1) * x);
+                    g = std::cos(2.0 * pi * (q + 1) * x);
+                }
+                tab[((size_t)t * N + i) * K + q] = f;
+                tab[((size_t)(2 + t) * N + i) * K + q] = g;
+            }
+        }
+}
+
 }  // namespace mlmc

@@ -21,6 +21,17 @@ struct KLModes {
 int kl_modes(double sigma2, double corr_len, int m, KLModes& out);
 // Phi[p*m + k] for the 2N^2 triangle centroids of an N x N mesh (R10 ordering).
 void build_phi(const mlmc_problem& pr, const KLModes& kl, int N, std::vector<double>& phi);
+// Separable form of the same synthesis (both fields are sums of products f_a(x1) g_b(x2)): mode k =
+// c_k f_{a_k}(x1) g_{b_k}(x2), the modes listed by x-function index a (CSR: aoff[K+1], mk = mode index,
+// mb = b_k, mc = c_k), and per mesh the four tables tab[t][i][a] (t = 0: f at (i + 1/3) h, 1: f at
+// (i + 2/3) h, 2: g at (i + 1/3) h, 3: g at (i + 2/3) h; i < N, a < K).
+struct SepModes {
+    int K = 0;
+    std::vector<int32_t> aoff, mk, mb;
+    std::vector<double> mc;
+};
+void build_sep_modes(const mlmc_problem& pr, const KLModes& kl, SepModes& out);
+void build_sep_tables(const mlmc_problem& pr, const KLModes& kl, const SepModes& sm, int N, std::vector<double>& tab);
 
 // ---------------------------------------------------------------- kernels
 // K0: xi[b*m + k] ~ N(0,1), b < nb, for global index first_index + b.
@@ -30,6 +41,12 @@ cudaError_t launch_rng(double* xi, int m, uint64_t nb, uint64_t seed, int level,
 // by the caller): keys[2b] = max_p a (bits), keys[2b+1] = ~min_p a (bits), the coefficient contrast.
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
                          unsigned long long* keys, cudaStream_t s);
+// K1s (default): the same a_T from the separable form, a = exp(f^T W) with W = sum_k c_k xi_k g (two small
+// contractions per sample instead of the P x m one); tab / aoff / mk / mb / mc as in SepModes (device).
+cudaError_t launch_field_sep(const double* tab, const int* aoff, const int* mk, const int* mb, const double* mc,
+                             int K, const double* xi, double* a, int N, int m, uint64_t nb, unsigned long long* keys,
+                             cudaStream_t s);
+bool field_use_dense();   // MLMC_FIELD_KERNEL=dense|ffma selects the P x m synthesis (A/B)
 // Longest-first order of nb <= kOrderMax systems by descending contrast max a / min a (a single-CTA
 // bitonic sort of the field keys): order[i] = system index.  The contrast predicts the MINRES
 // iteration count (correlation 0.83 on configs[1] level 3), so the job counter hands out the long

@@ -290,11 +290,157 @@ cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cud
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- K1s: separable synthesis
+// Both fields are sums of products: g(x1, x2) = sum_k c_k xi_k f_{a_k}(x1) g_{b_k}(x2) (the 2D KL modes of
+// the separable covariance, R11; Eq. (20)'s sin x cos terms).  With f, g tabulated at the N centroid
+// abscissae (i + 1/3) h, (i + 2/3) h of each axis, a lower triangle (centroid ((i+2/3)h, (j+1/3)h)) gets
+//     g_L(i, j) = sum_a f23[i][a] W_L[a][j],   W_L[a][j] = sum_{k: a_k = a} c_k xi_k g13[j][b_k],
+// an upper one the same with f13 and g23.  Per sample: 2 m N + 4 K N^2 flops instead of 4 m N^2 (K = the
+// number of 1D functions: 16 for configs[1], 30 for configs[4]); the same values as the P x m synthesis
+// up to the order of the binary64 sums.  A CTA takes SB samples x a TJ-row x TI-column tile of the mesh:
+// u = c xi (gathered in the CSR order), W_L / W_U for its rows, then the outputs (i fastest, so the
+// (lower, upper) pairs of a row are stored as contiguous double2), exp, and the contrast keys.
+__global__ void __launch_bounds__(256) field_sep_kernel(const double* __restrict__ tab, const int* __restrict__ aoff,
+                                                        const int* __restrict__ mk, const int* __restrict__ mb,
+                                                        const double* __restrict__ mc, int K,
+                                                        const double* __restrict__ xi, double* __restrict__ a, int N,
+                                                        int m, int nb, int SB, int TJ, int TI,
+                                                        unsigned long long* __restrict__ keys) {
+    extern __shared__ __align__(16) double fsm[];
+    double* u = fsm;                               // [SB][m] in CSR order
+    double* W0 = u + SB * m;                       // [SB][K][TJ]
+    double* W1 = W0 + SB * K * TJ;
+    double* F23 = W1 + SB * K * TJ;                // [K][TI]
+    double* F13 = F23 + K * TI;
+    double* G13 = F13 + K * TI;                    // [K][TJ]
+    double* G23 = G13 + K * TJ;
+    unsigned long long* kk = reinterpret_cast<unsigned long long*>(G23 + K * TJ);   // [SB][2]
+    const int tid = threadIdx.x;
+    const int b0 = blockIdx.x * SB, j0 = blockIdx.y * TJ, i0 = blockIdx.z * TI;
+    const int ns = min(SB, nb - b0), nj = min(TJ, N - j0), ni = min(TI, N - i0);
+    const size_t NK = (size_t)N * K;
+    for (int e = tid; e < SB * m; e += blockDim.x) {
+        const int sm = e / m, q = e % m;
+        u[e] = sm < ns ? __ldg(mc + q) * __ldg(xi + (size_t)(b0 + sm) * m + __ldg(mk + q)) : 0.0;
+    }
+    for (int e = tid; e < K * TI; e += blockDim.x) {
+        const int q = e / TI, ii = e % TI;
+        const bool in = ii < ni;
+        F13[e] = in ? __ldg(tab + (size_t)(i0 + ii) * K + q) : 0.0;
+        F23[e] = in ? __ldg(tab + NK + (size_t)(i0 + ii) * K + q) : 0.0;
+    }
+    for (int e = tid; e < K * TJ; e += blockDim.x) {
+        const int q = e / TJ, jj = e % TJ;
+        const bool in = jj < nj;
+        G13[e] = in ? __ldg(tab + 2 * NK + (size_t)(j0 + jj) * K + q) : 0.0;
+        G23[e] = in ? __ldg(tab + 3 * NK + (size_t)(j0 + jj) * K + q) : 0.0;
+    }
+    if (tid < 2 * SB) kk[tid] = 0ull;
+    __syncthreads();
+    for (int e = tid; e < SB * K * TJ; e += blockDim.x) {
+        const int sm = e / (K * TJ), r = e % (K * TJ), q = r / TJ, jj = r % TJ;
+        const double* us = u + sm * m;
+        double w0 = 0.0, w1 = 0.0;
+        const int e1 = __ldg(aoff + q + 1);
+        for (int c = __ldg(aoff + q); c < e1; ++c) {
+            const double uc = us[c];
+            const int bq = __ldg(mb + c);
+            w0 = fma(uc, G13[bq * TJ + jj], w0);
+            w1 = fma(uc, G23[bq * TJ + jj], w1);
+        }
+        W0[e] = w0;
+        W1[e] = w1;
+    }
+    __syncthreads();
+    const int P = 2 * N * N;
+    for (int e = tid; e < SB * TJ * TI; e += blockDim.x) {
+        const int sm = e / (TJ * TI), r = e % (TJ * TI), jj = r / TI, ii = r % TI;
+        const bool live = sm < ns && jj < nj && ii < ni;
+        double v0 = 0.0, v1 = 0.0;
+        if (live) {
+            const double* w0 = W0 + sm * K * TJ + jj;
+            const double* w1 = W1 + sm * K * TJ + jj;
+            double g0 = 0.0, g1 = 0.0;
+            for (int q = 0; q < K; ++q) {
+                g0 = fma(F23[q * TI + ii], w0[q * TJ], g0);
+                g1 = fma(F13[q * TI + ii], w1[q * TJ], g1);
+            }
+            v0 = exp(g0);
+            v1 = exp(g1);
+            *reinterpret_cast<double2*>(a + (size_t)(b0 + sm) * P + 2 * ((size_t)(j0 + jj) * N + i0 + ii)) =
+                make_double2(v0, v1);
+        }
+        if (keys) {
+            // contrast partials: a warp's outputs belong to one sample when TJ * TI is a multiple of 32
+            double mx = live ? fmax(v0, v1) : 0.0, mn = live ? fmin(v0, v1) : DBL_MAX;
+            const int s0 = __shfl_sync(0xffffffffu, sm, 0);
+            if (__all_sync(0xffffffffu, sm == s0)) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                }
+                if ((tid & 31) == 0 && s0 < ns) {
+                    atomicMax(kk + 2 * s0, (unsigned long long)__double_as_longlong(mx));
+                    atomicMax(kk + 2 * s0 + 1, ~(unsigned long long)__double_as_longlong(mn));
+                }
+            } else if (live) {
+                atomicMax(kk + 2 * sm, (unsigned long long)__double_as_longlong(mx));
+                atomicMax(kk + 2 * sm + 1, ~(unsigned long long)__double_as_longlong(mn));
+            }
+        }
+    }
+    if (keys) {
+        __syncthreads();
+        if (tid < ns) {
+            atomicMax(keys + 2 * (b0 + tid), kk[2 * tid]);
+            atomicMax(keys + 2 * (b0 + tid) + 1, kk[2 * tid + 1]);
+        }
+    }
+}
+
+cudaError_t launch_field_sep(const double* tab, const int* aoff, const int* mk, const int* mb, const double* mc,
+                             int K, const double* xi, double* a, int N, int m, uint64_t nb, unsigned long long* keys,
+                             cudaStream_t s) {
+    if (nb == 0) return cudaSuccess;
+    // tile: all of a small mesh per CTA with several samples, else 16 rows x 64 columns of one sample
+    int SB, TJ, TI;
+    if (N <= 8) { SB = 16; TJ = N; TI = N; }
+    else if (N <= 16) { SB = 4; TJ = N; TI = N; }
+    else if (N <= 32) { SB = 1; TJ = N; TI = N; }
+    else { SB = 1; TJ = 16; TI = 64; }
+    auto bytes = [&](int sb) {
+        return (size_t)8 * ((size_t)sb * m + 2 * (size_t)sb * K * TJ + 2 * (size_t)K * TI + 2 * (size_t)K * TJ) +
+               16 * (size_t)sb;
+    };
+    while (SB > 1 && bytes(SB) > 200 * 1024) SB /= 2;
+    const size_t smem = bytes(SB);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(field_sep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    const dim3 grid((unsigned)((nb + SB - 1) / SB), (unsigned)((N + TJ - 1) / TJ), (unsigned)((N + TI - 1) / TI));
+    field_sep_kernel<<<grid, 256, smem, s>>>(tab, aoff, mk, mb, mc, K, xi, a, N, m, (int)nb, SB, TJ, TI, keys);
+    return cudaGetLastError();
+}
+
 static bool field_use_ffma() {
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("MLMC_FIELD_KERNEL");
         v = (e && std::strcmp(e, "ffma") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+bool field_use_dense() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("MLMC_FIELD_KERNEL");
+        v = (e && (std::strcmp(e, "ffma") == 0 || std::strcmp(e, "dense") == 0)) ? 1 : 0;
     }
     return v == 1;
 }

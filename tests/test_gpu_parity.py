@@ -74,6 +74,24 @@ def test_rng_and_field_match_oracle(cfg_name):
     ctx.close()
 
 
+def test_field_synthesis_paths_match_oracle():
+    """configs[4] (m = 256, K = 30 one-dimensional functions): h = 1/8 takes the P x m synthesis on the FP64
+    tensor cores, h = 1/16 .. 1/64 the separable one (K1s; ragged sample blocks and 16 x 64 tiles);
+    both reproduce the oracle's centroid-by-centroid KL sum to 1e-12."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, L_max=3)
+    P = _oracle(cfg)
+    for level, mesh in ((0, 0), (1, 1), (3, 3), (3, 2)):
+        n = 37
+        xi, a = ctx.debug_field(level, mesh, n, seed=12, first_index=77)
+        xi, a = xi.cpu().numpy(), a.cpu().numpy()
+        N = cfg["h0_inv"] << mesh
+        for k in (0, 17, 36):
+            ref_a = P.field_triangles(N, oc.normals(12, level, 77 + k, cfg["m"]))
+            assert np.max(np.abs(a[k] / ref_a - 1)) < 1e-12, (level, mesh, k)
+    ctx.close()
+
+
 # ============================================================================ C1: fp64 parity 1e-10
 def test_C1_fp64_per_sample_parity_and_sums():
     cfg = W.CONFIGS["C1"]
