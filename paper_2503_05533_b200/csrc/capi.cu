@@ -182,9 +182,10 @@ struct LevelSched {
 // the separable one (K1s) where it needs several times fewer flops than the P x m contraction -- 4 m N +
 // 4 K N^2 against 4 m N^2, weighted 5x for the CUDA-core kernel against the DMMA one (measured: at N = 8
 // the DMMA kernel wins even at m = 256) -- or where Phi would not be small (> 256 MB); the P x m one
-// (K1, DMMA) otherwise.  MLMC_FIELD_KERNEL=dense|ffma forces the P x m one.
+// (K1, DMMA) otherwise.  MLMC_FIELD_KERNEL=dense|ffma forces the P x m one, =sep the separable one.
 bool field_sep(const mlmc_ctx* ctx, int N) {
     if (field_use_dense()) return false;
+    if (field_force_sep()) return true;
     const double m = ctx->pr.m, K = ctx->sep.K > 0 ? ctx->sep.K : m;
     const double phi_bytes = 8.0 * 2.0 * N * N * m;
     return 5.0 * (m + K * N) < N * m || phi_bytes > 256.0 * (1 << 20);

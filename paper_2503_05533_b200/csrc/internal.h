@@ -47,6 +47,7 @@ cudaError_t launch_field_sep(const double* tab, const int* aoff, const int* mk, 
                              int K, const double* xi, double* a, int N, int m, uint64_t nb, unsigned long long* keys,
                              cudaStream_t s);
 bool field_use_dense();   // MLMC_FIELD_KERNEL=dense|ffma selects the P x m synthesis (A/B)
+bool field_force_sep();   // MLMC_FIELD_KERNEL=sep selects the separable synthesis on every mesh (tests)
 // Longest-first order of nb <= kOrderMax systems by descending contrast max a / min a (a single-CTA
 // bitonic sort of the field keys): order[i] = system index.  The contrast predicts the MINRES
 // iteration count (correlation 0.83 on configs[1] level 3), so the job counter hands out the long

@@ -445,6 +445,15 @@ bool field_use_dense() {
     return v == 1;
 }
 
+bool field_force_sep() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("MLMC_FIELD_KERNEL");
+        v = (e && std::strcmp(e, "sep") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
                          unsigned long long* keys, cudaStream_t s) {
     if (nb == 0) return cudaSuccess;

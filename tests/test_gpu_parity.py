@@ -647,3 +647,38 @@ def test_c_quickstart(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("ok")
     assert "level 3:" in r.stdout and "adaptive MPML" in r.stdout
+
+
+def test_separable_synthesis_on_every_mesh_subprocess():
+    """MLMC_FIELD_KERNEL=sep (read once per process, hence a subprocess): the separable synthesis on every
+    mesh, for the BASELINE field (configs[1]) and the paper's Eq. (20) field, against the oracle."""
+    import subprocess
+    import textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import sys, numpy as np
+        sys.path.insert(0, %r); sys.path.insert(0, %r)
+        import workloads as W
+        from oracle import core as oc
+        from paper_2503_05533_b200 import Context
+        for name in ("C2", "EQ20"):
+            cfg = W.CONFIGS[name]
+            ctx = Context(field=cfg["field"], m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                          q_decay=cfg.get("q_decay", 2.0), h0_inv=cfg["h0_inv"], L_max=3, device=0,
+                          workspace_bytes=256 << 20)
+            P = oc.OracleProblem(cfg["field_code"], cfg["m"], cfg["sigma2"], cfg["corr_len"], cfg.get("q_decay", 2.0),
+                                 cfg["h0_inv"])
+            for level, mesh in ((0, 0), (1, 1), (3, 3), (3, 2)):
+                xi, a = ctx.debug_field(level, mesh, 21, seed=5, first_index=3)
+                a = a.cpu().numpy()
+                N = cfg["h0_inv"] << mesh
+                for k in (0, 20):
+                    ref = P.field_triangles(N, oc.normals(5, level, 3 + k, cfg["m"]))
+                    err = np.max(np.abs(a[k] / ref - 1))
+                    assert err < 1e-12, (name, level, mesh, k, err)
+            ctx.close()
+        print("sep ok")
+    """) % (root, os.path.join(root, "tests"))
+    env = dict(os.environ, MLMC_FIELD_KERNEL="sep")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0 and "sep ok" in r.stdout, r.stdout + r.stderr
