@@ -50,6 +50,12 @@ CPU_SAMPLE = {0: 2048, 1: 384, 2: 96, 3: 24}       # cpu_baseline: bounded oracl
 REF_SAMPLE = {0: 256, 1: 64, 2: 16, 3: 8}          # --impl reference: per-step oracle sample per level
 
 
+def _dbg(msg):
+    """BENCH_DEBUG=1: rank-tagged progress on stderr (multi-rank debugging)."""
+    if os.environ.get("BENCH_DEBUG"):
+        print(f"[rank {os.environ.get('RANK', '0')}] {msg}", file=sys.stderr, flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,10 +197,17 @@ def run_ours(args):
     if args.gpus != world and world == 1 and args.gpus > 1:
         print(json.dumps({"error": "--gpus > 1 must be launched with torch.distributed.run"}))
         sys.exit(2)
+    # BENCH_DIST_BACKEND=gloo with more ranks than GPUs exercises the multi-rank logic (sharding, all-reduce,
+    # max over ranks) on one GPU; its numbers are not scaling results.  The driver's runs use NCCL.
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import __graft_entry__
     if rank == 0 or world == 1:
@@ -223,9 +236,11 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(sums)
 
+    _dbg("context ready")
     clocks = ClockSampler(local)
     for i in range(args.warmup):
         step(10_000 + i)
+    _dbg("warm-up done")
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -323,16 +338,23 @@ def run_ours(args):
             "config": {"workload": "configs[1] (C2): 4-level MLMC h=1/8..1/64, KL m=64 (var 1, corr 0.3), "
                                    "N=(20000,5000,1200,300) per GPU, fp64 MINRES tols 1e-4/1e-5/1e-6/1e-8",
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"samples sharded, {world} rank(s), NCCL all-reduce of level sums"},
+                       "parallelism": f"samples sharded, {world} rank(s), "
+                                      f"{'NCCL' if backend == 'nccl' else backend} all-reduce of level sums"},
             "per_level": per_level, "roofline": roofline, "kernels": kernels, "gpu_launches": gpu_launches,
             "clocks": clk}
 
+    _dbg("timed steps and level pass done")
     if not args.no_extras:
         line["c2_step_with_mgpcg"] = mg_leg(ctx, cfg, args, world, rank, torch, dist, stream)
+        _dbg("mg leg done")
         line["e2e"] = e2e_leg(ctx, cfg, args, world, rank, torch, np, dist)
+        _dbg("e2e leg done")
         line["time_to_eps"] = adaptive_leg(args, world, rank, local, torch, dist)
+        _dbg("adaptive leg done")
         line["c3_cholesky_ir"] = c3_leg(local, torch)
+        _dbg("c3 leg done")
         line["k3c_fine_meshes"] = fine_leg(local, torch)
+        _dbg("fine leg done")
         if rank == 0:
             line["paper_mpml_vs_mlmc"] = paper_leg(local)
         if rank == 0 and world == 1:

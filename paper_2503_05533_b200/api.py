@@ -210,7 +210,7 @@ class Context:
                      fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None,
                      on_fail: int = 0) -> dict:
         """mlmc_adaptive_run (Algorithm 2).  With a torch.distributed group the per-round level sums are
-        all-reduced through it (NCCL on GPU tensors, gloo on CPU tensors)."""
+        all-reduced through it (NCCL on GPU tensors, gloo on CPU tensors); group=None runs locally."""
         rank, world, cb = _allreduce_callback(group, self.device)
         opts = K.AdaptiveOpts(k_p, fixed_tol, r_bias, N_init, policy, rank, world, max_rounds, seed, on_fail, 0)
         res = K.Result()
@@ -228,10 +228,12 @@ def _result_dict(res) -> dict:
 
 
 def _allreduce_callback(group, device):
-    """(rank, world, mlmc_allreduce_fn) for the torch.distributed group (or the default one if
-    initialised); NCCL groups reduce a tensor on `device`, others (gloo) on the CPU."""
+    """(rank, world, mlmc_allreduce_fn) for the torch.distributed group; group=None is a local run (world 1)
+    even when a default process group exists -- a multi-rank run names its group explicitly, so that a call
+    made by one rank alone (e.g. rank 0's extra measurements in bench.py) never waits on the others.  NCCL
+    groups reduce a tensor on `device`, others (gloo) on the CPU."""
     import torch as t
-    if group is None and not (t.distributed.is_available() and t.distributed.is_initialized()):
+    if group is None:
         return 0, 1, K.ALLREDUCE_FN(0)
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
