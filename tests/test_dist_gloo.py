@@ -130,3 +130,36 @@ def test_controller_standard_mlmc_mode_and_lmax():
     assert r["code"] in (0, 4)
     r = mlmc_adaptive_run_host(CFG["h0_inv"], 1, 2e-4, base, k_p=0.05, N_init=20, max_rounds=3)
     assert r["code"] == 4 and r["L"] == 1 and math.isfinite(r["estimate"])
+
+
+def _worker_local_on_one_rank(rank, world, port, q):
+    """A default process group exists, but only rank 0 runs an adaptive run with group=None: it must stay
+    local (world 1) instead of all-reducing through the default group while rank 1 waits in a barrier."""
+    import datetime
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
+    try:
+        r = _run(None) if rank == 0 else None
+        dist.barrier()
+        q.put((rank, r))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_group_none_is_local_even_with_a_default_group():
+    single = _run(None)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_local_on_one_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    r0 = res[0]
+    r0.pop("solve_seconds")
+    single.pop("solve_seconds")
+    assert res[1] is None and r0 == single
