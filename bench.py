@@ -351,6 +351,8 @@ def run_ours(args):
         _dbg("e2e leg done")
         line["time_to_eps"] = adaptive_leg(args, world, rank, local, torch, dist)
         _dbg("adaptive leg done")
+        line["c1_fp64"] = c1_leg(local, torch)
+        _dbg("c1 leg done")
         line["c3_cholesky_ir"] = c3_leg(local, torch)
         _dbg("c3 leg done")
         line["k3c_fine_meshes"] = fine_leg(local, torch)
@@ -411,6 +413,37 @@ def e2e_leg(ctx, cfg, args, world, rank, torch, np, dist):
             "api": "mlmc_sample_levels_xi (all levels concurrently; host pinned xi in, host per-sample records + "
                    "level sums out)",
             "clock": "host wall clock around the synchronous calls, max over ranks"}
+
+
+def c1_leg(local, torch):
+    """configs[0] (C1): both levels (h = 1/8, 1/16; N = 2000, 500 coupled samples) solved in binary64 to
+    relative residual 1e-12 -- the parity configuration -- with MINRES and with the binary64 banded
+    Cholesky (+ IR, u_s = binary64); device time of one sample_level call per level (median of 5)."""
+    from paper_2503_05533_b200 import Context, precision
+    cfg = W.CONFIGS["C1"]
+    ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
+                  L_max=cfg["L_max"], device=local, workspace_bytes=1 << 30)
+    stream = torch.cuda.current_stream()
+    sums = torch.zeros(12, dtype=torch.float64, device=torch.device("cuda", local))
+    out = {}
+    for name, prec in (("minres", precision("minres")), ("chol_fp64", precision("chol_ir", "d", "d"))):
+        for l, n in enumerate(cfg["N"]):
+            ctx.sample_level_async(l, n, cfg["seed"], 10**7, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
+            ts = []
+            for rep in range(5):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                ctx.sample_level_async(l, n, cfg["seed"], 0, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            s = sums.cpu().numpy()
+            ms = sorted(ts)[2]
+            out[f"l{l}_{name}"] = {"h": f"1/{cfg['h0_inv'] << l}", "samples": n, "ms": ms,
+                                   "samples_per_s": n / (ms / 1e3), "mean_steps_fine": s[7] / n,
+                                   "failures": s[6]}
+    ctx.close()
+    return out
 
 
 def c3_leg(local, torch):
