@@ -497,10 +497,13 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
     switch (N) {
         case 8:   // two systems per warp (16 threads each)
             if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            // (conductances in shared memory with 8 / 6 systems-pairs per SM: 0.133 / 0.127 ms vs 0.109 ms on
+            // configs[1] level 0; 16 systems per warp-pair cannot hide the extra shared loads)
             return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 16:
             if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            // (conductances in shared memory, 6 / 8 CTAs per SM: level-1 pass 0.60 / 0.61 ms vs 0.51 ms)
             return run_tile<16, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 32:
             if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
