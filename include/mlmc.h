@@ -77,9 +77,10 @@ typedef struct {
  *   arithmetic binary64, stop at the first k with phibar_k/||b|| <=
  *   tol (Eq. (2) with C = 1, R9).  u_* fields ignored.
  * solver = MLMC_SOLVER_CHOL_IR: Algorithm 1: banded Cholesky in
- *   u_f (MLMC_FMT_F16 / F32 / F64), initial and correction substitutions in
- *   u_s (F32 or F64, R24), residual in u_r and x in u (both F64), stop when
- *   ||r||/||b|| < tol, at most max_iter refinement steps.
+ *   u_f (MLMC_FMT_E4M3 / F16 / F32 / F64), initial and correction substitutions in
+ *   u_s (F32 or F64, R24), residual in u_r and x in u (u = u_r, F64 or F32 -- the
+ *   paper's "..ss" quads of Table 1 right), stop when ||r||/||b|| < tol
+ *   (P:120), at most max_iter refinement steps.
  * solver = MLMC_SOLVER_MGCG (NEXT-4 of SURVEY section 8(f), h = 1/8 .. 1/512): conjugate gradients in
  *   binary64 preconditioned by one symmetric multigrid V(1,1) cycle in binary32 (nested P1 meshes,
  *   Galerkin-exact coarse operators, red-black Gauss-Seidel), the same stopping rule ||r_k||/||b|| <=

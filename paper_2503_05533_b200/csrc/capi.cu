@@ -114,7 +114,7 @@ struct WsLayout {
 // Cholesky factor scratch of one solve (0 for MINRES / unsupported combinations)
 size_t chol_bytes(const mlmc_precision* p, int N, uint64_t batch) {
     if (!p || p->solver != MLMC_SOLVER_CHOL_IR || N < 2) return 0;
-    return chol_scratch_bytes(N, p->u_f, p->u_s, batch);
+    return chol_scratch_bytes(N, p->u_f, p->u_s, batch, p->u);
 }
 WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_precision* pf = nullptr,
                    const mlmc_precision* pc = nullptr) {
@@ -250,8 +250,8 @@ int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
         return MLMC_OK;
     }
     if (p->solver == MLMC_SOLVER_CHOL_IR) {
-        if (p->u != MLMC_FMT_F64 || p->u_r != MLMC_FMT_F64)
-            return fail(ctx, MLMC_EINVAL, "IR supports u = u_r = binary64 only");
+        if (p->u != p->u_r || (p->u != MLMC_FMT_F64 && p->u != MLMC_FMT_F32))
+            return fail(ctx, MLMC_EINVAL, "IR supports u = u_r in binary64 or binary32");
         if (!chol_supported(N, p->u_f, p->u_s))
             return fail(ctx, MLMC_EINVAL, "Cholesky-IR (u_f, u_s) not supported for N=" + std::to_string(N));
         return MLMC_OK;
@@ -323,7 +323,7 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
         CU(counted(ctx, ex.st, MLMC_K_CHOL_IR, N,
                    [&] {
                        return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ch_scratch, ch_bytes,
-                                             ex.st);
+                                             ex.st, p->u);
                    }));
     }
     return MLMC_OK;

@@ -90,11 +90,12 @@ cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of
 // chol_scratch_bytes(N, u_f, u_s, nb) bytes for a launch over nb systems (one factor per resident
 // warp segment; a smaller scratch shrinks the grid; 0 = unsupported).
+// u: the working precision u = u_r of x and the residual (MLMC_FMT_F64 default, or MLMC_FMT_F32).
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max,
                            double* out, int slot, unsigned* job_counter, void* fscratch, size_t fbytes,
-                           cudaStream_t s);
+                           cudaStream_t s, int u = MLMC_FMT_F64);
 bool chol_supported(int N, int u_f, int u_s);
-size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb);
+size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb, int u = MLMC_FMT_F64);
 // K5: per-level sums of the per-sample records into sums (accumulate = add to existing).
 cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,
                               double cost_f_fixed, double cost_f_step, double cost_c_fixed,

@@ -537,7 +537,8 @@ __device__ __forceinline__ void backward(R& ring, S* v, int l, bool leader) {
     __syncwarp();
 }
 
-template <int N, typename F, typename S, int NS, int WPC>
+// U: the working precision u = u_r of x and of the residual (Algorithm 1 steps 4 and 8; double or float)
+template <int N, typename F, typename S, int NS, int WPC, typename U = double>
 __global__ void __launch_bounds__(32 * WPC)
 chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_max, double* __restrict__ out,
                    int slot, unsigned* __restrict__ job_counter, const unsigned char* __restrict__ fac,
@@ -553,7 +554,7 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
     const bool leader = l == 0;
     unsigned char* base = smem + (size_t)(warp * SEGS + seg) * K::SEG_BYTES;
     S* v = reinterpret_cast<S*>(base + K::OFF_V);
-    double* xs = xscratch + (((size_t)blockIdx.x * WPC + warp) * SEGS + seg) * NPAD;
+    U* xs = reinterpret_cast<U*>(xscratch + (((size_t)blockIdx.x * WPC + warp) * SEGS + seg) * NPAD);
     Ring<NB, BLK, NS> ring;
     ring.buf = base;
     ring.sbuf = smem_u32(base);
@@ -600,17 +601,20 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
 #pragma unroll 4
                     for (int q = 0; q < PER; ++q) {
                         const int e = l + q * W;
-                        double r = 0.0;
+                        U r = (U)0;
                         if (e < n) {
                             const int i = e % (N - 1) + 1, j = e / (N - 1) + 1;
                             const double ce = A.cE(i, j), cw = A.cE(i - 1, j), cn = A.cN(i, j), cs = A.cN(i, j - 1);
-                            double Ax = ((ce + cw) + (cn + cs)) * xs[e];
-                            if (i < N - 1) Ax = fma(-ce, xs[e + 1], Ax);
-                            if (i > 1) Ax = fma(-cw, xs[e - 1], Ax);
-                            if (j < N - 1) Ax = fma(-cn, xs[e + N - 1], Ax);
-                            if (j > 1) Ax = fma(-cs, xs[e - (N - 1)], Ax);
-                            r = h2 - Ax;
-                            part = fma(r, r, part);
+                            // the matrix entries in u_r, every product and sum in u_r (fused where the
+                            // hardware fuses: one rounding per FMA)
+                            const U ue = (U)ce, uw = (U)cw, un = (U)cn, us = (U)cs, ud = (U)((ce + cw) + (cn + cs));
+                            U Ax = ud * xs[e];
+                            if (i < N - 1) Ax = fma(-ue, xs[e + 1], Ax);
+                            if (i > 1) Ax = fma(-uw, xs[e - 1], Ax);
+                            if (j < N - 1) Ax = fma(-un, xs[e + N - 1], Ax);
+                            if (j > 1) Ax = fma(-us, xs[e - (N - 1)], Ax);
+                            r = (U)h2 - Ax;
+                            part = fma((double)r, (double)r, part);
                         }
                         v[e] = (S)r;
                     }
@@ -631,17 +635,17 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
             backward<G, F, S>(ring, v, l, leader);
             if (it < 0) {
 #pragma unroll 4
-                for (int q = 0; q < PER; ++q) xs[l + q * W] = (double)v[l + q * W];
-            } else if (active) {
+                for (int q = 0; q < PER; ++q) xs[l + q * W] = (U)v[l + q * W];
+            } else if (active) {                       // step 8: x += d in u (d rounded to u first)
 #pragma unroll 4
-                for (int q = 0; q < PER; ++q) xs[l + q * W] += (double)v[l + q * W];
+                for (int q = 0; q < PER; ++q) xs[l + q * W] = xs[l + q * W] + (U)v[l + q * W];
             }
             if (it < 0 || active) ++it;
             __syncwarp(mask);
         }
         ring.drain();
         double sx = 0.0;
-        for (int q = 0; q < PER; ++q) sx += xs[l + q * W];      // padded rows hold exact zeros
+        for (int q = 0; q < PER; ++q) sx += (double)xs[l + q * W];   // padded rows hold exact zeros
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) sx += __shfl_xor_sync(mask, sx, o, W);
         if (live && leader) {
@@ -655,7 +659,7 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
 }
 
 // ======================================================================== launch
-template <int N, typename F, typename S, int NS = 3, int WPC = 4>
+template <int N, typename F, typename S, int NS = 3, int WPC = 4, typename U = double>
 struct Launch {
     using G = Geo<N, F, S>;
     using KF = FacCfg<N, F, S>;
@@ -666,7 +670,7 @@ struct Launch {
             cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel<N, F, S>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, KF::SMEM);
             if (e != cudaSuccess) return e;
-            auto kern = chol_refine_kernel<N, F, S, NS, WPC>;
+            auto kern = chol_refine_kernel<N, F, S, NS, WPC, U>;
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, KR::SMEM);
             if (e != cudaSuccess) return e;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * WPC, KR::SMEM);
@@ -704,8 +708,8 @@ struct Launch {
         chol_factor_kernel<N, F, S><<<(unsigned)fgrid, 32 * kFacWarps, KF::SMEM, s>>>(a, (int)nb, fac, out, slot);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         const uint64_t grid = std::min<uint64_t>((nb + per_cta - 1) / per_cta, (uint64_t)gm);
-        chol_refine_kernel<N, F, S, NS, WPC><<<(unsigned)grid, 32 * WPC, KR::SMEM, s>>>(a, (int)nb, tol, i_max, out,
-                                                                                     slot, ctr, fac, xs);
+        chol_refine_kernel<N, F, S, NS, WPC, U><<<(unsigned)grid, 32 * WPC, KR::SMEM, s>>>(a, (int)nb, tol, i_max,
+                                                                                        out, slot, ctr, fac, xs);
         return cudaGetLastError();
     }
 };
@@ -721,50 +725,60 @@ int chol_variant() {
     return v;
 }
 
-template <int N, typename F, typename S, class Fn>
-cudaError_t with_shape(Fn&& fn) {
+template <int N, typename F, typename S, typename U, class Fn>
+cudaError_t with_shape_u(Fn&& fn) {
     if constexpr (N == 32 && sizeof(S) == 4) {
-        switch (chol_variant()) {
-            // measured (configs[2] level 2, 100k coupled samples, fp16 / fp32 factor): <3,4> 72.5 / 42.4 ms,
-            // <4,4> 78.6 / 47.5, <2,4> 69.6 / 41.4, <2,2> 68.9 / 41.4, <3,8> 77.5 / 46.7
-            case 1: return fn(Launch<N, F, S, 4, 4>{});
-            case 2: return fn(Launch<N, F, S, 2, 4>{});
-            case 3: return fn(Launch<N, F, S, 3, 4>{});
-            case 4: return fn(Launch<N, F, S, 3, 8>{});
-            default: return fn(Launch<N, F, S, 2, 2>{});
+        if constexpr (sizeof(U) == 8) {
+            switch (chol_variant()) {
+                // measured (configs[2] level 2, 100k coupled samples, fp16 / fp32 factor): <3,4> 72.5 / 42.4 ms,
+                // <4,4> 78.6 / 47.5, <2,4> 69.6 / 41.4, <2,2> 68.9 / 41.4, <3,8> 77.5 / 46.7
+                case 1: return fn(Launch<N, F, S, 4, 4, U>{});
+                case 2: return fn(Launch<N, F, S, 2, 4, U>{});
+                case 3: return fn(Launch<N, F, S, 3, 4, U>{});
+                case 4: return fn(Launch<N, F, S, 3, 8, U>{});
+                default: break;
+            }
         }
+        return fn(Launch<N, F, S, 2, 2, U>{});
     } else {
-        return fn(Launch<N, F, S, 3, 4>{});
+        return fn(Launch<N, F, S, 3, 4, U>{});
     }
+}
+
+// u = u_r: binary64 (the default) or binary32 (the paper's "..ss" quads, Table 1 right)
+template <int N, typename F, typename S, class Fn>
+cudaError_t with_shape(bool vf32, Fn&& fn) {
+    if (vf32) return with_shape_u<N, F, S, float>(fn);
+    return with_shape_u<N, F, S, double>(fn);
 }
 
 // (u_f, u_s) -> instantiation; returns cudaErrorNotSupported for combinations not built.
 template <int N, class Fn>
-cudaError_t with_types(int u_f, int u_s, Fn&& fn) {
+cudaError_t with_types(int u_f, int u_s, bool vf32, Fn&& fn) {
     if (u_f == MLMC_FMT_E4M3) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, fp8, float>(fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, fp8, double>(fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, fp8, float>(vf32, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, fp8, double>(vf32, fn);
     } else if (u_f == MLMC_FMT_F16) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(vf32, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(vf32, fn);
     } else if (u_f == MLMC_FMT_F32) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, float, float>(fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, float, double>(fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, float, float>(vf32, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, float, double>(vf32, fn);
     } else if (u_f == MLMC_FMT_F64) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(vf32, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(vf32, fn);
     }
     return cudaErrorNotSupported;
 }
 
 template <class Fn>
-cudaError_t with_mesh(int N, int u_f, int u_s, Fn&& fn) {
+cudaError_t with_mesh(int N, int u_f, int u_s, bool vf32, Fn&& fn) {
     switch (N) {
-        case 2: return with_types<2>(u_f, u_s, fn);
-        case 4: return with_types<4>(u_f, u_s, fn);
-        case 8: return with_types<8>(u_f, u_s, fn);
-        case 16: return with_types<16>(u_f, u_s, fn);
-        case 32: return with_types<32>(u_f, u_s, fn);
+        case 2: return with_types<2>(u_f, u_s, vf32, fn);
+        case 4: return with_types<4>(u_f, u_s, vf32, fn);
+        case 8: return with_types<8>(u_f, u_s, vf32, fn);
+        case 16: return with_types<16>(u_f, u_s, vf32, fn);
+        case 32: return with_types<32>(u_f, u_s, vf32, fn);
         default: return cudaErrorNotSupported;
     }
 }
@@ -778,15 +792,15 @@ bool chol_supported(int N, int u_f, int u_s) {
     return true;
 }
 
-size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb) {
+size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb, int u) {
     size_t bytes = 0;
-    cudaError_t e = with_mesh(N, u_f, u_s, [&](auto L) { return decltype(L)::scratch(bytes, nb); });
+    cudaError_t e = with_mesh(N, u_f, u_s, u == MLMC_FMT_F32, [&](auto L) { return decltype(L)::scratch(bytes, nb); });
     return e == cudaSuccess ? bytes : 0;
 }
 
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max, double* out,
-                           int slot, unsigned* ctr, void* scratch, size_t bytes, cudaStream_t s) {
-    return with_mesh(N, u_f, u_s, [&](auto L) {
+                           int slot, unsigned* ctr, void* scratch, size_t bytes, cudaStream_t s, int u) {
+    return with_mesh(N, u_f, u_s, u == MLMC_FMT_F32, [&](auto L) {
         return decltype(L)::run(a, nb, tol, i_max, out, slot, ctr, scratch, bytes, s);
     });
 }

@@ -682,3 +682,33 @@ def test_separable_synthesis_on_every_mesh_subprocess():
     env = dict(os.environ, MLMC_FIELD_KERNEL="sep")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
     assert r.returncode == 0 and "sep ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("quad,level,tol", [("hsss", 0, 3.5e-3), ("ssss", 1, 8.7e-4), ("hsss", 1, 1e-5),
+                                            ("ssss", 2, 2.2e-4)])
+def test_ir_single_precision_working_vectors(quad, level, tol):
+    """Algorithm 1 with u = u_r = binary32 (the paper's "..ss" quads of Table 1 right; u_s = s by
+    R24) at tolerances of Table 1's order (a binary32 residual cannot certify much below ~1e-5 at h = 1/32:
+    its rounding error is ~u_s ||A|| ||x||, which is why the paper switches to ..dd there): converged samples
+    reach the tolerance, Q within the direct solve's residual bound, the step counts track the oracle's
+    Algorithm 1 emulating the same quad (every operation rounded to its format)."""
+    cfg = W.CONFIGS["C3"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    prec = precision("chol_ir", *quad)
+    n = {0: 2000, 1: 300, 2: 40}[level]
+    r = ctx.sample_level(level, n, seed=8, prec_fine=prec, prec_coarse=prec, tol_fine=tol, tol_coarse=tol,
+                         per_sample=True)
+    ps = r.per_sample
+    assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0)
+    assert np.all(ps[:, 4] < tol)
+    Nf = cfg["h0_inv"] << level
+    idx = list(range(0, n, max(1, n // 12)))
+    exs = _pmap(lambda k: _exact(P, Nf, oc.normals(8, level, k, cfg["m"])), idx)
+    for k, (q, bn, xn) in zip(idx, exs):
+        # the binary32 x adds its own rounding (|dx| <= u_fp32 |x|) to the residual bound
+        assert abs(ps[k, 0] - q) <= tol * bn * xn * (1 + 1e-6) + 2e-7 * q, (quad, level, k)
+    for k in idx[:3]:
+        o = P.solve_mesh(Nf, oc.normals(8, level, k, cfg["m"]), oc.SOLVER_IR, tol=tol, quad=quad, max_iter=50)
+        assert o["status"] == 0 and abs(o["iters"] - ps[k, 2]) <= max(2, 0.5 * o["iters"]), (o["iters"], ps[k, 2])
+    ctx.close()
