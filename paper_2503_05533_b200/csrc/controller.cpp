@@ -34,17 +34,19 @@ mlmc_precision minres_prec() {
     return mlmc_precision{MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
 }
 
-// Table 1 (right) quads on the levels where the shared-memory
-// banded factor exists (N <= 32); u = u_r = binary64 here (the paper's level
-// 0/1 working precisions h/s are not implemented), MINRES beyond (R14).
-mlmc_precision policy_prec(int policy, int level, int N) {
+// Table 1 (right) quads on the levels where the shared-memory banded factor exists (N <= 32):
+// level 0 hhss -> hsss, level 1 ssss, levels 2+ ssdd (u_s >= binary32, R24); binary32 working vectors only
+// where the level's tolerance is one a binary32 residual can certify (>= 1e-5; else ..dd), MINRES beyond
+// (R14).
+mlmc_precision policy_prec(int policy, int level, int N, double tol) {
     if (policy == 2 && N >= 32)   // NEXT-4: MG-PCG where it beats MINRES, h <= 1/32
         return mlmc_precision{MLMC_SOLVER_MGCG, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
     if (policy == 1 && N <= 32) {
+        const int vec = tol >= 1e-5 ? MLMC_FMT_F32 : MLMC_FMT_F64;
         if (level == 0)
-            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
+            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, vec, vec, 0, 0};
         if (level == 1)
-            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
+            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, vec, vec, 0, 0};
         return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
     }
     return minres_prec();
@@ -102,8 +104,8 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             lv.push_back(l);
             cnt.push_back(hi - lo);
             first.push_back(lo);
-            pf.push_back(policy_prec(o.policy, l, h0_inv << l));
-            pc.push_back(l > 0 ? policy_prec(o.policy, l - 1, h0_inv << (l - 1)) : pf.back());
+            pf.push_back(policy_prec(o.policy, l, h0_inv << l, epsl[l]));
+            pc.push_back(l > 0 ? policy_prec(o.policy, l - 1, h0_inv << (l - 1), epsl[l - 1]) : pf.back());
             tf.push_back(epsl[l]);
             tc.push_back(l > 0 ? epsl[l - 1] : epsl[l]);
         }
