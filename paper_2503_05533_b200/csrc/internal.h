@@ -90,7 +90,7 @@ cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of
 // chol_scratch_bytes(N, u_f, u_s, nb) bytes for a launch over nb systems (one factor per resident
 // warp segment; a smaller scratch shrinks the grid; 0 = unsupported).
-// u: the working precision u = u_r of x and the residual (MLMC_FMT_F64 default, or MLMC_FMT_F32).
+// u: the working precision u = u_r of x and the residual (MLMC_FMT_F64 default, MLMC_FMT_F32 or MLMC_FMT_F16).
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max,
                            double* out, int slot, unsigned* job_counter, void* fscratch, size_t fbytes,
                            cudaStream_t s, int u = MLMC_FMT_F64);

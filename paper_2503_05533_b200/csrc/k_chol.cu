@@ -425,6 +425,33 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
         : "memory");
 }
 
+// Working / residual precision u = u_r of Algorithm 1 (steps 4 and 8): binary64, binary32, or binary16 with
+// every operation computed in binary32 and rounded once to binary16 (as the factor formats, R17).
+template <typename U> struct VT {
+    static __device__ __forceinline__ U from(double v) { return (U)v; }
+    static __device__ __forceinline__ double to_d(U v) { return (double)v; }
+    static __device__ __forceinline__ U mul(U a, U b) { return a * b; }
+    static __device__ __forceinline__ U fnma(U a, U b, U c) { return fma(-a, b, c); }
+    static __device__ __forceinline__ U sub(U a, U b) { return a - b; }
+    static __device__ __forceinline__ U add(U a, U b) { return a + b; }
+};
+template <> struct VT<__half> {
+    static __device__ __forceinline__ __half from(double v) { return __double2half(v); }
+    static __device__ __forceinline__ double to_d(__half v) { return (double)__half2float(v); }
+    static __device__ __forceinline__ __half mul(__half a, __half b) {
+        return __float2half_rn(__half2float(a) * __half2float(b));
+    }
+    static __device__ __forceinline__ __half fnma(__half a, __half b, __half c) {
+        return __float2half_rn(fmaf(-__half2float(a), __half2float(b), __half2float(c)));
+    }
+    static __device__ __forceinline__ __half sub(__half a, __half b) {
+        return __float2half_rn(__half2float(a) - __half2float(b));
+    }
+    static __device__ __forceinline__ __half add(__half a, __half b) {
+        return __float2half_rn(__half2float(a) + __half2float(b));
+    }
+};
+
 template <int N, typename F, typename S, int NS_, int WPC_>
 struct RefCfg {
     using G = Geo<N, F, S>;
@@ -601,22 +628,25 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
 #pragma unroll 4
                     for (int q = 0; q < PER; ++q) {
                         const int e = l + q * W;
-                        U r = (U)0;
+                        using V = VT<U>;
+                        U r = V::from(0.0);
                         if (e < n) {
                             const int i = e % (N - 1) + 1, j = e / (N - 1) + 1;
                             const double ce = A.cE(i, j), cw = A.cE(i - 1, j), cn = A.cN(i, j), cs = A.cN(i, j - 1);
                             // the matrix entries in u_r, every product and sum in u_r (fused where the
                             // hardware fuses: one rounding per FMA)
-                            const U ue = (U)ce, uw = (U)cw, un = (U)cn, us = (U)cs, ud = (U)((ce + cw) + (cn + cs));
-                            U Ax = ud * xs[e];
-                            if (i < N - 1) Ax = fma(-ue, xs[e + 1], Ax);
-                            if (i > 1) Ax = fma(-uw, xs[e - 1], Ax);
-                            if (j < N - 1) Ax = fma(-un, xs[e + N - 1], Ax);
-                            if (j > 1) Ax = fma(-us, xs[e - (N - 1)], Ax);
-                            r = (U)h2 - Ax;
-                            part = fma((double)r, (double)r, part);
+                            const U ue = V::from(ce), uw = V::from(cw), un = V::from(cn), us = V::from(cs),
+                                    ud = V::from((ce + cw) + (cn + cs));
+                            U Ax = V::mul(ud, xs[e]);
+                            if (i < N - 1) Ax = V::fnma(ue, xs[e + 1], Ax);
+                            if (i > 1) Ax = V::fnma(uw, xs[e - 1], Ax);
+                            if (j < N - 1) Ax = V::fnma(un, xs[e + N - 1], Ax);
+                            if (j > 1) Ax = V::fnma(us, xs[e - (N - 1)], Ax);
+                            r = V::sub(V::from(h2), Ax);
+                            const double rd = V::to_d(r);
+                            part = fma(rd, rd, part);
                         }
-                        v[e] = (S)r;
+                        v[e] = (S)V::to_d(r);
                     }
                 }
 #pragma unroll
@@ -635,17 +665,18 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
             backward<G, F, S>(ring, v, l, leader);
             if (it < 0) {
 #pragma unroll 4
-                for (int q = 0; q < PER; ++q) xs[l + q * W] = (U)v[l + q * W];
+                for (int q = 0; q < PER; ++q) xs[l + q * W] = VT<U>::from((double)v[l + q * W]);
             } else if (active) {                       // step 8: x += d in u (d rounded to u first)
 #pragma unroll 4
-                for (int q = 0; q < PER; ++q) xs[l + q * W] = xs[l + q * W] + (U)v[l + q * W];
+                for (int q = 0; q < PER; ++q)
+                    xs[l + q * W] = VT<U>::add(xs[l + q * W], VT<U>::from((double)v[l + q * W]));
             }
             if (it < 0 || active) ++it;
             __syncwarp(mask);
         }
         ring.drain();
         double sx = 0.0;
-        for (int q = 0; q < PER; ++q) sx += (double)xs[l + q * W];   // padded rows hold exact zeros
+        for (int q = 0; q < PER; ++q) sx += VT<U>::to_d(xs[l + q * W]);   // padded rows hold exact zeros
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) sx += __shfl_xor_sync(mask, sx, o, W);
         if (live && leader) {
@@ -745,40 +776,42 @@ cudaError_t with_shape_u(Fn&& fn) {
     }
 }
 
-// u = u_r: binary64 (the default) or binary32 (the paper's "..ss" quads, Table 1 right)
+// u = u_r: binary64 (the default), binary32 or binary16 (the paper's "..ss" / "..hh" quads, Table 1 right,
+// P:596-607)
 template <int N, typename F, typename S, class Fn>
-cudaError_t with_shape(bool vf32, Fn&& fn) {
-    if (vf32) return with_shape_u<N, F, S, float>(fn);
+cudaError_t with_shape(int vfmt, Fn&& fn) {
+    if (vfmt == MLMC_FMT_F32) return with_shape_u<N, F, S, float>(fn);
+    if (vfmt == MLMC_FMT_F16) return with_shape_u<N, F, S, __half>(fn);
     return with_shape_u<N, F, S, double>(fn);
 }
 
 // (u_f, u_s) -> instantiation; returns cudaErrorNotSupported for combinations not built.
 template <int N, class Fn>
-cudaError_t with_types(int u_f, int u_s, bool vf32, Fn&& fn) {
+cudaError_t with_types(int u_f, int u_s, int vfmt, Fn&& fn) {
     if (u_f == MLMC_FMT_E4M3) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, fp8, float>(vf32, fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, fp8, double>(vf32, fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, fp8, float>(vfmt, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, fp8, double>(vfmt, fn);
     } else if (u_f == MLMC_FMT_F16) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(vf32, fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(vf32, fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(vfmt, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(vfmt, fn);
     } else if (u_f == MLMC_FMT_F32) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, float, float>(vf32, fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, float, double>(vf32, fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, float, float>(vfmt, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, float, double>(vfmt, fn);
     } else if (u_f == MLMC_FMT_F64) {
-        if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(vf32, fn);
-        if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(vf32, fn);
+        if (u_s == MLMC_FMT_F32) return with_shape<N, double, float>(vfmt, fn);
+        if (u_s == MLMC_FMT_F64) return with_shape<N, double, double>(vfmt, fn);
     }
     return cudaErrorNotSupported;
 }
 
 template <class Fn>
-cudaError_t with_mesh(int N, int u_f, int u_s, bool vf32, Fn&& fn) {
+cudaError_t with_mesh(int N, int u_f, int u_s, int vfmt, Fn&& fn) {
     switch (N) {
-        case 2: return with_types<2>(u_f, u_s, vf32, fn);
-        case 4: return with_types<4>(u_f, u_s, vf32, fn);
-        case 8: return with_types<8>(u_f, u_s, vf32, fn);
-        case 16: return with_types<16>(u_f, u_s, vf32, fn);
-        case 32: return with_types<32>(u_f, u_s, vf32, fn);
+        case 2: return with_types<2>(u_f, u_s, vfmt, fn);
+        case 4: return with_types<4>(u_f, u_s, vfmt, fn);
+        case 8: return with_types<8>(u_f, u_s, vfmt, fn);
+        case 16: return with_types<16>(u_f, u_s, vfmt, fn);
+        case 32: return with_types<32>(u_f, u_s, vfmt, fn);
         default: return cudaErrorNotSupported;
     }
 }
@@ -794,13 +827,13 @@ bool chol_supported(int N, int u_f, int u_s) {
 
 size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb, int u) {
     size_t bytes = 0;
-    cudaError_t e = with_mesh(N, u_f, u_s, u == MLMC_FMT_F32, [&](auto L) { return decltype(L)::scratch(bytes, nb); });
+    cudaError_t e = with_mesh(N, u_f, u_s, u, [&](auto L) { return decltype(L)::scratch(bytes, nb); });
     return e == cudaSuccess ? bytes : 0;
 }
 
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max, double* out,
                            int slot, unsigned* ctr, void* scratch, size_t bytes, cudaStream_t s, int u) {
-    return with_mesh(N, u_f, u_s, u == MLMC_FMT_F32, [&](auto L) {
+    return with_mesh(N, u_f, u_s, u, [&](auto L) {
         return decltype(L)::run(a, nb, tol, i_max, out, slot, ctr, scratch, bytes, s);
     });
 }

@@ -712,3 +712,26 @@ def test_ir_single_precision_working_vectors(quad, level, tol):
         o = P.solve_mesh(Nf, oc.normals(8, level, k, cfg["m"]), oc.SOLVER_IR, tol=tol, quad=quad, max_iter=50)
         assert o["status"] == 0 and abs(o["iters"] - ps[k, 2]) <= max(2, 0.5 * o["iters"]), (o["iters"], ps[k, 2])
     ctx.close()
+
+
+@pytest.mark.parametrize("quad", ["qshh", "hshh"])
+def test_ir_half_precision_working_vectors(quad):
+    """Algorithm 1 with u = u_r = binary16 (the paper's qhhh of the E4 experiment, with u_s = s by
+    R24) on the level-0 mesh of that setup (h0 = 1/4, eps_0 = sqrt(k_p) h0^2 = 0.04 for k_p = 0.4): the
+    solves converge, Q within the direct solve's residual bound (+ the binary16 rounding of x), and the
+    step counts track the oracle's emulation of the same quad."""
+    ctx = Context(field="eq20", m=1, sigma2=1.0, corr_len=0.0, q_decay=2.0, h0_inv=4, L_max=3, device=0,
+                  workspace_bytes=256 << 20)
+    P = oc.OracleProblem(1, 1, 1.0, 0.0, 2.0, 4)
+    tol = 0.04
+    prec = precision("chol_ir", *quad)
+    n = 500
+    ps = ctx.sample_level(0, n, seed=6, prec_fine=prec, tol_fine=tol, per_sample=True).per_sample
+    assert np.all(ps[:, 6] == 0) and np.all(ps[:, 4] < tol)
+    for k in range(0, n, 50):
+        xi = oc.normals(6, 0, k, 1)
+        q, bn, xn = _exact(P, 4, xi)
+        assert abs(ps[k, 0] - q) <= tol * bn * xn * (1 + 1e-6) + 2e-3 * q, (k, ps[k, 0], q)
+        o = P.solve_mesh(4, xi, oc.SOLVER_IR, tol=tol, quad=quad, max_iter=50)
+        assert o["status"] == 0 and abs(o["iters"] - ps[k, 2]) <= 2, (o["iters"], ps[k, 2])
+    ctx.close()
