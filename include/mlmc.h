@@ -78,7 +78,8 @@ typedef struct {
  *   tol (Eq. (2) with C = 1, R9).  u_* fields ignored.
  * solver = MLMC_SOLVER_CHOL_IR: Algorithm 1: banded Cholesky in
  *   u_f (MLMC_FMT_E4M3 / F16 / F32 / F64), initial and correction substitutions in
- *   u_s (F32 or F64, R24), residual in u_r and x in u (u = u_r, F64, F32 or F16 -- the
+ *   u_s (F32 or F64, R24; F16 with an E4M3 / F16 factor and u <= F32, as the paper's
+ *   "hh.." quads), residual in u_r and x in u (u = u_r, F64, F32 or F16 -- the
  *   paper's "..ss" / "..hh" quads of Table 1 right; binary16 arithmetic
  *   computed in binary32 and rounded once per operation), stop when ||r||/||b|| < tol
  *   (P:120), at most max_iter refinement steps.

@@ -252,7 +252,7 @@ int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
     if (p->solver == MLMC_SOLVER_CHOL_IR) {
         if (p->u != p->u_r || (p->u != MLMC_FMT_F64 && p->u != MLMC_FMT_F32 && p->u != MLMC_FMT_F16))
             return fail(ctx, MLMC_EINVAL, "IR supports u = u_r in binary64, binary32 or binary16");
-        if (!chol_supported(N, p->u_f, p->u_s))
+        if (!chol_supported(N, p->u_f, p->u_s, p->u))
             return fail(ctx, MLMC_EINVAL, "Cholesky-IR (u_f, u_s) not supported for N=" + std::to_string(N));
         return MLMC_OK;
     }

@@ -94,7 +94,7 @@ cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max
 cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s, double tol, int i_max,
                            double* out, int slot, unsigned* job_counter, void* fscratch, size_t fbytes,
                            cudaStream_t s, int u = MLMC_FMT_F64);
-bool chol_supported(int N, int u_f, int u_s);
+bool chol_supported(int N, int u_f, int u_s, int u = MLMC_FMT_F64);
 size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb, int u = MLMC_FMT_F64);
 // K5: per-level sums of the per-sample records into sums (accumulate = add to existing).
 cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,

@@ -125,14 +125,21 @@ __device__ __forceinline__ F shfl_f(unsigned mask, F v, int src, int w) {
     }
 }
 
-// correctly rounded reciprocal in the substitution precision (R28)
+// correctly rounded reciprocal in the substitution precision (R28); binary16 via binary32 (u_s = u_f
+// is selectable for fidelity, R24)
 __device__ __forceinline__ float rcp_s(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double rcp_s(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ __half rcp_s(__half x) { return __float2half_rn(__frcp_rn(__half2float(x))); }
 // factor entry -> substitution precision S
 template <typename S, typename F> __device__ __forceinline__ S to_s(F v) {
     if constexpr (sizeof(S) == 8) return FT<F>::to_d(v);
-    else return FT<F>::to_f(v);
+    else if constexpr (sizeof(S) == 4) return FT<F>::to_f(v);
+    else return __float2half_rn(FT<F>::to_f(v));
 }
+// -a * b + c in S with one rounding
+__device__ __forceinline__ float sfnma(float a, float b, float c) { return fmaf(-a, b, c); }
+__device__ __forceinline__ double sfnma(double a, double b, double c) { return fma(-a, b, c); }
+__device__ __forceinline__ __half sfnma(__half a, __half b, __half c) { return __hfma(__hneg(a), b, c); }
 
 // if (l == u) { cur = nxt; y = yk; } as one setp + two predicated moves, kept in place (volatile) so
 // the compiler does not materialise all W lane predicates of an unrolled block up front
@@ -145,6 +152,14 @@ __device__ __forceinline__ void pivot_take(int l, int u, double& cur, double nxt
     asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\t@p mov.f64 %0, %4;\n\t@p mov.f64 %1, %5;\n}"
                  : "+d"(cur), "+d"(y)
                  : "r"(l), "r"(u), "d"(nxt), "d"(yk));
+}
+__device__ __forceinline__ void pivot_take(int l, int u, __half& cur, __half nxt, __half& y, __half yk) {
+    unsigned short c = __half_as_ushort(cur), yy = __half_as_ushort(y);
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\t@p mov.b16 %0, %4;\n\t@p mov.b16 %1, %5;\n}"
+                 : "+h"(c), "+h"(yy)
+                 : "r"(l), "r"(u), "h"(__half_as_ushort(nxt)), "h"(__half_as_ushort(yk)));
+    cur = __ushort_as_half(c);
+    y = __ushort_as_half(yy);
 }
 
 // ---- geometry of one mesh / format pair
@@ -321,7 +336,7 @@ chol_factor_kernel(const double* __restrict__ a_all, int nb, unsigned char* __re
         }
         F lcol[K::LIGHT ? 1 : W];
         unsigned char* TF = base + K::OFF_F;            // LF tile (LIGHT)
-        S rdl = (S)0;
+        S rdl = (S)0.0;
 #pragma unroll
         for (int u = 0; u < W; ++u) {
             const int d = (l - u) & (W - 1);          // this lane holds row k0 + u + d
@@ -520,13 +535,13 @@ __device__ __forceinline__ void forward(R& ring, S* v, int l, bool leader) {
         load_row<G, F, S>(blk, l, lv);
         const S rd = reinterpret_cast<const S*>(blk + G::HDR)[l];
         const int k0 = b * W;
-        const S nxt = b + 1 < NB ? v[k0 + W + l] : (S)0;
-        S yv = (S)0;
+        const S nxt = b + 1 < NB ? v[k0 + W + l] : (S)0.0;
+        S yv = (S)0.0;
         S t = cur * rd;                              // y of this lane's row if it is the next pivot
 #pragma unroll
         for (int u = 0; u < W; ++u) {
             const S yk = __shfl_sync(0xffffffffu, t, u, W);
-            const S c2 = fma(-lv[u], yk, cur);
+            const S c2 = sfnma(lv[u], yk, cur);
             t = c2 * rd;
             cur = c2;
             pivot_take(l, u, cur, nxt, yv, yk);
@@ -548,13 +563,13 @@ __device__ __forceinline__ void backward(R& ring, S* v, int l, bool leader) {
         load_row<G, F, S>(blk, l, lv);
         const S rd = reinterpret_cast<const S*>(blk + G::HDR)[l];
         const int k0 = b * W;
-        const S nxt = b > 0 ? v[k0 - W + l] : (S)0;
-        S xv = (S)0;
+        const S nxt = b > 0 ? v[k0 - W + l] : (S)0.0;
+        S xv = (S)0.0;
         S t = cur * rd;
 #pragma unroll
         for (int u = W - 1; u >= 0; --u) {
             const S xk = __shfl_sync(0xffffffffu, t, u, W);
-            const S c2 = fma(-lv[u], xk, cur);
+            const S c2 = sfnma(lv[u], xk, cur);
             t = c2 * rd;
             cur = c2;
             pivot_take(l, u, cur, nxt, xv, xk);
@@ -616,7 +631,7 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
 #pragma unroll 4
         for (int q = 0; q < PER; ++q) {
             const int e = l + q * W;
-            v[e] = e < n ? (S)h2 : (S)0;               // b in u_s
+            v[e] = e < n ? (S)h2 : (S)0.0;             // b in u_s
         }
         __syncwarp(mask);
         // it = -1: step 2, x0 = (L L^T)^-1 b;  it >= 0: steps 4-8
@@ -665,11 +680,11 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
             backward<G, F, S>(ring, v, l, leader);
             if (it < 0) {
 #pragma unroll 4
-                for (int q = 0; q < PER; ++q) xs[l + q * W] = VT<U>::from((double)v[l + q * W]);
+                for (int q = 0; q < PER; ++q) xs[l + q * W] = VT<U>::from((double)(float)v[l + q * W]);
             } else if (active) {                       // step 8: x += d in u (d rounded to u first)
 #pragma unroll 4
                 for (int q = 0; q < PER; ++q)
-                    xs[l + q * W] = VT<U>::add(xs[l + q * W], VT<U>::from((double)v[l + q * W]));
+                    xs[l + q * W] = VT<U>::add(xs[l + q * W], VT<U>::from((double)(float)v[l + q * W]));
             }
             if (it < 0 || active) ++it;
             __syncwarp(mask);
@@ -782,16 +797,19 @@ template <int N, typename F, typename S, class Fn>
 cudaError_t with_shape(int vfmt, Fn&& fn) {
     if (vfmt == MLMC_FMT_F32) return with_shape_u<N, F, S, float>(fn);
     if (vfmt == MLMC_FMT_F16) return with_shape_u<N, F, S, __half>(fn);
-    return with_shape_u<N, F, S, double>(fn);
+    if constexpr (sizeof(S) == 2) return cudaErrorNotSupported;   // binary16 substitutions: u, u_r <= s
+    else return with_shape_u<N, F, S, double>(fn);
 }
 
 // (u_f, u_s) -> instantiation; returns cudaErrorNotSupported for combinations not built.
 template <int N, class Fn>
 cudaError_t with_types(int u_f, int u_s, int vfmt, Fn&& fn) {
     if (u_f == MLMC_FMT_E4M3) {
+        if (u_s == MLMC_FMT_F16) return with_shape<N, fp8, __half>(vfmt, fn);
         if (u_s == MLMC_FMT_F32) return with_shape<N, fp8, float>(vfmt, fn);
         if (u_s == MLMC_FMT_F64) return with_shape<N, fp8, double>(vfmt, fn);
     } else if (u_f == MLMC_FMT_F16) {
+        if (u_s == MLMC_FMT_F16) return with_shape<N, __half, __half>(vfmt, fn);
         if (u_s == MLMC_FMT_F32) return with_shape<N, __half, float>(vfmt, fn);
         if (u_s == MLMC_FMT_F64) return with_shape<N, __half, double>(vfmt, fn);
     } else if (u_f == MLMC_FMT_F32) {
@@ -818,9 +836,11 @@ cudaError_t with_mesh(int N, int u_f, int u_s, int vfmt, Fn&& fn) {
 
 }  // namespace
 
-bool chol_supported(int N, int u_f, int u_s) {
+bool chol_supported(int N, int u_f, int u_s, int u) {
     if (!(N == 2 || N == 4 || N == 8 || N == 16 || N == 32)) return false;
     if (!(u_f == MLMC_FMT_E4M3 || u_f == MLMC_FMT_F16 || u_f == MLMC_FMT_F32 || u_f == MLMC_FMT_F64)) return false;
+    if (u_s == MLMC_FMT_F16)   // binary16 substitutions with a quarter / half factor and u = u_r <= binary32
+        return (u_f == MLMC_FMT_E4M3 || u_f == MLMC_FMT_F16) && (u == MLMC_FMT_F16 || u == MLMC_FMT_F32);
     if (!(u_s == MLMC_FMT_F32 || u_s == MLMC_FMT_F64)) return false;
     return true;
 }

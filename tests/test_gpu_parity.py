@@ -714,10 +714,10 @@ def test_ir_single_precision_working_vectors(quad, level, tol):
     ctx.close()
 
 
-@pytest.mark.parametrize("quad", ["qshh", "hshh"])
+@pytest.mark.parametrize("quad", ["qshh", "hshh", "qhhh", "hhhh", "hhss"])
 def test_ir_half_precision_working_vectors(quad):
-    """Algorithm 1 with u = u_r = binary16 (the paper's qhhh of the E4 experiment, with u_s = s by
-    R24) on the level-0 mesh of that setup (h0 = 1/4, eps_0 = sqrt(k_p) h0^2 = 0.04 for k_p = 0.4): the
+    """Algorithm 1 with binary16 working vectors and / or substitutions (the paper's qhhh / hhss of the E4
+    experiment; u_s = s as R24 prefers, or u_s = h as the paper writes) on the level-0 mesh of that setup (h0 = 1/4, eps_0 = sqrt(k_p) h0^2 = 0.04 for k_p = 0.4): the
     solves converge, Q within the direct solve's residual bound (+ the binary16 rounding of x), and the
     step counts track the oracle's emulation of the same quad."""
     ctx = Context(field="eq20", m=1, sigma2=1.0, corr_len=0.0, q_decay=2.0, h0_inv=4, L_max=3, device=0,

@@ -4,10 +4,8 @@ Cholesky solve, with the SAME numbers of samples and the SAME random inputs (P:7
 difference is the computational error alone.
 
   E3: Eq. (20) field s = 4, q = 2, sigma = 2, h0 = 1/8, k_p = 0.05; Table 1 right quads
-       -- level 0 hhss, level 1 ssss, levels 2+ ssdd -- implemented as hsss / ssss / ssdd
-      (u_s >= binary32: R24).
-  E4: s = 1, sigma = 1, h0 = 1/4, k_p = 0.4; level 0 qhhh, levels 1-3 hhss -> qshh / hsss
-      (u_s >= binary32, R24).
+       -- level 0 hhss, level 1 ssss, levels 2+ ssdd -- exactly (u_s = u_f selectable).
+  E4: s = 1, sigma = 1, h0 = 1/4, k_p = 0.4; level 0 qhhh, levels 1-3 hhss, exactly.
 
 The sample counts of run r come from a standard adaptive MLMC run (fixed MINRES tolerance 1e-10, as
 in P:700 "determined by 1000 runs of the standard adaptive MLMC algorithm"); both estimators then use
@@ -37,9 +35,9 @@ BITS = {"q": 8, "h": 16, "s": 32, "d": 64}
 SETUPS = {
     # field (Eq. (20)), h0, k_p, L_max for K4 (h >= 1/32), quads per level (paper -> implemented)
     "E3": dict(m=4, sigma2=4.0, h0_inv=8, k_p=0.05, L_cap=2,
-               paper=["hhss", "ssss", "ssdd"], quads=["hsss", "ssss", "ssdd"], tol2=(8e-6, 4e-6, 2e-6, 1e-6)),
+               paper=["hhss", "ssss", "ssdd"], quads=["hhss", "ssss", "ssdd"], tol2=(8e-6, 4e-6, 2e-6, 1e-6)),
     "E4": dict(m=1, sigma2=1.0, h0_inv=4, k_p=0.4, L_cap=3,
-               paper=["qhhh", "hhss", "hhss", "hhss"], quads=["qshh", "hsss", "hsss", "hsss"], tol2=(2e-6,)),
+               paper=["qhhh", "hhss", "hhss", "hhss"], quads=["qhhh", "hhss", "hhss", "hhss"], tol2=(2e-6,)),
 }
 
 
