@@ -249,8 +249,8 @@ typedef struct {
     double  fixed_tol;   /* standard-MLMC solver tolerance (used when k_p <= 0) */
     double  r_bias;      /* the "r" of the bias test, R1: default 1 */
     int32_t N_init;      /* R6: default 100 */
-    int32_t policy;      /* 0 = MINRES everywhere (paper-minres), 1 = Table 1 IR quads (paper-ir: hsss /
-                            ssss / ssdd on h >= 1/32 with binary32 vectors where eps_l >= 1e-5, MINRES beyond),
+    int32_t policy;      /* 0 = MINRES everywhere (paper-minres), 1 = Table 1 IR quads (paper-ir: hhss /
+                            ssss / ssdd on h >= 1/32 where eps_l allows them, else wider; MINRES beyond),
                             2 = MG-PCG on h <= 1/32 and MINRES on h = 1/8, 1/16 (NEXT-4) */
     int32_t rank, world; /* this process's slice of every level's new indices */
     int32_t max_rounds;  /* safety cap (default 100) */

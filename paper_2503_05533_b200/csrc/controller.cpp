@@ -35,16 +35,17 @@ mlmc_precision minres_prec() {
 }
 
 // Table 1 (right) quads on the levels where the shared-memory banded factor exists (N <= 32):
-// level 0 hhss -> hsss, level 1 ssss, levels 2+ ssdd (u_s >= binary32, R24); binary32 working vectors only
-// where the level's tolerance is one a binary32 residual can certify (>= 1e-5; else ..dd), MINRES beyond
-// (R14).
+// level 0 hhss, level 1 ssss, levels 2+ ssdd, as written -- where the level's tolerance is one the reduced
+// precisions can certify (binary16 substitutions for tol >= 1e-3, binary32 vectors for tol >= 1e-5;
+// otherwise the next wider format), MINRES beyond (R14).
 mlmc_precision policy_prec(int policy, int level, int N, double tol) {
     if (policy == 2 && N >= 32)   // NEXT-4: MG-PCG where it beats MINRES, h <= 1/32
         return mlmc_precision{MLMC_SOLVER_MGCG, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
     if (policy == 1 && N <= 32) {
         const int vec = tol >= 1e-5 ? MLMC_FMT_F32 : MLMC_FMT_F64;
         if (level == 0)
-            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, vec, vec, 0, 0};
+            return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, tol >= 1e-3 ? MLMC_FMT_F16 : MLMC_FMT_F32, vec, vec,
+                                  0, 0};
         if (level == 1)
             return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, vec, vec, 0, 0};
         return mlmc_precision{MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
