@@ -251,6 +251,8 @@ typedef struct {
     int32_t N_init;      /* R6: default 100 */
     int32_t policy;      /* 0 = MINRES everywhere (paper-minres), 1 = Table 1 IR quads (paper-ir: hhss /
                             ssss / ssdd on h >= 1/32 where eps_l allows them, else wider; MINRES beyond),
+                            3 = auto: per mesh, the fastest admissible solver / precision
+                            timed on a pilot batch (see mlmc_auto_choice),
                             2 = MG-PCG on h <= 1/32 and MINRES on h = 1/8, 1/16 (NEXT-4) */
     int32_t rank, world; /* this process's slice of every level's new indices */
     int32_t max_rounds;  /* safety cap (default 100) */
@@ -279,6 +281,16 @@ typedef struct {
  * ELMAX (result still filled).                                              */
 int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
                       mlmc_allreduce_fn allreduce, void* user, mlmc_result* out);
+
+/* Policy 3 (auto) of mlmc_adaptive_run: on first use of a mesh the controller times every candidate --
+ * MINRES, MG-PCG and, on h >= 1/32, the Cholesky-IR quads the level tolerance admits (q/h/s factors with
+ * binary16/32 vectors, h/s factors with binary64 vectors) -- on a pilot batch of its own (seed ^ a
+ * constant, never part of the estimate; 8..512 samples by mesh size; kernel device time) and keeps the
+ * fastest whose pilot solves all converged; pilot times are summed across ranks so all ranks agree.  A
+ * choice is kept in the context per (mesh, tolerance class: >= 1e-3, >= 1e-5, below) for later runs.
+ * mlmc_auto_choice returns the latest precision chosen for mesh N (= 1/h) and its pilot cost in device
+ * ms per sample.  Errors: EINVAL (no choice made for N).                                                */
+int mlmc_auto_choice(const mlmc_ctx* ctx, int N, mlmc_precision* out, double* ms_per_sample);
 
 /* The same controller over a caller-supplied host sampler instead of the GPU
  * (CPU tests of Algorithm 2 and of the multi-rank exchange).  The sampler must

@@ -101,6 +101,7 @@ def lib():
     L.mlmc_sample_level_async.argtypes = [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(Precision),
                                           C.POINTER(Precision), C.c_double, C.c_double, vp, vp]
     L.mlmc_adaptive_run.argtypes = [vp, C.c_double, C.POINTER(AdaptiveOpts), ALLREDUCE_FN, vp, C.POINTER(Result)]
+    L.mlmc_auto_choice.argtypes = [vp, C.c_int, C.POINTER(Precision), dp]
     L.mlmc_eps_schedule.argtypes = [C.c_int, C.c_double, C.c_double, dp]
     L.mlmc_optimal_samples.argtypes = [C.c_int, dp, dp, C.c_double, dp]
     L.mlmc_kl_modes.argtypes = [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), dp, dp,

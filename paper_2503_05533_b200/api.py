@@ -206,6 +206,17 @@ class Context:
                                          C.c_void_p(xi.data_ptr()), C.c_void_p(a.data_ptr())), self.ctx)
         return xi[:n], a[:n]
 
+    def auto_choice(self, N: int):
+        """mlmc_auto_choice: the solver / precision policy 3 chose for mesh N (= 1/h), or None."""
+        p = K.Precision()
+        ms = C.c_double()
+        if K.lib().mlmc_auto_choice(self.ctx, N, C.byref(p), C.byref(ms)) != K.MLMC_OK:
+            return None
+        fmt = "qhsd"
+        name = {K.SOLVER_MINRES: "minres", K.SOLVER_CHOL_IR: "chol_ir", K.SOLVER_MGCG: "mgcg"}[p.solver]
+        quad = "".join(fmt[v] for v in (p.u_f, p.u_s, p.u, p.u_r)) if p.solver == K.SOLVER_CHOL_IR else None
+        return {"solver": name, "quad": quad, "ms_per_sample": ms.value}
+
     def adaptive_run(self, eps: float, k_p: float = 0.05, N_init: int = 100, policy: int = 0, seed: int = 0,
                      fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None,
                      on_fail: int = 0) -> dict:

@@ -30,6 +30,8 @@ struct mlmc_ctx {
     size_t ws_bytes = 0;
     double* sums_dev = nullptr;          // owned: MLMC_MAX_LEVELS * kSumsLen
     std::string err;
+    struct AutoChoice { int N, cls; mlmc_precision p; double ms; };
+    std::vector<AutoChoice> auto_choice;   // policy 3: per mesh, the solver the pilot chose
     // per-kernel accounting
     bool prof_on = false;
     std::vector<mlmc_kernel_stat> stats;
@@ -440,6 +442,18 @@ int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
 
 }  // namespace
 
+void mlmc::ctx_note_auto_choice(mlmc_ctx* ctx, int N, int cls, const mlmc_precision& p, double ms_per_sample) {
+    for (auto& e : ctx->auto_choice)
+        if (e.N == N && e.cls == cls) { e.p = p; e.ms = ms_per_sample; return; }
+    ctx->auto_choice.push_back({N, cls, p, ms_per_sample});
+}
+
+bool mlmc::ctx_find_auto_choice(const mlmc_ctx* ctx, int N, int cls, mlmc_precision* p) {
+    for (const auto& e : ctx->auto_choice)
+        if (e.N == N && e.cls == cls) { *p = e.p; return true; }
+    return false;
+}
+
 int mlmc::copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host) {
     CU(cudaMemcpyAsync(host, dev, sizeof(double) * kSumsLen * nlev, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -716,6 +730,17 @@ int mlmc_sample_level_xi(mlmc_ctx* ctx, int level, uint64_t n, const double* xi,
     CU(cudaMemcpyAsync(out_sums, ctx->sums_dev, sizeof(double) * kSumsLen, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return MLMC_OK;
+}
+
+int mlmc_auto_choice(const mlmc_ctx* ctx, int N, mlmc_precision* out, double* ms_per_sample) {
+    if (!ctx || !out) return MLMC_EINVAL;
+    for (auto it = ctx->auto_choice.rbegin(); it != ctx->auto_choice.rend(); ++it)   // the latest for N
+        if (it->N == N) {
+            *out = it->p;
+            if (ms_per_sample) *ms_per_sample = it->ms;
+            return MLMC_OK;
+        }
+    return MLMC_EINVAL;
 }
 
 int mlmc_profile_enable(mlmc_ctx* ctx, int on) {

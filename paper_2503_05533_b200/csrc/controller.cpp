@@ -59,8 +59,11 @@ using RoundSampler = std::function<int(int nlev, const int* levels, const uint64
                                        const mlmc_precision* pf, const mlmc_precision* pc, const double* tf,
                                        const double* tc, double* sums)>;
 
+// precision of the solves on mesh N of level `level` at tolerance tol
+using PrecChooser = std::function<int(int level, int N, double tol, mlmc_precision* out)>;
+
 int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o, const RoundSampler& sampler,
-                  mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
+                  const PrecChooser& choose, mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
     if (!(eps > 0.0) || o.world < 1 || o.rank < 0 || o.rank >= o.world || L_max < 1 || h0_inv < 2)
         return MLMC_EINVAL;
     if (o.world > 1 && !allreduce) return MLMC_EINVAL;
@@ -105,8 +108,12 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             lv.push_back(l);
             cnt.push_back(hi - lo);
             first.push_back(lo);
-            pf.push_back(policy_prec(o.policy, l, h0_inv << l, epsl[l]));
-            pc.push_back(l > 0 ? policy_prec(o.policy, l - 1, h0_inv << (l - 1), epsl[l - 1]) : pf.back());
+            mlmc_precision qf, qc;
+            int rcp = choose(l, h0_inv << l, epsl[l], &qf);
+            if (!rcp && l > 0) rcp = choose(l - 1, h0_inv << (l - 1), epsl[l - 1], &qc);
+            if (rcp) return rcp;
+            pf.push_back(qf);
+            pc.push_back(l > 0 ? qc : qf);
             tf.push_back(epsl[l]);
             tc.push_back(l > 0 ? epsl[l - 1] : epsl[l]);
         }
@@ -193,6 +200,85 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
 
 }  // namespace
 
+// Policy 3 (auto): on first use of a mesh, every admissible solver / precision is
+// timed on a pilot batch (its own seed, never part of the estimator; kernel device time from the library's
+// per-launch events) and the fastest per sample is kept for that mesh.  Admissibility is empirical: a
+// candidate with a failed pilot solve (breakdown, no convergence within the pilot's iteration cap:
+// Corollary 3.3's kappa u_f < 1/2 violated in practice) is out.  With several ranks the pilot times are
+// summed across them first, so every rank keeps the same choice.
+struct AutoChooser {
+    mlmc_ctx* ctx;
+    uint64_t seed;
+    mlmc_allreduce_fn allreduce;
+    void* user;
+    int world;
+
+    static mlmc_precision q(int solver, int uf, int us, int u, int max_iter = 0) {
+        return mlmc_precision{solver, uf, us, u, u, max_iter, 0};
+    }
+    std::vector<mlmc_precision> candidates(int N, double tol) const {
+        std::vector<mlmc_precision> c;
+        c.push_back(q(MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64));
+        c.push_back(q(MLMC_SOLVER_MGCG, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64));
+        if (N <= 32) {   // the banded factors (K4)
+            if (tol >= 1e-3) c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F16, MLMC_FMT_F32));
+            if (tol >= 1e-5) {
+                c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_E4M3, MLMC_FMT_F32, MLMC_FMT_F32));
+                c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F32));
+                c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F32, MLMC_FMT_F32));
+            }
+            c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F64));
+            c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64));
+        }
+        return c;
+    }
+    int choose(int level, int N, double tol, mlmc_precision* out) {
+        // the admissible candidates change at tol = 1e-3 and 1e-5: one choice per (mesh, tolerance class),
+        // kept in the context across runs
+        const int cls = tol >= 1e-3 ? 0 : tol >= 1e-5 ? 1 : 2;
+        if (mlmc::ctx_find_auto_choice(ctx, N, cls, out)) return MLMC_OK;
+        const int n_unk = (N - 1) * (N - 1);
+        const uint64_t npilot = (uint64_t)std::min(512, std::max(8, (1 << 20) / n_unk));
+        std::vector<mlmc_precision> cand = candidates(N, tol);
+        std::vector<double> ms(cand.size(), 0.0);
+        // the coarse half of a pilot sample is a loose MINRES solve (it only has to converge, not to be timed)
+        const mlmc_precision cheap = q(MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 4 * n_unk + 400);
+        for (size_t c = 0; c < cand.size(); ++c) {
+            mlmc_precision p = cand[c];
+            p.max_iter = p.solver == MLMC_SOLVER_CHOL_IR ? 50 : 4 * n_unk + 400;   // the pilot's budget
+            mlmc_level_sums sums;
+            int rc = mlmc_profile_enable(ctx, 1);
+            if (!rc) rc = mlmc_sample_level(ctx, level, npilot, seed ^ 0x9e3779b97f4a7c15ull, 0, &p, &cheap, tol, 0.5,
+                                            &sums, nullptr);
+            if (rc == MLMC_EINVAL) { mlmc_profile_enable(ctx, 0); ms[c] = -1.0; continue; }   // not built here
+            if (rc) return rc;
+            mlmc_kernel_stat st[64];
+            int cnt = 0;
+            mlmc_profile_read(ctx, st, 64, &cnt);
+            mlmc_profile_enable(ctx, 0);
+            double t = 0.0;
+            for (int i = 0; i < std::min(cnt, 64); ++i)
+                if (st[i].N == N && (st[i].kind == MLMC_K_MINRES || st[i].kind == MLMC_K_CHOL_IR)) t += st[i].ms;
+            ms[c] = sums.n_fail > 0 ? -1.0 : t;     // a failed pilot solve: inadmissible
+        }
+        if (world > 1 && allreduce) {
+            std::vector<double> buf(ms.size()), fail(ms.size());
+            for (size_t c = 0; c < ms.size(); ++c) { buf[c] = ms[c] < 0 ? 0.0 : ms[c]; fail[c] = ms[c] < 0 ? 1.0 : 0.0; }
+            if (allreduce(buf.data(), (int)buf.size(), 0, user) != 0) return MLMC_ECUDA;
+            if (allreduce(fail.data(), (int)fail.size(), 1, user) != 0) return MLMC_ECUDA;
+            for (size_t c = 0; c < ms.size(); ++c) ms[c] = fail[c] > 0 ? -1.0 : buf[c];
+        }
+        size_t best = 0;
+        for (size_t c = 1; c < ms.size(); ++c)
+            if (ms[c] >= 0 && (ms[best] < 0 || ms[c] < ms[best])) best = c;
+        mlmc_precision p = cand[best];
+        p.max_iter = 0;
+        mlmc::ctx_note_auto_choice(ctx, N, cls, p, ms[best] / (double)npilot);
+        *out = p;
+        return MLMC_OK;
+    }
+};
+
 extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
                                  mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
     if (!ctx || !opts || !out) return MLMC_EINVAL;
@@ -210,7 +296,14 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
         if (rc) return rc;
         return mlmc::copy_sums_to_host(ctx, dev, nlev, sums);
     };
-    int rc = adaptive_core(li0.N, L_max, eps, *opts, gpu, allreduce, user, out);
+    AutoChooser ac{ctx, seed, allreduce, user, opts->world};
+    const int policy = opts->policy;
+    PrecChooser choose = [&](int level, int N, double tol, mlmc_precision* p) -> int {
+        if (policy == 3) return ac.choose(level, N, tol, p);
+        *p = policy_prec(policy, level, N, tol);
+        return MLMC_OK;
+    };
+    int rc = adaptive_core(li0.N, L_max, eps, *opts, gpu, choose, allreduce, user, out);
     cudaFree(dev);
     return rc;
 }
@@ -228,5 +321,10 @@ extern "C" int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const m
         }
         return MLMC_OK;
     };
-    return adaptive_core(h0_inv, L_max, eps, *opts, host, allreduce, user, out);
+    const int policy = opts->policy == 3 ? 0 : opts->policy;   // no pilot timing over a host sampler
+    PrecChooser choose = [&](int level, int N, double tol, mlmc_precision* p) -> int {
+        *p = policy_prec(policy, level, N, tol);
+        return MLMC_OK;
+    };
+    return adaptive_core(h0_inv, L_max, eps, *opts, host, choose, allreduce, user, out);
 }

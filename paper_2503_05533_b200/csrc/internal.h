@@ -104,6 +104,9 @@ cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double 
 
 // Copy nlev level-sum records from the device to the host on the ctx's stream and wait.
 int copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host);
+// policy 3 (auto): the choice made for mesh N in tolerance class cls and its pilot cost (device ms/sample)
+void ctx_note_auto_choice(mlmc_ctx* ctx, int N, int cls, const mlmc_precision& p, double ms_per_sample);
+bool ctx_find_auto_choice(const mlmc_ctx* ctx, int N, int cls, mlmc_precision* p);
 
 constexpr int kSumsLen = MLMC_SUMS_LEN;
 constexpr int kRecLen = MLMC_SAMPLE_LEN;

@@ -735,3 +735,18 @@ def test_ir_half_precision_working_vectors(quad):
         o = P.solve_mesh(4, xi, oc.SOLVER_IR, tol=tol, quad=quad, max_iter=50)
         assert o["status"] == 0 and abs(o["iters"] - ps[k, 2]) <= 2, (o["iters"], ps[k, 2])
     ctx.close()
+
+
+def test_adaptive_auto_policy():
+    """Policy 3 (auto): every mesh the run uses gets a solver chosen by pilot timing among the
+    admissible candidates; the run converges to an estimate in the survey's sanity window, and the
+    choice is reported through mlmc_auto_choice."""
+    cfg = W.CONFIGS["C4"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    r = ctx.adaptive_run(2e-4, k_p=0.05, seed=3, policy=3)
+    assert r["code"] == 0 and r["n_fail"] == 0 and 0.033 < r["estimate"] < 0.036
+    for l in range(r["L"] + 1):
+        ch = ctx.auto_choice(cfg["h0_inv"] << l)
+        assert ch is not None and ch["solver"] in ("minres", "mgcg", "chol_ir") and ch["ms_per_sample"] > 0, (l, ch)
+    assert ctx.auto_choice(1024) is None
+    ctx.close()
