@@ -610,7 +610,9 @@ def paper_leg(local):
 
 
 def adaptive_leg(args, world, rank, local, torch, dist):
-    """Time-to-eps of Algorithm 2 for configs[3] (C4) and configs[4] (C5), wall clock, max over ranks."""
+    """Time-to-eps of Algorithm 2 for configs[3] (C4) and configs[4] (C5), wall clock, max over ranks: policy 0
+    (the paper's MINRES at eps_l) and policy 3 (auto: the solver / precision per mesh from pilot timings,
+    SURVEY A14; the timed run reuses the choice the untimed first run made)."""
     from paper_2503_05533_b200 import Context
     out = {}
     for name in ("C4", "C5"):
@@ -621,18 +623,26 @@ def adaptive_leg(args, world, rank, local, torch, dist):
             ctx.sample_level(l, 1, cfg["seed"] + 99, tol_fine=1e-2, tol_coarse=1e-2)
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = ctx.adaptive_run(cfg["eps"], k_p=cfg["k_p"], N_init=100, seed=cfg["seed"],
-                             group=dist.group.WORLD if world > 1 else None)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device=torch.device("cuda", local))
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
-        out[name] = {"eps": cfg["eps"], "seconds": el, "L": r["L"], "N": r["N"], "rounds": r["rounds"],
-                     "estimate": r["estimate"], "code": r["code"]}
+        grp = dist.group.WORLD if world > 1 else None
+        for policy, key in ((0, name), (3, f"{name}_auto")):
+            if policy == 3:   # the pilot runs once per mesh and tolerance class; the timed run reuses the choice
+                ctx.adaptive_run(cfg["eps"], k_p=cfg["k_p"], N_init=100, seed=cfg["seed"] + 1, policy=3, group=grp)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = ctx.adaptive_run(cfg["eps"], k_p=cfg["k_p"], N_init=100, seed=cfg["seed"], policy=policy, group=grp)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], dtype=torch.float64, device=torch.device("cuda", local))
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t.item())
+            out[key] = {"eps": cfg["eps"], "policy": policy, "seconds": el, "L": r["L"], "N": r["N"],
+                        "rounds": r["rounds"], "estimate": r["estimate"], "code": r["code"]}
+            if policy == 3:
+                out[key]["choice"] = {str(cfg["h0_inv"] << l): ctx.auto_choice(cfg["h0_inv"] << l)
+                                      for l in range(r["L"] + 1)}
         ctx.close()
     return out
 
