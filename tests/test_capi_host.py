@@ -110,3 +110,30 @@ def test_controller_failed_solves_abort_or_are_counted():
     calls["n"] = 0
     r = mlmc_adaptive_run_host(8, 4, 2e-3, sampler, N_init=50, on_fail=1)
     assert r["n_fail"] == 1 and r["code"] in (K.MLMC_OK, K.MLMC_ELMAX) and r["L"] >= 1
+
+
+def test_null_context_calls_are_rejected():
+    """Host-side argument checks of the C ABI (no device needed)."""
+    p = K.Precision()
+    ms = C.c_double()
+    assert K.lib().mlmc_auto_choice(None, 8, C.byref(p), C.byref(ms)) == K.MLMC_EINVAL
+    out = C.c_size_t()
+    assert K.lib().mlmc_workspace_bytes(None, 0, 10, C.byref(out)) == K.MLMC_EINVAL
+    assert K.lib().mlmc_profile_enable(None, 1) == K.MLMC_EINVAL
+
+
+def test_host_controller_auto_policy_falls_back_to_minres_quads():
+    """Policy 3 (auto) needs the GPU's pilot timings; over a host sampler it runs as policy 0 (MINRES
+    precisions are handed to the sampler)."""
+    seen = []
+
+    def sampler(level, n, first, pf, pc, tf, tc):
+        seen.append(pf.solver)
+        rng = np.random.default_rng(level * 1000 + first)
+        y = rng.normal(0.03 / 4 ** level, 0.01 / 4 ** level, n)
+        s = np.zeros(12)
+        s[0], s[1], s[4], s[5] = y.sum(), (y * y).sum(), n * 4.0 ** level, n
+        return s
+
+    r = api.mlmc_adaptive_run_host(8, 3, 2e-3, sampler, k_p=0.05, N_init=20, policy=3, seed=1)
+    assert r["code"] in (0, 4) and set(seen) == {K.SOLVER_MINRES}
