@@ -249,6 +249,7 @@ def run_ours(args):
     clocks.start()
     total_ms = 0.0
     iters_f = [0.0] * L
+    iters_max = [[0.0, 0.0] for _ in range(L)]
     iters_c = [0.0] * L
     for i in range(args.steps):
         flush.zero_()                                                   # L2 flush between timed steps
@@ -263,6 +264,7 @@ def run_ours(args):
         for l in range(L):
             iters_f[l] += s[l, 7] / world
             iters_c[l] += s[l, 8] / world
+            iters_max[l] = [max(iters_max[l][0], s[l, 9]), max(iters_max[l][1], s[l, 10])]
     torch.cuda.synchronize()
     clk = clocks.stop()
     if world > 1:
@@ -299,7 +301,8 @@ def run_ours(args):
                            "samples_per_s": world * Nl[l] * args.steps / (level_ms[l] / 1e3),
                            "ms_alone": level_ms[l] / args.steps,
                            "mean_iters_fine": iters_f[l] / (Nl[l] * args.steps),
-                           "mean_iters_coarse": iters_c[l] / (Nl[l] * args.steps) if l else 0.0}
+                           "mean_iters_coarse": iters_c[l] / (Nl[l] * args.steps) if l else 0.0,
+                           "max_iters_fine": iters_max[l][0], "max_iters_coarse": iters_max[l][1] if l else 0.0}
                  for l in range(L)}
 
     # ---- roofline of the dominant kernel (largest device time in the timed region)
