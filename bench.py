@@ -302,7 +302,9 @@ def run_ours(args):
                            "ms_alone": level_ms[l] / args.steps,
                            "mean_iters_fine": iters_f[l] / (Nl[l] * args.steps),
                            "mean_iters_coarse": iters_c[l] / (Nl[l] * args.steps) if l else 0.0,
-                           "max_iters_fine": iters_max[l][0], "max_iters_coarse": iters_max[l][1] if l else 0.0}
+                           # (the step's all-reduce adds the per-rank maxima: reported at N = 1 only)
+                           "max_iters_fine": iters_max[l][0] if world == 1 else None,
+                           "max_iters_coarse": (iters_max[l][1] if l else 0.0) if world == 1 else None}
                  for l in range(L)}
 
     # ---- roofline of the dominant kernel (largest device time in the timed region)
