@@ -98,6 +98,9 @@ typedef enum { MLMC_FMT_E4M3 = 0, MLMC_FMT_F16 = 1, MLMC_FMT_F32 = 2, MLMC_FMT_F
 typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1, MLMC_SOLVER_MGCG = 2 } mlmc_solver;
 
 #define MLMC_FLAG_VERIFY 1   /* MINRES: also keep x_k and report the true residual */
+#define MLMC_FLAG_ESCALATE 2 /* MINRES / CHOL_IR: a failed solve (max_iter, breakdown, limiting accuracy) is
+                                solved again by MG-PCG to the same tolerance; if that converges the sample's
+                                status is 4 */
 
 typedef struct {
     int32_t solver;
@@ -119,14 +122,14 @@ typedef struct {
     double n_fail;               /* samples with a non-converged / failed solve */
     double iters_f, iters_c;     /* summed MINRES iterations or IR steps */
     double iters_f_max, iters_c_max;
-    double reserved;
+    double n_escalated;          /* samples with a solve repaired by escalation (status 4; not failures) */
 } mlmc_level_sums;
 
 /* per-sample record (MLMC_SAMPLE_LEN doubles, sample-major):
  *   [0] Q_f   [1] Q_c (0 at level 0)   [2] iters_f   [3] iters_c
  *   [4] relative residual of the fine solve (MINRES: phibar/||b||, or the true
  *       ||b-Ax||/||b|| with MLMC_FLAG_VERIFY; IR: the true residual)  [5] coarse
- *   [6] status_f  [7] status_c   (0 ok, 1 max_iter, 2 breakdown, 3 non-finite) */
+ *   [6] status_f  [7] status_c   (0 ok, 1 max_iter, 2 breakdown, 3 non-finite, 4 ok after escalation) */
 
 typedef struct mlmc_ctx mlmc_ctx;   /* opaque */
 
@@ -259,7 +262,9 @@ typedef struct {
     uint64_t seed;
     int32_t on_fail;     /* a solve that misses its tolerance (max_iter, breakdown; R15): 0 = stop with
                             MLMC_ESOLVER, 1 = keep the sample (Q of the last iterate) and count it in
-                            mlmc_result.n_fail -- never resampled either way */
+                            mlmc_result.n_fail, 2 = escalate (MINRES / IR solves carry MLMC_FLAG_ESCALATE: a
+                            failed one is solved again by MG-PCG; what still fails is kept and counted as with 1)
+                            -- never resampled in any case */
     int32_t reserved0;
 } mlmc_adaptive_opts;
 

@@ -18,6 +18,7 @@ FIELD_EXPCOV_KL, FIELD_PAPER_EQ20 = 0, 1
 FMT = {"q": 0, "h": 1, "s": 2, "d": 3}
 SOLVER_MINRES, SOLVER_CHOL_IR, SOLVER_MGCG = 0, 1, 2
 FLAG_VERIFY = 1
+FLAG_ESCALATE = 2
 
 
 class Problem(C.Structure):
@@ -33,7 +34,7 @@ class Precision(C.Structure):
 
 class LevelSums(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail",
-                                          "iters_f", "iters_c", "iters_f_max", "iters_c_max", "reserved")]
+                                          "iters_f", "iters_c", "iters_f_max", "iters_c_max", "n_escalated")]
 
 
 class LevelInfo(C.Structure):

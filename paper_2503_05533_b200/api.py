@@ -20,15 +20,17 @@ __all__ = ["Context", "precision", "mlmc_plan_levels", "mlmc_sample_level", "mlm
            "mlmc_debug_field", "mlmc_workspace_bytes", "SUM_FIELDS"]
 
 SUM_FIELDS = ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail", "iters_f", "iters_c",
-              "iters_f_max", "iters_c_max", "reserved")
+              "iters_f_max", "iters_c_max", "n_escalated")
 
 
 def precision(solver: str = "minres", u_f: str = "s", u_s: str = "s", u: str = "d", u_r: str = "d",
-              max_iter: int = 0, verify: bool = False) -> K.Precision:
+              max_iter: int = 0, verify: bool = False, escalate: bool = False) -> K.Precision:
     """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad.
-    verify=True (MINRES): also carry x_k and report the true residual."""
+    verify=True (MINRES): also carry x_k and report the true residual; escalate=True (MINRES, IR): a failed solve
+    is solved again by MG-PCG (status 4 when that converges)."""
     s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR, "mgcg": K.SOLVER_MGCG}[solver]
-    return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter, K.FLAG_VERIFY if verify else 0)
+    flags = (K.FLAG_VERIFY if verify else 0) | (K.FLAG_ESCALATE if escalate else 0)
+    return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter, flags)
 
 
 def _as_prec(p) -> K.Precision:

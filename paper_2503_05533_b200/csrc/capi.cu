@@ -110,7 +110,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Workspace layout for one pass of `batch` samples of `level`.
 struct WsLayout {
-    size_t xi, a_f, a_c, rec, chunks, ctr, keys_f, keys_c, ord_f, ord_c, gm, ch_f, ch_c, ch_f_bytes, ch_c_bytes, total;
+    size_t xi, a_f, a_c, rec, chunks, ctr, keys_f, keys_c, ord_f, ord_c, esc_f, esc_c, gm, ch_f, ch_c, ch_f_bytes,
+        ch_c_bytes, total;
     int gm_ctas;
 };
 // Cholesky factor scratch of one solve (0 for MINRES / unsupported combinations)
@@ -134,10 +135,16 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.keys_c = off; off += align256(sizeof(unsigned long long) * 2 * batch);
     L.ord_f = off;  off += align256(sizeof(int) * batch);
     L.ord_c = off;  off += align256(sizeof(int) * batch);
+    // escalation lists of the fine / coarse solves: [count | indices]
+    L.esc_f = off;  off += align256(sizeof(int) * (batch + 4));
+    L.esc_c = off;  off += align256(sizeof(int) * (batch + 4));
     L.gm = off;
     L.gm_ctas = 0;
     if (Nf >= kGmMinN) {   // per-CTA scratch of the streamed-mesh solvers (fine and coarse share it)
-        const bool mg = (pf && pf->solver == MLMC_SOLVER_MGCG) || (pc && pc->solver == MLMC_SOLVER_MGCG);
+        auto uses_mg = [](const mlmc_precision* p) {
+            return p && (p->solver == MLMC_SOLVER_MGCG || (p->flags & MLMC_FLAG_ESCALATE));
+        };
+        const bool mg = uses_mg(pf) || uses_mg(pc);
         const int per_sm = mg ? mgcg_ctas_per_sm(Nf) : 1;
         L.gm_ctas = (int)std::min<uint64_t>(batch, (uint64_t)std::max(c->sms, 1) * per_sm);
         size_t per_cta = std::max(minres_gm_scratch_per_cta(Nf), minres_stream_scratch_per_cta(Nf));
@@ -298,7 +305,7 @@ bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
 
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
                double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas, void* ch_scratch,
-               size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr) {
+               size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr, int* esc = nullptr) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;   // finite-precision Lanczos at contrast ~1e7 (Eq. (20), sigma = 2) needs > n
@@ -316,6 +323,7 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
         else
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
                        [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, keys ? order : nullptr, ex.st); }));
+
     } else if (p->solver == MLMC_SOLVER_MGCG) {
         int mi = p->max_iter > 0 ? p->max_iter : 1000;
         CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
@@ -327,6 +335,16 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
                        return launch_chol_ir(N, a, nb, p->u_f, p->u_s, tol, mi, rec, slot, ctr, ch_scratch, ch_bytes,
                                              ex.st, p->u);
                    }));
+    }
+    // escalation (on_fail = 2): the failed MINRES / Cholesky-IR solves of this launch (max_iter,
+    // breakdown, limiting accuracy) are solved again by MG-PCG to the same tolerance; converged ones are
+    // recorded with status 4 and counted apart
+    if (p->solver != MLMC_SOLVER_MGCG && (p->flags & MLMC_FLAG_ESCALATE) && esc && mgcg_supported(N)) {
+        CU(cudaMemsetAsync(esc, 0, sizeof(int), ex.st));
+        CU(launch_escalate_collect(rec, nb, slot, esc + 4, esc, ex.st));
+        CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
+            return launch_mgcg(N, a, nb, tol, 1000, rec, slot, ctr + 8, esc + 4, gm_scratch, gm_ctas, ex.st, esc, 4);
+        }));
     }
     return MLMC_OK;
 }
@@ -402,17 +420,19 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         }
         void* chf = ex.ws + L.ch_f;
         void* chc = ex.ws + L.ch_c;
-        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes, kf, of)))
+        int* ef = reinterpret_cast<int*>(ex.ws + L.esc_f);
+        int* ec = reinterpret_cast<int*>(ex.ws + L.esc_c);
+        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes, kf, of, ef)))
             return rc;
         if (fork) {
             const Exec exc{ex.ws, ex.bytes, sch->st_c};
             if ((rc = solve_mesh(ctx, exc, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc, L.ch_c_bytes, kc,
-                                 oc)))
+                                 oc, ec)))
                 return rc;
             CU(cudaEventRecord(sch->join, sch->st_c));
             CU(cudaStreamWaitEvent(st, sch->join, 0));
         } else if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc,
-                                                 L.ch_c_bytes, kc, oc))) {
+                                                 L.ch_c_bytes, kc, oc, ec))) {
             return rc;
         }
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {

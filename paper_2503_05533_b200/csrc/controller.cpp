@@ -112,6 +112,10 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             int rcp = choose(l, h0_inv << l, epsl[l], &qf);
             if (!rcp && l > 0) rcp = choose(l - 1, h0_inv << (l - 1), epsl[l - 1], &qc);
             if (rcp) return rcp;
+            if (o.on_fail == 2) {   // escalation of failed MINRES / IR solves to MG-PCG (MLMC_FLAG_ESCALATE)
+                if (qf.solver != MLMC_SOLVER_MGCG) qf.flags |= MLMC_FLAG_ESCALATE;
+                if (l > 0 && qc.solver != MLMC_SOLVER_MGCG) qc.flags |= MLMC_FLAG_ESCALATE;
+            }
             pf.push_back(qf);
             pc.push_back(l > 0 ? qc : qf);
             tf.push_back(epsl[l]);
@@ -154,7 +158,7 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             n_fail += (int64_t)rs[6];
         }
         // a failed solve is never resampled (R15): stop, or keep it and count it (on_fail = 1)
-        if (failed && o.on_fail != 1) { code = MLMC_ESOLVER; break; }
+        if (failed && o.on_fail == 0) { code = MLMC_ESOLVER; break; }
         // steps 5-7
         std::vector<double> mean(L + 1), V(L + 1), C(L + 1), Nopt(L + 1);
         for (int l = 0; l <= L; ++l) stats(l, mean[l], V[l], C[l]);

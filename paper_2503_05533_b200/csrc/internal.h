@@ -85,8 +85,11 @@ int minres_stream_cluster(int N);   // CTAs per system of a streamed MINRES laun
 bool mgcg_supported(int N);
 size_t mgcg_scratch_per_cta(int N);
 int mgcg_ctas_per_sm(int N);   // resident systems per SM of the streamed-mesh MG-PCG
+// nb_dev (optional, device): the number of systems, read by the kernel (escalation lists); ok_status: the
+// status recorded for a converged solve (0; 4 = converged after escalation).
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                        unsigned* job_counter, const int* order, void* scratch, int nctas, cudaStream_t s);
+                        unsigned* job_counter, const int* order, void* scratch, int nctas, cudaStream_t s,
+                        const int* nb_dev = nullptr, int ok_status = 0);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of
 // chol_scratch_bytes(N, u_f, u_s, nb) bytes for a launch over nb systems (one factor per resident
 // warp segment; a smaller scratch shrinks the grid; 0 = unsupported).
@@ -96,6 +99,8 @@ cudaError_t launch_chol_ir(int N, const double* a, uint64_t nb, int u_f, int u_s
                            cudaStream_t s, int u = MLMC_FMT_F64);
 bool chol_supported(int N, int u_f, int u_s, int u = MLMC_FMT_F64);
 size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb, int u = MLMC_FMT_F64);
+// Escalation: the samples of `rec` whose slot-`slot` solve failed -> list[*count] (count zeroed by caller).
+cudaError_t launch_escalate_collect(const double* rec, uint64_t nb, int slot, int* list, int* count, cudaStream_t s);
 // K5: per-level sums of the per-sample records into sums (accumulate = add to existing).
 cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,
                               double cost_f_fixed, double cost_f_step, double cost_c_fixed,

@@ -320,7 +320,9 @@ __device__ __forceinline__ void mg_setup(const double* __restrict__ a, double* c
 template <int N, int T, int GROUPS>
 __global__ void __launch_bounds__(MgCfg<N, T, GROUPS>::BLOCK)
 mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
-            unsigned* __restrict__ job_counter, const int* __restrict__ order) {
+            unsigned* __restrict__ job_counter, const int* __restrict__ order, const int* __restrict__ nb_dev,
+            int ok_status) {
+    if (nb_dev) nb = *nb_dev;
     using K = MgCfg<N, T, GROUPS>;
     constexpr int G = K::G, C = K::C, n = K::n, PER = K::PER, P = 2 * N * N;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -440,7 +442,7 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
             o[0 + slot] = h2 * Xq;
             o[2 + slot] = (double)it;
             o[4 + slot] = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-            o[6 + slot] = (double)status;
+            o[6 + slot] = (double)(status == 0 ? ok_status : status);
         }
         gsync<T, GROUPS>(g);
     }
@@ -466,7 +468,9 @@ struct MgGm {
 template <int N>
 __global__ void __launch_bounds__(MG_GM_T, 1)
 mgcg_gm_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
-               unsigned* __restrict__ job_counter, const int* __restrict__ order, unsigned char* __restrict__ scratch) {
+               unsigned* __restrict__ job_counter, const int* __restrict__ order, unsigned char* __restrict__ scratch,
+               const int* __restrict__ nb_dev, int ok_status) {
+    if (nb_dev) nb = *nb_dev;
     using K = MgGm<N>;
     constexpr int T = K::T, G = K::G, C = N - 1, n = C * C, P = 2 * N * N;
     __shared__ double red[2 * (T / 32)];
@@ -572,7 +576,7 @@ mgcg_gm_kernel(const double* __restrict__ a_all, int nb, double tol, int max_ite
             o[0 + slot] = h2 * Xq;
             o[2 + slot] = (double)it;
             o[4 + slot] = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-            o[6 + slot] = (double)status;
+            o[6 + slot] = (double)(status == 0 ? ok_status : status);
         }
         __syncthreads();
     }
@@ -669,7 +673,9 @@ __global__ void __launch_bounds__(tl::T, 1)
 mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant__ CUtensorMap m32,
                  const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
                  int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order,
-                 unsigned char* __restrict__ scratch) {
+                 unsigned char* __restrict__ scratch,
+                 const int* __restrict__ nb_dev, int ok_status) {
+    if (nb_dev) nb = *nb_dev;
     using K = MgTl<N>;
     constexpr int T = tl::T, GP = K::GP, C = N - 1, P = 2 * N * N;
     constexpr int BX = tl::BX, BN = tl::BN, H = tl::H, TX = tl::TX, TY = tl::TY, NT = K::NT;
@@ -968,7 +974,7 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
             o[0 + slot] = h2 * Xq;
             o[2 + slot] = (double)it;
             o[4 + slot] = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-            o[6 + slot] = (double)status;
+            o[6 + slot] = (double)(status == 0 ? ok_status : status);
         }
         __syncthreads();
     }
@@ -976,7 +982,7 @@ mgcg_tile_kernel(const __grid_constant__ CUtensorMap m64, const __grid_constant_
 
 template <int N>
 cudaError_t run_mg_tile(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
-                        const int* order, void* scratch, int nctas, cudaStream_t s) {
+                        const int* order, void* scratch, int nctas, cudaStream_t s, const int* nb_dev, int ok_status) {
     using K = MgTl<N>;
     if (!scratch || nctas < 1) return cudaErrorInvalidValue;
     static bool attr = false;
@@ -999,7 +1005,7 @@ cudaError_t run_mg_tile(const double* a, uint64_t nb, double tol, int max_iter, 
         !encode_tensor_map(&m32, false, 4, sc + K::D_BYTES, d32, s32, box))
         return cudaErrorInvalidValue;
     mgcg_tile_kernel<N><<<(unsigned)grid, tl::T, tl::SMEM, s>>>(m64, m32, a, (int)nb, tol, max_iter, out, slot, ctr,
-                                                               order, sc);
+                                                               order, sc, nb_dev, ok_status);
     return cudaGetLastError();
 }
 
@@ -1015,7 +1021,7 @@ bool use_mg_plain() {
 
 template <int N, int T, int GROUPS>
 cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
-                   const int* order, cudaStream_t s) {
+                   const int* order, cudaStream_t s, const int* nb_dev, int ok_status) {
     using K = MgCfg<N, T, GROUPS>;
     auto kern = mgcg_kernel<N, T, GROUPS>;
     static int bps = -1, sms = 0;
@@ -1031,18 +1037,19 @@ cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, doubl
     }
     const uint64_t grid = std::min<uint64_t>((nb + GROUPS - 1) / GROUPS, (uint64_t)bps * sms);
     if (grid == 0) return cudaSuccess;
-    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order);
+    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order, nb_dev,
+                                                 ok_status);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t run_mg_gm(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
-                      const int* order, void* scratch, int nctas, cudaStream_t s) {
+                      const int* order, void* scratch, int nctas, cudaStream_t s, const int* nb_dev, int ok_status) {
     if (!scratch || nctas < 1) return cudaErrorInvalidValue;
     const uint64_t grid = std::min<uint64_t>(nb, (uint64_t)nctas);
     if (grid == 0) return cudaSuccess;
     mgcg_gm_kernel<N><<<(unsigned)grid, MgGm<N>::T, 0, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order,
-                                                           static_cast<unsigned char*>(scratch));
+                                                           static_cast<unsigned char*>(scratch), nb_dev, ok_status);
     return cudaGetLastError();
 }
 
@@ -1063,22 +1070,23 @@ size_t mgcg_scratch_per_cta(int N) {
 int mgcg_ctas_per_sm(int N) { (void)N; return 1; }
 
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                        unsigned* ctr, const int* order, void* scratch, int nctas, cudaStream_t s) {
+                        unsigned* ctr, const int* order, void* scratch, int nctas, cudaStream_t s, const int* nb_dev,
+                        int ok_status) {
     const bool plain = use_mg_plain();
     switch (N) {
-        case 8: return run_mg<8, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-        case 16: return run_mg<16, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-        case 32: return run_mg<32, 128, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-        case 64: return run_mg<64, 256, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        case 8: return run_mg<8, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s, nb_dev, ok_status);
+        case 16: return run_mg<16, 32, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s, nb_dev, ok_status);
+        case 32: return run_mg<32, 128, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s, nb_dev, ok_status);
+        case 64: return run_mg<64, 256, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s, nb_dev, ok_status);
         case 128:
-            return plain ? run_mg_gm<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s)
-                         : run_mg_tile<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+            return plain ? run_mg_gm<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+                         : run_mg_tile<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
         case 256:
-            return plain ? run_mg_gm<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s)
-                         : run_mg_tile<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+            return plain ? run_mg_gm<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+                         : run_mg_tile<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
         case 512:
-            return plain ? run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s)
-                         : run_mg_tile<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s);
+            return plain ? run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+                         : run_mg_tile<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
         default: return cudaErrorNotSupported;
     }
 }

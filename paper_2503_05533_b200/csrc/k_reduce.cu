@@ -7,6 +7,7 @@
 // Deterministic: fixed 4096-sample chunks, a fixed per-thread stride and xor
 // butterflies inside a chunk, then the chunk partials added in chunk order.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.h"
@@ -38,7 +39,9 @@ __global__ void __launch_bounds__(RT) chunk_sums_kernel(const double* __restrict
         const double qf = r[0], qc = level > 0 ? r[1] : 0.0;
         const double y = qf - qc;
         const double itf = r[2], itc = level > 0 ? r[3] : 0.0;
-        const bool fail = r[6] != 0.0 || (level > 0 && r[7] != 0.0);
+        // status 4 = converged after escalation (a failed MINRES solve re-solved by MG-PCG): a success
+        const bool fail = (r[6] != 0.0 && r[6] != 4.0) || (level > 0 && r[7] != 0.0 && r[7] != 4.0);
+        const bool esc = r[6] == 4.0 || (level > 0 && r[7] == 4.0);
         v[0] += y;
         v[1] = fma(y, y, v[1]);
         v[2] += qf;
@@ -50,6 +53,7 @@ __global__ void __launch_bounds__(RT) chunk_sums_kernel(const double* __restrict
         v[8] += itc;
         v[9] = fmax(v[9], itf);
         v[10] = fmax(v[10], itc);
+        v[11] += esc ? 1.0 : 0.0;
     }
     __shared__ double sh[RT / 32][kSumsLen];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -67,6 +71,23 @@ __global__ void __launch_bounds__(RT) chunk_sums_kernel(const double* __restrict
             if (lane == 0) partial[blockIdx.x * kSumsLen + k] = t;
         }
     }
+}
+
+// escalation (R15 / SURVEY A15): the indices of the samples whose solve of record slot `slot` failed
+// (status 1-3), appended to list (order irrelevant: every listed system is re-solved independently)
+__global__ void escalate_collect_kernel(const double* __restrict__ rec, uint64_t nb, int slot, int* __restrict__ list,
+                                        int* __restrict__ count) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nb; s += (uint64_t)gridDim.x * blockDim.x) {
+        const double st = rec[s * kRecLen + 6 + slot];
+        if (st != 0.0 && st != 4.0) list[atomicAdd(count, 1)] = (int)s;
+    }
+}
+
+cudaError_t launch_escalate_collect(const double* rec, uint64_t nb, int slot, int* list, int* count, cudaStream_t s) {
+    if (nb == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<uint64_t>((nb + 255) / 256, 148ull * 8);
+    escalate_collect_kernel<<<grid, 256, 0, s>>>(rec, nb, slot, list, count);
+    return cudaGetLastError();
 }
 
 __global__ void combine_chunks_kernel(const double* __restrict__ partial, int nchunks, double* __restrict__ sums,

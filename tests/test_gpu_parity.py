@@ -279,7 +279,7 @@ def test_concurrent_levels_equal_sequential_levels():
         for q, (l, first) in enumerate(zip([3, 1, 0, 2], [7, 5, 3, 11])):
             ref = ctx.sample_level(l, Nl[l], seed=1, first_index=first, tol_fine=tols[l], tol_coarse=tc[l]).sums
             ref = np.array([ref[f] for f in ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail",
-                                             "iters_f", "iters_c", "iters_f_max", "iters_c_max", "reserved")])
+                                             "iters_f", "iters_c", "iters_f_max", "iters_c_max", "n_escalated")])
             if ws > (64 << 20):      # one pass on both sides: bit-identical
                 assert np.array_equal(got[q], ref), (ws, l)
             else:                    # passes smaller than a 4096-chunk: summation order differs
@@ -749,4 +749,30 @@ def test_adaptive_auto_policy():
         ch = ctx.auto_choice(cfg["h0_inv"] << l)
         assert ch is not None and ch["solver"] in ("minres", "mgcg", "chol_ir") and ch["ms_per_sample"] > 0, (l, ch)
     assert ctx.auto_choice(1024) is None
+    ctx.close()
+
+
+def test_escalation_repairs_failed_minres_solves():
+    """on_fail = 2 / MLMC_FLAG_ESCALATE: MINRES capped far below what the tolerance needs fails
+    on every sample; escalation solves each again with MG-PCG, so every record ends with status 4, the
+    level sums count them as escalated (not failed), and Q meets the direct solve's residual bound -- on an
+    on-chip mesh (h = 1/32) and a streamed one (h = 1/128, fine and coarse)."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=4 << 30)
+    P = _oracle(cfg)
+    tol = 1e-8
+    capped = precision("minres", max_iter=20, escalate=True)
+    for level, n in ((2, 40), (4, 3)):
+        r = ctx.sample_level(level, n, seed=31, prec_fine=capped, prec_coarse=capped, tol_fine=tol, tol_coarse=tol,
+                             per_sample=True)
+        ps = r.per_sample
+        assert np.all(ps[:, 6] == 4) and np.all(ps[:, 7] == 4)
+        assert r.sums["n_fail"] == 0 and r.sums["n_escalated"] == n
+        Nf = 8 << level
+        for k in (0, n - 1):
+            qf, bf, xf = _exact(P, Nf, oc.normals(31, level, k, cfg["m"]))
+            assert abs(ps[k, 0] - qf) <= tol * bf * xf * (1 + 1e-6) + 1e-14 * qf
+    # without the flag the same cap is a counted failure
+    r = ctx.sample_level(2, 40, seed=31, prec_fine=precision("minres", max_iter=20), tol_fine=tol, tol_coarse=tol)
+    assert r.sums["n_fail"] == 40 and r.sums["n_escalated"] == 0
     ctx.close()
