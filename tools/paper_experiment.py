@@ -8,6 +8,7 @@ paper uses a direct double-precision solve for it).  Cost = the deterministic wo
 time of the sampling calls.
 
   python tools/paper_experiment.py [R] [out.json]
+  python tools/paper_experiment.py kp [R] [out.json]     # the k_p sensitivity study
 """
 import json
 import math
@@ -73,7 +74,29 @@ def run(R=100, tol2s=(8e-6, 4e-6, 2e-6, 1e-6), k_p=0.05, std_tol=1e-6, N_init=10
     return out
 
 
+def kp_sweep(R=1000, kps=(0.05, 0.1, 0.2, 0.4), tol2=2e-6):
+    """The k_p sensitivity study (the paper's MSE-vs-k_p figure): MPML at TOL^2 = 2e-6 for k_p = 0.05,
+    0.1, 0.2, 0.4 against standard MLMC with the MINRES tolerance at 1e-10, R runs each."""
+    out = {"tol2": tol2, "R": R, "mlmc_minres_tol": 1e-10, "k_p": {}}
+    for kp in kps:
+        r = run(R, tol2s=(tol2,), k_p=kp, std_tol=1e-10)
+        e = r["tol2"][f"{tol2:g}"]
+        out["k_p"][f"{kp:g}"] = {"mse_mpml": e["mpml"]["mse"], "mse_mpml_ci95": e["mpml"]["mse_ci95"],
+                                 "mse_mlmc": e["mlmc"]["mse"], "mse_mlmc_ci95": e["mlmc"]["mse_ci95"],
+                                 "N_mean_mpml": e["mpml"]["N_mean"], "N_mean_mlmc": e["mlmc"]["N_mean"],
+                                 "cost_ratio": e["cost_ratio_mlmc_over_mpml"]}
+        print(json.dumps({f"k_p={kp:g}": out["k_p"][f"{kp:g}"]}), flush=True)
+    return out
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "kp":
+        R = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+        res = kp_sweep(R)
+        path = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/paper_kp_sweep.json"
+        os.makedirs(os.path.dirname(path) or ".", exist_ok=True)
+        json.dump(res, open(path, "w"), indent=1)
+        sys.exit(0)
     R = int(sys.argv[1]) if len(sys.argv) > 1 else 100
     res = run(R, N_init=int(os.environ.get("N_INIT", "10")), verbose=True)
     path = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/paper_experiment.json"
