@@ -517,11 +517,16 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
         case 64:
             // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67, v4 2.97
             // (v4: every conductance in shared memory, two systems per SM; bit-identical records, but the
-            // ~60 shared loads per thread and step outweigh the second resident system)
+            // ~60 shared loads per thread and step outweigh the second resident system); per launch
+            // (tools/tune_minres.py): v0 1.671 ms, v5 (west conductances in shared memory, no in-loop
+            // spills) 1.723, v6 (diagonal in shared memory) 1.722, v1 1.711 -- v0's few L1-resident
+            // spill reloads cost less than the shared loads that remove them
             if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             if (var == 4) return run_tile<64, 8, 2, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 5) return run_tile<64, 8, 1, 2, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            if (var == 6) return run_tile<64, 8, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         default: return cudaErrorNotSupported;
     }
