@@ -281,7 +281,10 @@ typedef struct {
 } mlmc_result;
 
 /* Run Algorithm 2 to RMSE eps (R16: TOL = eps).  Every rank calls this with
- * identical arguments except opts->rank; all ranks return identical results.
+ * identical arguments except opts->rank; all ranks return identical results,
+ * and the results (estimate, N, mean, var, cost) are bit-identical for any
+ * world size: the level sums are exact 256-bit fixed-point totals exchanged
+ * through the same all-reduce.
  * Errors: EINVAL, ECUDA, ESOLVER (a failed solve under the abort policy),
  * ELMAX (result still filled).                                              */
 int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,

@@ -29,6 +29,8 @@ struct mlmc_ctx {
     unsigned char* ws = nullptr;         // borrowed workspace
     size_t ws_bytes = 0;
     double* sums_dev = nullptr;          // owned: MLMC_MAX_LEVELS * kSumsLen
+    unsigned long long* xsums_dev = nullptr;   // owned: MLMC_MAX_LEVELS * kXLen exact sums of the last call
+    bool want_xsums = false;             // form them (inside mlmc_adaptive_run only)
     std::string err;
     struct AutoChoice { int N, cls; mlmc_precision p; double ms; };
     std::vector<AutoChoice> auto_choice;   // policy 3: per mesh, the solver the pilot chose
@@ -128,7 +130,7 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.a_f = off;    off += align256(sizeof(double) * batch * 2 * (size_t)Nf * Nf);
     L.a_c = off;    off += align256(sizeof(double) * batch * 2 * (size_t)Nc * Nc);
     L.rec = off;    off += align256(sizeof(double) * batch * kRecLen);
-    L.chunks = off; off += align256(sizeof(double) * kSumsLen * ((batch + kChunk - 1) / kChunk + 1));
+    L.chunks = off; off += align256(sizeof(double) * (kSumsLen + kXLen) * ((batch + kChunk - 1) / kChunk + 1));
     L.ctr = off;    off += align256(sizeof(unsigned) * 16);
     // contrast keys and longest-first orders of the fine / coarse MINRES solves (order_kernel)
     L.keys_f = off; off += align256(sizeof(unsigned long long) * 2 * batch);
@@ -365,7 +367,7 @@ int validate_level(mlmc_ctx* ctx, int level, const mlmc_precision* pf, const mlm
 int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t seed, uint64_t first_index,
               const mlmc_precision* pf, const mlmc_precision* pc, double tol_f, double tol_c, double* sums_dev,
               double* per_sample, bool per_sample_is_dev, const double* xi_in, bool xi_in_is_dev,
-              const LevelSched* sch = nullptr) {
+              const LevelSched* sch = nullptr, unsigned long long* xsums = nullptr) {
     const int Nf = level_N(ctx, level), Nc = level > 0 ? level_N(ctx, level - 1) : 0;
     uint64_t B = max_batch(ctx, level, ex.bytes, pf, pc);
     if (B == 0 && n > 0) return fail(ctx, MLMC_ENOMEM, "workspace too small for one sample");
@@ -386,6 +388,7 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
     const cudaStream_t st = ex.st;
     int rc;
     CU(cudaMemsetAsync(sums_dev, 0, sizeof(double) * kSumsLen, st));
+    if (xsums) CU(cudaMemsetAsync(xsums, 0, sizeof(unsigned long long) * kXLen, st));
     for (uint64_t done = 0; done < n;) {
         const uint64_t nb = std::min<uint64_t>(B, n - done);
         CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, st));
@@ -436,7 +439,7 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
             return rc;
         }
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
-            return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, st);
+            return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, st, xsums);
         }));
         if (per_sample) {
             double* dst = per_sample + done * kRecLen;
@@ -457,7 +460,8 @@ int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
     if (rc) return rc;
     if (!ctx->ws) return fail(ctx, MLMC_ENOMEM, "no workspace bound");
     return run_level(ctx, Exec{ctx->ws, ctx->ws_bytes, ctx->stream}, level, n, seed, first_index, pf, pc, tol_f, tol_c,
-                     sums_dev, per_sample, per_sample_is_dev, xi_in, xi_in_is_dev);
+                     sums_dev, per_sample, per_sample_is_dev, xi_in, xi_in_is_dev, nullptr,
+                     ctx->want_xsums ? ctx->xsums_dev : nullptr);
 }
 
 }  // namespace
@@ -476,6 +480,15 @@ bool mlmc::ctx_find_auto_choice(const mlmc_ctx* ctx, int N, int cls, mlmc_precis
 
 int mlmc::copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host) {
     CU(cudaMemcpyAsync(host, dev, sizeof(double) * kSumsLen * nlev, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MLMC_OK;
+}
+
+void mlmc::ctx_want_xsums(mlmc_ctx* ctx, bool on) { ctx->want_xsums = on; }
+
+int mlmc::copy_xsums_to_host(mlmc_ctx* ctx, int nlev, unsigned long long* host) {
+    CU(cudaMemcpyAsync(host, ctx->xsums_dev, sizeof(unsigned long long) * kXLen * nlev, cudaMemcpyDeviceToHost,
+                       ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return MLMC_OK;
 }
@@ -536,6 +549,7 @@ int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->sums_dev, sizeof(double) * kSumsLen * MLMC_MAX_LEVELS);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->xsums_dev, sizeof(unsigned long long) * kXLen * MLMC_MAX_LEVELS);
     if (e != cudaSuccess) {
         std::string msg = cudaGetErrorString(e);
         mlmc_destroy(ctx);
@@ -562,6 +576,7 @@ void mlmc_destroy(mlmc_ctx* ctx) {
     if (ctx->sep_i) cudaFree(ctx->sep_i);
     if (ctx->sep_c) cudaFree(ctx->sep_c);
     if (ctx->sums_dev) cudaFree(ctx->sums_dev);
+    if (ctx->xsums_dev) cudaFree(ctx->xsums_dev);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -702,7 +717,8 @@ int sample_levels_impl(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_
         double* pq = per_sample ? per_sample[q] : nullptr;
         int rc = run_level(ctx, Exec{ctx->ws + offs[q], slice[q], st}, levels[q], n[q], seed, first_index[q],
                            &prec_fine[q], &prec_coarse[q], tol_fine[q], tol_coarse[q], sums_dev + (size_t)q * kSumsLen,
-                           pq, pq && is_device_ptr(pq), xq, xq && is_device_ptr(xq), &sch);
+                           pq, pq && is_device_ptr(pq), xq, xq && is_device_ptr(xq), &sch,
+                           ctx->want_xsums ? ctx->xsums_dev + (size_t)q * kXLen : nullptr);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->join_ev[k], st));
     }

@@ -25,10 +25,56 @@
 
 namespace {
 
+using u64 = unsigned long long;
+using mlmc::kXFields;
+using mlmc::kXLen;
+using mlmc::kXScale;
+using mlmc::kXWords;
+
 struct LevelAcc {
     double s[MLMC_SUMS_LEN] = {0};
+    u64 x[kXLen] = {0};   // exact fixed-point Y, Y^2, Q_f, Q_c, cost sums (internal.h kX*)
     uint64_t drawn = 0;
 };
+
+// 256-bit two's-complement addition (mod 2^256) of field f's limbs
+void x_add(u64* a, const u64* b) {
+    u64 c = 0;
+    for (int i = 0; i < 4; ++i) {
+        const u64 s = a[i] + b[i];
+        const u64 c1 = s < a[i];
+        a[i] = s + c;
+        c = c1 | (a[i] < s);
+    }
+}
+
+// The exact fixed-point value (4 limbs, units of 2^-kXScale) rounded to the nearest double, ties to even.
+// A function of the integer alone, so every rank converts an identical total to identical bits.
+double x_to_double(const u64* w) {
+    u64 a[4] = {w[0], w[1], w[2], w[3]};
+    const bool neg = a[3] >> 63;
+    if (neg) {   // |value|
+        for (int i = 0; i < 4; ++i) a[i] = ~a[i];
+        const u64 one[4] = {1, 0, 0, 0};
+        x_add(a, one);
+    }
+    int msb = -1;
+    for (int i = 3; i >= 0 && msb < 0; --i)
+        if (a[i]) msb = 64 * i + 63 - __builtin_clzll(a[i]);
+    if (msb < 0) return 0.0;
+    auto bit = [&](int i) -> u64 { return (i >= 0 && i < 256) ? (a[i >> 6] >> (i & 63)) & 1ull : 0ull; };
+    u64 mant = 0;   // bits msb .. msb-52
+    for (int b = 0; b < 53; ++b) mant |= bit(msb - 52 + b) << b;
+    const u64 guard = bit(msb - 53);
+    bool sticky = false;
+    for (int i = msb - 54; i >= 0 && !sticky; --i) sticky = bit(i) != 0;
+    int e = msb - 52 - kXScale;
+    if (guard && (sticky || (mant & 1ull))) {
+        if (++mant == (1ull << 53)) { mant >>= 1; ++e; }
+    }
+    const double v = std::ldexp((double)mant, e);
+    return neg ? -v : v;
+}
 
 mlmc_precision minres_prec() {
     return mlmc_precision{MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
@@ -55,15 +101,19 @@ mlmc_precision policy_prec(int policy, int level, int N, double tol) {
 
 // Draw one round: for each q, n[q] samples of levels[q] from first[q]; write
 // MLMC_SUMS_LEN sums per entry to sums (host).
+// xs (exact runners only): nlev x kXLen fixed-point words of the same sums.
 using RoundSampler = std::function<int(int nlev, const int* levels, const uint64_t* n, const uint64_t* first,
                                        const mlmc_precision* pf, const mlmc_precision* pc, const double* tf,
-                                       const double* tc, double* sums)>;
+                                       const double* tc, double* sums, u64* xs)>;
 
 // precision of the solves on mesh N of level `level` at tolerance tol
 using PrecChooser = std::function<int(int level, int N, double tol, mlmc_precision* out)>;
 
+// exact: the sampler also returns the fixed-point sums; they are what the ranks exchange and what the
+// statistics use (bit-identical sums and decisions for any number of ranks).
 int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o, const RoundSampler& sampler,
-                  const PrecChooser& choose, mlmc_allreduce_fn allreduce, void* user, mlmc_result* out) {
+                  const PrecChooser& choose, mlmc_allreduce_fn allreduce, void* user, mlmc_result* out,
+                  bool exact = false) {
     if (!(eps > 0.0) || o.world < 1 || o.rank < 0 || o.rank >= o.world || L_max < 1 || h0_inv < 2)
         return MLMC_EINVAL;
     if (o.world > 1 && !allreduce) return MLMC_EINVAL;
@@ -81,11 +131,16 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
     double solve_s = 0.0;
     int64_t n_fail = 0;
 
+    // field f (0 Y, 1 Y^2, 2 Q_f, 3 Q_c, 4 cost) of level l: the exact sum rounded once where it exists
+    auto sum = [&](int l, int f) {
+        const u64* x = acc[l].x + f * kXWords;
+        return exact && x[4] == 0 ? x_to_double(x) : acc[l].s[f];
+    };
     auto stats = [&](int l, double& mean, double& var, double& cost) {
         const double n = acc[l].s[5];
-        mean = n > 0 ? acc[l].s[0] / n : 0.0;
-        var = n > 0 ? std::max(0.0, acc[l].s[1] / n - mean * mean) : 0.0;   // Eq. (4) with 1/N_l (R4)
-        cost = n > 0 ? acc[l].s[4] / n : 0.0;
+        mean = n > 0 ? sum(l, 0) / n : 0.0;
+        var = n > 0 ? std::max(0.0, sum(l, 1) / n - mean * mean) : 0.0;   // Eq. (4) with 1/N_l (R4)
+        cost = n > 0 ? sum(l, 4) / n : 0.0;
     };
 
     while (L <= L_max && rounds < max_rounds) {
@@ -93,6 +148,7 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
         epsl.assign(L + 1, o.fixed_tol > 0 ? o.fixed_tol : 1e-10);
         if (o.k_p > 0.0) mlmc_eps_schedule(L, h0, o.k_p, epsl.data());   // step 2, Eq. (16)
         std::vector<double> round_sums((size_t)(L + 1) * MLMC_SUMS_LEN, 0.0);
+        std::vector<u64> round_x((size_t)(L + 1) * kXLen, 0);
         std::vector<uint64_t> dN(L + 1, 0);
         // steps 3-4: this rank's slice of every level's new indices, all levels in one call
         std::vector<int> lv;
@@ -123,14 +179,17 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
         }
         if (!lv.empty()) {
             std::vector<double> s(lv.size() * MLMC_SUMS_LEN, 0.0);
+            std::vector<u64> xs(exact ? lv.size() * kXLen : 0, 0);
             auto t0 = std::chrono::steady_clock::now();
             int rc = sampler((int)lv.size(), lv.data(), cnt.data(), first.data(), pf.data(), pc.data(), tf.data(),
-                             tc.data(), s.data());
+                             tc.data(), s.data(), exact ? xs.data() : nullptr);
             solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             if (rc) return rc;
-            for (size_t q = 0; q < lv.size(); ++q)
+            for (size_t q = 0; q < lv.size(); ++q) {
                 std::memcpy(&round_sums[(size_t)lv[q] * MLMC_SUMS_LEN], &s[q * MLMC_SUMS_LEN],
                             sizeof(double) * MLMC_SUMS_LEN);
+                if (exact) std::memcpy(&round_x[(size_t)lv[q] * kXLen], &xs[q * kXLen], sizeof(u64) * kXLen);
+            }
         }
         // one exchange per round: SUM of the additive fields, MAX of the two maxima
         if (o.world > 1) {
@@ -141,8 +200,38 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 9] = 0.0;
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = 0.0;
             }
+            // exact sums: each field's 256-bit integer as eight 32-bit pieces (doubles, so the SUM over up to
+            // 2^21 ranks stays exact), then the carries are propagated; the overflow counts are plain sums
+            constexpr int XD = kXFields * 9;
+            const size_t base = round_sums.size();
+            if (exact) {
+                round_sums.resize(base + (size_t)(L + 1) * XD, 0.0);
+                for (int l = 0; l <= L; ++l)
+                    for (int f = 0; f < kXFields; ++f) {
+                        const u64* x = &round_x[(size_t)l * kXLen + f * kXWords];
+                        double* d = &round_sums[base + (size_t)l * XD + f * 9];
+                        for (int i = 0; i < 8; ++i) d[i] = (double)((x[i / 2] >> (32 * (i % 2))) & 0xffffffffull);
+                        d[8] = (double)x[4];
+                    }
+            }
             if (allreduce(round_sums.data(), (int)round_sums.size(), 0, user) != 0) return MLMC_ECUDA;
             if (allreduce(mx.data(), (int)mx.size(), 1, user) != 0) return MLMC_ECUDA;
+            if (exact) {
+                for (int l = 0; l <= L; ++l)
+                    for (int f = 0; f < kXFields; ++f) {
+                        u64* x = &round_x[(size_t)l * kXLen + f * kXWords];
+                        const double* d = &round_sums[base + (size_t)l * XD + f * 9];
+                        u64 carry = 0;
+                        for (int i = 0; i < 4; ++i) x[i] = 0;
+                        for (int i = 0; i < 8; ++i) {
+                            const u64 t = (u64)d[i] + carry;
+                            x[i / 2] |= (t & 0xffffffffull) << (32 * (i % 2));
+                            carry = t >> 32;
+                        }
+                        x[4] = (u64)d[8];
+                    }
+                round_sums.resize(base);
+            }
             for (int l = 0; l <= L; ++l) {
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 9] = mx[2 * l];
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = mx[2 * l + 1];
@@ -153,6 +242,12 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             const double* rs = &round_sums[(size_t)l * MLMC_SUMS_LEN];
             for (int k = 0; k < MLMC_SUMS_LEN; ++k)
                 acc[l].s[k] = (k == 9 || k == 10) ? std::max(acc[l].s[k], rs[k]) : acc[l].s[k] + rs[k];
+            if (exact)
+                for (int f = 0; f < kXFields; ++f) {
+                    const u64* rx = &round_x[(size_t)l * kXLen + f * kXWords];
+                    x_add(acc[l].x + f * kXWords, rx);
+                    acc[l].x[f * kXWords + 4] += rx[4];
+                }
             acc[l].drawn += dN[l];
             if (rs[6] > 0) failed = true;
             n_fail += (int64_t)rs[6];
@@ -295,10 +390,12 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
     if (cudaMalloc(&dev, sizeof(double) * MLMC_MAX_LEVELS * MLMC_SUMS_LEN) != cudaSuccess) return MLMC_ECUDA;
     const uint64_t seed = opts->seed;
     RoundSampler gpu = [&](int nlev, const int* lv, const uint64_t* n, const uint64_t* first, const mlmc_precision* pf,
-                           const mlmc_precision* pc, const double* tf, const double* tc, double* sums) -> int {
+                           const mlmc_precision* pc, const double* tf, const double* tc, double* sums,
+                           u64* xs) -> int {
         int rc = mlmc_sample_levels_async(ctx, nlev, lv, n, seed, first, pf, pc, tf, tc, dev);
         if (rc) return rc;
-        return mlmc::copy_sums_to_host(ctx, dev, nlev, sums);
+        rc = mlmc::copy_sums_to_host(ctx, dev, nlev, sums);
+        return rc || !xs ? rc : mlmc::copy_xsums_to_host(ctx, nlev, xs);
     };
     AutoChooser ac{ctx, seed, allreduce, user, opts->world};
     const int policy = opts->policy;
@@ -307,7 +404,9 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
         *p = policy_prec(policy, level, N, tol);
         return MLMC_OK;
     };
-    int rc = adaptive_core(li0.N, L_max, eps, *opts, gpu, choose, allreduce, user, out);
+    mlmc::ctx_want_xsums(ctx, true);
+    int rc = adaptive_core(li0.N, L_max, eps, *opts, gpu, choose, allreduce, user, out, true);
+    mlmc::ctx_want_xsums(ctx, false);
     cudaFree(dev);
     return rc;
 }
@@ -317,7 +416,8 @@ extern "C" int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const m
                                       void* user, mlmc_result* out) {
     if (!opts || !out || !sampler) return MLMC_EINVAL;
     RoundSampler host = [&](int nlev, const int* lv, const uint64_t* n, const uint64_t* first, const mlmc_precision* pf,
-                            const mlmc_precision* pc, const double* tf, const double* tc, double* sums) -> int {
+                            const mlmc_precision* pc, const double* tf, const double* tc, double* sums,
+                            u64*) -> int {
         for (int q = 0; q < nlev; ++q) {
             int rc = sampler(lv[q], n[q], first[q], &pf[q], &pc[q], tf[q], tc[q], sums + (size_t)q * MLMC_SUMS_LEN,
                              sampler_user);

@@ -102,10 +102,15 @@ size_t chol_scratch_bytes(int N, int u_f, int u_s, uint64_t nb, int u = MLMC_FMT
 // Escalation: the samples of `rec` whose slot-`slot` solve failed -> list[*count] (count zeroed by caller).
 cudaError_t launch_escalate_collect(const double* rec, uint64_t nb, int slot, int* list, int* count, cudaStream_t s);
 // K5: per-level sums of the per-sample records into sums (accumulate = add to existing).
+// xsums (optional, device, kXLen words): the exact fixed-point sums, accumulated like sums.  chunk_scratch
+// holds (kSumsLen + kXLen) x 8 bytes per chunk.
 cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,
                               double cost_f_fixed, double cost_f_step, double cost_c_fixed,
                               double cost_c_step, double* chunk_scratch, double* sums, bool accumulate,
-                              cudaStream_t s);
+                              cudaStream_t s, unsigned long long* xsums = nullptr);
+// The exact fixed-point sums of the levels of the last mlmc_sample_levels(_async) call (nlev x kXLen words)
+int copy_xsums_to_host(mlmc_ctx* ctx, int nlev, unsigned long long* host);
+void ctx_want_xsums(mlmc_ctx* ctx, bool on);   // form the exact sums in the sampling calls that follow
 
 // Copy nlev level-sum records from the device to the host on the ctx's stream and wait.
 int copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host);
@@ -113,7 +118,33 @@ int copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host);
 void ctx_note_auto_choice(mlmc_ctx* ctx, int N, int cls, const mlmc_precision& p, double ms_per_sample);
 bool ctx_find_auto_choice(const mlmc_ctx* ctx, int N, int cls, mlmc_precision* p);
 
+// Launch limits of a kernel, computed once per template instance: callers keep them in a function-local
+// `static const KernelOcc` initialised by a lambda (C++11 guarantees that initialisation runs once, also
+// when several host threads drive their own contexts), so no thread can see a half-written pair.
+struct KernelOcc {
+    cudaError_t err = cudaSuccess;
+    int per_sm = 0;   // resident blocks per SM
+    int sms = 0;
+};
+template <class Kern>
+KernelOcc kernel_occ(Kern kern, int block, size_t smem) {
+    KernelOcc o;
+    o.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (o.err == cudaSuccess) o.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.per_sm, kern, block, smem);
+    int dev = 0;
+    if (o.err == cudaSuccess) o.err = cudaGetDevice(&dev);
+    if (o.err == cudaSuccess) o.err = cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (o.err == cudaSuccess && o.per_sm < 1) o.err = cudaErrorInvalidConfiguration;
+    return o;
+}
+
 constexpr int kSumsLen = MLMC_SUMS_LEN;
+// Reproducible level sums: the five real-valued sums (Y, Y^2, Q_f, Q_c, cost) are also kept as
+// exact fixed-point integers -- each per-sample value rounded once to a multiple of 2^-kXScale, added as a
+// 256-bit two's-complement integer (4 little-endian 64-bit limbs) plus a count of values outside
+// |x| < 2^62 (NaN, inf, huge; the double sums are used then).  Integer addition is associative, so the
+// totals do not depend on how the samples were split over passes, chunks or ranks.
+constexpr int kXFields = 5, kXWords = 5, kXLen = kXFields * kXWords, kXScale = 192;
 constexpr int kRecLen = MLMC_SAMPLE_LEN;
 constexpr uint64_t kChunk = 4096;
 

@@ -711,22 +711,14 @@ struct Launch {
     using KF = FacCfg<N, F, S>;
     using KR = RefCfg<N, F, S, NS, WPC>;
     static cudaError_t setup(int& grid_max) {
-        static int bps = -1, sms = 0;
-        if (bps < 0) {
-            cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel<N, F, S>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, KF::SMEM);
-            if (e != cudaSuccess) return e;
-            auto kern = chol_refine_kernel<N, F, S, NS, WPC, U>;
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, KR::SMEM);
-            if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * WPC, KR::SMEM);
-            if (e != cudaSuccess) return e;
-            int dev;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (bps < 1) { bps = -1; return cudaErrorInvalidConfiguration; }
-        }
-        grid_max = bps * sms;
+        static const KernelOcc occ = [] {
+            KernelOcc o;
+            o.err = cudaFuncSetAttribute(chol_factor_kernel<N, F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         KF::SMEM);
+            return o.err == cudaSuccess ? kernel_occ(chol_refine_kernel<N, F, S, NS, WPC, U>, 32 * WPC, KR::SMEM) : o;
+        }();
+        if (occ.err != cudaSuccess) return occ.err;
+        grid_max = occ.per_sm * occ.sms;
         return cudaSuccess;
     }
     static constexpr uint64_t per_cta = (uint64_t)WPC * G::SEGS;

@@ -1024,18 +1024,9 @@ cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, doubl
                    const int* order, cudaStream_t s, const int* nb_dev, int ok_status) {
     using K = MgCfg<N, T, GROUPS>;
     auto kern = mgcg_kernel<N, T, GROUPS>;
-    static int bps = -1, sms = 0;
-    if (bps < 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, K::BLOCK, K::SMEM);
-        if (e != cudaSuccess) return e;
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (bps < 1) { bps = -1; return cudaErrorInvalidConfiguration; }
-    }
-    const uint64_t grid = std::min<uint64_t>((nb + GROUPS - 1) / GROUPS, (uint64_t)bps * sms);
+    static const KernelOcc occ = kernel_occ(kern, K::BLOCK, K::SMEM);
+    if (occ.err != cudaSuccess) return occ.err;
+    const uint64_t grid = std::min<uint64_t>((nb + GROUPS - 1) / GROUPS, (uint64_t)occ.per_sm * occ.sms);
     if (grid == 0) return cudaSuccess;
     kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order, nb_dev,
                                                  ok_status);

@@ -359,19 +359,10 @@ static cudaError_t run_minres(const double* a, uint64_t nb, double tol, int max_
                               unsigned* ctr, cudaStream_t s) {
     using K = StripCfg<N, R, MINB, CS>;
     auto kern = minres_strip_kernel<N, R, MINB, VERIFY, PIPE, CS>;
-    static int blocks_per_sm = -1, sms = 0;
-    if (blocks_per_sm < 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, K::BLOCK, K::SMEM);
-        if (e != cudaSuccess) return e;
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
-    }
+    static const KernelOcc occ = kernel_occ(kern, K::BLOCK, K::SMEM);
+    if (occ.err != cudaSuccess) return occ.err;
     uint64_t need = (nb + K::GROUPS - 1) / K::GROUPS;
-    uint64_t grid = std::min<uint64_t>(need, (uint64_t)blocks_per_sm * sms);
+    uint64_t grid = std::min<uint64_t>(need, (uint64_t)occ.per_sm * occ.sms);
     if (grid == 0) return cudaSuccess;
     kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr);
     return cudaGetLastError();

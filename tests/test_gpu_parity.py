@@ -776,3 +776,75 @@ def test_escalation_repairs_failed_minres_solves():
     r = ctx.sample_level(2, 40, seed=31, prec_fine=precision("minres", max_iter=20), tol_fine=tol, tol_coarse=tol)
     assert r.sums["n_fail"] == 40 and r.sums["n_escalated"] == 0
     ctx.close()
+
+
+# ============================================================================ SURVEY 8(e): rank independence
+def _adaptive_threads(cfg, world, eps, **kw):
+    """world ranks of mlmc_adaptive_run as host threads, one context each on cuda:0, exchanging through a
+    thread-barrier all-reduce (the same C callback torch.distributed drives; the kernels of the ranks never
+    wait on one another)."""
+    import ctypes as C
+    import threading
+    from paper_2503_05533_b200 import _capi as K
+    from paper_2503_05533_b200.api import _result_dict
+    bar = threading.Barrier(world)
+    bufs = [None] * world
+    ctxs = [_ctx(cfg, ws=512 << 20) for _ in range(world)]
+    out = [None] * world
+
+    def rank_main(r):
+        def _allreduce(buf, count, op, user):
+            arr = np.ctypeslib.as_array(buf, shape=(count,))
+            bufs[r] = arr.copy()
+            bar.wait()
+            tot = bufs[0].copy()
+            for q in range(1, world):
+                tot = tot + bufs[q] if op == 0 else np.maximum(tot, bufs[q])
+            bar.wait()
+            arr[:] = tot
+            return 0
+        cb = K.ALLREDUCE_FN(_allreduce)
+        opts = K.AdaptiveOpts(kw.get("k_p", 0.0), kw.get("fixed_tol", 1e-8), 1.0, kw.get("N_init", 50), 0, r, world,
+                              kw.get("max_rounds", 8), kw.get("seed", 11), 1, 0)
+        res = K.Result()
+        rc = K.lib().mlmc_adaptive_run(ctxs[r].ctx, eps, C.byref(opts), cb, None, C.byref(res))
+        out[r] = (rc, _result_dict(res))
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for c in ctxs:
+        c.close()
+    return out
+
+
+def test_adaptive_sums_exact_and_rank_independent():
+    """the controller's level sums are exact fixed-point totals, so (i) each level mean and
+    variance equals the correctly rounded sum of the per-sample Y and Y^2 (math.fsum) divided by N_l, and
+    (ii) 1, 2 and 3 ranks produce bit-identical estimates, sample counts, means, variances and costs."""
+    cfg = W.CONFIGS["C4"]
+    eps = cfg["eps"]
+    kw = dict(k_p=0.0, fixed_tol=1e-8, N_init=50, seed=11, max_rounds=8)
+    runs = {w: _adaptive_threads(cfg, w, eps, **kw) for w in (1, 2, 3)}
+    rc1, g = runs[1][0]
+    assert rc1 in (0, 4) and g["L"] >= 1
+    for w in (2, 3):
+        for rc, r in runs[w]:
+            assert rc == rc1
+            for key in ("estimate", "L", "rounds", "N", "mean", "var", "cost", "n_fail"):
+                assert r[key] == g[key], (w, key, r[key], g[key])
+    # (i) against the per-sample records of the same indices (batch-independent; fixed tolerance 1e-8)
+    ctx = _ctx(cfg, ws=512 << 20)
+    for l in range(g["L"] + 1):
+        lr = ctx.sample_level(l, g["N"][l], seed=11, first_index=0, prec_fine="minres", prec_coarse="minres",
+                              tol_fine=1e-8, tol_coarse=1e-8, per_sample=True)
+        rec = np.asarray(lr.per_sample).reshape(-1, 8)
+        y = rec[:, 0] - (rec[:, 1] if l > 0 else 0.0)
+        n = float(g["N"][l])
+        mean = math.fsum(y.tolist()) / n
+        assert g["mean"][l] == mean, (l, g["mean"][l], mean)
+        var = max(0.0, math.fsum((y * y).tolist()) / n - mean * mean)
+        assert g["var"][l] == var, (l, g["var"][l], var)
+    ctx.close()
