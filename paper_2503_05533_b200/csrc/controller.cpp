@@ -48,6 +48,34 @@ void x_add(u64* a, const u64* b) {
     }
 }
 
+// x rounded once (nearest even) to a multiple of 2^-kXScale as 4 limbs + overflow word (the host twin of
+// k_reduce.cu's x_acc, for the host runner's per-rank sums)
+void x_from_double(double x, u64* w) {
+    for (int i = 0; i < kXWords; ++i) w[i] = 0;
+    if (x == 0.0) return;
+    if (!(std::fabs(x) < 0x1p62)) { w[4] = 1; return; }
+    const double X = std::ldexp(x, kXScale);
+    u64 v[4] = {0, 0, 0, 0};
+    if (std::fabs(X) < 0x1p62) {
+        const long long i = std::llrint(X);   // default rounding: to nearest even
+        v[0] = (u64)i;
+        v[1] = v[2] = v[3] = i < 0 ? ~0ull : 0ull;
+    } else {
+        int e;
+        const double f = std::frexp(std::fabs(X), &e);
+        const u64 m = (u64)(f * 0x1p53);
+        const int k = e - 53, q = k >> 6, r = k & 63;
+        v[q] = m << r;
+        if (r && q + 1 < 4) v[q + 1] = m >> (64 - r);
+        if (x < 0.0) {
+            for (int i = 0; i < 4; ++i) v[i] = ~v[i];
+            const u64 one[4] = {1, 0, 0, 0};
+            x_add(v, one);
+        }
+    }
+    for (int i = 0; i < 4; ++i) w[i] = v[i];
+}
+
 // The exact fixed-point value (4 limbs, units of 2^-kXScale) rounded to the nearest double, ties to even.
 // A function of the integer alone, so every rank converts an identical total to identical bits.
 double x_to_double(const u64* w) {
@@ -417,11 +445,15 @@ extern "C" int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const m
     if (!opts || !out || !sampler) return MLMC_EINVAL;
     RoundSampler host = [&](int nlev, const int* lv, const uint64_t* n, const uint64_t* first, const mlmc_precision* pf,
                             const mlmc_precision* pc, const double* tf, const double* tc, double* sums,
-                            u64*) -> int {
+                            u64* xs) -> int {
         for (int q = 0; q < nlev; ++q) {
-            int rc = sampler(lv[q], n[q], first[q], &pf[q], &pc[q], tf[q], tc[q], sums + (size_t)q * MLMC_SUMS_LEN,
-                             sampler_user);
+            double* s = sums + (size_t)q * MLMC_SUMS_LEN;
+            int rc = sampler(lv[q], n[q], first[q], &pf[q], &pc[q], tf[q], tc[q], s, sampler_user);
             if (rc) return rc;
+            // a host sampler returns its slice's sums already rounded: they enter the exact exchange as they
+            // are (so the ranks still agree bit for bit; independence of the slicing needs per-sample values)
+            if (xs)
+                for (int f = 0; f < kXFields; ++f) x_from_double(s[f], xs + (size_t)q * kXLen + f * kXWords);
         }
         return MLMC_OK;
     };
@@ -430,5 +462,5 @@ extern "C" int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const m
         *p = policy_prec(policy, level, N, tol);
         return MLMC_OK;
     };
-    return adaptive_core(h0_inv, L_max, eps, *opts, host, choose, allreduce, user, out);
+    return adaptive_core(h0_inv, L_max, eps, *opts, host, choose, allreduce, user, out, true);
 }

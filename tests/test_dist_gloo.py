@@ -163,3 +163,66 @@ def test_group_none_is_local_even_with_a_default_group():
     r0.pop("solve_seconds")
     single.pop("solve_seconds")
     assert res[1] is None and r0 == single
+
+
+# ---------------------------------------------------------------------------- exact level sums
+def _dyadic_sampler(level, n, first, pf, pc, tf, tc):
+    """Synthetic coupled differences that are dyadic rationals (multiples of 2^-(2l+12), about a third of
+    them negative), so every rank's double partial sums are exact whatever its slice: the exchange of the
+    exact fixed-point sums (32-bit pieces, carries, two's complement) must then reproduce the 1-rank run
+    bit for bit."""
+    k = np.arange(first, first + n, dtype=np.int64)
+    noise = ((k * 2654435761 + 97 * level) % 2001 - 1000).astype(np.float64)
+    y = (2.0 ** (-2 * level - 4)) + noise * 2.0 ** (-2 * level - 12)
+    s = np.zeros(12)
+    s[0] = y.sum()
+    s[1] = (y * y).sum()
+    s[2] = s[0]
+    s[4] = float(n) * 100.0 * 4 ** level
+    s[5] = n
+    s[7] = 10.0 * n
+    s[9] = 10.0
+    return s
+
+
+def _run_dyadic(group=None):
+    from paper_2503_05533_b200.api import mlmc_adaptive_run_host
+    return mlmc_adaptive_run_host(8, 4, 1e-3, _dyadic_sampler, k_p=0.05, N_init=40, seed=1, group=group)
+
+
+def _worker_dyadic(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, _run_dyadic(dist.group.WORLD)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exact_sum_exchange_two_ranks_bit_identical():
+    from fractions import Fraction
+    single = _run_dyadic(None)
+    assert single["code"] == 0 and single["L"] == 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dyadic, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    single.pop("solve_seconds")
+    for r in res.values():
+        r.pop("solve_seconds")
+        assert r == single                                           # bit-identical, every field
+    # the level means are the exact sums over all drawn samples, rounded once
+    for l in range(single["L"] + 1):
+        n = single["N"][l]
+        y = _dyadic_sampler(l, n, 0, None, None, 0, 0)[0]
+        k = np.arange(0, n, dtype=np.int64)
+        noise = ((k * 2654435761 + 97 * l) % 2001 - 1000)
+        exact = sum((Fraction(1, 2 ** (2 * l + 4)) + Fraction(int(v), 2 ** (2 * l + 12)) for v in noise), Fraction(0))
+        assert single["mean"][l] == float(exact / n) and y == float(exact)
