@@ -15,6 +15,8 @@ Textbook definitions in binary64, written so that a reader can check them one by
   the start of every level.
 * ``pcg``: conjugate gradients from x0 = 0 preconditioned by one V-cycle, stopped at the first k with
   ||r_k||_2 / ||b||_2 <= tol, r_k the CG recurrence residual (reading R30).
+* ``cg``: plain conjugate gradients (Hestenes-Stiefel) from x0 = 0 with the same stopping rule -- the
+  Krylov solver the paper names beside MINRES for the SPD systems (NEXT-4).
 
 Every step is plain numpy / scipy.sparse (a library sparse product and matrix-vector product); no
 blocking or fusion.
@@ -153,6 +155,35 @@ def pcg(N: int, a_tri, tol: float, max_iter: int = 1000) -> dict:
         rz_new = r @ z
         p = z + (rz_new / rz) * p
         rz = rz_new
+    h = 1.0 / N
+    return {"Q": h * h * x.sum(), "iters": it, "status": status, "x": x,
+            "relres_true": np.linalg.norm(b - A @ x) / bnorm}
+
+
+def cg(N: int, a_tri, tol: float, max_iter: int = 100000) -> dict:
+    """Unpreconditioned CG from x0 = 0 (P:102); stop at the first k with ||r_k|| / ||b|| <= tol (R30);
+    Q = h^2 1^T x."""
+    A, b = stiffness(N, a_tri)
+    x = np.zeros_like(b)
+    r = b.copy()
+    p = r.copy()
+    rr = r @ r
+    bnorm = np.sqrt(rr)
+    it, status = 0, 1
+    if bnorm == 0.0:
+        status = 0
+    while status == 1 and it < max_iter:
+        q = A @ p
+        alpha = rr / (p @ q)
+        x += alpha * p
+        r -= alpha * q
+        it += 1
+        rr_new = r @ r
+        if np.sqrt(rr_new) <= tol * bnorm:
+            status = 0
+            break
+        p = r + (rr_new / rr) * p
+        rr = rr_new
     h = 1.0 / N
     return {"Q": h * h * x.sum(), "iters": it, "status": status, "x": x,
             "relres_true": np.linalg.norm(b - A @ x) / bnorm}

@@ -123,3 +123,41 @@ def test_pcg_constant_coefficient_reference_values():
     ref = {8: 0.033423031078, 16: 0.034702752314, 32: 0.035033019542, 64: 0.035116381629}
     for N, q in ref.items():
         assert abs(mg.pcg(N, np.ones(2 * N * N), 1e-12)["Q"] - q) < 1e-11
+
+
+# ---------------------------------------------------------------------------- plain CG
+def test_cg_converges_in_as_many_steps_as_distinct_excited_eigenvalues():
+    """a = 1, N = 4: A is the 5-point Laplacian (9 unknowns) and b = h^2 1 has components only along the
+    eigenvectors sin(i pi x) sin(j pi y) with i, j odd -- (1,1), (1,3), (3,1), (3,3) -- whose eigenvalues
+    4 - 2cos(i pi/4) - 2cos(j pi/4) take 3 distinct values, so exact CG terminates at step 3."""
+    r = mg.cg(4, np.ones(32), 1e-12)
+    assert r["status"] == 0 and r["iters"] == 3
+    assert r["relres_true"] < 1e-13
+
+
+def test_cg_matches_library_cg_and_direct_solve():
+    """Iterates of the textbook CG against scipy's CG (an independent implementation, same stopping rule on
+    the recurrence residual) and the solution against a sparse direct solve."""
+    N, tol = 16, 1e-10
+    a = _lognormal_triangles(N, 3)
+    r = mg.cg(N, a, tol)
+    A, b = mg.stiffness(N, a)
+    its = []
+    xs, info = spla.cg(A, b, rtol=tol, atol=0.0, maxiter=10000, callback=lambda xk: its.append(1))
+    assert info == 0 and abs(len(its) - r["iters"]) <= 1
+    xd = spla.spsolve(A.tocsc(), b)
+    assert np.linalg.norm(r["x"] - xd) <= 1e-8 * np.linalg.norm(xd)
+    Qd = (1.0 / N) ** 2 * xd.sum()
+    assert abs(r["Q"] - Qd) <= tol * np.linalg.norm(b) * np.linalg.norm(xd) * (1 + 1e-6)
+
+
+def test_minres_needs_no_more_steps_than_cg():
+    """For SPD A, MINRES minimises ||b - A x|| over the same Krylov space CG works in, so at a given
+    residual tolerance it stops no later than CG (one step of slack for rounding)."""
+    from oracle import core as oc
+    for seed, N in ((5, 8), (6, 16)):
+        a = _lognormal_triangles(N, seed)
+        r = mg.cg(N, a, 1e-8)
+        AB, _, b = oc.assemble(N, a)
+        _, m_iters, _, st = oc.minres_band(AB, b, 1e-8)
+        assert st == 0 and m_iters <= r["iters"] + 1
