@@ -88,6 +88,9 @@ typedef struct {
  *   Galerkin-exact coarse operators, red-black Gauss-Seidel), the same stopping rule ||r_k||/||b|| <=
  *   tol (r_k the CG recurrence residual) and the same records; iterations are CG steps.  u_* ignored.
  *   h >= 1/64: every grid on chip; h <= 1/128: one CTA per system over workspace scratch.
+ * solver = MLMC_SOLVER_CG (NEXT-4; h = 1/8 .. 1/64): plain conjugate gradients in binary64 from x0 = 0,
+ *   the other Krylov method the paper names for these SPD systems; stopping rule and records as
+ *   MG-PCG, default max_iter as MINRES, cost model as MINRES (iterations x n).  u_* ignored.
  * max_iter = 0 selects the default (MINRES: 16n+1000 -- loss of orthogonality
  * at coefficient contrasts ~1e7 takes well over n steps; IR: 50).
  * MINRES reports phibar_k/||b|| (the stopping quantity) as the residual and
@@ -95,7 +98,7 @@ typedef struct {
  * MLMC_FLAG_VERIFY it also carries x_k and reports ||b - A x_k||/||b||, with
  * bit-identical Q.                                                          */
 typedef enum { MLMC_FMT_E4M3 = 0, MLMC_FMT_F16 = 1, MLMC_FMT_F32 = 2, MLMC_FMT_F64 = 3 } mlmc_fmt;
-typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1, MLMC_SOLVER_MGCG = 2 } mlmc_solver;
+typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1, MLMC_SOLVER_MGCG = 2, MLMC_SOLVER_CG = 3 } mlmc_solver;
 
 #define MLMC_FLAG_VERIFY 1   /* MINRES: also keep x_k and report the true residual */
 #define MLMC_FLAG_ESCALATE 2 /* MINRES / CHOL_IR: a failed solve (max_iter, breakdown, limiting accuracy) is

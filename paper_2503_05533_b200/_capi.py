@@ -16,7 +16,7 @@ MLMC_OK, MLMC_EINVAL, MLMC_ESOLVER, MLMC_ELMAX, MLMC_ECUDA, MLMC_ENOMEM = 0, 2, 
 MLMC_MAX_LEVELS, MLMC_SUMS_LEN, MLMC_SAMPLE_LEN = 16, 12, 8
 FIELD_EXPCOV_KL, FIELD_PAPER_EQ20 = 0, 1
 FMT = {"q": 0, "h": 1, "s": 2, "d": 3}
-SOLVER_MINRES, SOLVER_CHOL_IR, SOLVER_MGCG = 0, 1, 2
+SOLVER_MINRES, SOLVER_CHOL_IR, SOLVER_MGCG, SOLVER_CG = 0, 1, 2, 3
 FLAG_VERIFY = 1
 FLAG_ESCALATE = 2
 

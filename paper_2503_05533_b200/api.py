@@ -28,7 +28,7 @@ def precision(solver: str = "minres", u_f: str = "s", u_s: str = "s", u: str = "
     """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad.
     verify=True (MINRES): also carry x_k and report the true residual; escalate=True (MINRES, IR): a failed solve
     is solved again by MG-PCG (status 4 when that converges)."""
-    s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR, "mgcg": K.SOLVER_MGCG}[solver]
+    s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR, "mgcg": K.SOLVER_MGCG, "cg": K.SOLVER_CG}[solver]
     flags = (K.FLAG_VERIFY if verify else 0) | (K.FLAG_ESCALATE if escalate else 0)
     return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter, flags)
 
@@ -215,7 +215,7 @@ class Context:
         if K.lib().mlmc_auto_choice(self.ctx, N, C.byref(p), C.byref(ms)) != K.MLMC_OK:
             return None
         fmt = "qhsd"
-        name = {K.SOLVER_MINRES: "minres", K.SOLVER_CHOL_IR: "chol_ir", K.SOLVER_MGCG: "mgcg"}[p.solver]
+        name = {K.SOLVER_MINRES: "minres", K.SOLVER_CHOL_IR: "chol_ir", K.SOLVER_MGCG: "mgcg", K.SOLVER_CG: "cg"}[p.solver]
         quad = "".join(fmt[v] for v in (p.u_f, p.u_s, p.u, p.u_r)) if p.solver == K.SOLVER_CHOL_IR else None
         return {"solver": name, "quad": quad, "ms_per_sample": ms.value}
 

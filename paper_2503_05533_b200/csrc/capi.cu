@@ -260,6 +260,10 @@ int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
         if (!mgcg_supported(N)) return fail(ctx, MLMC_EINVAL, "MG-PCG kernel not built for N=" + std::to_string(N));
         return MLMC_OK;
     }
+    if (p->solver == MLMC_SOLVER_CG) {
+        if (!cg_supported(N)) return fail(ctx, MLMC_EINVAL, "CG kernel not built for N=" + std::to_string(N));
+        return MLMC_OK;
+    }
     if (p->solver == MLMC_SOLVER_CHOL_IR) {
         if (p->u != p->u_r || (p->u != MLMC_FMT_F64 && p->u != MLMC_FMT_F32 && p->u != MLMC_FMT_F16))
             return fail(ctx, MLMC_EINVAL, "IR supports u = u_r in binary64, binary32 or binary16");
@@ -275,7 +279,7 @@ double fmt_bits(int f) { return f == MLMC_FMT_F16 ? 16 : f == MLMC_FMT_F32 ? 32 
 // cost model R5: fixed + per-iteration work of one solve on mesh N
 void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
     double n = (double)(N - 1) * (N - 1), bw = N - 1;
-    if (p->solver == MLMC_SOLVER_MINRES) { fixed = 0.0; step = n; }
+    if (p->solver == MLMC_SOLVER_MINRES || p->solver == MLMC_SOLVER_CG) { fixed = 0.0; step = n; }
     else if (p->solver == MLMC_SOLVER_MGCG) { fixed = 8.0 * n; step = 8.0 * n; }   // ~ a V-cycle + matvec per step
     else { fixed = n * bw * bw * fmt_bits(p->u_f) / 64.0; step = 4.0 * n * bw; }
 }
@@ -326,6 +330,10 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
                        [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, keys ? order : nullptr, ex.st); }));
 
+    } else if (p->solver == MLMC_SOLVER_CG) {
+        int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;
+        CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
+                   [&] { return launch_cg(N, a, nb, tol, mi, rec, slot, ctr, nullptr, ex.st); }));
     } else if (p->solver == MLMC_SOLVER_MGCG) {
         int mi = p->max_iter > 0 ? p->max_iter : 1000;
         CU(counted(ctx, ex.st, MLMC_K_MINRES, N,

@@ -90,6 +90,10 @@ int mgcg_ctas_per_sm(int N);   // resident systems per SM of the streamed-mesh M
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                         unsigned* job_counter, const int* order, void* scratch, int nctas, cudaStream_t s,
                         const int* nb_dev = nullptr, int ok_status = 0);
+// Plain CG (NEXT-4): the on-chip MG-PCG kernel without its preconditioner (z = r), N = 8 .. 64.
+bool cg_supported(int N);
+cudaError_t launch_cg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                      unsigned* ctr, const int* order, cudaStream_t s);
 // K4: banded Cholesky in u_f + Algorithm 1 refinement.  The factors go to a global scratch of
 // chol_scratch_bytes(N, u_f, u_s, nb) bytes for a launch over nb systems (one factor per resident
 // warp segment; a smaller scratch shrinks the grid; 0 = unsupported).

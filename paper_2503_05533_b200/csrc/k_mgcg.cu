@@ -317,7 +317,8 @@ __device__ __forceinline__ void mg_setup(const double* __restrict__ a, double* c
     }
 }
 
-template <int N, int T, int GROUPS>
+// PC = false: plain CG (NEXT-4) -- z = r, no V-cycle; everything else identical
+template <int N, int T, int GROUPS, bool PC = true>
 __global__ void __launch_bounds__(MgCfg<N, T, GROUPS>::BLOCK)
 mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
             unsigned* __restrict__ job_counter, const int* __restrict__ order, const int* __restrict__ nb_dev,
@@ -366,16 +367,18 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             r[k] = live(k) ? h2 : 0.0;
-            if (live(k)) L0.f[cidx(k)] = (float)h2;
+            if (PC && live(k)) L0.f[cidx(k)] = (float)h2;
             rr = fma(r[k], r[k], rr);
         }
-        gsync<T, GROUPS>(g);
-        vcycle();
+        if constexpr (PC) {
+            gsync<T, GROUPS>(g);
+            vcycle();
+        }
         double rz = 0.0;
 #pragma unroll
         for (int k = 0; k < PER; ++k)
             if (live(k)) {
-                const double z = (double)L0.u[cidx(k)];
+                const double z = PC ? (double)L0.u[cidx(k)] : r[k];
                 pg[cidx(k)] = z;
                 rz = fma(r[k], z, rz);
             }
@@ -413,17 +416,19 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 r[k] = fma(-alpha, q[k], r[k]);
-                if (live(k)) L0.f[cidx(k)] = (float)r[k];
+                if (PC && live(k)) L0.f[cidx(k)] = (float)r[k];
                 rr = fma(r[k], r[k], rr);
             }
             ++it;
-            gsync<T, GROUPS>(g);
-            vcycle();
+            if constexpr (PC) {
+                gsync<T, GROUPS>(g);
+                vcycle();
+            }
             double rz_new = 0.0;
             double zk[PER];
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
-                zk[k] = live(k) ? (double)L0.u[cidx(k)] : 0.0;
+                zk[k] = live(k) ? (PC ? (double)L0.u[cidx(k)] : r[k]) : 0.0;
                 rz_new = fma(r[k], zk[k], rz_new);
             }
             S = gsum2<T, GROUPS>(rz_new, rr, red, tg, g);
@@ -1019,11 +1024,11 @@ bool use_mg_plain() {
     return v == 1;
 }
 
-template <int N, int T, int GROUPS>
+template <int N, int T, int GROUPS, bool PC = true>
 cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
                    const int* order, cudaStream_t s, const int* nb_dev, int ok_status) {
     using K = MgCfg<N, T, GROUPS>;
-    auto kern = mgcg_kernel<N, T, GROUPS>;
+    auto kern = mgcg_kernel<N, T, GROUPS, PC>;
     static const KernelOcc occ = kernel_occ(kern, K::BLOCK, K::SMEM);
     if (occ.err != cudaSuccess) return occ.err;
     const uint64_t grid = std::min<uint64_t>((nb + GROUPS - 1) / GROUPS, (uint64_t)occ.per_sm * occ.sms);
@@ -1078,6 +1083,19 @@ cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max
         case 512:
             return plain ? run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
                          : run_mg_tile<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+bool cg_supported(int N) { return N == 8 || N == 16 || N == 32 || N == 64; }
+
+cudaError_t launch_cg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                      unsigned* ctr, const int* order, cudaStream_t s) {
+    switch (N) {
+        case 8: return run_mg<8, 32, 4, false>(a, nb, tol, max_iter, out, slot, ctr, order, s, nullptr, 0);
+        case 16: return run_mg<16, 32, 4, false>(a, nb, tol, max_iter, out, slot, ctr, order, s, nullptr, 0);
+        case 32: return run_mg<32, 128, 1, false>(a, nb, tol, max_iter, out, slot, ctr, order, s, nullptr, 0);
+        case 64: return run_mg<64, 256, 1, false>(a, nb, tol, max_iter, out, slot, ctr, order, s, nullptr, 0);
         default: return cudaErrorNotSupported;
     }
 }

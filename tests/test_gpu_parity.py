@@ -848,3 +848,29 @@ def test_adaptive_sums_exact_and_rank_independent():
         var = max(0.0, math.fsum((y * y).tolist()) / n - mean * mean)
         assert g["var"][l] == var, (l, g["var"][l], var)
     ctx.close()
+
+
+@pytest.mark.parametrize("level", [0, 1, 2, 3])
+def test_cg_tracks_oracle_cg_and_minres(level):
+    """Plain CG (MLMC_SOLVER_CG) against the oracle's textbook CG on the same fields: QoIs within the
+    residual bound of each other, step counts within 2% + 2 (finite-precision CG amplifies rounding
+    differences), and -- MINRES minimising the residual over the same Krylov space -- MINRES on the same
+    samples stops no later than CG (+1), with CG at most 1.5x MINRES on average ("similar")."""
+    from oracle import mg as omg
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    tol, n = 1e-8, 8
+    r = ctx.sample_level(level, n, seed=19, prec_fine=precision("cg"), prec_coarse=precision("cg"),
+                         tol_fine=tol, tol_coarse=tol, per_sample=True).per_sample
+    m = ctx.sample_level(level, n, seed=19, prec_fine=precision("minres"), prec_coarse=precision("minres"),
+                         tol_fine=tol, tol_coarse=tol, per_sample=True).per_sample
+    Nf = 8 << level
+    outs = _pmap(lambda k: omg.cg(Nf, P.field_triangles(Nf, oc.normals(19, level, k, cfg["m"])), tol), range(n))
+    for k, o in enumerate(outs):
+        assert r[k, 6] == 0 and o["status"] == 0
+        assert abs(int(r[k, 2]) - o["iters"]) <= 0.02 * o["iters"] + 2, (level, k, r[k, 2], o["iters"])
+        assert abs(r[k, 0] - o["Q"]) <= 2 * 1.5 * tol * o["Q"], (level, k)
+        assert m[k, 2] <= r[k, 2] + 1, (level, k, m[k, 2], r[k, 2])
+    assert r[:, 2].mean() <= 1.5 * m[:, 2].mean()
+    ctx.close()
