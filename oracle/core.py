@@ -72,6 +72,7 @@ def lib():
             L.or_round.argtypes = [C.c_double, C.c_int]
             L.or_round.restype = C.c_double
             L.or_chol_band_rounded.argtypes = [C.c_int, C.c_int, dp, dp, C.c_int]
+            L.or_band_solve_rounded.argtypes = [C.c_int, C.c_int, dp, dp, dp, C.c_int]
             L.or_ir_band.argtypes = [C.c_int, C.c_int, dp, dp, ip, C.c_double, C.c_int, dp,
                                      C.POINTER(C.c_int), C.POINTER(C.c_double)]
             L.or_solve_level_mesh.argtypes = [C.POINTER(Problem), C.c_int, dp, C.c_int, ip,
@@ -225,6 +226,23 @@ def minres_band(AB, b, tol: float, max_iter: int = 100000):
 
 def round_to(x: float, fmt: str) -> float:
     return lib().or_round(float(x), FMT[fmt])
+
+
+def chol_band_rounded(AB, fmt: str):
+    """Algorithm 1 step 1: the band factor with every operation rounded to ``fmt``."""
+    n, bwp1 = AB.shape
+    L = np.zeros(n * bwp1, np.float64)
+    st = lib().or_chol_band_rounded(n, bwp1 - 1, np.ascontiguousarray(AB).ravel(), L, FMT[fmt])
+    return L.reshape(n, bwp1), st
+
+
+def band_solve_rounded(L, rhs, fmt: str):
+    """Algorithm 1 steps 2 / 7: forward + backward substitution rounded to ``fmt``."""
+    n, bwp1 = L.shape
+    x = np.zeros(n, np.float64)
+    lib().or_band_solve_rounded(n, bwp1 - 1, np.ascontiguousarray(L).ravel(),
+                                np.ascontiguousarray(rhs, np.float64), x, FMT[fmt])
+    return x
 
 
 def ir_band(AB, b, quad: str, tol: float, i_max: int = 50):

@@ -543,6 +543,12 @@ static void band_solve_rounded(int n, int bw, const double* L, const double* rhs
     free(y);
 }
 
+/* Exported for the Algorithm 1 emulation pins (tests/test_oracle_alg1_minres.py); the
+ * arithmetic is band_solve_rounded's, unchanged. */
+OR_EXPORT void or_band_solve_rounded(int n, int bw, const double* L, const double* rhs, double* x, int fs) {
+    band_solve_rounded(n, bw, L, rhs, x, fs);
+}
+
 OR_EXPORT int or_chol_band_rounded(int n, int bw, const double* AB, double* L, int ff) {
     for (int j = 0; j < n; ++j) {
         for (int i = j; i < n && i <= j + bw; ++i) {
