@@ -33,8 +33,28 @@ import workloads as W  # noqa: E402
 
 METRIC = "coupled level samples/sec per level and time-to-eps at 1/2/4/8 B200; HBM GB/s vs peak"
 UNIT = "coupled samples/s"
-FLOPS_PER_NODE_ITER = 25.0       # algorithmic fp64 flops of one MINRES iteration per unknown
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+# algorithmic fp64 flops of one MINRES iteration per unknown: SURVEY section 8(d)'s count (5-point matvec 13,
+# two dots 4, Lanczos / w / x updates 11); the kernel's own one-reduction form needs 25
+FLOPS_PER_NODE_ITER = 28.0
+
+
+def _measured_alu_peaks() -> dict:
+    """ALU peaks measured on this pool by tools/peak_alu.cu (profiles/r02_peaks.json, committed with its clock
+    record); MEASURED_PEAKS.json has no FP64/FP32 entries.  Fallback only if the file is missing: the guide's unit
+    counts (148 SMs x 64 FP64 / 128 FP32 FMA per clock x 2 x 1.965 GHz)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_peaks.json")))
+        return {"fp64": float(d["fp64_fma_tflops"]), "fp32": float(d["fp32_fma_tflops"]),
+                "source": "measured: DFMA / FFMA microbenchmark tools/peak_alu.cu at "
+                          f"{d['clocks']['sm_mhz']:.0f} MHz (profiles/r02_peaks.json)"}
+    except Exception:
+        return {"fp64": 148 * 64 * 2 * 1.965e9 / 1e12, "fp32": 148 * 128 * 2 * 1.965e9 / 1e12,
+                "source": "derived (profiles/r02_peaks.json missing): unit counts x 1.965 GHz"}
+
+
+ALU = _measured_alu_peaks()
+FP64_PEAK_TFLOPS = ALU["fp64"]
+FP32_PEAK_TFLOPS = ALU["fp32"]
 
 
 def _measured_hbm_gbs() -> float:
@@ -46,8 +66,6 @@ def _measured_hbm_gbs() -> float:
 
 
 HBM_PEAK_GBS = _measured_hbm_gbs()
-CPU_SAMPLE = {0: 2048, 1: 384, 2: 96, 3: 24}       # cpu_baseline: bounded oracle sample per level
-REF_SAMPLE = {0: 256, 1: 64, 2: 16, 3: 8}          # --impl reference: per-step oracle sample per level
 
 
 def _dbg(msg):
@@ -134,30 +152,69 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_rate(sample: dict, seed: int, threads: int) -> dict:
-    """Run the oracle's MINRES path (same algorithm, same tolerances) on `sample[l]`
-    coupled samples per level; returns per-level rates and the C2-mix rate."""
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ref_counts(div: int) -> dict:
+    """A bounded sample of the configs[1] step with the same level mix: N_l / div samples per level (>= 1)."""
+    return {l: max(1, n // div) for l, n in enumerate(W.CONFIGS["C2"]["N"])}
+
+
+def oracle_step(counts: dict, seed: int, threads: int, first: int = 10_000_000) -> float:
+    """Wall seconds for the oracle (oracle/oracle.c: KL field, element-by-element assembly, textbook MINRES to the
+    same tolerances, coarse half at tol_{l-1}) on counts[l] coupled samples of each configs[1] level, all levels'
+    samples in one pool of `threads` host threads, longest (finest) first."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import core as oc
     cfg = W.CONFIGS["C2"]
     P = oc.OracleProblem(0, cfg["m"], cfg["sigma2"], cfg["corr_len"], 2.0, cfg["h0_inv"])
     tols = cfg["tols"]
-    rates = {}
-    cpu_s = 0.0
-    with ThreadPoolExecutor(threads) as ex:
-        for l, s in sample.items():
-            tf, tc = tols[l], (tols[l - 1] if l else tols[0])
-            t0 = time.perf_counter()
-            c0 = time.process_time()
-            list(ex.map(lambda k: P.coupled_sample(l, seed, 10_000_000 + k, solver=oc.SOLVER_MINRES, tol_f=tf,
-                                                   tol_c=tc), range(s)))
-            cpu_s += time.process_time() - c0
-            rates[l] = s / (time.perf_counter() - t0)
-    step_s = sum(cfg["N"][l] / rates[l] for l in rates)
-    return {"rates": rates, "value": sum(cfg["N"]) / step_s, "cpu_seconds": cpu_s}
+    tasks = [(l, first + k) for l in sorted(counts, reverse=True) for k in range(counts[l])]
+
+    def one(t):
+        l, k = t
+        return P.coupled_sample(l, seed, k, solver=oc.SOLVER_MINRES, tol_f=tols[l], tol_c=tols[l - 1] if l else tols[0])
+    t0 = time.perf_counter()
+    if threads == 1:
+        for t in tasks:
+            one(t)
+    else:
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, tasks))
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(seed: int) -> dict:
+    """The oracle as it stands on this box's host cores (rank 0, N = 1): all cores on 1/20 of the configs[1] step
+    and one core on 1/100 of it (same level mix), coupled samples per second."""
+    from oracle import core as oc
+    oc.build()
+    threads = os.cpu_count() or 1
+    c_all, c_one = ref_counts(20), ref_counts(100)
+    t_all = oracle_step(c_all, seed, threads)
+    t_one = oracle_step(c_one, seed, 1, first=20_000_000)
+    n_all, n_one = sum(c_all.values()), sum(c_one.values())
+    return {"value": n_all / t_all, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{'/'.join(str(c_all[l]) for l in sorted(c_all))} coupled samples of levels 0..3 "
+                      "(1/20 of the configs[1] step, same mix) through the oracle's KL field, element-by-element "
+                      "assembly and textbook MINRES at the same tolerances, on all host threads",
+            "seconds": t_all,
+            "single_thread": {"value": n_one / t_one, "seconds": t_one,
+                              "sample": f"{'/'.join(str(c_one[l]) for l in sorted(c_one))} (1/100 of the step)"},
+            "cpu_model": _cpu_model()}
 
 
 def run_reference(args):
+    """--impl reference: the CPU oracle, as it stands, on this box's host cores; rank 0 only.  A step is a bounded
+    sample of the configs[1] step (1/20 of each level's count, same level mix), wall-timed; value = coupled samples
+    per second over the K timed steps.  Same metric, unit and config as our arm."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
@@ -166,23 +223,35 @@ def run_reference(args):
     oc.build()
     threads = os.cpu_count() or 1
     cfg = W.CONFIGS["C2"]
-    for _ in range(args.warmup):
-        oracle_rate({0: 16, 1: 4, 2: 2, 3: 1}, cfg["seed"], threads)
-    t0 = time.perf_counter()
-    vals = [oracle_rate(REF_SAMPLE, cfg["seed"], threads)["value"] for _ in range(args.steps)]
-    wall = time.perf_counter() - t0
-    value = sum(vals) / len(vals)
-    sample = "per step: " + ", ".join(f"{REF_SAMPLE[l]} level-{l} samples" for l in REF_SAMPLE) + \
-             " of configs[1], rate extrapolated to the (20000,5000,1200,300) mix"
+    counts = ref_counts(20)
+    per_step = sum(counts.values())
+    for i in range(args.warmup):
+        oracle_step(counts, cfg["seed"], threads, first=30_000_000 + i * per_step)
+    walls = [oracle_step(counts, cfg["seed"], threads, first=40_000_000 + i * per_step) for i in range(args.steps)]
+    wall = sum(walls)
+    value = per_step * args.steps / wall
+    sample = (f"per step: {'/'.join(str(counts[l]) for l in sorted(counts))} coupled samples of levels 0..3 "
+              "(1/20 of the configs[1] step, same level mix), wall-timed")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(cfg["N"]) / value,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] (C2): 4-level MLMC h=1/8..1/64, KL m=64, fixed N, MINRES tols "
-                                   "1e-4/1e-5/1e-6/1e-8", "engine": "CPU oracle (oracle/oracle.c), textbook MINRES"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "config": c2_config(world, "nccl"),
+            "engine": f"CPU oracle (oracle/oracle.c), textbook MINRES, {threads} host threads ({_cpu_model()})",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
+
+
+C2_CONFIG = {"workload": "configs[1] (C2): 4-level MLMC h=1/8..1/64, KL m=64 (var 1, corr 0.3), "
+                         "N=(20000,5000,1200,300) per GPU, fp64 MINRES tols 1e-4/1e-5/1e-6/1e-8",
+             "l2": "flushed between timed steps (256 MiB write)"}
+
+
+def c2_config(world: int, backend: str) -> dict:
+    return {**C2_CONFIG, "parallelism": f"samples sharded, {world} rank(s), "
+                                        f"{'NCCL' if backend == 'nccl' else backend} all-reduce of level sums"}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -330,7 +399,9 @@ def run_ours(args):
             traffic = None
     roofline = {"kernel": f"{top[0]} N={top[1]}", "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md section 6)",
+                "peak_source": ALU["source"],
+                "flops_basis": f"{FLOPS_PER_NODE_ITER:.0f} flops per unknown per MINRES iteration (SURVEY 8(d)) x "
+                               "unknowns x iterations of the kernel's launches",
                 "share_of_level_pass": top[3] / per_level_total_ms,
                 "timing": "library CUDA events around each launch during the per-level pass (levels one at a time)",
                 "launches": top[2], "ms_per_launch": ms_per_launch}
@@ -340,11 +411,7 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] (C2): 4-level MLMC h=1/8..1/64, KL m=64 (var 1, corr 0.3), "
-                                   "N=(20000,5000,1200,300) per GPU, fp64 MINRES tols 1e-4/1e-5/1e-6/1e-8",
-                       "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"samples sharded, {world} rank(s), "
-                                      f"{'NCCL' if backend == 'nccl' else backend} all-reduce of level sums"},
+            "config": c2_config(world, backend),
             "per_level": per_level, "roofline": roofline, "kernels": kernels, "gpu_launches": gpu_launches,
             "clocks": clk}
 
@@ -365,16 +432,7 @@ def run_ours(args):
         if rank == 0:
             line["paper_mpml_vs_mlmc"] = paper_leg(local)
         if rank == 0 and world == 1:
-            from oracle import core as oc
-            oc.build()
-            threads = os.cpu_count() or 1
-            r = oracle_rate(CPU_SAMPLE, seed, threads)
-            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "oracle",
-                                    "sample": ", ".join(f"{CPU_SAMPLE[l]} level-{l}" for l in CPU_SAMPLE) +
-                                              " coupled samples of configs[1] through the oracle's textbook MINRES "
-                                              "(same tolerances), rate extrapolated to the full step mix",
-                                    "cpu_seconds": r["cpu_seconds"],
-                                    "per_level_samples_per_s": r["rates"]}
+            line["cpu_baseline"] = cpu_baseline(seed)
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)

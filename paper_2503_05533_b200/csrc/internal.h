@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstddef>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -122,13 +123,33 @@ int copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host);
 void ctx_note_auto_choice(mlmc_ctx* ctx, int N, int cls, const mlmc_precision& p, double ms_per_sample);
 bool ctx_find_auto_choice(const mlmc_ctx* ctx, int N, int cls, mlmc_precision* p);
 
-// Launch limits of a kernel, computed once per template instance: callers keep them in a function-local
-// `static const KernelOcc` initialised by a lambda (C++11 guarantees that initialisation runs once, also
-// when several host threads drive their own contexts), so no thread can see a half-written pair.
+// Launch limits of a kernel.  cudaFuncSetAttribute (MaxDynamicSharedMemorySize) is per DEVICE, so the
+// limits are cached per device ordinal: each call site keeps a `static PerDevice<KernelOcc>` and asks it with
+// the launching device current; the first call on a device runs the initialiser under std::call_once, so
+// several host threads driving contexts on one or several GPUs never see a half-written entry
+// (a process-wide static skipped the attribute on a second device).
 struct KernelOcc {
     cudaError_t err = cudaSuccess;
     int per_sm = 0;   // resident blocks per SM
     int sms = 0;
+};
+constexpr int kMaxDevices = 64;
+template <class T>
+struct PerDevice {
+    T val[kMaxDevices];
+    std::once_flag once[kMaxDevices];
+    // the entry of the current device, initialised by init() on first use; dev_err set if no device
+    template <class Init>
+    const T& get(Init&& init, cudaError_t* dev_err = nullptr) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+            if (dev_err) *dev_err = e != cudaSuccess ? e : cudaErrorInvalidDevice;
+            dev = 0;
+        }
+        std::call_once(once[dev], [&] { val[dev] = init(); });
+        return val[dev];
+    }
 };
 template <class Kern>
 KernelOcc kernel_occ(Kern kern, int block, size_t smem) {
@@ -139,6 +160,14 @@ KernelOcc kernel_occ(Kern kern, int block, size_t smem) {
     if (o.err == cudaSuccess) o.err = cudaGetDevice(&dev);
     if (o.err == cudaSuccess) o.err = cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev);
     if (o.err == cudaSuccess && o.per_sm < 1) o.err = cudaErrorInvalidConfiguration;
+    return o;
+}
+// cached per device: `static PerDevice<KernelOcc> cache; const KernelOcc occ = occ_of(cache, kern, block, smem);`
+template <class Kern>
+KernelOcc occ_of(PerDevice<KernelOcc>& cache, Kern kern, int block, size_t smem) {
+    cudaError_t de = cudaSuccess;
+    KernelOcc o = cache.get([&] { return kernel_occ(kern, block, smem); }, &de);
+    if (de != cudaSuccess) o.err = de;
     return o;
 }
 

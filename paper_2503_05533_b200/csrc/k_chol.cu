@@ -136,6 +136,11 @@ template <typename S, typename F> __device__ __forceinline__ S to_s(F v) {
     else if constexpr (sizeof(S) == 4) return FT<F>::to_f(v);
     else return __float2half_rn(FT<F>::to_f(v));
 }
+// a substitution-precision value, exactly, in binary64 (d is rounded once, straight to u: Algorithm 1 step 8,
+// a binary32 detour dropped the bits of binary64 corrections)
+__device__ __forceinline__ double s_to_d(double v) { return v; }
+__device__ __forceinline__ double s_to_d(float v) { return (double)v; }
+__device__ __forceinline__ double s_to_d(__half v) { return (double)__half2float(v); }
 // -a * b + c in S with one rounding
 __device__ __forceinline__ float sfnma(float a, float b, float c) { return fmaf(-a, b, c); }
 __device__ __forceinline__ double sfnma(double a, double b, double c) { return fma(-a, b, c); }
@@ -680,11 +685,11 @@ chol_refine_kernel(const double* __restrict__ a_all, int nb, double tol, int i_m
             backward<G, F, S>(ring, v, l, leader);
             if (it < 0) {
 #pragma unroll 4
-                for (int q = 0; q < PER; ++q) xs[l + q * W] = VT<U>::from((double)(float)v[l + q * W]);
+                for (int q = 0; q < PER; ++q) xs[l + q * W] = VT<U>::from(s_to_d(v[l + q * W]));
             } else if (active) {                       // step 8: x += d in u (d rounded to u first)
 #pragma unroll 4
                 for (int q = 0; q < PER; ++q)
-                    xs[l + q * W] = VT<U>::add(xs[l + q * W], VT<U>::from((double)(float)v[l + q * W]));
+                    xs[l + q * W] = VT<U>::add(xs[l + q * W], VT<U>::from(s_to_d(v[l + q * W])));
             }
             if (it < 0 || active) ++it;
             __syncwarp(mask);
@@ -711,12 +716,15 @@ struct Launch {
     using KF = FacCfg<N, F, S>;
     using KR = RefCfg<N, F, S, NS, WPC>;
     static cudaError_t setup(int& grid_max) {
-        static const KernelOcc occ = [] {
+        static PerDevice<KernelOcc> cache;                 // the smem attributes are per device
+        cudaError_t de = cudaSuccess;
+        KernelOcc occ = cache.get([] {
             KernelOcc o;
             o.err = cudaFuncSetAttribute(chol_factor_kernel<N, F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          KF::SMEM);
             return o.err == cudaSuccess ? kernel_occ(chol_refine_kernel<N, F, S, NS, WPC, U>, 32 * WPC, KR::SMEM) : o;
-        }();
+        }, &de);
+        if (de != cudaSuccess) occ.err = de;
         if (occ.err != cudaSuccess) return occ.err;
         grid_max = occ.per_sm * occ.sms;
         return cudaSuccess;

@@ -990,13 +990,13 @@ cudaError_t run_mg_tile(const double* a, uint64_t nb, double tol, int max_iter, 
                         const int* order, void* scratch, int nctas, cudaStream_t s, const int* nb_dev, int ok_status) {
     using K = MgTl<N>;
     if (!scratch || nctas < 1) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(mgcg_tile_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)tl::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDevice<cudaError_t> attr;              // the attribute is per device
+    cudaError_t de = cudaSuccess;
+    const cudaError_t ae = attr.get([] {
+        return cudaFuncSetAttribute(mgcg_tile_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tl::SMEM);
+    }, &de);
+    if (de != cudaSuccess) return de;
+    if (ae != cudaSuccess) return ae;
     const uint64_t grid = std::min<uint64_t>(nb, (uint64_t)nctas);
     if (grid == 0) return cudaSuccess;
     CUtensorMap m64, m32;
@@ -1029,7 +1029,8 @@ cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, doubl
                    const int* order, cudaStream_t s, const int* nb_dev, int ok_status) {
     using K = MgCfg<N, T, GROUPS>;
     auto kern = mgcg_kernel<N, T, GROUPS, PC>;
-    static const KernelOcc occ = kernel_occ(kern, K::BLOCK, K::SMEM);
+    static PerDevice<KernelOcc> occ_cache;
+    const KernelOcc occ = occ_of(occ_cache, kern, K::BLOCK, K::SMEM);
     if (occ.err != cudaSuccess) return occ.err;
     const uint64_t grid = std::min<uint64_t>((nb + GROUPS - 1) / GROUPS, (uint64_t)occ.per_sm * occ.sms);
     if (grid == 0) return cudaSuccess;

@@ -359,7 +359,8 @@ static cudaError_t run_minres(const double* a, uint64_t nb, double tol, int max_
                               unsigned* ctr, cudaStream_t s) {
     using K = StripCfg<N, R, MINB, CS>;
     auto kern = minres_strip_kernel<N, R, MINB, VERIFY, PIPE, CS>;
-    static const KernelOcc occ = kernel_occ(kern, K::BLOCK, K::SMEM);
+    static PerDevice<KernelOcc> occ_cache;
+    const KernelOcc occ = occ_of(occ_cache, kern, K::BLOCK, K::SMEM);
     if (occ.err != cudaSuccess) return occ.err;
     uint64_t need = (nb + K::GROUPS - 1) / K::GROUPS;
     uint64_t grid = std::min<uint64_t>(need, (uint64_t)occ.per_sm * occ.sms);

@@ -382,29 +382,31 @@ template <int CS>
 cudaError_t run_stream(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                        unsigned* ctr, double* scratch, int nctas, const int* order, cudaStream_t s) {
     auto kern = minres_stream_kernel<CS>;
-    static int max_clusters = -1;
-    if (max_clusters < 0) {
+    // per device: the smem attribute is set per device and the cluster occupancy is queried there
+    static PerDevice<int> mc_cache;
+    cudaError_t de = cudaSuccess;
+    const int max_clusters = mc_cache.get([&]() -> int {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e != cudaSuccess) return e;
-        if (CS > 1) {
-            cudaLaunchConfig_t qc = {};
-            cudaLaunchAttribute qa[1];
-            qa[0].id = cudaLaunchAttributeClusterDimension;
-            qa[0].val.clusterDim.x = CS;
-            qa[0].val.clusterDim.y = 1;
-            qa[0].val.clusterDim.z = 1;
-            qc.gridDim = dim3(CS * 16);
-            qc.blockDim = dim3(ST);
-            qc.dynamicSmemBytes = SMEM;
-            qc.attrs = qa;
-            qc.numAttrs = 1;
-            e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &qc);
-            if (e != cudaSuccess) return e;
-            if (max_clusters < 1) { max_clusters = -1; return cudaErrorInvalidConfiguration; }
-        } else {
-            max_clusters = 1 << 30;
-        }
-    }
+        if (e != cudaSuccess) return -(int)e;
+        if (CS == 1) return 1 << 30;
+        cudaLaunchConfig_t qc = {};
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = CS;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.gridDim = dim3(CS * 16);
+        qc.blockDim = dim3(ST);
+        qc.dynamicSmemBytes = SMEM;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int mcl = 0;
+        e = cudaOccupancyMaxActiveClusters(&mcl, kern, &qc);
+        if (e != cudaSuccess) return -(int)e;
+        return mcl < 1 ? -(int)cudaErrorInvalidConfiguration : mcl;
+    }, &de);
+    if (de != cudaSuccess) return de;
+    if (max_clusters < 0) return (cudaError_t)(-max_clusters);
     const int systems = (int)std::min<uint64_t>(std::min<uint64_t>(nb, (uint64_t)nctas), (uint64_t)max_clusters);
     if (systems <= 0) return cudaSuccess;
     CUtensorMap map;

@@ -455,7 +455,8 @@ cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, dou
                      const int* order, cudaStream_t s) {
     using K = TileCfg<N, R, MINB, CM>;
     auto kern = minres_tile_kernel<N, R, MINB, CM, VERIFY>;
-    static const KernelOcc occ = kernel_occ(kern, K::BLOCK, K::SMEM);
+    static PerDevice<KernelOcc> occ_cache;
+    const KernelOcc occ = occ_of(occ_cache, kern, K::BLOCK, K::SMEM);
     if (occ.err != cudaSuccess) return occ.err;
     const uint64_t need = (nb + K::GROUPS - 1) / K::GROUPS;
     const uint64_t grid = std::min<uint64_t>(need, (uint64_t)occ.per_sm * occ.sms);

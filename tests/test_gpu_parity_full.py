@@ -1,0 +1,185 @@
+"""GPU parity at the sizes BASELINE.json configs[4] names, against the CPU oracle (-m gpu).
+VERDICT r01 "Missing #6": the streamed MINRES (K3c) and the tiled MG-PCG (K3m-t) at h = 1/256 and
+h = 1/512 against the oracle's binary64 banded Cholesky (O-exact); Algorithm 2 on configs[4] against the
+oracle's Algorithm 2 driven by oracle MINRES samples; the replicate-RMSE estimator pin with the reference
+computed by the oracle (every sample of the reference run's index sets solved by the oracle's direct fp64
+solver, "a direct, double precision linear solver").
+
+Tolerances: per-sample |Q_gpu - Q_exact| <= tol ||b|| ||x_exact|| (1 + 1e-6) + 1e-14 Q
+(w = b, A SPD -- rigorous); estimates: RMSE over replicate seeds <= eps (north star).
+"""
+import math
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import core as oc  # noqa: E402
+from oracle import mlmc as om  # noqa: E402
+from paper_2503_05533_b200 import Context, precision  # noqa: E402
+import workloads as W  # noqa: E402
+
+THREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _ctx(cfg, ws=8 << 30):
+    return Context(field=cfg["field"], m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                   q_decay=cfg.get("q_decay", 2.0), h0_inv=cfg["h0_inv"], L_max=cfg["L_max"], device=0,
+                   workspace_bytes=ws)
+
+
+def _oracle(cfg):
+    return oc.OracleProblem(cfg["field_code"], cfg["m"], cfg["sigma2"], cfg["corr_len"], cfg.get("q_decay", 2.0),
+                            cfg["h0_inv"])
+
+
+def _exact(P, N, xi):
+    a = P.field_triangles(N, xi)
+    AB, _, b = oc.assemble(N, a)
+    x, _ = oc.chol_band_solve(AB, b)
+    return (1.0 / N) ** 2 * x.sum(), np.linalg.norm(b), np.linalg.norm(x)
+
+
+def _pmap(f, xs, threads=THREADS):
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(f, xs))
+
+
+def _check_bound(ps, k, ex, tol_f, tol_c, tag):
+    (qf, bf, xf), (qc, bc, xc) = ex
+    assert abs(ps[k, 0] - qf) <= tol_f * bf * xf * (1 + 1e-6) + 1e-14 * qf, (tag, k, ps[k, 0], qf)
+    assert abs(ps[k, 1] - qc) <= tol_c * bc * xc * (1 + 1e-6) + 1e-14 * qc, (tag, k, ps[k, 1], qc)
+
+
+# ============================================================================ h = 1/256: K3c and K3m-t
+def test_fine_mesh_h256_minres_and_mgpcg_vs_oracle_direct():
+    """configs[4] level 5 (h = 1/256 fine, 1/128 coarse): the streamed MINRES (K3c, 2-CTA clusters) and
+    the tiled MG-PCG (K3m-t) per sample against the oracle's binary64 banded Cholesky, at a tight and a
+    loose tolerance; at 1e-10 both agree with the exact Q to 1e-9 relative."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    n, seed, level = 3, 31, 5
+    exs = _pmap(lambda k: (_exact(P, 256, oc.normals(seed, level, k, cfg["m"])),
+                           _exact(P, 128, oc.normals(seed, level, k, cfg["m"]))), list(range(n)))
+    for name in ("minres", "mgcg"):
+        for tol in (1e-10, 1e-6):
+            pr = precision(name)
+            r = ctx.sample_level(level, n, seed=seed, prec_fine=pr, prec_coarse=pr, tol_fine=tol, tol_coarse=tol,
+                                 per_sample=True)
+            ps = r.per_sample
+            assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0), (name, tol)
+            assert np.all(ps[:, 4] <= tol * 1.0001), (name, tol, ps[:, 4])
+            for k in range(n):
+                _check_bound(ps, k, exs[k], tol, tol, (name, tol))
+            if tol < 1e-9:
+                qf = np.array([e[0][0] for e in exs])
+                assert np.max(np.abs(ps[:, 0] / qf - 1)) < 1e-9, name
+    ctx.close()
+
+
+@pytest.mark.slow
+def test_finest_mesh_h512_minres_and_mgpcg_vs_oracle_direct():
+    """configs[4] level 6 (h = 1/512, n = 261121; the oracle's banded Cholesky takes ~1 min): one coupled
+    sample through K3c MINRES and K3m-t MG-PCG, each within the residual bound of the exact solve."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=12 << 30)
+    P = _oracle(cfg)
+    seed, level, k = 32, 6, 0
+    xi = oc.normals(seed, level, k, cfg["m"])
+    ex = _pmap(lambda N: _exact(P, N, xi), [512, 256], threads=2)
+    for name, tol in (("minres", 1e-9), ("mgcg", 1e-10)):
+        pr = precision(name)
+        r = ctx.sample_level(level, 1, seed=seed, first_index=k, prec_fine=pr, prec_coarse=pr, tol_fine=tol,
+                             tol_coarse=tol, per_sample=True)
+        ps = r.per_sample
+        assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0), name
+        _check_bound(ps, 0, ex, tol, tol, name)
+        assert abs(ps[0, 0] / ex[0][0] - 1) < 10 * tol, name
+    ctx.close()
+
+
+# ============================================================================ Algorithm 2 on configs[4]
+def test_adaptive_C5_matches_oracle_controller():
+    """configs[4] (m = 256, sigma^2 = 2, l = 0.1, eps = 2.5e-4, L_max = 6) through mlmc_adaptive_run vs the
+    oracle's Algorithm 2 (oracle/mlmc.py, step by step from P:357-379) driven by the oracle's textbook MINRES
+    on the same (seed, level, index) samples: same final L, N_l within a sample or two (a +-1 MINRES
+    iteration moves C_l), estimates within the per-sample solve bounds or 0.1 eps."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, ws=2 << 30)
+    seed = cfg["seed"]
+    g = ctx.adaptive_run(cfg["eps"], k_p=cfg["k_p"], N_init=100, seed=seed)
+    assert g["code"] == 0
+    P = _oracle(cfg)
+
+    def sampler(l, first, count, tf, tc):
+        outs = _pmap(lambda k: P.coupled_sample(l, seed, k, solver=oc.SOLVER_MINRES, tol_f=tf, tol_c=tc),
+                     range(first, first + count))
+        nf = ((cfg["h0_inv"] << l) - 1) ** 2
+        nc = ((cfg["h0_inv"] << (l - 1)) - 1) ** 2 if l else 0
+        assert all(o[6] == 0 and o[7] == 0 for o in outs)
+        return [o[0] - o[1] for o in outs], [o[2] * nf + o[3] * nc for o in outs]
+
+    o = om.adaptive_mpml(sampler, cfg["eps"], 1 / cfg["h0_inv"], cfg["k_p"], L_max=cfg["L_max"], N_init=100)
+    assert o.code == 0 and o.L == g["L"], (o.L, g["L"])
+    assert all(abs(a - b) <= max(2, 0.02 * b) for a, b in zip(o.N, g["N"])), (o.N, g["N"])
+    bound = sum(2 * 1.5 * 0.06 * (e + (g["eps"][l - 1] if l else 0.0)) for l, e in enumerate(g["eps"]))
+    if o.N == g["N"]:
+        assert abs(o.estimate - g["estimate"]) < bound, (o.estimate, g["estimate"])
+    else:
+        assert abs(o.estimate - g["estimate"]) < 0.1 * cfg["eps"], (o.estimate, g["estimate"])
+    # the controller's statistics agree level by level (same samples, different solvers within eps_l)
+    for l in range(g["L"] + 1):
+        assert abs(o.means[l] - g["mean"][l]) <= 0.1 * cfg["eps"]
+        assert abs(o.variances[l] / g["var"][l] - 1) < 0.05 or abs(o.variances[l] - g["var"][l]) < 1e-12
+    ctx.close()
+
+
+# ============================================================================ estimator pin, oracle reference
+def _oracle_reference(cfg, ref_seed, N):
+    """Q_ref = sum_l (1/N_l) sum_k Y_l(k), every Y_l(k) = Q_l - Q_{l-1} of sample (ref_seed, l, k) from the
+    oracle's binary64 banded Cholesky (O-exact) -- the index sets of the GPU's eps/5 run."""
+    P = _oracle(cfg)
+    tasks = [(l, k) for l in range(len(N) - 1, -1, -1) for k in range(N[l])]     # finest first
+
+    def one(t):
+        l, k = t
+        o = P.coupled_sample(l, ref_seed, k, solver=oc.SOLVER_DIRECT)
+        assert o[6] == 0 and o[7] == 0
+        return o[0] - o[1]
+    ys = _pmap(one, tasks)
+    return sum(math.fsum([y for (l2, _), y in zip(tasks, ys) if l2 == l]) / N[l] for l in range(len(N)))
+
+
+@pytest.mark.parametrize("name,R", [("C4", 50), ("C5", 30)])
+def test_replicate_rmse_within_eps_of_oracle_reference(name, R):
+    """North star: the MLMC estimate lies within eps RMSE of the fp64 oracle over repeated seeds.  Q_ref is
+    the oracle's exact-solve evaluation of the GPU eps/5 run's samples (so Q_ref's own RMSE is ~eps/5);
+    R replicate adaptive runs at eps (seeds 0..R-1): RMSE(Q_hat - Q_ref) <= eps."""
+    cfg = W.CONFIGS[name]
+    ctx = _ctx(cfg)
+    eps, ref_seed = cfg["eps"], 10 ** 6
+    ref = ctx.adaptive_run(eps / 5, k_p=cfg["k_p"], seed=ref_seed, on_fail=1)
+    t0 = time.perf_counter()
+    q_ref = _oracle_reference(cfg, ref_seed, ref["N"])
+    t_or = time.perf_counter() - t0
+    # the GPU eps/5 estimate and its oracle evaluation differ only by the eps_l-solve errors (<= 1.5 eps_l Q)
+    assert abs(q_ref - ref["estimate"]) < 0.2 * eps / 5, (q_ref, ref["estimate"])
+    est = np.array([ctx.adaptive_run(eps, k_p=cfg["k_p"], seed=r)["estimate"] for r in range(R)])
+    ctx.close()
+    rmse = float(np.sqrt(np.mean((est - q_ref) ** 2)))
+    print(f"{name}: Q_ref(oracle) {q_ref:.6f} (L={ref['L']}, N={ref['N']}, oracle {t_or:.0f} s), "
+          f"RMSE/eps {rmse / eps:.3f}")
+    assert rmse <= eps, (rmse, eps)
