@@ -315,6 +315,52 @@ int mlmc_adaptive_run_host(int h0_inv, int L_max, double eps, const mlmc_adaptiv
                            mlmc_level_sampler_fn sampler, void* sampler_user,
                            mlmc_allreduce_fn allreduce, void* user, mlmc_result* out);
 
+/* ---- K3d: MINRES of ONE sample over row slabs ----------
+ * The finest levels hold few samples (N_L ~ 100) and each
+ * is one serial MINRES chain, which sets the critical path of an
+ * adaptive run.  K3d solves ONE system -- sample (seed, level, index) on the
+ * mesh of `mesh_level` (level or level-1, i.e. the fine or the coarse half) --
+ * with the same method and stopping rule as mlmc_sample_level's MINRES (R9,
+ * R26, R27), its grid split into row slabs: rank r of `world` owns interior
+ * rows j0 <= j < j1 (an even split of 1..N-1, >= 2 rows each) and keeps rows
+ * j0-2 .. j1+1 of five binary64 planes in a caller-allocated device workspace.
+ * One MINRES step = mlmc_dd_pass, then the CALLER's exchange, then
+ * mlmc_dd_scalar:
+ *   - all-reduce (SUM, in place, identical result on every rank) of the 3
+ *     doubles at byte offset layout.sums_off of the workspace;
+ *   - halo rows: mlmc_dd_exchange_rows(layout, step) gives byte offsets of
+ *     [send to rank-1, receive from rank-1, send to rank+1, receive from
+ *     rank+1] (-1 = no neighbour), each `pitch` doubles; rank r's send to
+ *     rank r+1 is rank r+1's receive from rank r.
+ * With world = 1 nothing is exchanged and mlmc_dd_run_local runs the solve
+ * (chunks of 32 steps as one CUDA graph).  All launches are on the ctx's
+ * stream.  Errors: EINVAL (bad level / partition / tolerance), ENOMEM (work-
+ * space smaller than layout.bytes), ECUDA.                                     */
+typedef struct {
+    int32_t N, rank, world, j0, j1, rows, pitch, tiles;
+    uint64_t bytes;          /* device workspace bytes (caller allocates, owns) */
+    uint64_t plane_off[5];   /* Lanczos vectors P0, P1, P2 (rotating), cE, cN: rows x pitch doubles */
+    uint64_t sums_off;       /* 3 doubles: partial sums of the last pass (SUM-all-reduce in place) */
+    uint64_t state_off, partials_off, counter_off, xi_off, a_off;   /* internal */
+} mlmc_dd_layout;
+typedef struct mlmc_dd mlmc_dd;
+/* host only: the partition and workspace layout of rank/world on mesh N = 1/h (m KL terms) */
+int  mlmc_dd_layout_get(int N, int m, int rank, int world, mlmc_dd_layout* out);
+/* host only: the halo rows of the exchange that follows pass `step` (0, 1, ...) */
+int  mlmc_dd_exchange_rows(const mlmc_dd_layout* layout, int step, int64_t offs[4]);
+/* bind a slab solver to ctx (dev_ws: >= layout.bytes of device memory, borrowed until destroy) */
+int  mlmc_dd_create(mlmc_ctx* ctx, int mesh_level, int rank, int world, void* dev_ws, size_t bytes,
+                    mlmc_dd** out);
+/* field of sample (seed, level, index) on the slab's mesh, planes, state reset (async) */
+int  mlmc_dd_begin(mlmc_dd* dd, uint64_t seed, int level, uint64_t index, double tol, int max_iter);
+int  mlmc_dd_pass(mlmc_dd* dd);     /* one pass: p_{j+1}, t_{j+1}, partial sums (async; no-op when done) */
+int  mlmc_dd_scalar(mlmc_dd* dd);   /* Givens step + stopping test on the reduced sums (async) */
+/* synchronous: out = {Q (h^2 1^T x), MINRES iterations, phibar/||b||, status (0 ok, 1 max_iter,
+ * 3 non-finite), done (0/1)} -- Q valid once done */
+int  mlmc_dd_result(mlmc_dd* dd, double out[5]);
+int  mlmc_dd_run_local(mlmc_dd* dd, double out[5]);   /* world = 1: the whole solve, then mlmc_dd_result */
+void mlmc_dd_destroy(mlmc_dd* dd);
+
 /* ---- host-only helpers (no device needed; used by the controller) ---------- */
 /* Eq. (16): eps[l] = sqrt(k_p) h_l^2 for l < L, eps[L] = k_p h_L^2. */
 int mlmc_eps_schedule(int L, double h0, double k_p, double* eps_out);

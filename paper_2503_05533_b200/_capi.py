@@ -54,6 +54,13 @@ class Result(C.Structure):
                 ("cost", C.c_double * MLMC_MAX_LEVELS), ("solve_seconds", C.c_double)]
 
 
+class DDLayout(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("N", "rank", "world", "j0", "j1", "rows", "pitch", "tiles")] + \
+               [("bytes", C.c_uint64), ("plane_off", C.c_uint64 * 5), ("sums_off", C.c_uint64),
+                ("state_off", C.c_uint64), ("partials_off", C.c_uint64), ("counter_off", C.c_uint64),
+                ("xi_off", C.c_uint64), ("a_off", C.c_uint64)]
+
+
 class KernelStat(C.Structure):
     _fields_ = [("kind", C.c_int32), ("N", C.c_int32), ("launches", C.c_uint64), ("ms", C.c_double)]
 
@@ -120,6 +127,16 @@ def lib():
                                          ALLREDUCE_FN, vp, C.POINTER(Result)]
     L.mlmc_profile_enable.argtypes = [vp, C.c_int]
     L.mlmc_profile_read.argtypes = [vp, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)]
+    L.mlmc_dd_layout_get.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(DDLayout)]
+    L.mlmc_dd_exchange_rows.argtypes = [C.POINTER(DDLayout), C.c_int, C.POINTER(C.c_int64)]
+    L.mlmc_dd_create.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_size_t, C.POINTER(vp)]
+    L.mlmc_dd_begin.argtypes = [vp, C.c_uint64, C.c_int, C.c_uint64, C.c_double, C.c_int]
+    L.mlmc_dd_pass.argtypes = [vp]
+    L.mlmc_dd_scalar.argtypes = [vp]
+    L.mlmc_dd_result.argtypes = [vp, dp]
+    L.mlmc_dd_run_local.argtypes = [vp, dp]
+    L.mlmc_dd_destroy.argtypes = [vp]
+    L.mlmc_dd_destroy.restype = None
     _lib = L
     return L
 

@@ -12,10 +12,10 @@ BUILD = os.path.join(HERE, "_build")
 SO = os.path.join(HERE, "libmlmc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wno-attributes", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
 SOURCES = ["host_kl.cpp", "capi.cu", "controller.cpp", "k_field.cu", "k_minres.cu", "k_minres_tile.cu", "k_minres_gm.cu", "k_minres_stream.cu", "k_mgcg.cu", "k_chol.cu",
-           "k_reduce.cu"]
+           "k_reduce.cu", "k_dd.cu"]
 
 
 def _needs(obj: str, deps) -> bool:

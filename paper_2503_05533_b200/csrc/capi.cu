@@ -859,3 +859,183 @@ int mlmc_kl_modes(double sigma2, double corr_len, int m, int32_t* ik, int32_t* j
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- K3d: one sample over row slabs (NEXT-3)
+int mlmc_dd_layout_get(int N, int m, int rank, int world, mlmc_dd_layout* out) {
+    if (!out || N < 4 || world < 1 || rank < 0 || rank >= world || m < 1) return MLMC_EINVAL;
+    const int C = N - 1;
+    const int j0 = 1 + (int)((int64_t)rank * C / world), j1 = 1 + (int)((int64_t)(rank + 1) * C / world);
+    if (j1 - j0 < 2) return MLMC_EINVAL;                  // a slab sends its second row: >= 2 rows each
+    mlmc_dd_layout L{};
+    L.N = N; L.rank = rank; L.world = world; L.j0 = j0; L.j1 = j1;
+    L.rows = j1 - j0 + 4;                                 // rows j0-2 .. j1+1
+    L.pitch = N + 2;                                      // columns i = -1 .. N at i + 1
+    L.tiles = dd_tiles(N, j0, j1);
+    const size_t plane = align256(sizeof(double) * (size_t)L.rows * L.pitch);
+    size_t off = 0;
+    for (int q = 0; q < 5; ++q) { L.plane_off[q] = off; off += plane; }
+    L.sums_off = off;  off += align256(sizeof(double) * 4);
+    L.state_off = off; off += align256(sizeof(DDState));
+    L.partials_off = off; off += align256(sizeof(double) * 3 * (size_t)L.tiles);
+    L.counter_off = off; off += align256(sizeof(unsigned) * 4);
+    L.xi_off = off;    off += align256(sizeof(double) * (size_t)m);
+    L.a_off = off;     off += align256(sizeof(double) * 2 * (size_t)N * N);
+    L.bytes = off;
+    *out = L;
+    return MLMC_OK;
+}
+
+int mlmc_dd_exchange_rows(const mlmc_dd_layout* L, int step, int64_t offs[4]) {
+    if (!L || !offs || step < 0) return MLMC_EINVAL;
+    const uint64_t plane = L->plane_off[(step + 2) % 3];   // p_{j+1} formed by pass `step`
+    const uint64_t row = sizeof(double) * (uint64_t)L->pitch;
+    auto at = [&](int j) { return (int64_t)(plane + row * (uint64_t)(j - (L->j0 - 2))); };
+    const bool lo = L->rank > 0, hi = L->rank + 1 < L->world;
+    offs[0] = lo ? at(L->j0 + 1) : -1;   // send to rank-1: its ghost row j1' + 1 = j0 + 1
+    offs[1] = lo ? at(L->j0 - 2) : -1;   // receive rank-1's row j0 - 2
+    offs[2] = hi ? at(L->j1 - 2) : -1;   // send to rank+1: its ghost row j0' - 2 = j1 - 2
+    offs[3] = hi ? at(L->j1 + 1) : -1;   // receive rank+1's row j1 + 1
+    return MLMC_OK;
+}
+
+struct mlmc_dd {
+    mlmc_ctx* ctx = nullptr;
+    int mesh_level = 0;
+    mlmc_dd_layout L{};
+    unsigned char* ws = nullptr;
+    cudaGraphExec_t chunk = nullptr;      // mlmc_dd_run_local: kChunk steps (pass + scalar) as one graph
+};
+
+namespace {
+constexpr int kDDChunk = 32;
+int dd_check(mlmc_dd* dd) {
+    if (!dd || !dd->ctx || !dd->ws) return MLMC_EINVAL;
+    return cudaSetDevice(dd->ctx->device) == cudaSuccess ? MLMC_OK : fail(dd->ctx, MLMC_ECUDA, "cudaSetDevice");
+}
+cudaError_t dd_pass(mlmc_dd* dd, cudaStream_t s, bool fuse_scalar = false) {
+    const mlmc_dd_layout& L = dd->L;
+    return launch_dd_pass(L.N, L.j0, L.j1, L.rows, L.pitch, reinterpret_cast<double*>(dd->ws + L.plane_off[0]),
+                          (L.plane_off[1] - L.plane_off[0]) / sizeof(double),
+                          reinterpret_cast<DDState*>(dd->ws + L.state_off),
+                          reinterpret_cast<double*>(dd->ws + L.partials_off),
+                          reinterpret_cast<unsigned*>(dd->ws + L.counter_off),
+                          reinterpret_cast<double*>(dd->ws + L.sums_off), fuse_scalar, s);
+}
+cudaError_t dd_scalar(mlmc_dd* dd, cudaStream_t s) {
+    return launch_dd_scalar(reinterpret_cast<DDState*>(dd->ws + dd->L.state_off),
+                            reinterpret_cast<const double*>(dd->ws + dd->L.sums_off), dd->L.N, s);
+}
+}  // namespace
+
+int mlmc_dd_create(mlmc_ctx* ctx, int mesh_level, int rank, int world, void* dev_ws, size_t bytes, mlmc_dd** out) {
+    if (!ctx || !out) return MLMC_EINVAL;
+    if (mesh_level < 0 || mesh_level > ctx->pr.L_max) return fail(ctx, MLMC_EINVAL, "bad mesh level");
+    mlmc_dd_layout L{};
+    if (mlmc_dd_layout_get(level_N(ctx, mesh_level), ctx->pr.m, rank, world, &L) != MLMC_OK)
+        return fail(ctx, MLMC_EINVAL, "slab partition: world too large for the mesh (>= 2 rows per rank)");
+    if (!dev_ws || bytes < L.bytes) return fail(ctx, MLMC_ENOMEM, "dd workspace smaller than mlmc_dd_layout.bytes");
+    auto* dd = new mlmc_dd;
+    dd->ctx = ctx;
+    dd->mesh_level = mesh_level;
+    dd->L = L;
+    dd->ws = static_cast<unsigned char*>(dev_ws);
+    *out = dd;
+    return MLMC_OK;
+}
+
+int mlmc_dd_begin(mlmc_dd* dd, uint64_t seed, int level, uint64_t index, double tol, int max_iter) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dd->ctx;
+    if (!(level == dd->mesh_level || level == dd->mesh_level + 1) || level > ctx->pr.L_max)
+        return fail(ctx, MLMC_EINVAL, "mlmc_dd_begin: level must be mesh_level or mesh_level + 1");
+    if (!(tol > 0.0) || !std::isfinite(tol)) return fail(ctx, MLMC_EINVAL, "tolerance must be > 0");
+    rc = ensure_phi(ctx, dd->mesh_level);
+    if (rc) return rc;
+    const mlmc_dd_layout& L = dd->L;
+    const int n = (L.N - 1) * (L.N - 1);
+    if (max_iter <= 0) max_iter = 16 * n + 1000;           // the MINRES default cap
+    double* xi = reinterpret_cast<double*>(dd->ws + L.xi_off);
+    double* a = reinterpret_cast<double*>(dd->ws + L.a_off);
+    cudaStream_t s = ctx->stream;
+    CU(counted(ctx, s, 0, L.N, [&] { return launch_rng(xi, ctx->pr.m, 1, seed, level, index, s); }));
+    CU(counted(ctx, s, 1, L.N, [&] { return field(ctx, dd->mesh_level, xi, a, 1, nullptr, s); }));
+    CU(cudaMemsetAsync(dd->ws + L.counter_off, 0, sizeof(unsigned) * 4, s));
+    CU(counted(ctx, s, 2, L.N, [&] {
+        return launch_dd_init(a, L.N, L.j0, L.rows, L.pitch, reinterpret_cast<double*>(dd->ws + L.plane_off[0]),
+                              (L.plane_off[1] - L.plane_off[0]) / sizeof(double),
+                              reinterpret_cast<DDState*>(dd->ws + L.state_off), tol, max_iter, s);
+    }));
+    return MLMC_OK;
+}
+
+int mlmc_dd_pass(mlmc_dd* dd) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dd->ctx;
+    CU(counted(ctx, ctx->stream, 2, dd->L.N, [&] { return dd_pass(dd, ctx->stream); }));
+    return MLMC_OK;
+}
+
+int mlmc_dd_scalar(mlmc_dd* dd) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dd->ctx;
+    CU(counted(ctx, ctx->stream, 2, dd->L.N, [&] { return dd_scalar(dd, ctx->stream); }));
+    return MLMC_OK;
+}
+
+int mlmc_dd_result(mlmc_dd* dd, double out[5]) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    if (!out) return MLMC_EINVAL;
+    mlmc_ctx* ctx = dd->ctx;
+    DDState st{};
+    CU(cudaMemcpyAsync(&st, dd->ws + dd->L.state_off, sizeof(DDState), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    out[0] = st.done ? st.Q : 0.0;
+    out[1] = st.k;
+    out[2] = st.done ? st.relres : (st.beta1 > 0 ? st.phibar * st.inv_beta1 : 1.0);
+    out[3] = st.status;
+    out[4] = st.done;
+    return MLMC_OK;
+}
+
+int mlmc_dd_run_local(mlmc_dd* dd, double out[5]) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dd->ctx;
+    if (dd->L.world != 1) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_local needs world = 1 (no exchange)");
+    cudaStream_t s = ctx->stream;
+    if (!dd->chunk) {
+        // kDDChunk steps as one graph: every launch takes its step-dependent values from the device state
+        cudaStream_t cs = nullptr;
+        CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g = nullptr;
+        CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = cudaSuccess;
+        for (int k = 0; k < kDDChunk && e == cudaSuccess; ++k) e = dd_pass(dd, cs, true);   // scalar step fused
+        cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (e != cudaSuccess || e2 != cudaSuccess) return fail(ctx, MLMC_ECUDA, "dd graph capture failed");
+        CU(cudaGraphInstantiate(&dd->chunk, g, 0));
+        cudaGraphDestroy(g);
+    }
+    DDState* st_dev = reinterpret_cast<DDState*>(dd->ws + dd->L.state_off);
+    int done = 0;
+    const int max_chunks = (int)(((int64_t)16 * (dd->L.N - 1) * (dd->L.N - 1) + 1000) / kDDChunk + 2);
+    const int idx = stat_index(ctx, 2, dd->L.N);
+    for (int c = 0; c < max_chunks && !done; ++c) {
+        CU(cudaGraphLaunch(dd->chunk, s));
+        ctx->stats[idx].launches += kDDChunk;                // the graph's kernels
+        CU(cudaMemcpyAsync(&done, &st_dev->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    return mlmc_dd_result(dd, out);
+}
+
+void mlmc_dd_destroy(mlmc_dd* dd) {
+    if (!dd) return;
+    if (dd->chunk) cudaGraphExecDestroy(dd->chunk);
+    delete dd;
+}

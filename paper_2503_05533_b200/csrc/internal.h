@@ -171,6 +171,20 @@ KernelOcc occ_of(PerDevice<KernelOcc>& cache, Kern kern, int block, size_t smem)
     return o;
 }
 
+// K3d (k_dd.cu, NEXT-3): MINRES of one sample over row slabs; state of the scalar recurrences (device).
+struct DDState {
+    double tol, beta1, inv_beta1, tol_b, invb_prev, alpha_prev, sigma_prev, dbar, epsln, phibar, cs, sn, s1q, s2q,
+        Xq, ct, c1, c0, Q, relres;
+    int max_iter, k, step, status, done, pad;
+};
+int dd_tiles(int N, int j0, int j1);
+cudaError_t launch_dd_init(const double* a, int N, int j0, int rows, int pitch, double* planes, size_t plane_stride,
+                           DDState* st, double tol, int max_iter, cudaStream_t s);
+cudaError_t launch_dd_pass(int N, int j0, int j1, int rows, int pitch, double* planes, size_t plane_stride,
+                           DDState* st, double* partials, unsigned* counter, double* sums, bool fuse_scalar,
+                           cudaStream_t s);
+cudaError_t launch_dd_scalar(DDState* st, const double* sums, int N, cudaStream_t s);
+
 constexpr int kSumsLen = MLMC_SUMS_LEN;
 // Reproducible level sums: the five real-valued sums (Y, Y^2, Q_f, Q_c, cost) are also kept as
 // exact fixed-point integers -- each per-sample value rounded once to a multiple of 2^-kXScale, added as a

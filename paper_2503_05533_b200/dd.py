@@ -1,0 +1,136 @@
+"""K3d binding and host driver: MINRES of ONE sample over row slabs (include/mlmc.h "K3d"; SURVEY 8(f)
+NEXT-3).  Argument marshalling and the exchange schedule only -- every step of the solve runs in
+libmlmc.so (dd_pass_kernel, dd_scalar_kernel); torch.distributed carries the per-step all-reduce of three
+doubles and the one-row halo exchange with each neighbour (NCCL over NVLink on GPUs).
+
+    lay = layout(N, m, rank, world)          # host: partition + workspace layout (mlmc_dd_layout_get)
+    s = SlabSolver(ctx, mesh_level, rank, world); s.begin(seed, level, index, tol)
+    Q, iters, relres, status = dd_solve(s, group)          # world ranks, one slab each
+    Q, ... = s.run_local()                                  # world = 1: whole GPU on one system
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _capi as K
+
+
+def layout(N: int, m: int, rank: int, world: int) -> K.DDLayout:
+    lay = K.DDLayout()
+    K.check(K.lib().mlmc_dd_layout_get(N, m, rank, world, C.byref(lay)))
+    return lay
+
+
+def exchange_rows(lay: K.DDLayout, step: int) -> list:
+    """Byte offsets [send to rank-1, receive from rank-1, send to rank+1, receive from rank+1] (-1: none)."""
+    offs = (C.c_int64 * 4)()
+    K.check(K.lib().mlmc_dd_exchange_rows(C.byref(lay), step, offs))
+    return list(offs)
+
+
+class SlabSolver:
+    """One rank's slab of one system on the device (mlmc_dd_*); the workspace is a torch tensor."""
+
+    def __init__(self, ctx, mesh_level: int, rank: int = 0, world: int = 1):
+        import torch
+        self.ctx = ctx
+        N = ctx.h0_inv << mesh_level
+        self.lay = layout(N, ctx.m, rank, world)
+        self.rank, self.world = rank, world
+        self.ws = torch.zeros(int(self.lay.bytes), dtype=torch.uint8, device=ctx.device)
+        dd = C.c_void_p()
+        K.check(K.lib().mlmc_dd_create(ctx.ctx, mesh_level, rank, world, C.c_void_p(self.ws.data_ptr()),
+                                       C.c_size_t(self.ws.numel()), C.byref(dd)), ctx.ctx)
+        self.dd = dd
+        self.sums = self.ws[self.lay.sums_off:self.lay.sums_off + 24].view(torch.float64)
+
+    def row(self, off: int):
+        return self.ws[off:off + 8 * self.lay.pitch].view(self._dtype())
+
+    def _dtype(self):
+        import torch
+        return torch.float64
+
+    def begin(self, seed: int, level: int, index: int, tol: float, max_iter: int = 0):
+        K.check(K.lib().mlmc_dd_begin(self.dd, seed, level, index, tol, max_iter), self.ctx.ctx)
+
+    def pass_(self):
+        K.check(K.lib().mlmc_dd_pass(self.dd), self.ctx.ctx)
+
+    def scalar(self):
+        K.check(K.lib().mlmc_dd_scalar(self.dd), self.ctx.ctx)
+
+    def exchange_offsets(self, step: int) -> list:
+        return exchange_rows(self.lay, step)
+
+    def result(self) -> dict:
+        out = (C.c_double * 5)()
+        K.check(K.lib().mlmc_dd_result(self.dd, out), self.ctx.ctx)
+        return {"Q": out[0], "iters": int(out[1]), "relres": out[2], "status": int(out[3]), "done": bool(out[4])}
+
+    def done(self) -> bool:
+        return self.result()["done"]
+
+    def run_local(self) -> dict:
+        out = (C.c_double * 5)()
+        K.check(K.lib().mlmc_dd_run_local(self.dd, out), self.ctx.ctx)
+        return {"Q": out[0], "iters": int(out[1]), "relres": out[2], "status": int(out[3]), "done": bool(out[4])}
+
+    def close(self):
+        if getattr(self, "dd", None):
+            K.lib().mlmc_dd_destroy(self.dd)
+            self.dd = None
+
+    __del__ = close
+
+
+def dd_solve(engine, group=None, check_every: int = 32, max_steps: int = 10 ** 7) -> dict:
+    """One rank's side of a slab-decomposed solve: per MINRES step pass -> all-reduce(SUM) of the three
+    partial sums + one-row halo exchange with each neighbour -> scalar step.  Every rank decides `done` from
+    identical reduced sums at the same step, so all leave the loop together.  `engine` is a SlabSolver (or any
+    object with its interface: pass_, scalar, sums, row, exchange_offsets, result, rank, world)."""
+    import torch.distributed as dist
+    world, rank = engine.world, engine.rank
+    for step in range(max_steps):
+        engine.pass_()
+        if world > 1:
+            dist.all_reduce(engine.sums, group=group)
+            o = engine.exchange_offsets(step)
+            ops = []
+            if o[0] >= 0:
+                ops.append(dist.P2POp(dist.isend, engine.row(o[0]), rank - 1, group))
+                ops.append(dist.P2POp(dist.irecv, engine.row(o[1]), rank - 1, group))
+            if o[2] >= 0:
+                ops.append(dist.P2POp(dist.isend, engine.row(o[2]), rank + 1, group))
+                ops.append(dist.P2POp(dist.irecv, engine.row(o[3]), rank + 1, group))
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        engine.scalar()
+        if (step + 1) % check_every == 0 and engine.done():
+            break
+    return engine.result()
+
+
+def dd_solve_emulated(engines: list, check_every: int = 32, max_steps: int = 10 ** 7) -> dict:
+    """All ranks of one solve in one process (e.g. G slabs on one GPU): the all-reduce is the sum of the
+    ranks' partials in rank order, the halo rows are copied between the slabs' workspaces.  Same kernels and
+    exchange schedule as dd_solve; no launch waits on another (the host orders them)."""
+    G = len(engines)
+    for step in range(max_steps):
+        for e in engines:
+            e.pass_()
+        if G > 1:
+            tot = engines[0].sums.clone()
+            for e in engines[1:]:
+                tot += e.sums
+            for e in engines:
+                e.sums.copy_(tot)
+            offs = [e.exchange_offsets(step) for e in engines]
+            for g in range(G - 1):          # rank g <-> rank g+1
+                engines[g + 1].row(offs[g + 1][1]).copy_(engines[g].row(offs[g][2]))
+                engines[g].row(offs[g][3]).copy_(engines[g + 1].row(offs[g + 1][0]))
+        for e in engines:
+            e.scalar()
+        if (step + 1) % check_every == 0 and engines[0].done():
+            break
+    return [e.result() for e in engines]

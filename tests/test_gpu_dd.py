@@ -1,0 +1,107 @@
+"""K3d (NEXT-3, domain-decomposed MINRES of one sample) on the GPU (-m gpu).
+
+One B200 runs every rank: G slabs of one system in one process (paper_2503_05533_b200.dd.dd_solve_emulated:
+the all-reduce is the rank-order sum of the slabs' partials, the halo rows are device copies between the
+slab workspaces; launches never wait on one another).  The kernels, layouts and exchange schedule are the
+multi-GPU ones (dd_solve over NCCL differs only in who moves the rows).
+
+Checks against the oracle (configs[4] field): Q within the per-sample residual bound of the binary64 direct
+solve; G = 1 / 2 / 3 / 4 agree with each other to rounding and with the streamed MINRES (K3c) of the same
+sample within both solves' bounds; iteration counts within 1% of K3c's; max_iter exhaustion is reported.
+"""
+import time
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import core as oc  # noqa: E402
+from paper_2503_05533_b200 import Context, precision  # noqa: E402
+from paper_2503_05533_b200.dd import SlabSolver, dd_solve_emulated, layout  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _ctx(ws=4 << 30):
+    cfg = W.CONFIGS["C5"]
+    return cfg, Context(field=cfg["field"], m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                        h0_inv=cfg["h0_inv"], L_max=cfg["L_max"], device=0, workspace_bytes=ws)
+
+
+def _exact(cfg, N, seed, level, k):
+    P = oc.OracleProblem(0, cfg["m"], cfg["sigma2"], cfg["corr_len"], 2.0, cfg["h0_inv"])
+    a = P.field_triangles(N, oc.normals(seed, level, k, cfg["m"]))
+    AB, _, b = oc.assemble(N, a)
+    x, _ = oc.chol_band_solve(AB, b)
+    return x.sum() / N ** 2, np.linalg.norm(b), np.linalg.norm(x)
+
+
+def _solve(ctx, mesh_level, G, seed, level, k, tol, max_iter=0):
+    engines = [SlabSolver(ctx, mesh_level, g, G) for g in range(G)]
+    for e in engines:
+        e.begin(seed, level, k, tol, max_iter)
+    if G == 1:
+        res = [engines[0].run_local()]
+    else:
+        res = dd_solve_emulated(engines)
+    for e in engines:
+        e.close()
+    return res
+
+
+def test_dd_h256_matches_oracle_and_k3c():
+    """h = 1/256 (configs[4] level 5, fine half): G = 1, 2, 3 slabs vs the oracle's direct solve and K3c."""
+    cfg, ctx = _ctx()
+    seed, level, k, tol = 41, 5, 2, 1e-10
+    q, bn, xn = _exact(cfg, 256, seed, level, k)
+    ref = ctx.sample_level(level, 1, seed=seed, first_index=k, prec_fine=precision("minres"), tol_fine=tol,
+                           tol_coarse=tol, per_sample=True).per_sample[0]
+    out = {}
+    for G in (1, 2, 3):
+        res = _solve(ctx, level, G, seed, level, k, tol)
+        assert all(r == res[0] for r in res)                     # every rank holds the same result
+        r = res[0]
+        assert r["done"] and r["status"] == 0 and r["relres"] <= tol
+        assert abs(r["Q"] - q) <= tol * bn * xn * (1 + 1e-6) + 1e-14 * q, (G, r["Q"], q)
+        assert abs(r["iters"] - ref[2]) <= max(2, 0.01 * ref[2]), (G, r["iters"], ref[2])
+        out[G] = r
+    for G in (2, 3):
+        assert abs(out[G]["Q"] / out[1]["Q"] - 1) < 1e-11
+    # the coarse half of the same coupled sample (mesh level 4 of level 5)
+    qc, bc, xc = _exact(cfg, 128, seed, level, k)
+    rc = _solve(ctx, level - 1, 2, seed, level, k, tol)[0]
+    assert abs(rc["Q"] - qc) <= tol * bc * xc * (1 + 1e-6) + 1e-14 * qc
+    ctx.close()
+
+
+def test_dd_h512_single_system_and_slabs():
+    """h = 1/512 (configs[4] level 6): one system on the whole GPU (G = 1) and as 4 slabs, against K3c's
+    2-CTA-cluster solve of the same sample: both within tol ||b|| ||x|| <= 1.5 tol Q of the exact Q."""
+    cfg, ctx = _ctx(ws=8 << 30)
+    seed, level, k, tol = 42, 6, 0, 1e-8
+    ref = ctx.sample_level(level, 1, seed=seed, first_index=k, prec_fine=precision("minres"), tol_fine=tol,
+                           tol_coarse=tol, per_sample=True).per_sample[0]
+    for G in (1, 4):
+        r = _solve(ctx, level, G, seed, level, k, tol)[0]
+        assert r["status"] == 0 and r["relres"] <= tol
+        assert abs(r["Q"] - ref[0]) <= 2 * 1.5 * tol * abs(ref[0]), (G, r["Q"], ref[0])
+        assert abs(r["iters"] - ref[2]) <= max(2, 0.01 * ref[2]), (G, r["iters"], ref[2])
+    ctx.close()
+
+
+def test_dd_edge_cases():
+    cfg, ctx = _ctx()
+    r = _solve(ctx, 4, 1, 1, 4, 0, 1e-12, max_iter=50)[0]
+    assert r["done"] and r["status"] == 1 and r["iters"] == 50     # max_iter exhaustion reported, not hidden
+    with pytest.raises(RuntimeError):
+        layout(128, cfg["m"], 0, 100)                                # 127 rows over 100 ranks
+    with pytest.raises(RuntimeError):
+        SlabSolver(ctx, 4, 0, 1).begin(1, 6, 0, 1e-6)                 # level must be mesh_level or +1
+    ctx.close()
