@@ -12,7 +12,7 @@ BUILD = os.path.join(HERE, "_build")
 SO = os.path.join(HERE, "libmlmc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wno-attributes", "--expt-relaxed-constexpr",
+FLAGS = (["-DMLMC_TUNING"] if os.environ.get("MLMC_TUNING") == "1" else []) + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wno-attributes", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
 SOURCES = ["host_kl.cpp", "capi.cu", "controller.cpp", "k_field.cu", "k_minres.cu", "k_minres_tile.cu", "k_minres_gm.cu", "k_minres_stream.cu", "k_mgcg.cu", "k_chol.cu",
            "k_reduce.cu", "k_dd.cu"]
@@ -26,6 +26,9 @@ def _needs(obj: str, deps) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Production build.  MLMC_TUNING=1 in the environment also compiles the measured-slower A/B kernel variants
+    (env-selected tuning shapes, the global-memory K3 / K3m, the FFMA field kernel) -- tools only; that build
+    writes the same libmlmc.so, so rebuild without it before tests or bench."""
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, "internal.h"), os.path.join(HERE, "..", "include", "mlmc.h")]
     jobs = []

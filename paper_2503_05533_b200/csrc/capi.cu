@@ -286,6 +286,9 @@ void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
 
 // MLMC_MINRES_GM=1 selects the three-phase global-memory MINRES instead of the streamed one (A/B).
 bool use_gm_kernel() {
+#ifndef MLMC_TUNING
+    return false;      // production build: K3c only
+#endif
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("MLMC_MINRES_GM");

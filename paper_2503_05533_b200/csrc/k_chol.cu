@@ -760,21 +760,30 @@ struct Launch {
     }
 };
 
+#ifdef MLMC_TUNING
+constexpr bool kTuning = true;
+#else
+constexpr bool kTuning = false;
+#endif
 // Ring depth / CTA shape of the refinement kernel for the h = 1/32 factors (MLMC_CHOL_VARIANT
 // selects for tuning runs).
 int chol_variant() {
+#ifndef MLMC_TUNING
+    return 0;
+#else
     static int v = -2;
     if (v == -2) {
         const char* e = std::getenv("MLMC_CHOL_VARIANT");
         v = e ? std::atoi(e) : 0;
     }
     return v;
+#endif
 }
 
 template <int N, typename F, typename S, typename U, class Fn>
 cudaError_t with_shape_u(Fn&& fn) {
     if constexpr (N == 32 && sizeof(S) == 4) {
-        if constexpr (sizeof(U) == 8) {
+        if constexpr (sizeof(U) == 8 && kTuning) {
             switch (chol_variant()) {
                 // measured (configs[2] level 2, 100k coupled samples, fp16 / fp32 factor): <3,4> 72.5 / 42.4 ms,
                 // <4,4> 78.6 / 47.5, <2,4> 69.6 / 41.4, <2,2> 68.9 / 41.4, <3,8> 77.5 / 46.7

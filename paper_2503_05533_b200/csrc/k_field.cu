@@ -428,6 +428,9 @@ cudaError_t launch_field_sep(const double* tab, const int* aoff, const int* mk, 
 }
 
 static bool field_use_ffma() {
+#ifndef MLMC_TUNING
+    return false;      // production build: DMMA (the FFMA64 kernel is an A/B variant, tools only)
+#endif
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("MLMC_FIELD_KERNEL");
@@ -458,7 +461,8 @@ cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, 
                          unsigned long long* keys, cudaStream_t s) {
     if (nb == 0) return cudaSuccess;
     // grid.y (sample blocks) is capped at 65535: larger batches go in slices of whole sample blocks
-    const bool ffma = field_use_ffma() || (P & 1);
+    if (P & 1) return cudaErrorInvalidValue;          // P = 2 N^2 is always even (DMMA tiles pairs of centroids)
+    const bool ffma = field_use_ffma();
     const uint64_t per = 65535ull * (ffma ? FT_B : FD_B);
     for (uint64_t b0 = 0; b0 < nb; b0 += per) {
         const uint64_t nbs = std::min<uint64_t>(per, nb - b0);
@@ -466,8 +470,10 @@ cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, 
         double* as = a + b0 * (uint64_t)P;
         unsigned long long* ks = keys ? keys + 2 * b0 : nullptr;
         if (ffma) {
+#ifdef MLMC_TUNING
             dim3 grid((P + FT_P - 1) / FT_P, (unsigned)((nbs + FT_B - 1) / FT_B));
             field_kernel<<<grid, 256, 0, s>>>(phi, xs, as, P, m, (int)nbs, ks);
+#endif
         } else {
             dim3 grid((P + FD_P - 1) / FD_P, (unsigned)((nbs + FD_B - 1) / FD_B));
             field_dmma_kernel<<<grid, 256, 0, s>>>(phi, xs, as, P, m, (int)nbs, ks);

@@ -1016,6 +1016,9 @@ cudaError_t run_mg_tile(const double* a, uint64_t nb, double tol, int max_iter, 
 
 // MLMC_MG_GM=plain selects the ten-pass global-memory kernel (A/B runs).
 bool use_mg_plain() {
+#ifndef MLMC_TUNING
+    return false;      // production build: the tiled kernel (K3m-t) only
+#endif
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("MLMC_MG_GM");
@@ -1057,15 +1060,20 @@ bool mgcg_supported(int N) { return N == 8 || N == 16 || N == 32 || N == 64 || N
 size_t mgcg_scratch_per_cta(int N) {
     const bool plain = use_mg_plain();
     switch (N) {
-        case 128: return plain ? MgGm<128>::SYS : MgTl<128>::SYS;
-        case 256: return plain ? MgGm<256>::SYS : MgTl<256>::SYS;
-        case 512: return plain ? MgGm<512>::SYS : MgTl<512>::SYS;
+        case 128: return plain ? (size_t)MgGm<128>::SYS : (size_t)MgTl<128>::SYS;
+        case 256: return plain ? (size_t)MgGm<256>::SYS : (size_t)MgTl<256>::SYS;
+        case 512: return plain ? (size_t)MgGm<512>::SYS : (size_t)MgTl<512>::SYS;
         default: return 0;
     }
 }
 
 int mgcg_ctas_per_sm(int N) { (void)N; return 1; }
 
+#ifdef MLMC_TUNING
+#define MG_GM(n) run_mg_gm<n>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+#else
+#define MG_GM(n) cudaErrorNotSupported
+#endif
 cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                         unsigned* ctr, const int* order, void* scratch, int nctas, cudaStream_t s, const int* nb_dev,
                         int ok_status) {
@@ -1076,13 +1084,13 @@ cudaError_t launch_mgcg(int N, const double* a, uint64_t nb, double tol, int max
         case 32: return run_mg<32, 128, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s, nb_dev, ok_status);
         case 64: return run_mg<64, 256, 1>(a, nb, tol, max_iter, out, slot, ctr, order, s, nb_dev, ok_status);
         case 128:
-            return plain ? run_mg_gm<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+            return plain ? MG_GM(128)
                          : run_mg_tile<128>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
         case 256:
-            return plain ? run_mg_gm<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+            return plain ? MG_GM(256)
                          : run_mg_tile<256>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
         case 512:
-            return plain ? run_mg_gm<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status)
+            return plain ? MG_GM(512)
                          : run_mg_tile<512>(a, nb, tol, max_iter, out, slot, ctr, order, scratch, nctas, s, nb_dev, ok_status);
         default: return cudaErrorNotSupported;
     }

@@ -375,7 +375,7 @@ bool minres_supported(int N) {
 
 // Kernel shape per mesh (rows per thread R, register budget MINB); alternatives
 // selectable with MLMC_MINRES_VARIANT_N<N>=<index> for tuning runs.
-static int variant(int N) {
+[[maybe_unused]] static int variant(int N) {
     static int v[8] = {-2, -2, -2, -2, -2, -2, -2, -2};
     int slot = N == 8 ? 0 : N == 16 ? 1 : N == 32 ? 2 : N == 64 ? 3 : 4;
     if (v[slot] == -2) {
@@ -394,6 +394,7 @@ static cudaError_t minres_dispatch(int N, const double* a, uint64_t nb, double t
     switch (N) {
         case 2:  return run_minres<2, 1, 8, V>(a, nb, tol, max_iter, out, slot, ctr, s);
         case 4:  return run_minres<4, 1, 8, V>(a, nb, tol, max_iter, out, slot, ctr, s);
+#ifdef MLMC_TUNING
         case 8:
             if (var == 1) return run_minres<8, 2, 6, V, false>(a, nb, tol, max_iter, out, slot, ctr, s);
             if (var == 2) return run_minres<8, 2, 8, V>(a, nb, tol, max_iter, out, slot, ctr, s);
@@ -415,6 +416,7 @@ static cudaError_t minres_dispatch(int N, const double* a, uint64_t nb, double t
             if (var == 2) return run_minres<64, 16, 1, V, false>(a, nb, tol, max_iter, out, slot, ctr, s);
             if (var == 3) return run_minres<64, 8, 1, V, false, true>(a, nb, tol, max_iter, out, slot, ctr, s);
             return run_minres<64, 16, 1, V, true, true>(a, nb, tol, max_iter, out, slot, ctr, s);
+#endif
         default: return cudaErrorNotSupported;
     }
 }

@@ -34,10 +34,15 @@ __device__ __forceinline__ double gm_block_sum(double v, double* buf) {
 }
 
 size_t minres_gm_scratch_per_cta(int N) {
+#ifndef MLMC_TUNING
+    (void)N;
+    return 0;          // production build: K3c (k_minres_stream.cu) only; this kernel is an A/B variant
+#endif
     const size_t G = (size_t)N + 1, n = (size_t)(N - 1) * (N - 1);
     return sizeof(double) * (3 * G * G + 3 * n) + 256;
 }
 
+#ifdef MLMC_TUNING
 __global__ void __launch_bounds__(GMT) minres_gm_kernel(int N, const double* __restrict__ a_all, int nb, double tol,
                                                         int max_iter, double* __restrict__ out, int slot,
                                                         unsigned* __restrict__ job_counter, double* scratch,
@@ -148,13 +153,20 @@ __global__ void __launch_bounds__(GMT) minres_gm_kernel(int N, const double* __r
     }
 }
 
+#endif  // MLMC_TUNING
+
 cudaError_t launch_minres_gm(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                              unsigned* ctr, double* scratch, int nctas, cudaStream_t s) {
     if (nb == 0) return cudaSuccess;
+#ifndef MLMC_TUNING
+    (void)N; (void)a; (void)tol; (void)max_iter; (void)out; (void)slot; (void)ctr; (void)scratch; (void)nctas; (void)s;
+    return cudaErrorNotSupported;
+#else
     const int grid = (int)std::min<uint64_t>(nb, (uint64_t)nctas);
     minres_gm_kernel<<<grid, GMT, 0, s>>>(N, a, (int)nb, tol, max_iter, out, slot, ctr, scratch,
                                           minres_gm_scratch_per_cta(N) / sizeof(double));
     return cudaGetLastError();
+#endif
 }
 
 }  // namespace mlmc

@@ -441,6 +441,10 @@ cudaError_t run_stream(int N, const double* a, uint64_t nb, double tol, int max_
 // 0.80 / 0.76 of HBM at h = 1/256 and 0.78 / 0.78 at 1/512 for 1 / 2 CTAs, but 0.57 / 0.63 for 4 (clusters
 // of 4 leave SMs of every GPC idle); 441 systems at h = 1/128: 122 / 135 ms for 1 / 2.
 int minres_stream_cluster(int N) {
+#ifndef MLMC_TUNING
+    (void)N;
+    return 2;          // production build: 2-CTA clusters on every streamed mesh
+#endif
     static int env = -2;
     if (env == -2) {
         const char* e = std::getenv("MLMC_STREAM_CLUSTER");
@@ -455,12 +459,16 @@ cudaError_t launch_minres_stream(int N, const double* a, uint64_t nb, double tol
                                  unsigned* ctr, double* scratch, int nctas, cudaStream_t s, const int* order) {
     if (nb == 0) return cudaSuccess;
     if (!minres_stream_supported(N)) return cudaErrorNotSupported;
+#ifdef MLMC_TUNING
     switch (minres_stream_cluster(N)) {
         case 8: return run_stream<8>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
         case 4: return run_stream<4>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
         case 2: return run_stream<2>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
         default: return run_stream<1>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
     }
+#else
+    return run_stream<2>(N, a, nb, tol, max_iter, out, slot, ctr, scratch, nctas, order, s);
+#endif
 }
 
 }  // namespace mlmc

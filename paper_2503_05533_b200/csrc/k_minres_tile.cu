@@ -470,9 +470,12 @@ cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, dou
 // Tile shape per mesh: MLMC_MINRES_TILE_N<N>=<index> selects an alternative for tuning runs;
 // -1 hands the mesh back to the column-strip kernel (k_minres.cu).
 int minres_tile_variant(int N) {
-    static int v[4] = {-2, -2, -2, -2};
     const int slot = N == 8 ? 3 : N == 16 ? 0 : N == 32 ? 1 : N == 64 ? 2 : -1;
     if (slot < 0) return -1;
+#ifndef MLMC_TUNING
+    return 0;          // the production build carries only the measured-best shape per mesh (v0)
+#else
+    static int v[4] = {-2, -2, -2, -2};
     if (v[slot] == -2) {
         char name[64];
         std::snprintf(name, sizeof(name), "MLMC_MINRES_TILE_N%d", N);
@@ -480,31 +483,37 @@ int minres_tile_variant(int N) {
         v[slot] = e ? std::atoi(e) : 0;
     }
     return v[slot];
+#endif
 }
 
+#ifdef MLMC_TUNING
+#define IF_TUNING(...) __VA_ARGS__
+#else
+#define IF_TUNING(...)
+#endif
 // Variant table (index = MLMC_MINRES_TILE_N<N>): <N, R, MINB, CM>; measured with tools/tune_minres.py.
 template <bool V>
 static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, double tol, int max_iter, double* out,
                                  int slot, unsigned* ctr, const int* order, cudaStream_t s) {
     switch (N) {
         case 8:   // two systems per warp (16 threads each)
-            if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
             // (conductances in shared memory with 8 / 6 systems-pairs per SM: 0.133 / 0.127 ms vs 0.109 ms on
             // configs[1] level 0; 16 systems per warp-pair cannot hide the extra shared loads)
             return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 16:
-            if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
             // (conductances in shared memory, 6 / 8 CTAs per SM: level-1 pass 0.60 / 0.61 ms vs 0.51 ms)
             return run_tile<16, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 32:
-            if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
             // v4 / v5 (conductances in shared memory, 5 / 4 systems per SM): 0.80 / 0.81 ms vs v0 0.74 ms
             // on configs[1] level 2, bit-identical records
-            if (var == 4) return run_tile<32, 4, 5, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 5) return run_tile<32, 4, 4, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 4) return run_tile<32, 4, 5, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 5) return run_tile<32, 4, 4, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
             return run_tile<32, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         case 64:
             // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67, v4 2.97
@@ -513,12 +522,12 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             // (tools/tune_minres.py): v0 1.671 ms, v5 (west conductances in shared memory, no in-loop
             // spills) 1.723, v6 (diagonal in shared memory) 1.722, v1 1.711 -- v0's few L1-resident
             // spill reloads cost less than the shared loads that remove them
-            if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 4) return run_tile<64, 8, 2, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 5) return run_tile<64, 8, 1, 2, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
-            if (var == 6) return run_tile<64, 8, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 4) return run_tile<64, 8, 2, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 5) return run_tile<64, 8, 1, 2, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 6) return run_tile<64, 8, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
             return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
         default: return cudaErrorNotSupported;
     }
