@@ -104,6 +104,11 @@ typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1, MLMC_SOLVER_MGCG
 #define MLMC_FLAG_ESCALATE 2 /* MINRES / CHOL_IR: a failed solve (max_iter, breakdown, limiting accuracy) is
                                 solved again by MG-PCG to the same tolerance; if that converges the sample's
                                 status is 4 */
+#define MLMC_FLAG_C2F 4      /* on prec_fine, MINRES both halves, fine mesh h = 1/16, 1/32 or 1/64 (NEXT-4,
+                                P:97-102, R32): the fine half starts from x0 = P x_c, the P1 interpolation of
+                                the coarse half's solution of the same sample (solved first), instead of 0; the
+                                stopping rule stays ||b - A x_k|| <= tol ||b|| (phibar_k <= tol ||b||), the
+                                reported iterations are the fine half's from x0 */
 
 typedef struct {
     int32_t solver;
@@ -302,6 +307,12 @@ int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
  * mlmc_auto_choice returns the latest precision chosen for mesh N (= 1/h) and its pilot cost in device
  * ms per sample.  Errors: EINVAL (no choice made for N).                                                */
 int mlmc_auto_choice(const mlmc_ctx* ctx, int N, mlmc_precision* out, double* ms_per_sample);
+/* Record a choice for mesh N and tolerance class tol_class (0: tol >= 1e-3, 1: >= 1e-5, 2: below) before a
+ * policy-3 run, so that the run does not time pilots: a run driven by recorded choices (e.g. the ones
+ * mlmc_auto_choice reported on another box) takes the same decisions everywhere.  ms_per_sample reads -1
+ * for a recorded choice.  Errors: EINVAL (N not a mesh of the plan, class out of range, solver not built
+ * for N).                                                                                                */
+int mlmc_auto_choice_set(mlmc_ctx* ctx, int N, int tol_class, const mlmc_precision* p);
 
 /* The same controller over a caller-supplied host sampler instead of the GPU
  * (CPU tests of Algorithm 2 and of the multi-rank exchange).  The sampler must

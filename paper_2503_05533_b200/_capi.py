@@ -110,6 +110,7 @@ def lib():
                                           C.POINTER(Precision), C.c_double, C.c_double, vp, vp]
     L.mlmc_adaptive_run.argtypes = [vp, C.c_double, C.POINTER(AdaptiveOpts), ALLREDUCE_FN, vp, C.POINTER(Result)]
     L.mlmc_auto_choice.argtypes = [vp, C.c_int, C.POINTER(Precision), dp]
+    L.mlmc_auto_choice_set.argtypes = [vp, C.c_int, C.c_int, C.POINTER(Precision)]
     L.mlmc_eps_schedule.argtypes = [C.c_int, C.c_double, C.c_double, dp]
     L.mlmc_optimal_samples.argtypes = [C.c_int, dp, dp, C.c_double, dp]
     L.mlmc_kl_modes.argtypes = [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), dp, dp,

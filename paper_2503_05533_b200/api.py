@@ -219,6 +219,12 @@ class Context:
         quad = "".join(fmt[v] for v in (p.u_f, p.u_s, p.u, p.u_r)) if p.solver == K.SOLVER_CHOL_IR else None
         return {"solver": name, "quad": quad, "ms_per_sample": ms.value}
 
+    def auto_choice_set(self, N: int, tol_class: int, prec) -> None:
+        """mlmc_auto_choice_set: record policy 3's choice for mesh N and tolerance class (0: tol >= 1e-3,
+        1: >= 1e-5, 2: below) so that a run reproduces recorded decisions without pilot timings."""
+        p = _as_prec(prec)
+        K.check(K.lib().mlmc_auto_choice_set(self.ctx, N, tol_class, C.byref(p)), self.ctx)
+
     def adaptive_run(self, eps: float, k_p: float = 0.05, N_init: int = 100, policy: int = 0, seed: int = 0,
                      fixed_tol: float = 1e-10, r_bias: float = 1.0, max_rounds: int = 100, group=None,
                      on_fail: int = 0) -> dict:
@@ -252,12 +258,30 @@ def _allreduce_callback(group, device):
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = device if dist.get_backend(group) == "nccl" else t.device("cpu")
 
+    # persistent staging: one pinned host buffer and one buffer on the collective's device, grown on demand, so a
+    # round's exchange is two copies and ONE all-reduce (the controller sends everything in one SUM call)
+    bufs = {}
+
+    def _staging(count):
+        if bufs.get("n", 0) < count:
+            n = max(count, 2 * bufs.get("n", 0), 256)
+            pin = dev.type == "cuda"
+            bufs["h"] = t.empty(n, dtype=t.float64, pin_memory=pin)
+            bufs["d"] = t.empty(n, dtype=t.float64, device=dev) if pin else bufs["h"]
+            bufs["n"] = n
+        return bufs["h"][:count], bufs["d"][:count]
+
     def _allreduce(buf, count, op, user):
         try:
             arr = np.ctypeslib.as_array(buf, shape=(count,))
-            ten = t.from_numpy(arr.copy()).to(dev)
-            dist.all_reduce(ten, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
-            arr[:] = ten.cpu().numpy()
+            h, d = _staging(count)
+            h.numpy()[:] = arr
+            if d is not h:
+                d.copy_(h, non_blocking=True)
+            dist.all_reduce(d, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+            if d is not h:
+                h.copy_(d)
+            arr[:] = h.numpy()
             return 0
         except Exception:  # noqa: BLE001 -- reported to the C side as a failure
             return 1

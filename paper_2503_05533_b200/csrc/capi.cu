@@ -113,7 +113,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // Workspace layout for one pass of `batch` samples of `level`.
 struct WsLayout {
     size_t xi, a_f, a_c, rec, chunks, ctr, keys_f, keys_c, ord_f, ord_c, esc_f, esc_c, gm, ch_f, ch_c, ch_f_bytes,
-        ch_c_bytes, total;
+        ch_c_bytes, xc, total;
     int gm_ctas;
 };
 // Cholesky factor scratch of one solve (0 for MINRES / unsupported combinations)
@@ -158,6 +158,9 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.ch_c_bytes = level > 0 ? chol_bytes(pc, Nc, batch) : 0;
     L.ch_f = off;   off += align256(L.ch_f_bytes);
     L.ch_c = off;   off += align256(L.ch_c_bytes);
+    // coarse solutions of a coarse-to-fine pair (MLMC_FLAG_C2F): [batch][(Nc - 1)^2]
+    L.xc = off;
+    if (pf && (pf->flags & MLMC_FLAG_C2F) && level > 0) off += align256(sizeof(double) * batch * (size_t)(Nc - 1) * (Nc - 1));
     L.total = off;
     return L;
 }
@@ -276,12 +279,42 @@ int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
 
 double fmt_bits(int f) { return f == MLMC_FMT_F16 ? 16 : f == MLMC_FMT_F32 ? 32 : f == MLMC_FMT_E4M3 ? 8 : 64; }
 
-// cost model R5: fixed + per-iteration work of one solve on mesh N
+// Cost model R5 of one solve on mesh N: fixed + step x iterations, in one commensurate unit across solvers --
+// the device time of one MINRES node-step (one unknown, one MINRES iteration) on the same mesh class.  MINRES
+// itself costs n per step: the paper's cost measure (PETSc FLOPs of MINRES, proportional to
+// iterations x unknowns), so policy 0 is exactly the paper's model.  The other solvers' weights were measured
+// once on B200 (round 1) and are frozen here, so a run's N_l decisions never depend on
+// the box or on timing noise:
+//   MG-PCG step       on chip (N <= 64): ~20 MINRES steps of the same system (profiles/r01p_cg_vs_minres.jsonl,
+//                     DESIGN.md K3m); streamed (N >= 128): 162 vs 40 B per node-step at 2.56 vs 5.04 TB/s -> 8
+//   CG step           1.5 (the MG kernel's layout, 1.2-2.9x slower passes than K3, profiles/r01p_*)
+//   Cholesky-IR       factorisation 2.5 n bw (binary32 factor; 3.6 binary16 / E4M3, 5 binary64), each
+//                     substitution pair + residual 0.7 n bw (K4 launch times of profiles/r01c_ncu_k4.md against
+//                     the K3 node-step time at h = 1/32)
 void cost_model(const mlmc_precision* p, int N, double& fixed, double& step) {
-    double n = (double)(N - 1) * (N - 1), bw = N - 1;
-    if (p->solver == MLMC_SOLVER_MINRES || p->solver == MLMC_SOLVER_CG) { fixed = 0.0; step = n; }
-    else if (p->solver == MLMC_SOLVER_MGCG) { fixed = 8.0 * n; step = 8.0 * n; }   // ~ a V-cycle + matvec per step
-    else { fixed = n * bw * bw * fmt_bits(p->u_f) / 64.0; step = 4.0 * n * bw; }
+    const double n = (double)(N - 1) * (N - 1), bw = N - 1;
+    if (p->solver == MLMC_SOLVER_MINRES) { fixed = 0.0; step = n; }
+    else if (p->solver == MLMC_SOLVER_CG) { fixed = 0.0; step = 1.5 * n; }
+    else if (p->solver == MLMC_SOLVER_MGCG) { const double w = N <= 64 ? 20.0 : 8.0; fixed = w * n; step = w * n; }
+    else {
+        const double cf = p->u_f == MLMC_FMT_F32 ? 2.5 : p->u_f == MLMC_FMT_F64 ? 5.0 : 3.6;
+        fixed = (cf + 0.7) * n * bw;                   // factor + the initial solve x0
+        step = 0.7 * n * bw;
+    }
+}
+
+// cost of an escalated half (status 4): the failed attempt (run to its iteration cap) + MG-PCG's fixed part,
+// then MG-PCG's per-step cost times the recorded MG-PCG steps
+void escalation_cost(const mlmc_precision* p, int N, double& fixed, double& step) {
+    double f0, s0;
+    cost_model(p, N, f0, s0);
+    const int n = (N - 1) * (N - 1);
+    const double cap = p->max_iter > 0 ? p->max_iter : (p->solver == MLMC_SOLVER_CHOL_IR ? 50.0 : 16.0 * n + 1000.0);
+    const mlmc_precision mg{MLMC_SOLVER_MGCG, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 0, 0};
+    double fm, sm;
+    cost_model(&mg, N, fm, sm);
+    fixed = f0 + s0 * cap + fm;
+    step = sm;
 }
 
 // MLMC_MINRES_GM=1 selects the three-phase global-memory MINRES instead of the streamed one (A/B).
@@ -314,7 +347,8 @@ bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
 
 int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, double tol, const double* a, uint64_t nb,
                double* rec, int slot, unsigned* ctr, double* gm_scratch, int gm_ctas, void* ch_scratch,
-               size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr, int* esc = nullptr) {
+               size_t ch_bytes, const unsigned long long* keys = nullptr, int* order = nullptr, int* esc = nullptr,
+               int xmode = 0, double* xio = nullptr) {
     int n = (N - 1) * (N - 1);
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;   // finite-precision Lanczos at contrast ~1e7 (Eq. (20), sigma = 2) needs > n
@@ -331,7 +365,10 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
             }));
         else
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N,
-                       [&] { return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, keys ? order : nullptr, ex.st); }));
+                       [&] {
+                           return launch_minres(N, a, nb, tol, mi, rec, slot, ctr, verify, keys ? order : nullptr, ex.st,
+                                                xmode, xio);
+                       }));
 
     } else if (p->solver == MLMC_SOLVER_CG) {
         int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;
@@ -371,6 +408,11 @@ int validate_level(mlmc_ctx* ctx, int level, const mlmc_precision* pf, const mlm
     if (level > 0 && (rc = check_prec(ctx, pc, Nc, tol_c))) return rc;
     if ((rc = ensure_phi(ctx, level))) return rc;
     if (level > 0 && (rc = ensure_phi(ctx, level - 1))) return rc;
+    if (pf->flags & MLMC_FLAG_C2F) {   // coarse-to-fine initial guess: both halves MINRES on tile meshes
+        if (level == 0 || pf->solver != MLMC_SOLVER_MINRES || !pc || pc->solver != MLMC_SOLVER_MINRES ||
+            !(Nf == 16 || Nf == 32 || Nf == 64) || minres_tile_variant(Nf) < 0 || minres_tile_variant(Nc) < 0)
+            return fail(ctx, MLMC_EINVAL, "MLMC_FLAG_C2F needs level >= 1, MINRES on both halves and h = 1/16..1/64");
+    }
     return MLMC_OK;
 }
 
@@ -392,9 +434,13 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
     double* chunks = reinterpret_cast<double*>(ex.ws + L.chunks);
     unsigned* ctr = reinterpret_cast<unsigned*>(ex.ws + L.ctr);
     double* gm = reinterpret_cast<double*>(ex.ws + L.gm);
-    double cff, cfs, ccf = 0, ccs = 0;
-    cost_model(pf, Nf, cff, cfs);
-    if (level > 0) cost_model(pc, Nc, ccf, ccs);
+    CostParams cp{};
+    cost_model(pf, Nf, cp.f_fixed, cp.f_step);
+    escalation_cost(pf, Nf, cp.f_esc, cp.f_esc_step);
+    if (level > 0) {
+        cost_model(pc, Nc, cp.c_fixed, cp.c_step);
+        escalation_cost(pc, Nc, cp.c_esc, cp.c_esc_step);
+    }
     const int m = ctx->pr.m;
     const cudaStream_t st = ex.st;
     int rc;
@@ -426,8 +472,11 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         const bool sched = sch && nb == n;               // single pass only
         if (sched && sch->prep) CU(cudaEventRecord(sch->prep, st));
         if (sched && sch->gate) CU(cudaStreamWaitEvent(st, sch->gate, 0));
-        // the global-memory MINRES shares one scratch between the fine and coarse solves: no fork then
-        const bool fork = sched && level > 0 && sch->st_c && Nf < kGmMinN;
+        // the global-memory MINRES shares one scratch between the fine and coarse solves: no fork then; a
+        // coarse-to-fine pair (MLMC_FLAG_C2F) runs the coarse half first, the fine half from its solution
+        const bool c2f = level > 0 && (pf->flags & MLMC_FLAG_C2F);
+        double* xc = reinterpret_cast<double*>(ex.ws + L.xc);
+        const bool fork = sched && level > 0 && sch->st_c && Nf < kGmMinN && !c2f;
         if (fork) {
             CU(cudaEventRecord(sch->fork, st));
             CU(cudaStreamWaitEvent(sch->st_c, sch->fork, 0));
@@ -436,7 +485,15 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         void* chc = ex.ws + L.ch_c;
         int* ef = reinterpret_cast<int*>(ex.ws + L.esc_f);
         int* ec = reinterpret_cast<int*>(ex.ws + L.esc_c);
-        if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes, kf, of, ef)))
+        if (c2f) {
+            if ((rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc, L.ch_c_bytes, kc,
+                                 oc, ec, 1, xc)))
+                return rc;
+            if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes, kf, of,
+                                 ef, 2, xc)))
+                return rc;
+        } else if ((rc = solve_mesh(ctx, ex, Nf, pf, tol_f, af, nb, rec, 0, ctr, gm, L.gm_ctas, chf, L.ch_f_bytes, kf,
+                                    of, ef)))
             return rc;
         if (fork) {
             const Exec exc{ex.ws, ex.bytes, sch->st_c};
@@ -445,12 +502,12 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
                 return rc;
             CU(cudaEventRecord(sch->join, sch->st_c));
             CU(cudaStreamWaitEvent(st, sch->join, 0));
-        } else if (level > 0 && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm, L.gm_ctas, chc,
-                                                 L.ch_c_bytes, kc, oc, ec))) {
+        } else if (level > 0 && !c2f && (rc = solve_mesh(ctx, ex, Nc, pc, tol_c, ac, nb, rec, 1, ctr + 4, gm,
+                                                         L.gm_ctas, chc, L.ch_c_bytes, kc, oc, ec))) {
             return rc;
         }
         CU(counted(ctx, st, MLMC_K_SUMS, Nf, [&] {
-            return launch_level_sums(rec, nb, level, 0, 0, cff, cfs, ccf, ccs, chunks, sums_dev, true, st, xsums);
+            return launch_level_sums(rec, nb, level, cp, chunks, sums_dev, true, st, xsums);
         }));
         if (per_sample) {
             double* dst = per_sample + done * kRecLen;
@@ -788,6 +845,21 @@ int mlmc_auto_choice(const mlmc_ctx* ctx, int N, mlmc_precision* out, double* ms
             return MLMC_OK;
         }
     return MLMC_EINVAL;
+}
+
+int mlmc_auto_choice_set(mlmc_ctx* ctx, int N, int tol_class, const mlmc_precision* p) {
+    if (!ctx || !p || tol_class < 0 || tol_class > 2) return MLMC_EINVAL;
+    int level = -1;
+    for (int l = 0; l <= ctx->pr.L_max; ++l)
+        if (level_N(ctx, l) == N) level = l;
+    if (level < 0) return fail(ctx, MLMC_EINVAL, "mlmc_auto_choice_set: N is not a mesh of the plan");
+    const double tol = tol_class == 0 ? 1e-3 : tol_class == 1 ? 1e-5 : 1e-8;
+    int rc = check_prec(ctx, p, N, tol);
+    if (rc) return rc;
+    mlmc_precision q = *p;
+    q.max_iter = 0;
+    mlmc::ctx_note_auto_choice(ctx, N, tol_class, q, -1.0);   // recorded, not measured
+    return MLMC_OK;
 }
 
 int mlmc_profile_enable(mlmc_ctx* ctx, int on) {

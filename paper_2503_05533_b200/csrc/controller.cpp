@@ -195,7 +195,7 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             mlmc_precision qf, qc;
             int rcp = choose(l, h0_inv << l, epsl[l], &qf);
             if (!rcp && l > 0) rcp = choose(l - 1, h0_inv << (l - 1), epsl[l - 1], &qc);
-            if (rcp) return rcp;
+            if (rcp) return rcp;   // the chooser has already agreed its outcome across the ranks
             if (o.on_fail == 2) {   // escalation of failed MINRES / IR solves to MG-PCG (MLMC_FLAG_ESCALATE)
                 if (qf.solver != MLMC_SOLVER_MGCG) qf.flags |= MLMC_FLAG_ESCALATE;
                 if (l > 0 && qc.solver != MLMC_SOLVER_MGCG) qc.flags |= MLMC_FLAG_ESCALATE;
@@ -205,26 +205,29 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             tf.push_back(epsl[l]);
             tc.push_back(l > 0 ? epsl[l - 1] : epsl[l]);
         }
+        int local_rc = MLMC_OK;
         if (!lv.empty()) {
             std::vector<double> s(lv.size() * MLMC_SUMS_LEN, 0.0);
             std::vector<u64> xs(exact ? lv.size() * kXLen : 0, 0);
             auto t0 = std::chrono::steady_clock::now();
-            int rc = sampler((int)lv.size(), lv.data(), cnt.data(), first.data(), pf.data(), pc.data(), tf.data(),
-                             tc.data(), s.data(), exact ? xs.data() : nullptr);
+            local_rc = sampler((int)lv.size(), lv.data(), cnt.data(), first.data(), pf.data(), pc.data(), tf.data(),
+                               tc.data(), s.data(), exact ? xs.data() : nullptr);
             solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (rc) return rc;
+            // a rank-local failure must not leave the other ranks waiting in the exchange: the error
+            // travels in the round's all-reduce and every rank returns together
+            if (local_rc && o.world == 1) return local_rc;
+            if (local_rc) { std::fill(s.begin(), s.end(), 0.0); std::fill(xs.begin(), xs.end(), 0ull); }
             for (size_t q = 0; q < lv.size(); ++q) {
                 std::memcpy(&round_sums[(size_t)lv[q] * MLMC_SUMS_LEN], &s[q * MLMC_SUMS_LEN],
                             sizeof(double) * MLMC_SUMS_LEN);
                 if (exact) std::memcpy(&round_x[(size_t)lv[q] * kXLen], &xs[q * kXLen], sizeof(u64) * kXLen);
             }
         }
-        // one exchange per round: SUM of the additive fields, MAX of the two maxima
+        // ONE exchange per round: a SUM all-reduce of the additive fields (the per-rank iteration maxima, fields
+        // 9/10, are diagnostics the controller never uses: they are not exchanged), the exact sums' 32-bit
+        // pieces and an error flag
         if (o.world > 1) {
-            std::vector<double> mx((size_t)(L + 1) * 2);
             for (int l = 0; l <= L; ++l) {
-                mx[2 * l] = round_sums[(size_t)l * MLMC_SUMS_LEN + 9];
-                mx[2 * l + 1] = round_sums[(size_t)l * MLMC_SUMS_LEN + 10];
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 9] = 0.0;
                 round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = 0.0;
             }
@@ -242,8 +245,11 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
                         d[8] = (double)x[4];
                     }
             }
+            round_sums.push_back(local_rc ? 1.0 : 0.0);                  // ranks that failed this round
             if (allreduce(round_sums.data(), (int)round_sums.size(), 0, user) != 0) return MLMC_ECUDA;
-            if (allreduce(mx.data(), (int)mx.size(), 1, user) != 0) return MLMC_ECUDA;
+            const bool any_err = round_sums.back() > 0.0;
+            round_sums.pop_back();
+            if (any_err) return local_rc ? local_rc : MLMC_ESOLVER;
             if (exact) {
                 for (int l = 0; l <= L; ++l)
                     for (int f = 0; f < kXFields; ++f) {
@@ -259,10 +265,6 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
                         x[4] = (u64)d[8];
                     }
                 round_sums.resize(base);
-            }
-            for (int l = 0; l <= L; ++l) {
-                round_sums[(size_t)l * MLMC_SUMS_LEN + 9] = mx[2 * l];
-                round_sums[(size_t)l * MLMC_SUMS_LEN + 10] = mx[2 * l + 1];
             }
         }
         bool failed = false;
@@ -378,7 +380,15 @@ struct AutoChooser {
             if (!rc) rc = mlmc_sample_level(ctx, level, npilot, seed ^ 0x9e3779b97f4a7c15ull, 0, &p, &cheap, tol, 0.5,
                                             &sums, nullptr);
             if (rc == MLMC_EINVAL) { mlmc_profile_enable(ctx, 0); ms[c] = -1.0; continue; }   // not built here
-            if (rc) return rc;
+            if (rc) {                            // agree on the failure before leaving
+                mlmc_profile_enable(ctx, 0);
+                if (world > 1 && allreduce) {
+                    std::vector<double> buf(2 * ms.size() + 1, 0.0);
+                    buf.back() = 1.0;
+                    allreduce(buf.data(), (int)buf.size(), 0, user);
+                }
+                return rc;
+            }
             mlmc_kernel_stat st[64];
             int cnt = 0;
             mlmc_profile_read(ctx, st, 64, &cnt);
@@ -388,12 +398,13 @@ struct AutoChooser {
                 if (st[i].N == N && (st[i].kind == MLMC_K_MINRES || st[i].kind == MLMC_K_CHOL_IR)) t += st[i].ms;
             ms[c] = sums.n_fail > 0 ? -1.0 : t;     // a failed pilot solve: inadmissible
         }
-        if (world > 1 && allreduce) {
-            std::vector<double> buf(ms.size()), fail(ms.size());
-            for (size_t c = 0; c < ms.size(); ++c) { buf[c] = ms[c] < 0 ? 0.0 : ms[c]; fail[c] = ms[c] < 0 ? 1.0 : 0.0; }
+        if (world > 1 && allreduce) {   // one SUM all-reduce: pilot times, failure counts, error flag
+            const size_t C = ms.size();
+            std::vector<double> buf(2 * C + 1, 0.0);
+            for (size_t c = 0; c < C; ++c) { buf[c] = ms[c] < 0 ? 0.0 : ms[c]; buf[C + c] = ms[c] < 0 ? 1.0 : 0.0; }
             if (allreduce(buf.data(), (int)buf.size(), 0, user) != 0) return MLMC_ECUDA;
-            if (allreduce(fail.data(), (int)fail.size(), 1, user) != 0) return MLMC_ECUDA;
-            for (size_t c = 0; c < ms.size(); ++c) ms[c] = fail[c] > 0 ? -1.0 : buf[c];
+            if (buf[2 * C] > 0.0) return MLMC_ECUDA;          // another rank's pilot failed
+            for (size_t c = 0; c < C; ++c) ms[c] = buf[C + c] > 0 ? -1.0 : buf[c];
         }
         size_t best = 0;
         for (size_t c = 1; c < ms.size(); ++c)

@@ -58,12 +58,16 @@ cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cud
 // K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].  order (optional,
 // device, nb ints): the sequence in which the systems are taken (order_kernel: longest first).
 cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                          int slot, unsigned* job_counter, bool verify, const int* order, cudaStream_t s);
+                          int slot, unsigned* job_counter, bool verify, const int* order, cudaStream_t s,
+                          int xmode = 0, double* xio = nullptr);
 bool minres_supported(int N);
 // K3 v2 (k_minres_tile.cu): 2-column register tiles for N = 8, 16, 32, 64; variant < 0 = not used for N.
 int minres_tile_variant(int N);
-cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                               int slot, unsigned* job_counter, bool verify, const int* order, cudaStream_t s);
+// xmode (coarse-to-fine initial guess, NEXT-4): 0 none; 1 write the final x of every system to xio (coarse half;
+// carries x, i.e. the VERIFY arithmetic); 2 start from the P1 interpolation of the coarse solutions in xio.
+cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                               unsigned* ctr, bool verify, const int* order, cudaStream_t s, int xmode = 0,
+                               double* xio = nullptr);
 // K3 for N >= 128: vectors in a per-CTA global scratch (nctas CTAs, minres_gm_scratch_per_cta(N) bytes each).
 constexpr int kGmMinN = 128;
 size_t minres_gm_scratch_per_cta(int N);
@@ -109,10 +113,13 @@ cudaError_t launch_escalate_collect(const double* rec, uint64_t nb, int slot, in
 // K5: per-level sums of the per-sample records into sums (accumulate = add to existing).
 // xsums (optional, device, kXLen words): the exact fixed-point sums, accumulated like sums.  chunk_scratch
 // holds (kSumsLen + kXLen) x 8 bytes per chunk.
-cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,
-                              double cost_f_fixed, double cost_f_step, double cost_c_fixed,
-                              double cost_c_step, double* chunk_scratch, double* sums, bool accumulate,
-                              cudaStream_t s, unsigned long long* xsums = nullptr);
+// Work model of one coupled sample's halves (R5): fixed + step x iterations; *_esc: an escalated half
+// (status 4: failed attempt + MG-PCG re-solve, the record holding the MG-PCG steps).
+struct CostParams {
+    double f_fixed, f_step, f_esc, f_esc_step, c_fixed, c_step, c_esc, c_esc_step;
+};
+cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, const CostParams& cp, double* chunk_scratch,
+                              double* sums, bool accumulate, cudaStream_t s, unsigned long long* xsums = nullptr);
 // The exact fixed-point sums of the levels of the last mlmc_sample_levels(_async) call (nlev x kXLen words)
 int copy_xsums_to_host(mlmc_ctx* ctx, int nlev, unsigned long long* host);
 void ctx_want_xsums(mlmc_ctx* ctx, bool on);   // form the exact sums in the sampling calls that follow

@@ -34,7 +34,9 @@
 namespace mlmc {
 namespace {
 
-template <int N, int T, int GROUPS_>
+// PC = false (plain CG): only the binary64 grids -- no binary32 V-cycle hierarchy (it reserved
+// ~114 KB at N = 64 that CG never reads and halved its residency)
+template <int N, int T, int GROUPS_, bool PC = true>
 struct MgCfg {
     static constexpr int GROUPS = GROUPS_;
     static constexpr int BLOCK = T * GROUPS;
@@ -51,7 +53,7 @@ struct MgCfg {
         for (int k = 0; k < l; ++k) o += 5 * gl(k) * gl(k);
         return o;
     }
-    static constexpr int F_END = (foff(LV) + 3) / 4 * 4;       // keeps what follows 16-byte aligned
+    static constexpr int F_END = PC ? (foff(LV) + 3) / 4 * 4 : 0;   // keeps what follows 16-byte aligned
     static constexpr int NW = T >= 32 ? T / 32 : 1;
     static constexpr size_t SYS = (((size_t)D_END * 8 + (size_t)F_END * 4 + (size_t)2 * NW * 8 + 16) + 127) / 128 * 128;
     static constexpr size_t SMEM = SYS * GROUPS;
@@ -317,14 +319,32 @@ __device__ __forceinline__ void mg_setup(const double* __restrict__ a, double* c
     }
 }
 
+// Plain CG's set-up (PC = false): the binary64 fine conductances and p = 0 only
+template <int N, int T, int GROUPS>
+__device__ __forceinline__ void cg_setup(const double* __restrict__ a, double* cE, double* cN, double* pg, int tg,
+                                         int g) {
+    constexpr int G = N + 1;
+    for (int c = tg; c < G * G; c += T) {
+        const int i = c % G, j = c / G;
+        const double ce = (i < N && j >= 1 && j < N)
+                              ? 0.5 * (__ldg(a + 2 * (j * N + i)) + __ldg(a + 2 * ((j - 1) * N + i) + 1)) : 0.0;
+        const double cn = (i >= 1 && i < N && j < N)
+                              ? 0.5 * (__ldg(a + 2 * (j * N + i) + 1) + __ldg(a + 2 * (j * N + i - 1))) : 0.0;
+        cE[c] = ce;
+        cN[c] = cn;
+        pg[c] = 0.0;
+    }
+    gsync<T, GROUPS>(g);
+}
+
 // PC = false: plain CG (NEXT-4) -- z = r, no V-cycle; everything else identical
 template <int N, int T, int GROUPS, bool PC = true>
-__global__ void __launch_bounds__(MgCfg<N, T, GROUPS>::BLOCK)
+__global__ void __launch_bounds__(MgCfg<N, T, GROUPS, PC>::BLOCK)
 mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out, int slot,
             unsigned* __restrict__ job_counter, const int* __restrict__ order, const int* __restrict__ nb_dev,
             int ok_status) {
     if (nb_dev) nb = *nb_dev;
-    using K = MgCfg<N, T, GROUPS>;
+    using K = MgCfg<N, T, GROUPS, PC>;
     constexpr int G = K::G, C = K::C, n = K::n, PER = K::PER, P = 2 * N * N;
     extern __shared__ __align__(128) unsigned char smem[];
     const int g = threadIdx.x / T, tg = threadIdx.x % T;
@@ -358,7 +378,8 @@ mgcg_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, 
         if (job >= nb) break;
         const int sj = order ? __ldg(order + job) : job;
         const double* a = a_all + (size_t)sj * P;
-        mg_setup<N, T, GROUPS>(a, cE, cN, pg, fb, tg, g);
+        if constexpr (PC) mg_setup<N, T, GROUPS>(a, cE, cN, pg, fb, tg, g);
+        else cg_setup<N, T, GROUPS>(a, cE, cN, pg, tg, g);
         const Lvl L0 = level_rt<N>(fb, 0);
 
         // ---- PCG from x0 = 0: r = b, z = M^-1 r, p = z
@@ -1030,7 +1051,7 @@ bool use_mg_plain() {
 template <int N, int T, int GROUPS, bool PC = true>
 cudaError_t run_mg(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
                    const int* order, cudaStream_t s, const int* nb_dev, int ok_status) {
-    using K = MgCfg<N, T, GROUPS>;
+    using K = MgCfg<N, T, GROUPS, PC>;
     auto kern = mgcg_kernel<N, T, GROUPS, PC>;
     static PerDevice<KernelOcc> occ_cache;
     const KernelOcc occ = occ_of(occ_cache, kern, K::BLOCK, K::SMEM);

@@ -422,9 +422,10 @@ static cudaError_t minres_dispatch(int N, const double* a, uint64_t nb, double t
 }
 
 cudaError_t launch_minres(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                          unsigned* ctr, bool verify, const int* order, cudaStream_t s) {
+                          unsigned* ctr, bool verify, const int* order, cudaStream_t s, int xmode, double* xio) {
     if (minres_tile_variant(N) >= 0)
-        return launch_minres_tile(N, a, nb, tol, max_iter, out, slot, ctr, verify, order, s);
+        return launch_minres_tile(N, a, nb, tol, max_iter, out, slot, ctr, verify, order, s, xmode, xio);
+    if (xmode) return cudaErrorNotSupported;
     // the column-strip kernel takes the systems in index order
     return verify ? minres_dispatch<true>(N, a, nb, tol, max_iter, out, slot, ctr, s)
                   : minres_dispatch<false>(N, a, nb, tol, max_iter, out, slot, ctr, s);

@@ -142,10 +142,17 @@ __device__ __forceinline__ double4 tsum3(double a, double b, double c, double* b
 // Rayleigh quotient (Lanczos variant "A1") instead of v^T (A v - beta v_prev).  Three vectors per
 // node (p_{j-1}, p_j, t) instead of five; 11 fp64 operations per node and step.  VERIFY also
 // carries w_k and x_k (textbook updates) to report the true residual.
-template <int N, int R, int MINB, int CM, bool VERIFY>
+// XM (coarse-to-fine initial guess, NEXT-4, R32): 0 = x0 = 0; 1 = also write the final x_k of every
+// system to xio[job][(N-1)^2] (needs VERIFY: x is carried); 2 = start from x0 = P x_c, the P1 interpolation
+// of the coarse solution xio[job][(N/2-1)^2] of the same sample (the coarse half of the coupled sample): MINRES
+// then runs on A e = r0 = b - A x0 with the SAME stopping rule ||b - A x_k|| <= tol ||b|| (phibar_k <= tol
+// ||b||, not tol ||r0||), and Q = h^2 (1^T x0 + 1^T e_k).
+template <int N, int R, int MINB, int CM, bool VERIFY, int XM = 0>
 __global__ void __launch_bounds__(TileCfg<N, R, MINB, CM>::BLOCK, MINB)
 minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
-                   int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order) {
+                   int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order,
+                   double* __restrict__ xio) {
+    static_assert(XM != 1 || VERIFY, "writing x needs the VERIFY instantiation (x carried)");
     using K = TileCfg<N, R, MINB, CM>;
     constexpr int PAIRS = K::PAIRS, PW = K::PW, RP = K::RP, TPS = K::TPS, GROUPS = K::GROUPS;
     constexpr bool DS = K::DS, WS = K::WS, CS = K::CS;
@@ -292,20 +299,73 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
         double X0[R], X1[R], Y0[R], Y1[R], T0[R], T1[R];
         double Wa0[VERIFY ? R : 1], Wa1[VERIFY ? R : 1], Wb0[VERIFY ? R : 1], Wb1[VERIFY ? R : 1];
         double x0[VERIFY ? R : 1], x1[VERIFY ? R : 1];
+        double sum_x0 = 0.0;                                 // 1^T x0 (XM = 2)
+        if constexpr (XM == 2) {
+            // x0 = P x_c: the coarse P1 function at the fine nodes (coarse SW-NE triangles, R10): a fine node on
+            // a coarse node takes its value, one on a horizontal / vertical / diagonal coarse edge the edge mean
+            constexpr int CC = N / 2 - 1;
+            const double* xc = xio + (size_t)sj * CC * CC;
+            auto xcv = [&](int I, int J) -> double {
+                return (I >= 1 && I <= CC && J >= 1 && J <= CC) ? __ldg(xc + (J - 1) * CC + (I - 1)) : 0.0;
+            };
+            auto x0f = [&](int i, int j) -> double {
+                if (i > K::C || j > K::C) return 0.0;          // phantom nodes
+                const int I = i >> 1, J = j >> 1;
+                if (!(i & 1) && !(j & 1)) return xcv(I, J);
+                if ((i & 1) && !(j & 1)) return 0.5 * (xcv(I, J) + xcv(I + 1, J));
+                if (!(i & 1) && (j & 1)) return 0.5 * (xcv(I, J) + xcv(I, J + 1));
+                return 0.5 * (xcv(I, J) + xcv(I + 1, J + 1));
+            };
+            double XA[R], XB[R];
+            double s0 = 0.0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const bool rl = (r < R - 1) || top_live;
-            const double b0 = rl ? h2 : 0.0;
-            const double b1 = rl && col1_live ? h2 : 0.0;
-            X0[r] = 0.0; X1[r] = 0.0; Y0[r] = b0; Y1[r] = b1;
-            if constexpr (VERIFY) {
-                Wa0[VERIFY ? r : 0] = Wa1[VERIFY ? r : 0] = Wb0[VERIFY ? r : 0] = Wb1[VERIFY ? r : 0] = 0.0;
-                x0[VERIFY ? r : 0] = x1[VERIFY ? r : 0] = 0.0;
+            for (int r = 0; r < R; ++r) {
+                XA[r] = x0f(i0, j0 + r);
+                XB[r] = x0f(i1, j0 + r);
+                s0 += XA[r] + XB[r];
+                own[r * RP] = XA[r];
+                own[r * RP + PW] = XB[r];
             }
-            own[r * RP] = b0;
-            own[r * RP + PW] = b1;
+            tsync<TPS, GROUPS>(g);                           // the grid holds x0
+            double sc0 = 0.0, sc1 = 0.0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {                    // r0 = b - A x0 (phantom nodes stay 0)
+                double t0, t1;
+                if constexpr (CS) stencil_cs(XA, XB, r, t0, t1, sc0, sc1);
+                else stencil(XA, XB, r, westp, eastp, own, t0, t1);
+                const bool rl = (r < R - 1) || top_live;
+                Y0[r] = rl ? h2 - t0 : 0.0;
+                Y1[r] = rl && col1_live ? h2 - t1 : 0.0;
+                X0[r] = 0.0; X1[r] = 0.0;
+                if constexpr (VERIFY) {
+                    Wa0[VERIFY ? r : 0] = Wa1[VERIFY ? r : 0] = Wb0[VERIFY ? r : 0] = Wb1[VERIFY ? r : 0] = 0.0;
+                    x0[VERIFY ? r : 0] = XA[r];
+                    x1[VERIFY ? r : 0] = XB[r];
+                }
+            }
+            sum_x0 = tsum3<TPS, GROUPS>(s0, 0.0, 0.0, red, tg, g).x;   // its barrier also ends the x0 reads
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                own[r * RP] = Y0[r];
+                own[r * RP + PW] = Y1[r];
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool rl = (r < R - 1) || top_live;
+                const double b0 = rl ? h2 : 0.0;
+                const double b1 = rl && col1_live ? h2 : 0.0;
+                X0[r] = 0.0; X1[r] = 0.0; Y0[r] = b0; Y1[r] = b1;
+                if constexpr (VERIFY) {
+                    Wa0[VERIFY ? r : 0] = Wa1[VERIFY ? r : 0] = Wb0[VERIFY ? r : 0] = Wb1[VERIFY ? r : 0] = 0.0;
+                    x0[VERIFY ? r : 0] = x1[VERIFY ? r : 0] = 0.0;
+                }
+                own[r * RP] = b0;
+                own[r * RP + PW] = b1;
+            }
         }
-        tsync<TPS, GROUPS>(g);                               // the grid holds p_1 = b
+        tsync<TPS, GROUPS>(g);                               // the grid holds p_1 = b (XM = 2: r0)
+        const double bnorm = h2 * (double)K::C;              // ||b||_2 = h^2 sqrt(n), n = C^2
         const double m1 = col1_live ? 1.0 : 0.0, mt = top_live ? 1.0 : 0.0;
         double beta1 = 0.0, tol_b = 0.0, inv_beta1 = 0.0;
         double invb_prev = 0.0, beta_prev = 0.0, alpha_prev = 0.0, sigma_prev = 0.0;
@@ -357,10 +417,10 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 s2q = s1q;
                 s1q = sq;
                 Xq = __fma_rn(phi, sq, Xq);
-            } else {                                         // j = 1: beta_1 = ||b||
+            } else {                                         // j = 1: beta_1 = ||b|| (XM = 2: ||r0||)
                 beta1 = beta;
                 inv_beta1 = invb;
-                tol_b = tol * beta1;
+                tol_b = XM == 2 ? tol * bnorm : tol * beta1;  // Eq. (2) is relative to ||b|| either way
                 phibar = beta1;
             }
             if constexpr (VERIFY) {
@@ -397,6 +457,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
             // last step is discarded
             if (k == 0) {
                 if (beta1 == 0.0) { status = 0; return false; }
+                if (XM == 2 && beta1 <= tol_b) { status = 0; return false; }   // x0 already meets the tolerance
             } else {
                 if (!(phibar == phibar) || !(beta == beta)) { status = 3; return false; }
                 if (phibar <= tol_b) { status = 0; return false; }       // phibar / ||b|| <= tol
@@ -415,7 +476,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
             if (!step(Y0, Y1, X0, X1)) break;
         }
         (void)beta_prev;
-        double relres = phibar * inv_beta1;
+        double relres = XM == 2 ? phibar / bnorm : phibar * inv_beta1;
         if constexpr (VERIFY) {
             // true residual ||b - A x|| / ||b||: x goes through the grid (the last step's grid reads
             // precede its reduction barrier)
@@ -437,11 +498,21 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 rr = fma(res0, res0, fma(res1, res1, rr));
             }
             rr = tsum3<TPS, GROUPS>(rr, 0.0, 0.0, red, tg, g).x;
-            relres = sqrt(rr) * inv_beta1;
+            relres = XM == 2 ? sqrt(rr) / bnorm : sqrt(rr) * inv_beta1;
+            if constexpr (XM == 1) {                         // the coarse solution for the fine half's x0
+                double* xo = xio + (size_t)sj * K::C * K::C;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int j = j0 + r;
+                    if (j > K::C) continue;
+                    xo[(j - 1) * K::C + (i0 - 1)] = x0[VERIFY ? r : 0];
+                    if (col1_live) xo[(j - 1) * K::C + (i1 - 1)] = x1[VERIFY ? r : 0];
+                }
+            }
         }
         if (tg == 0) {
             double* o = out + (size_t)sj * kRecLen;
-            o[0 + slot] = h2 * Xq;
+            o[0 + slot] = h2 * (XM == 2 ? sum_x0 + Xq : Xq);
             o[2 + slot] = (double)k;
             o[4 + slot] = relres;
             o[6 + slot] = (double)status;
@@ -450,19 +521,25 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
     }
 }
 
-template <int N, int R, int MINB, int CM, bool VERIFY>
+template <int N, int R, int MINB, int CM, bool VERIFY, int XM = 0>
 cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
-                     const int* order, cudaStream_t s) {
+                     const int* order, double* xio, cudaStream_t s) {
+    // x-modes exist where the coupled sample's other half is a tile mesh: XM 1 on N <= 32 (coarse halves),
+    // XM 2 on N >= 16 (fine halves)
+    if constexpr ((XM == 1 && N > 32) || (XM == 2 && N < 16) || (XM == 1 && !VERIFY)) {
+        return cudaErrorNotSupported;
+    } else {
     using K = TileCfg<N, R, MINB, CM>;
-    auto kern = minres_tile_kernel<N, R, MINB, CM, VERIFY>;
+    auto kern = minres_tile_kernel<N, R, MINB, CM, VERIFY, XM>;
     static PerDevice<KernelOcc> occ_cache;
     const KernelOcc occ = occ_of(occ_cache, kern, K::BLOCK, K::SMEM);
     if (occ.err != cudaSuccess) return occ.err;
     const uint64_t need = (nb + K::GROUPS - 1) / K::GROUPS;
     const uint64_t grid = std::min<uint64_t>(need, (uint64_t)occ.per_sm * occ.sms);
     if (grid == 0) return cudaSuccess;
-    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order);
+    kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order, xio);
     return cudaGetLastError();
+    }
 }
 
 }  // namespace
@@ -492,29 +569,30 @@ int minres_tile_variant(int N) {
 #define IF_TUNING(...)
 #endif
 // Variant table (index = MLMC_MINRES_TILE_N<N>): <N, R, MINB, CM>; measured with tools/tune_minres.py.
-template <bool V>
+template <bool V, int XM>
 static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, double tol, int max_iter, double* out,
-                                 int slot, unsigned* ctr, const int* order, cudaStream_t s) {
+                                 int slot, unsigned* ctr, const int* order, double* xio, cudaStream_t s) {
+    (void)var;
     switch (N) {
         case 8:   // two systems per warp (16 threads each)
-            IF_TUNING(if (var == 1) return run_tile<8, 2, 5, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 1) return run_tile<8, 2, 5, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             // (conductances in shared memory with 8 / 6 systems-pairs per SM: 0.133 / 0.127 ms vs 0.109 ms on
             // configs[1] level 0; 16 systems per warp-pair cannot hide the extra shared loads)
-            return run_tile<8, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            return run_tile<8, 2, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 16:
-            IF_TUNING(if (var == 1) return run_tile<16, 2, 4, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 2) return run_tile<16, 2, 6, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 1) return run_tile<16, 2, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 2) return run_tile<16, 2, 6, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             // (conductances in shared memory, 6 / 8 CTAs per SM: level-1 pass 0.60 / 0.61 ms vs 0.51 ms)
-            return run_tile<16, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            return run_tile<16, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 32:
-            IF_TUNING(if (var == 1) return run_tile<32, 4, 4, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 2) return run_tile<32, 4, 4, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 3) return run_tile<32, 2, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
+            IF_TUNING(if (var == 1) return run_tile<32, 4, 4, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 2) return run_tile<32, 4, 4, 3, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 3) return run_tile<32, 2, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             // v4 / v5 (conductances in shared memory, 5 / 4 systems per SM): 0.80 / 0.81 ms vs v0 0.74 ms
             // on configs[1] level 2, bit-identical records
-            IF_TUNING(if (var == 4) return run_tile<32, 4, 5, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 5) return run_tile<32, 4, 4, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            return run_tile<32, 4, 3, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 4) return run_tile<32, 4, 5, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 5) return run_tile<32, 4, 4, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            return run_tile<32, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 64:
             // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67, v4 2.97
             // (v4: every conductance in shared memory, two systems per SM; bit-identical records, but the
@@ -522,22 +600,27 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             // (tools/tune_minres.py): v0 1.671 ms, v5 (west conductances in shared memory, no in-loop
             // spills) 1.723, v6 (diagonal in shared memory) 1.722, v1 1.711 -- v0's few L1-resident
             // spill reloads cost less than the shared loads that remove them
-            IF_TUNING(if (var == 1) return run_tile<64, 8, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 2) return run_tile<64, 4, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 3) return run_tile<64, 4, 1, 3, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 4) return run_tile<64, 8, 2, 4, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 5) return run_tile<64, 8, 1, 2, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            IF_TUNING(if (var == 6) return run_tile<64, 8, 1, 1, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);)
-            return run_tile<64, 8, 1, 0, V>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+            IF_TUNING(if (var == 1) return run_tile<64, 8, 1, 3, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 2) return run_tile<64, 4, 1, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 3) return run_tile<64, 4, 1, 3, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 4) return run_tile<64, 8, 2, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 5) return run_tile<64, 8, 1, 2, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 6) return run_tile<64, 8, 1, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            return run_tile<64, 8, 1, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         default: return cudaErrorNotSupported;
     }
 }
 
 cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
-                               unsigned* ctr, bool verify, const int* order, cudaStream_t s) {
+                               unsigned* ctr, bool verify, const int* order, cudaStream_t s, int xmode, double* xio) {
     const int var = minres_tile_variant(N);
-    return verify ? tile_dispatch<true>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, s)
-                  : tile_dispatch<false>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, s);
+    if (xmode == 1)   // coarse half of a coarse-to-fine pair: x is carried (VERIFY) and written out
+        return tile_dispatch<true, 1>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
+    if (xmode == 2)
+        return verify ? tile_dispatch<true, 2>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, xio, s)
+                      : tile_dispatch<false, 2>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
+    return verify ? tile_dispatch<true, 0>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, nullptr, s)
+                  : tile_dispatch<false, 0>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, nullptr, s);
 }
 
 }  // namespace mlmc

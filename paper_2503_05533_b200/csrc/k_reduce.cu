@@ -80,8 +80,7 @@ __device__ __forceinline__ void x_warp(X256& a, u64& ovf) {
 }
 
 __global__ void __launch_bounds__(RT) chunk_sums_kernel(const double* __restrict__ rec, uint64_t nb, int level,
-                                                        double n_f, double n_c, double cff, double cfs,
-                                                        double ccf, double ccs, double* __restrict__ partial,
+                                                        const CostParams cp, double* __restrict__ partial,
                                                         u64* __restrict__ xpart) {
     const uint64_t c0 = blockIdx.x * kChunk;
     double v[kSumsLen];
@@ -102,7 +101,11 @@ __global__ void __launch_bounds__(RT) chunk_sums_kernel(const double* __restrict
         // status 4 = converged after escalation (a failed MINRES solve re-solved by MG-PCG): a success
         const bool fail = (r[6] != 0.0 && r[6] != 4.0) || (level > 0 && r[7] != 0.0 && r[7] != 4.0);
         const bool esc = r[6] == 4.0 || (level > 0 && r[7] == 4.0);
-        const double cost = (cff + cfs * itf) + (level > 0 ? (ccf + ccs * itc) : 0.0);
+        // cost model (R5): fixed + step x iterations; an escalated half (status 4) is charged the failed first
+        // attempt plus the MG-PCG re-solve, whose steps the record holds
+        const double cf = r[6] == 4.0 ? cp.f_esc + cp.f_esc_step * itf : cp.f_fixed + cp.f_step * itf;
+        const double cc = level > 0 ? (r[7] == 4.0 ? cp.c_esc + cp.c_esc_step * itc : cp.c_fixed + cp.c_step * itc) : 0.0;
+        const double cost = cf + cc;
         v[0] += y;
         v[1] = fma(y, y, v[1]);
         v[2] += qf;
@@ -220,14 +223,12 @@ __global__ void combine_chunks_kernel(const double* __restrict__ partial, int nc
     sums[k] = t;
 }
 
-cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, double n_f, double n_c,
-                              double cost_f_fixed, double cost_f_step, double cost_c_fixed, double cost_c_step,
-                              double* chunk_scratch, double* sums, bool accumulate, cudaStream_t s, u64* xsums) {
+cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, const CostParams& cp, double* chunk_scratch,
+                              double* sums, bool accumulate, cudaStream_t s, u64* xsums) {
     const int nchunks = (int)((nb + kChunk - 1) / kChunk);
     u64* xpart = xsums ? reinterpret_cast<u64*>(chunk_scratch + (size_t)kSumsLen * nchunks) : nullptr;
     if (nchunks > 0)
-        chunk_sums_kernel<<<nchunks, RT, 0, s>>>(rec, nb, level, n_f, n_c, cost_f_fixed, cost_f_step,
-                                                  cost_c_fixed, cost_c_step, chunk_scratch, xpart);
+        chunk_sums_kernel<<<nchunks, RT, 0, s>>>(rec, nb, level, cp, chunk_scratch, xpart);
     combine_chunks_kernel<<<1, 32, 0, s>>>(chunk_scratch, nchunks, sums, accumulate ? 1 : 0, xpart, xsums);
     return cudaGetLastError();
 }

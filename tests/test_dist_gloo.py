@@ -226,3 +226,43 @@ def test_exact_sum_exchange_two_ranks_bit_identical():
         noise = ((k * 2654435761 + 97 * l) % 2001 - 1000)
         exact = sum((Fraction(1, 2 ** (2 * l + 4)) + Fraction(int(v), 2 ** (2 * l + 12)) for v in noise), Fraction(0))
         assert single["mean"][l] == float(exact / n) and y == float(exact)
+
+
+# ---------------------------------------------------------------------------- a rank-local failure
+def _worker_fail(rank, world, port, q):
+    """Rank 1's sampler raises in the second round: both ranks must leave mlmc_adaptive_run_host with an
+    error (the failure travels in the round's single all-reduce) instead of rank 0 waiting forever."""
+    import datetime
+    import torch.distributed as dist
+    from paper_2503_05533_b200.api import mlmc_adaptive_run_host
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
+    calls = {"n": 0}
+
+    def sampler(level, n, first, pf, pc, tf, tc):
+        calls["n"] += 1
+        if rank == 1 and calls["n"] > 2:
+            raise RuntimeError("injected rank-local failure")
+        return _dyadic_sampler(level, n, first, pf, pc, tf, tc)
+    try:
+        try:
+            mlmc_adaptive_run_host(8, 4, 1e-3, sampler, k_p=0.05, N_init=40, seed=1, group=dist.group.WORLD)
+            q.put((rank, "no error"))
+        except RuntimeError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_local_sampler_failure_stops_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_fail, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0] != "no error" and res[1] != "no error", res
