@@ -69,6 +69,8 @@ def lib():
             L.or_chol_dense_solve.argtypes = [C.c_int, dp, dp, dp]
             L.or_minres_band.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, C.c_int, dp,
                                          C.POINTER(C.c_int), C.POINTER(C.c_double)]
+            L.or_minres_band_x0.argtypes = [C.c_int, C.c_int, dp, dp, dp, C.c_double, C.c_int, dp,
+                                            C.POINTER(C.c_int), C.POINTER(C.c_double)]
             L.or_round.argtypes = [C.c_double, C.c_int]
             L.or_round.restype = C.c_double
             L.or_chol_band_rounded.argtypes = [C.c_int, C.c_int, dp, dp, C.c_int]
@@ -221,6 +223,16 @@ def minres_band(AB, b, tol: float, max_iter: int = 100000):
     it, rr = C.c_int(), C.c_double()
     st = lib().or_minres_band(n, bwp1 - 1, np.ascontiguousarray(AB).ravel(), np.ascontiguousarray(b, np.float64),
                               tol, max_iter, x, C.byref(it), C.byref(rr))
+    return x, it.value, rr.value, st
+
+
+def minres_band_x0(AB, b, x0, tol: float, max_iter: int = 100000):
+    """MINRES from the initial guess x0 (or_minres_band_x0): stops at phibar_k <= tol ||b||."""
+    n, bwp1 = AB.shape
+    x = np.zeros(n, np.float64)
+    it, rr = C.c_int(), C.c_double()
+    st = lib().or_minres_band_x0(n, bwp1 - 1, np.ascontiguousarray(AB).ravel(), np.ascontiguousarray(b, np.float64),
+                                 np.ascontiguousarray(x0, np.float64), tol, max_iter, x, C.byref(it), C.byref(rr))
     return x, it.value, rr.value, st
 
 

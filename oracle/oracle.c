@@ -491,6 +491,65 @@ done:
     return status;
 }
 
+/* 6b. MINRES from an initial guess x0 (NEXT-4, coarse-to-fine; reading R32): Paige-Saunders on  */
+/*     A e = r0 = b - A x0, x = x0 + e, stopped at the first k with phibar_k <= tol ||b|| -- the relative-   */
+/*     residual criterion of Eq. (2) is relative to ||b||, not to ||r0||.  x0 = 0 gives or_minres_band.      */
+OR_EXPORT int or_minres_band_x0(int n, int bw, const double* AB, const double* b, const double* x0, double tol,
+                                int max_iter, double* x, int* iters_out, double* relres_out) {
+    double *r1 = malloc(sizeof(double) * n), *r2 = malloc(sizeof(double) * n),
+           *y = malloc(sizeof(double) * n), *v = malloc(sizeof(double) * n),
+           *w = malloc(sizeof(double) * n), *w1 = malloc(sizeof(double) * n),
+           *w2 = malloc(sizeof(double) * n);
+    or_band_matvec(n, bw, AB, x0, y);
+    for (int i = 0; i < n; ++i) { r1[i] = r2[i] = y[i] = b[i] - y[i]; w[i] = w2[i] = 0.0; x[i] = x0[i]; }
+    double bnorm = sqrt(dot(n, b, b));
+    double beta1 = sqrt(dot(n, r1, r1));
+    double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, phibar = beta1;
+    double cs = -1.0, sn = 0.0;
+    int k = 0, status = 1;
+    if (beta1 <= tol * bnorm) { status = 0; goto done; }
+    while (k < max_iter) {
+        ++k;
+        for (int i = 0; i < n; ++i) v[i] = y[i] / beta;
+        or_band_matvec(n, bw, AB, v, y);
+        if (k >= 2)
+            for (int i = 0; i < n; ++i) y[i] -= (beta / oldb) * r1[i];
+        double alpha = dot(n, v, y);
+        for (int i = 0; i < n; ++i) y[i] -= (alpha / beta) * r2[i];
+        for (int i = 0; i < n; ++i) { r1[i] = r2[i]; r2[i] = y[i]; }
+        oldb = beta;
+        beta = sqrt(dot(n, r2, r2));
+        double oldeps = epsln;
+        double delta = cs * dbar + sn * alpha;
+        double gbar = sn * dbar - cs * alpha;
+        epsln = sn * beta;
+        dbar = -cs * beta;
+        double gamma = hypot(gbar, beta);
+        if (gamma < DBL_MIN) gamma = DBL_MIN;
+        cs = gbar / gamma;
+        sn = beta / gamma;
+        double phi = cs * phibar;
+        phibar = sn * phibar;
+        for (int i = 0; i < n; ++i) {
+            w1[i] = w2[i];
+            w2[i] = w[i];
+            w[i] = (v[i] - oldeps * w1[i] - delta * w2[i]) / gamma;
+            x[i] += phi * w[i];
+        }
+        if (phibar <= tol * bnorm) { status = 0; break; }
+    }
+done:
+    if (iters_out) *iters_out = k;
+    if (relres_out) {
+        or_band_matvec(n, bw, AB, x, y);
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) { double r = b[i] - y[i]; s += r * r; }
+        *relres_out = bnorm > 0 ? sqrt(s) / bnorm : 0.0;
+    }
+    free(r1); free(r2); free(y); free(v); free(w); free(w1); free(w2);
+    return status;
+}
+
 /* ------------------------------------------------------------------------- */
 /* 7. Precision emulation: round to a binary format with t          */
 /*    significand bits (incl. the implicit one), minimum normal exponent      */

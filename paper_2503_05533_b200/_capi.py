@@ -19,6 +19,7 @@ FMT = {"q": 0, "h": 1, "s": 2, "d": 3}
 SOLVER_MINRES, SOLVER_CHOL_IR, SOLVER_MGCG, SOLVER_CG = 0, 1, 2, 3
 FLAG_VERIFY = 1
 FLAG_ESCALATE = 2
+FLAG_C2F = 4
 
 
 class Problem(C.Structure):

@@ -24,12 +24,13 @@ SUM_FIELDS = ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail", 
 
 
 def precision(solver: str = "minres", u_f: str = "s", u_s: str = "s", u: str = "d", u_r: str = "d",
-              max_iter: int = 0, verify: bool = False, escalate: bool = False) -> K.Precision:
+              max_iter: int = 0, verify: bool = False, escalate: bool = False, c2f: bool = False) -> K.Precision:
     """MINRES (all binary64) or Cholesky-IR with Algorithm 1's quad.
     verify=True (MINRES): also carry x_k and report the true residual; escalate=True (MINRES, IR): a failed solve
-    is solved again by MG-PCG (status 4 when that converges)."""
+    is solved again by MG-PCG (status 4 when that converges); c2f=True (on prec_fine, MINRES): the fine half starts
+    from the P1 interpolation of the coarse half's solution (MLMC_FLAG_C2F, NEXT-4)."""
     s = {"minres": K.SOLVER_MINRES, "chol_ir": K.SOLVER_CHOL_IR, "ir": K.SOLVER_CHOL_IR, "mgcg": K.SOLVER_MGCG, "cg": K.SOLVER_CG}[solver]
-    flags = (K.FLAG_VERIFY if verify else 0) | (K.FLAG_ESCALATE if escalate else 0)
+    flags = (K.FLAG_VERIFY if verify else 0) | (K.FLAG_ESCALATE if escalate else 0) | (K.FLAG_C2F if c2f else 0)
     return K.Precision(s, K.FMT[u_f], K.FMT[u_s], K.FMT[u], K.FMT[u_r], max_iter, flags)
 
 

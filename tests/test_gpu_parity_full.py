@@ -183,3 +183,38 @@ def test_replicate_rmse_within_eps_of_oracle_reference(name, R):
     print(f"{name}: Q_ref(oracle) {q_ref:.6f} (L={ref['L']}, N={ref['N']}, oracle {t_or:.0f} s), "
           f"RMSE/eps {rmse / eps:.3f}")
     assert rmse <= eps, (rmse, eps)
+
+
+# ============================================================================ NEXT-4: coarse-to-fine x0
+@pytest.mark.parametrize("level,n", [(1, 64), (2, 32), (3, 12)])
+def test_coarse_to_fine_initial_guess_matches_oracle(level, n):
+    """MLMC_FLAG_C2F (the fine half from the P1 interpolation of the coarse half's solution, R32) on configs[1]
+    levels 1-3 against the oracle's coarse-to-fine MINRES (oracle/c2f.py) on the same samples: Q_f within the
+    rigorous residual bound of the direct solve, fine iteration counts within max(2, 3%) of the oracle's, the
+    VERIFY true residual <= tol (relative to ||b||), and the coarse half bit-identical to the plain path."""
+    from oracle import c2f
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    P = _oracle(cfg)
+    tf, tc = cfg["tols"][level], cfg["tols"][level - 1]
+    seed = 77
+    mr = precision("minres")
+    plain = ctx.sample_level(level, n, seed=seed, prec_fine=mr, prec_coarse=mr, tol_fine=tf, tol_coarse=tc,
+                             per_sample=True).per_sample
+    pf = precision("minres", c2f=True)
+    ps = ctx.sample_level(level, n, seed=seed, prec_fine=pf, prec_coarse=mr, tol_fine=tf, tol_coarse=tc,
+                          per_sample=True).per_sample
+    assert np.all(ps[:, 6:8] == 0)
+    assert np.array_equal(ps[:, 1], plain[:, 1]) and np.array_equal(ps[:, 3], plain[:, 3])   # coarse half
+    pv = ctx.sample_level(level, n, seed=seed, prec_fine=precision("minres", c2f=True, verify=True), prec_coarse=mr,
+                          tol_fine=tf, tol_coarse=tc, per_sample=True).per_sample
+    assert np.array_equal(pv[:, 0], ps[:, 0]) and np.all(pv[:, 4] <= tf * 1.01)
+    refs = _pmap(lambda k: c2f.coupled_sample_c2f(P, level, seed, k, tf, tc), list(range(n)))
+    Nf = cfg["h0_inv"] << level
+    for k, r in enumerate(refs):
+        x, _ = oc.chol_band_solve(r["AB"], r["b"])
+        q = x.sum() / Nf ** 2
+        assert abs(ps[k, 0] - q) <= tf * np.linalg.norm(r["b"]) * np.linalg.norm(x) * (1 + 1e-6) + 1e-14 * q, k
+        assert abs(ps[k, 2] - r["iters_f"]) <= max(2, 0.03 * r["iters_f"]), (k, ps[k, 2], r["iters_f"])
+    print(f"level {level}: mean fine MINRES steps {plain[:, 2].mean():.1f} from 0, {ps[:, 2].mean():.1f} from P x_c")
+    ctx.close()
