@@ -430,6 +430,10 @@ def run_ours(args):
         line["k3c_fine_meshes"] = fine_leg(local, torch)
         _dbg("fine leg done")
         if rank == 0:
+            line["fine_single_system"] = dd_leg(local, torch)
+            line["c2_level3_coarse_to_fine"] = c2f_leg(local, torch)
+        _dbg("dd / c2f legs done")
+        if rank == 0:
             line["paper_mpml_vs_mlmc"] = paper_leg(local)
         if rank == 0 and world == 1:
             line["cpu_baseline"] = cpu_baseline(seed)
@@ -545,8 +549,20 @@ def c3_leg(local, torch):
                 fac = (N - 1) ** 2 * N * bf                      # band factor n (bw + 1) b_f
                 return n * fac * 3 + fac * 2 * steps_sum + n * 16 * N * N
 
-            alg = solve_bytes(Nf, s[7]) + (solve_bytes(Nc, s[8]) if l else 0.0)
-            gbs = alg / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+            def solve_flops(N, steps_sum):
+                # n bw^2 per factorisation, 4 n bw per substitution pair (x0 and every correction),
+                # 10 n per binary64 residual (one per pair)
+                nn, bw = (N - 1) ** 2, N - 1
+                return n * (nn * bw * bw + 4 * nn * bw + 10 * nn) + steps_sum * (4 * nn * bw + 10 * nn)
+
+            stream_bytes = solve_bytes(Nf, s[7]) + (solve_bytes(Nc, s[8]) if l else 0.0)
+            flops = solve_flops(Nf, s[7]) + (solve_flops(Nc, s[8]) if l else 0.0)
+            # the HBM bytes the method itself needs once the factor is on chip: the triangle
+            # coefficients of both meshes read, the per-sample record written
+            alg = n * (16 * Nf * Nf + (16 * Nc * Nc if l else 0) + 64)
+            tflops = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
+            gbs = stream_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+            key = f"chol_ir_N{Nf}_{'fp16' if uf == 'h' else 'fp32'}_bytes_per_sample"
             # IR-step histogram of the fine solves: a separate untimed pass over
             # the same samples with per-sample records
             ps = ctx.sample_level(l, n, cfg["seed"], 0, prec, prec, cfg["tol"], cfg["tol"], per_sample=True).per_sample
@@ -555,8 +571,90 @@ def c3_leg(local, torch):
                 "h": f"1/{Nf}", "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
                 "mean_ir_steps_fine": s[7] / n, "max_ir_steps_fine": s[9], "failures": s[6],
                 "ir_steps_histogram_fine": {str(int(a)): int(b) for a, b in zip(steps, counts)},
-                "k4_ms": k_ms, "k4_algorithmic_GB": alg / 1e9, "k4_achieved_GBs": gbs,
-                "k4_hbm_frac": gbs / HBM_PEAK_GBS}
+                "k4_ms": k_ms,
+                "k4_roofline": {"bound": "alu", "achieved": tflops, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                "frac": tflops / FP32_PEAK_TFLOPS, "peak_source": ALU["source"] + " (FFMA)",
+                                "flops_basis": "SURVEY 8(d): n bw^2 per factorisation + 4 n bw per substitution "
+                                               "pair + 10 n per residual, fine + coarse"},
+                "k4_algorithmic_bytes_per_sample": alg / n,
+                "k4_dram_bytes_per_sample_ncu": _ncu_traffic(key),
+                "k4_factor_stream_GBs": gbs, "k4_factor_stream_hbm_frac": gbs / HBM_PEAK_GBS}
+    ctx.close()
+    return out
+
+
+def _ncu_traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch / sample from a committed ncu capture
+    (profiles/ncu_traffic.json, written from the round's ncu reports), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(key)
+    except Exception:
+        return None
+
+
+def dd_leg(local, torch):
+    """NEXT-3 / the fine-level critical path: ONE configs[4] system at h = 1/512 to the finest tolerance of an L = 6
+    run (eps_6 = k_p h^2), fine half only -- by K3c in a 2-CTA cluster (what mlmc_sample_level does per sample)
+    and by K3d on the whole GPU (mlmc_dd_run_local, one slab).  Device time, CUDA events."""
+    from paper_2503_05533_b200 import Context, precision
+    from paper_2503_05533_b200.dd import SlabSolver
+    cfg = W.CONFIGS["C5"]
+    ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
+                  L_max=cfg["L_max"], device=local, workspace_bytes=2 << 30)
+    N, level = 512, 6
+    tol = cfg["k_p"] / N ** 2
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r = fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return r, a.elapsed_time(b)
+    mr = precision("minres")
+    ctx.sample_level(level, 1, 7, first_index=99, prec_fine=mr, tol_fine=1e-3, tol_coarse=1e-3)
+    ctx.profile_enable(True)
+    r, ms = timed(lambda: ctx.sample_level(level, 1, 7, first_index=0, prec_fine=mr, tol_fine=tol, tol_coarse=tol,
+                                           per_sample=True).per_sample[0])
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    k3c_ms = sum(p[3] for p in prof if p[0] == "minres" and p[1] == N)
+    eng = SlabSolver(ctx, level, 0, 1)
+    eng.begin(7, level, 0, tol)
+    d, dms = timed(eng.run_local)
+    eng.close()
+    ctx.close()
+    return {"h": "1/512", "tol": tol, "k3c_cluster2": {"ms_fine_kernel": k3c_ms, "iters": r[2], "Q": r[0]},
+            "k3d_whole_gpu": {"ms": dms, "iters": d["iters"], "us_per_step": 1e3 * dms / max(d["iters"], 1),
+                              "Q": d["Q"]},
+            "speedup": k3c_ms / dms if dms > 0 else None}
+
+
+def c2f_leg(local, torch):
+    """NEXT-4 coarse-to-fine x0 on the configs[1] level-3 pass (300 coupled samples, tol 1e-8 / 1e-6): device
+    time of the pass and mean fine MINRES steps from x0 = 0 and from the P1 interpolation of the coarse solution."""
+    from paper_2503_05533_b200 import Context, precision
+    cfg = W.CONFIGS["C2"]
+    ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=8, L_max=3,
+                  device=local, workspace_bytes=1 << 30)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=torch.device("cuda", local))
+    mr = precision("minres")
+    out = {}
+    for name, pf in (("x0=0", mr), ("x0=Pxc", precision("minres", c2f=True))):
+        ctx.sample_level(3, 300, 5, first_index=10**6, prec_fine=pf, prec_coarse=mr, tol_fine=1e-8, tol_coarse=1e-6)
+        ts, its = [], []
+        for rep in range(5):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            r = ctx.sample_level(3, 300, 5, first_index=300 * rep, prec_fine=pf, prec_coarse=mr, tol_fine=1e-8,
+                                 tol_coarse=1e-6)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+            its.append(r.sums["iters_f"] / 300)
+        out[name] = {"ms_median": sorted(ts)[2], "mean_fine_steps": sum(its) / len(its)}
     ctx.close()
     return out
 

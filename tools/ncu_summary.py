@@ -50,7 +50,12 @@ def launches(path):
 
 
 def raw(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """The raw page of an ncu report (or of its CSV export `ncu -i rep --page raw --csv > rep.raw.csv`, made on
+    the GPU box so that the large .ncu-rep need not travel back)."""
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return r[0], r[1], r[2:]
 
