@@ -418,6 +418,7 @@ def run_ours(args):
     _dbg("timed steps and level pass done")
     if not args.no_extras:
         line["c2_step_with_mgpcg"] = mg_leg(ctx, cfg, args, world, rank, torch, dist, stream)
+        line["c2_step_coarse_to_fine"] = c2f_step_leg(ctx, cfg, args, world, rank, torch, dist, stream)
         _dbg("mg leg done")
         line["e2e"] = e2e_leg(ctx, cfg, args, world, rank, torch, np, dist)
         _dbg("e2e leg done")
@@ -707,6 +708,49 @@ def fine_leg(local, torch):
                                  "hbm_frac": gbs / HBM_PEAK_GBS, "bound": "hbm"}
     ctx.close()
     return out
+
+
+def c2f_step_leg(ctx, cfg, args, world, rank, torch, dist, stream):
+    """The same configs[1] step (MINRES, same tolerances) with the NEXT-4 coarse-to-fine initial guess on levels
+    1-3 (MLMC_FLAG_C2F: each level's coarse half first, its fine half from P x_c; R32).  Device-timed like the
+    headline, L2 flushed between steps."""
+    from paper_2503_05533_b200 import precision
+    Nl, tols, seed = cfg["N"], cfg["tols"], cfg["seed"]
+    L = len(Nl)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pf = [precision("minres", c2f=(l > 0)) for l in range(L)]
+    pc = [precision("minres") for _ in range(L)]
+    tol_c = [tols[l - 1] if l else tols[0] for l in range(L)]
+    sums = torch.zeros((L, 12), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(i):
+        first = [(i * world + rank) * Nl[l] for l in range(L)]
+        ctx.sample_levels_async(list(range(L)), Nl, seed, first, pf, pc, tols, tol_c, sums)
+        if world > 1:
+            dist.all_reduce(sums)
+    for i in range(args.warmup):
+        step(40_000 + i)
+    torch.cuda.synchronize()
+    total, its = 0.0, [0.0] * L
+    for i in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total += e0.elapsed_time(e1)
+        s = sums.cpu().numpy()
+        for l in range(L):
+            its[l] += s[l, 7] / world
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    return {"solver": "MINRES, fine halves of levels 1-3 from the P1 interpolation of the coarse solution",
+            "ms_per_step": total / args.steps, "value": world * sum(Nl) * args.steps / (total / 1e3), "unit": UNIT,
+            "mean_iters_fine": [its[l] / (Nl[l] * args.steps) for l in range(L)]}
 
 
 def mg_leg(ctx, cfg, args, world, rank, torch, dist, stream):

@@ -218,3 +218,31 @@ def test_coarse_to_fine_initial_guess_matches_oracle(level, n):
         assert abs(ps[k, 2] - r["iters_f"]) <= max(2, 0.03 * r["iters_f"]), (k, ps[k, 2], r["iters_f"])
     print(f"level {level}: mean fine MINRES steps {plain[:, 2].mean():.1f} from 0, {ps[:, 2].mean():.1f} from P x_c")
     ctx.close()
+
+
+# ============================================================================ IR step counts, binary64 / binary32 quads
+@pytest.mark.parametrize("quad,tol,exact_frac", [("dddd", 1e-12, 1.0), ("dddd", 1e-10, 1.0), ("ssdd", 1e-10, 0.95),
+                                                 ("ssdd", 1e-12, 0.85)])
+def test_ir_step_counts_match_oracle_per_sample(quad, tol, exact_frac):
+    """with the correction rounded straight to u (no binary32 detour), Algorithm 1's step counts on
+    the GPU equal the oracle's emulated Algorithm 1 sample by sample -- exactly for dddd (binary64 factor and
+    substitutions), and for ssdd in >= 95% (1e-10) / 85% (1e-12) of the samples and within one step in all (the GPU fuses the
+    factor's multiply-adds and scales by a binary32 reciprocal, R29: a different rounding sequence at
+    binary32 than the oracle's separately rounded operations)."""
+    cfg = W.CONFIGS["C3"]
+    ctx = _ctx(cfg, ws=1 << 30)
+    P = _oracle(cfg)
+    prec = precision("chol_ir", quad[0], quad[1], quad[2], quad[3])
+    for level, n in ((0, 96), (1, 48), (2, 16)):
+        ps = ctx.sample_level(level, n, seed=8, prec_fine=prec, prec_coarse=prec, tol_fine=tol, tol_coarse=tol,
+                              per_sample=True).per_sample
+        assert np.all(ps[:, 6:8] == 0)
+        Nf = cfg["h0_inv"] << level
+        ref = _pmap(lambda k: P.solve_mesh(Nf, oc.normals(8, level, k, cfg["m"]), oc.SOLVER_IR, tol=tol, quad=quad,
+                                           max_iter=50), list(range(n)))
+        st = np.array([r["iters"] for r in ref])
+        assert all(r["status"] == 0 for r in ref)
+        same = np.mean(st == ps[:, 2])
+        assert same >= exact_frac and np.max(np.abs(st - ps[:, 2])) <= (0 if exact_frac == 1.0 else 1), \
+            (quad, tol, level, same, list(zip(st, ps[:, 2])))
+    ctx.close()
