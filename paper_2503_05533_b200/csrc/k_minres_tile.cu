@@ -112,22 +112,19 @@ __device__ __forceinline__ double4 tsum3(double a, double b, double c, double* b
     if constexpr (TPS <= 32) {
         return make_double4(__shfl_sync(msk, v, 0, W), __shfl_sync(msk, v, O2, W), __shfl_sync(msk, v, 2 * O2, W), 0.0);
     } else {
+        // across the NW warps: lane L < 3 NW of every warp loads warp (L mod NW)'s total of quantity L / NW,
+        // an xor butterfly over the NW lanes of each group adds them -- ((w0 + w1) + (w2 + w3)) + ..., the same
+        // association in every lane (IEEE addition commutes) -- and three shuffles broadcast the totals: per
+        // thread 1 load and log2(NW) adds instead of NW double4 loads and 3 (NW - 1) adds
         constexpr int NW = TPS / 32;
+        static_assert(3 * NW <= 32 && (NW & (NW - 1)) == 0, "one warp holds the 3 x NW warp totals");
         if ((lane & (O2 - 1)) == 0 && lane < 3 * O2) buf[4 * (tg >> 5) + lane / O2] = v;
         tsync<TPS, GROUPS>(g);
-        double4 vv[NW];
+        double u = lane < 3 * NW ? buf[4 * (lane % NW) + lane / NW] : 0.0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) vv[w] = reinterpret_cast<const double4*>(buf)[w];
-#pragma unroll
-        for (int st = 1; st < NW; st *= 2) {
-#pragma unroll
-            for (int w = 0; w + st < NW; w += 2 * st) {
-                vv[w].x += vv[w + st].x;
-                vv[w].y += vv[w + st].y;
-                vv[w].z += vv[w + st].z;
-            }
-        }
-        return vv[0];
+        for (int o = 1; o < NW; o <<= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+        return make_double4(__shfl_sync(0xffffffffu, u, 0), __shfl_sync(0xffffffffu, u, NW),
+                            __shfl_sync(0xffffffffu, u, 2 * NW), 0.0);
     }
 }
 
