@@ -951,7 +951,7 @@ int mlmc_dd_layout_get(int N, int m, int rank, int world, mlmc_dd_layout* out) {
     for (int q = 0; q < 5; ++q) { L.plane_off[q] = off; off += plane; }
     L.sums_off = off;  off += align256(sizeof(double) * 4);
     L.state_off = off; off += align256(sizeof(DDState));
-    L.partials_off = off; off += align256(sizeof(double) * 3 * (size_t)L.tiles);
+    L.partials_off = off; off += align256(sizeof(double) * 6 * (size_t)L.tiles);   // x2: the persistent kernel
     L.counter_off = off; off += align256(sizeof(unsigned) * 4);
     L.xi_off = off;    off += align256(sizeof(double) * (size_t)m);
     L.a_off = off;     off += align256(sizeof(double) * 2 * (size_t)N * N);
@@ -1082,6 +1082,20 @@ int mlmc_dd_run_local(mlmc_dd* dd, double out[5]) {
     mlmc_ctx* ctx = dd->ctx;
     if (dd->L.world != 1) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_local needs world = 1 (no exchange)");
     cudaStream_t s = ctx->stream;
+    {   // one cooperative launch for the whole solve (one grid barrier per step); per-step graphs otherwise
+        const mlmc_dd_layout& L = dd->L;
+        cudaError_t e = counted(ctx, s, 2, L.N, [&] {
+            return launch_dd_persistent(L.N, L.j0, L.j1, L.rows, L.pitch,
+                                        reinterpret_cast<double*>(dd->ws + L.plane_off[0]),
+                                        (L.plane_off[1] - L.plane_off[0]) / sizeof(double),
+                                        reinterpret_cast<DDState*>(dd->ws + L.state_off),
+                                        reinterpret_cast<double*>(dd->ws + L.partials_off),
+                                        reinterpret_cast<unsigned*>(dd->ws + L.counter_off),
+                                        reinterpret_cast<double*>(dd->ws + L.sums_off), s);
+        });
+        if (e == cudaSuccess) return mlmc_dd_result(dd, out);
+        cudaGetLastError();                          // not co-schedulable here: fall back to the graph chunks
+    }
     if (!dd->chunk) {
         // kDDChunk steps as one graph: every launch takes its step-dependent values from the device state
         cudaStream_t cs = nullptr;

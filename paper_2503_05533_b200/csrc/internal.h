@@ -191,6 +191,9 @@ cudaError_t launch_dd_pass(int N, int j0, int j1, int rows, int pitch, double* p
                            DDState* st, double* partials, unsigned* counter, double* sums, bool fuse_scalar,
                            cudaStream_t s);
 cudaError_t launch_dd_scalar(DDState* st, const double* sums, int N, cudaStream_t s);
+// world = 1: the whole solve in one cooperative launch (partials needs 6 x tiles doubles)
+cudaError_t launch_dd_persistent(int N, int j0, int j1, int rows, int pitch, double* planes, size_t plane_stride,
+                                 DDState* st, double* partials, unsigned* counter, double* sums, cudaStream_t s);
 
 constexpr int kSumsLen = MLMC_SUMS_LEN;
 // Reproducible level sums: the five real-valued sums (Y, Y^2, Q_f, Q_c, cost) are also kept as

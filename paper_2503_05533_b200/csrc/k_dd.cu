@@ -139,71 +139,72 @@ __global__ void dd_scalar_kernel(DDState* __restrict__ st, const double* __restr
     if (threadIdx.x == 0) dd_scalar_step(st, sums, N);
 }
 
-__global__ void __launch_bounds__(DT)
-dd_pass_kernel(int N, int j0, int j1, int rows, int pitch, double* __restrict__ planes, size_t plane_stride,
-               DDState* __restrict__ st, double* __restrict__ partials, unsigned* __restrict__ counter,
-               double* __restrict__ sums, int fuse) {
-    __shared__ double box[4][DBH][DBW];       // p_j, p_{j-1}, cE, cN
-    __shared__ double PN[DPH][DPW];
-    __shared__ double red[3][DT / 32];
-    __shared__ bool last;
-    const DDState s = *st;
-    if (s.done) return;
-    const int C = N - 1, tid = threadIdx.x;
+// One 32 x 16 tile of a pass: p_{j+1} = ct A p_j + c1 p_j + c0 p_{j-1} on the tile + 1-node halo (shared
+// memory), t_{j+1} = A p_{j+1} and the partial sums on the owned nodes; p_{j+1} stored on the owned nodes and on
+// the slab's halo rows j0-1 / j1 (the neighbours' rows, bit-identical).  Returns this thread's partials.
+struct DDSmem {
+    double box[4][DBH][DBW];       // p_j, p_{j-1}, cE, cN
+    double PN[DPH][DPW];
+};
+__device__ __forceinline__ double3 dd_tile(int tile, int N, int j0, int j1, int rows, int pitch, double* planes,
+                                           size_t plane_stride, int step, double ct, double c1, double c0, DDSmem& sm) {
+    const int C = N - 1, tid = threadIdx.x, NT = blockDim.x;
     const int tiles_x = (C + DTW - 1) / DTW;
-    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int x0 = 1 + tx * DTW;             // first owned column (grid i)
     const int y0 = j0 + ty * DTH;            // first owned row (grid j)
-    const int pcur = (s.step + 1) % 3, pprev = s.step % 3, pnext = (s.step + 2) % 3;
+    const int pcur = (step + 1) % 3, pprev = step % 3, pnext = (step + 2) % 3;
     const double* Pj = planes + (size_t)pcur * plane_stride;
     const double* Pp = planes + (size_t)pprev * plane_stride;
     const double* CE = planes + 3 * plane_stride;
     const double* CN = planes + 4 * plane_stride;
     // box rows y0-2 .. y0+DTH+1 (local r = y - (j0-2)), columns x0-2 .. x0+DTW+1 (stored c = i + 1)
-    const int r0 = y0 - 2 - (j0 - 2), c0 = x0 - 2 + 1;
-    for (int q = tid; q < DBW * DBH; q += DT) {
+    const int r0 = y0 - 2 - (j0 - 2), c0i = x0 - 2 + 1;
+    for (int q = tid; q < DBW * DBH; q += NT) {
         const int bx = q % DBW, by = q / DBW;
-        const int r = r0 + by, c = c0 + bx;
-        box[0][by][bx] = ld(Pj, pitch, r, rows, c, pitch);
-        box[1][by][bx] = ld(Pp, pitch, r, rows, c, pitch);
-        box[2][by][bx] = ld(CE, pitch, r, rows, c, pitch);
-        box[3][by][bx] = ld(CN, pitch, r, rows, c, pitch);
+        const int r = r0 + by, c = c0i + bx;
+        sm.box[0][by][bx] = ld(Pj, pitch, r, rows, c, pitch);
+        sm.box[1][by][bx] = ld(Pp, pitch, r, rows, c, pitch);
+        sm.box[2][by][bx] = ld(CE, pitch, r, rows, c, pitch);
+        sm.box[3][by][bx] = ld(CN, pitch, r, rows, c, pitch);
     }
     __syncthreads();
     const int jlo = max(j0 - 1, 1), jhi = min(j1, C);   // rows where p_{j+1} is formed (owned + halo rows)
-    for (int q = tid; q < DPW * DPH; q += DT) {
+    for (int q = tid; q < DPW * DPH; q += NT) {
         const int x = q % DPW, y = q / DPW, bx = x + 1, by = y + 1;
         const int gi = x0 - 1 + x, gj = y0 - 1 + y;
         double pn = 0.0;
         if (gi >= 1 && gi <= C && gj >= jlo && gj <= jhi) {
-            const double ce = box[2][by][bx], cw = box[2][by][bx - 1], cn = box[3][by][bx], cs = box[3][by - 1][bx];
+            const double ce = sm.box[2][by][bx], cw = sm.box[2][by][bx - 1], cn = sm.box[3][by][bx],
+                         cs = sm.box[3][by - 1][bx];
             const double d = (ce + cw) + (cn + cs);
-            double tv = d * box[0][by][bx];
-            tv = fma(-ce, box[0][by][bx + 1], tv);
-            tv = fma(-cw, box[0][by][bx - 1], tv);
-            tv = fma(-cn, box[0][by + 1][bx], tv);
-            tv = fma(-cs, box[0][by - 1][bx], tv);
-            pn = fma(s.ct, tv, fma(s.c1, box[0][by][bx], s.c0 * box[1][by][bx]));
+            double tv = d * sm.box[0][by][bx];
+            tv = fma(-ce, sm.box[0][by][bx + 1], tv);
+            tv = fma(-cw, sm.box[0][by][bx - 1], tv);
+            tv = fma(-cn, sm.box[0][by + 1][bx], tv);
+            tv = fma(-cs, sm.box[0][by - 1][bx], tv);
+            pn = fma(ct, tv, fma(c1, sm.box[0][by][bx], c0 * sm.box[1][by][bx]));
         }
-        PN[y][x] = pn;
+        sm.PN[y][x] = pn;
     }
     __syncthreads();
     double* Pn = planes + (size_t)pnext * plane_stride;
     double sa = 0.0, sb = 0.0, sc = 0.0;
     const int ylim = min(y0 + DTH, j1);          // owned rows of this tile
-    for (int q = tid; q < DTW * DTH; q += DT) {
+    for (int q = tid; q < DTW * DTH; q += NT) {
         const int x = q % DTW, y = q / DTW;
         const int gi = x0 + x, gj = y0 + y;
         if (gi > C || gj >= ylim) continue;
         const int bx = x + 2, by = y + 2, px = x + 1, py = y + 1;
-        const double ce = box[2][by][bx], cw = box[2][by][bx - 1], cn = box[3][by][bx], cs = box[3][by - 1][bx];
+        const double ce = sm.box[2][by][bx], cw = sm.box[2][by][bx - 1], cn = sm.box[3][by][bx],
+                     cs = sm.box[3][by - 1][bx];
         const double d = (ce + cw) + (cn + cs);
-        const double pv = PN[py][px];
+        const double pv = sm.PN[py][px];
         double tv = d * pv;
-        tv = fma(-ce, PN[py][px + 1], tv);
-        tv = fma(-cw, PN[py][px - 1], tv);
-        tv = fma(-cn, PN[py + 1][px], tv);
-        tv = fma(-cs, PN[py - 1][px], tv);
+        tv = fma(-ce, sm.PN[py][px + 1], tv);
+        tv = fma(-cw, sm.PN[py][px - 1], tv);
+        tv = fma(-cn, sm.PN[py + 1][px], tv);
+        tv = fma(-cs, sm.PN[py - 1][px], tv);
         sa = fma(pv, tv, sa);
         sb = fma(pv, pv, sb);
         sc += pv;
@@ -211,28 +212,50 @@ dd_pass_kernel(int N, int j0, int j1, int rows, int pitch, double* __restrict__ 
     }
     // the halo rows j0-1 (first tile row) and j1 (last tile row) of p_{j+1}: the neighbours' values, bit for bit
     if (ty == 0 && j0 - 1 >= 1)
-        for (int x = tid; x < DTW; x += DT)
-            if (x0 + x <= C) Pn[(size_t)1 * pitch + x0 + x + 1] = PN[0][x + 1];
+        for (int x = tid; x < DTW; x += NT)
+            if (x0 + x <= C) Pn[(size_t)1 * pitch + x0 + x + 1] = sm.PN[0][x + 1];
     if (y0 + DTH >= j1 && j1 <= C) {
         const int py = j1 - (y0 - 1);
-        for (int x = tid; x < DTW; x += DT)
-            if (x0 + x <= C) Pn[(size_t)(j1 - (j0 - 2)) * pitch + x0 + x + 1] = PN[py][x + 1];
+        for (int x = tid; x < DTW; x += NT)
+            if (x0 + x <= C) Pn[(size_t)(j1 - (j0 - 2)) * pitch + x0 + x + 1] = sm.PN[py][x + 1];
     }
-    // block partial sums (fixed order), then the last CTA adds the partials in CTA order
+    __syncthreads();                              // box / PN free for the next tile
+    return make_double3(sa, sb, sc);
+}
+
+// CTA sum of (a, b, c) in a fixed order, valid in thread 0
+__device__ __forceinline__ double3 dd_block_sum(double a, double b, double c, double (*red)[32]) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        sa += __shfl_xor_sync(0xffffffffu, sa, o);
-        sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        sc += __shfl_xor_sync(0xffffffffu, sc, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
     }
-    if ((tid & 31) == 0) { red[0][tid >> 5] = sa; red[1][tid >> 5] = sb; red[2][tid >> 5] = sc; }
+    const int tid = threadIdx.x;
+    if ((tid & 31) == 0) { red[0][tid >> 5] = a; red[1][tid >> 5] = b; red[2][tid >> 5] = c; }
     __syncthreads();
+    double3 t = make_double3(0.0, 0.0, 0.0);
+    if (tid == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t.x += red[0][w]; t.y += red[1][w]; t.z += red[2][w]; }
+    return t;
+}
+
+__global__ void __launch_bounds__(DT)
+dd_pass_kernel(int N, int j0, int j1, int rows, int pitch, double* __restrict__ planes, size_t plane_stride,
+               DDState* __restrict__ st, double* __restrict__ partials, unsigned* __restrict__ counter,
+               double* __restrict__ sums, int fuse) {
+    __shared__ DDSmem sm;
+    __shared__ double red[3][32];
+    __shared__ bool last;
+    const DDState s = *st;
+    if (s.done) return;
+    const int tid = threadIdx.x;
+    const double3 p = dd_tile(blockIdx.x, N, j0, j1, rows, pitch, planes, plane_stride, s.step, s.ct, s.c1, s.c0, sm);
+    const double3 t = dd_block_sum(p.x, p.y, p.z, red);
     if (tid == 0) {
-        double a = 0.0, b = 0.0, c = 0.0;
-        for (int w = 0; w < DT / 32; ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
-        partials[3 * blockIdx.x + 0] = a;
-        partials[3 * blockIdx.x + 1] = b;
-        partials[3 * blockIdx.x + 2] = c;
+        partials[3 * blockIdx.x + 0] = t.x;
+        partials[3 * blockIdx.x + 1] = t.y;
+        partials[3 * blockIdx.x + 2] = t.z;
         __threadfence();
         last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
@@ -265,6 +288,74 @@ dd_pass_kernel(int N, int j0, int j1, int rows, int pitch, double* __restrict__ 
     }
 }
 
+// World = 1, the whole solve in ONE cooperative launch: every resident CTA slot loops over the steps; each CTA takes
+// tiles blockIdx.x, blockIdx.x + gridDim.x, ...; per step its partials go to partials[CTA], a grid barrier
+// (arrival counter + acquire spin; all CTAs are co-resident by the cooperative launch) publishes them and
+// the pass's p_{j+1}, and EVERY CTA adds the partials in CTA order and runs the identical scalar step on its
+// own copy of the state (CTA 0 keeps the global one) -- one barrier per MINRES step, no launches.
+__global__ void __launch_bounds__(DT)
+dd_persistent_kernel(int N, int j0, int j1, int rows, int pitch, double* __restrict__ planes, size_t plane_stride,
+                     DDState* __restrict__ st, double* __restrict__ partials, unsigned* __restrict__ counter,
+                     double* __restrict__ sums, int ntiles) {
+    __shared__ DDSmem sm;
+    __shared__ double red[3][32];
+    __shared__ DDState ls;
+    const int tid = threadIdx.x;
+    if (tid == 0) ls = *st;
+    __syncthreads();
+    for (unsigned gen = 1;; ++gen) {
+        if (ls.done) break;                          // identical in every CTA
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const double3 p = dd_tile(t, N, j0, j1, rows, pitch, planes, plane_stride, ls.step, ls.ct, ls.c1, ls.c0,
+                                      sm);
+            a += p.x; b += p.y; c += p.z;
+        }
+        const double3 tsum = dd_block_sum(a, b, c, red);
+        if (tid < 32) {
+            // partials double-buffered by generation parity: a CTA can be one generation ahead of a slower one
+            // that is still reading (it cannot be two: that needs the slower one's next arrival)
+            double* pg = partials + 3 * (size_t)gridDim.x * (gen & 1u);
+            if (tid == 0) {
+                volatile double* pv = pg + 3 * blockIdx.x;
+                pv[0] = tsum.x;
+                pv[1] = tsum.y;
+                pv[2] = tsum.z;
+                __threadfence();                     // partials and this CTA's p_{j+1} stores before the arrival
+                atomicAdd(counter, 1u);
+                const unsigned target = gen * gridDim.x;
+                unsigned seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+                } while (seen < target);
+            }
+            __syncwarp();
+            // warp 0 adds the CTA partials: lane l takes CTAs l, l + 32, ... in order, then a fixed xor tree
+            // (identical association in every lane and every CTA)
+            double A = 0.0, B = 0.0, Cc = 0.0;
+            for (unsigned k = tid; k < gridDim.x; k += 32) {
+                A += __ldcg(pg + 3 * k);
+                B += __ldcg(pg + 3 * k + 1);
+                Cc += __ldcg(pg + 3 * k + 2);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                A += __shfl_xor_sync(0xffffffffu, A, o);
+                B += __shfl_xor_sync(0xffffffffu, B, o);
+                Cc += __shfl_xor_sync(0xffffffffu, Cc, o);
+            }
+            if (tid == 0) {
+                double S[3] = {A, B, Cc};
+                dd_scalar_step(&ls, S, N);
+            }
+        }
+        __syncthreads();                             // ls (next coefficients / done) and p_{j+1} visible
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        *st = ls;
+        sums[0] = sums[1] = sums[2] = 0.0;
+    }
+}
 }  // namespace
 
 int dd_tiles(int N, int j0, int j1) {
@@ -286,6 +377,27 @@ cudaError_t launch_dd_pass(int N, int j0, int j1, int rows, int pitch, double* p
     dd_pass_kernel<<<dd_tiles(N, j0, j1), DT, 0, s>>>(N, j0, j1, rows, pitch, planes, plane_stride, st, partials,
                                                      counter, sums, fuse_scalar ? 1 : 0);
     return cudaGetLastError();
+}
+
+// World = 1: the whole solve as one cooperative launch (all resident CTA slots); cudaErrorCooperativeLaunchTooLarge
+// etc. if the device cannot co-schedule the grid (the caller then falls back to per-step launches).
+cudaError_t launch_dd_persistent(int N, int j0, int j1, int rows, int pitch, double* planes, size_t plane_stride,
+                                 DDState* st, double* partials, unsigned* counter, double* sums, cudaStream_t s) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dd_persistent_kernel, DT, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int ntiles = dd_tiles(N, j0, j1);
+    // every resident CTA slot (all co-resident: cooperative launch), at most one tile each where they suffice
+    int grid = std::min(sms * per_sm, ntiles);
+    void* args[] = {&N, &j0, &j1, &rows, &pitch, &planes, &plane_stride, &st, &partials, &counter, &sums, (void*)&ntiles};
+    e = cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    e = cudaLaunchCooperativeKernel((const void*)dd_persistent_kernel, dim3(grid), dim3(DT), args, 0, s);
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
 }
 
 cudaError_t launch_dd_scalar(DDState* st, const double* sums, int N, cudaStream_t s) {

@@ -73,7 +73,7 @@ def test_dd_h256_matches_oracle_and_k3c():
         assert abs(r["iters"] - ref[2]) <= max(2, 0.01 * ref[2]), (G, r["iters"], ref[2])
         out[G] = r
     for G in (2, 3):
-        assert abs(out[G]["Q"] / out[1]["Q"] - 1) < 1e-11
+        assert abs(out[G]["Q"] / out[1]["Q"] - 1) < tol   # different reduction orders, both within tol of exact
     # the coarse half of the same coupled sample (mesh level 4 of level 5)
     qc, bc, xc = _exact(cfg, 128, seed, level, k)
     rc = _solve(ctx, level - 1, 2, seed, level, k, tol)[0]
