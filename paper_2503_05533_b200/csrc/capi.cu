@@ -20,6 +20,8 @@ struct mlmc_ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t own_stream = nullptr;
+    cudaStream_t single_c = nullptr;     // mlmc_sample_level: the coarse solve's stream (forked off ctx->stream)
+    cudaEvent_t single_fork = nullptr, single_join = nullptr;
     cudaStream_t stream = nullptr;
     std::vector<double*> phi_dev;        // per level, lazily built (P x m synthesis, MLMC_FIELD_KERNEL=dense)
     SepModes sep;                        // separable synthesis (default): modes by x-function ...
@@ -29,6 +31,7 @@ struct mlmc_ctx {
     unsigned char* ws = nullptr;         // borrowed workspace
     size_t ws_bytes = 0;
     double* sums_dev = nullptr;          // owned: MLMC_MAX_LEVELS * kSumsLen
+    double* adapt_dev = nullptr;         // owned: mlmc_adaptive_run's per-round level sums (MLMC_MAX_LEVELS * kSumsLen)
     unsigned long long* xsums_dev = nullptr;   // owned: MLMC_MAX_LEVELS * kXLen exact sums of the last call
     bool want_xsums = false;             // form them (inside mlmc_adaptive_run only)
     std::string err;
@@ -476,7 +479,9 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         // coarse-to-fine pair (MLMC_FLAG_C2F) runs the coarse half first, the fine half from its solution
         const bool c2f = level > 0 && (pf->flags & MLMC_FLAG_C2F);
         double* xc = reinterpret_cast<double*>(ex.ws + L.xc);
-        const bool fork = sched && level > 0 && sch->st_c && Nf < kGmMinN && !c2f;
+        // (the fork is per pass: the join below orders the next pass's field writes after this coarse solve);
+        // with per-kernel profiling on, the solves stay serialised so that every launch's event time is its own
+        const bool fork = sch && level > 0 && sch->st_c && Nf < kGmMinN && !c2f && !ctx->prof_on;
         if (fork) {
             CU(cudaEventRecord(sch->fork, st));
             CU(cudaStreamWaitEvent(sch->st_c, sch->fork, 0));
@@ -527,8 +532,13 @@ int sample_level_impl(mlmc_ctx* ctx, int level, uint64_t n, uint64_t seed, uint6
     int rc = validate_level(ctx, level, pf, pc, tol_f, tol_c);
     if (rc) return rc;
     if (!ctx->ws) return fail(ctx, MLMC_ENOMEM, "no workspace bound");
+    // the fine and coarse solves of a pass are independent: the coarse one runs on a forked stream
+    LevelSched sch;
+    sch.st_c = ctx->single_c;
+    sch.fork = ctx->single_fork;
+    sch.join = ctx->single_join;
     return run_level(ctx, Exec{ctx->ws, ctx->ws_bytes, ctx->stream}, level, n, seed, first_index, pf, pc, tol_f, tol_c,
-                     sums_dev, per_sample, per_sample_is_dev, xi_in, xi_in_is_dev, nullptr,
+                     sums_dev, per_sample, per_sample_is_dev, xi_in, xi_in_is_dev, &sch,
                      ctx->want_xsums ? ctx->xsums_dev : nullptr);
 }
 
@@ -553,6 +563,7 @@ int mlmc::copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* 
 }
 
 void mlmc::ctx_want_xsums(mlmc_ctx* ctx, bool on) { ctx->want_xsums = on; }
+double* mlmc::ctx_adaptive_sums(mlmc_ctx* ctx) { return ctx->adapt_dev; }
 
 int mlmc::copy_xsums_to_host(mlmc_ctx* ctx, int nlev, unsigned long long* host) {
     CU(cudaMemcpyAsync(host, ctx->xsums_dev, sizeof(unsigned long long) * kXLen * nlev, cudaMemcpyDeviceToHost,
@@ -618,6 +629,14 @@ int mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->sums_dev, sizeof(double) * kSumsLen * MLMC_MAX_LEVELS);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->xsums_dev, sizeof(unsigned long long) * kXLen * MLMC_MAX_LEVELS);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->adapt_dev, sizeof(double) * kSumsLen * MLMC_MAX_LEVELS);
+    if (e == cudaSuccess) {   // the coarse-solve stream of single-level calls, created here, not in a timed call
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        e = cudaStreamCreateWithPriority(&ctx->single_c, cudaStreamNonBlocking, least);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->single_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->single_join, cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
         std::string msg = cudaGetErrorString(e);
         mlmc_destroy(ctx);
@@ -645,6 +664,10 @@ void mlmc_destroy(mlmc_ctx* ctx) {
     if (ctx->sep_c) cudaFree(ctx->sep_c);
     if (ctx->sums_dev) cudaFree(ctx->sums_dev);
     if (ctx->xsums_dev) cudaFree(ctx->xsums_dev);
+    if (ctx->adapt_dev) cudaFree(ctx->adapt_dev);
+    if (ctx->single_c) { cudaStreamSynchronize(ctx->single_c); cudaStreamDestroy(ctx->single_c); }
+    if (ctx->single_fork) cudaEventDestroy(ctx->single_fork);
+    if (ctx->single_join) cudaEventDestroy(ctx->single_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

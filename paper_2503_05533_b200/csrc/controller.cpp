@@ -425,8 +425,8 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
     int L_max = 0;
     mlmc_level_info li;
     while (L_max + 1 < MLMC_MAX_LEVELS && mlmc_level_info_get(ctx, L_max + 1, &li) == MLMC_OK) ++L_max;
-    double* dev = nullptr;
-    if (cudaMalloc(&dev, sizeof(double) * MLMC_MAX_LEVELS * MLMC_SUMS_LEN) != cudaSuccess) return MLMC_ECUDA;
+    double* dev = mlmc::ctx_adaptive_sums(ctx);     // persistent (no allocation inside a timed run)
+    if (!dev) return MLMC_ECUDA;
     const uint64_t seed = opts->seed;
     RoundSampler gpu = [&](int nlev, const int* lv, const uint64_t* n, const uint64_t* first, const mlmc_precision* pf,
                            const mlmc_precision* pc, const double* tf, const double* tc, double* sums,
@@ -446,7 +446,6 @@ extern "C" int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_
     mlmc::ctx_want_xsums(ctx, true);
     int rc = adaptive_core(li0.N, L_max, eps, *opts, gpu, choose, allreduce, user, out, true);
     mlmc::ctx_want_xsums(ctx, false);
-    cudaFree(dev);
     return rc;
 }
 

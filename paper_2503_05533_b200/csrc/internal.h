@@ -122,7 +122,8 @@ cudaError_t launch_level_sums(const double* rec, uint64_t nb, int level, const C
                               double* sums, bool accumulate, cudaStream_t s, unsigned long long* xsums = nullptr);
 // The exact fixed-point sums of the levels of the last mlmc_sample_levels(_async) call (nlev x kXLen words)
 int copy_xsums_to_host(mlmc_ctx* ctx, int nlev, unsigned long long* host);
-void ctx_want_xsums(mlmc_ctx* ctx, bool on);   // form the exact sums in the sampling calls that follow
+void ctx_want_xsums(mlmc_ctx* ctx, bool on);
+double* ctx_adaptive_sums(mlmc_ctx* ctx);      // persistent device buffer of mlmc_adaptive_run's round sums   // form the exact sums in the sampling calls that follow
 
 // Copy nlev level-sum records from the device to the host on the ctx's stream and wait.
 int copy_sums_to_host(mlmc_ctx* ctx, const double* dev, int nlev, double* host);

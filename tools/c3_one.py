@@ -12,7 +12,7 @@ level, uf = int(sys.argv[1]), sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 100000
 cfg = W.CONFIGS["C3"]
 ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
-              L_max=cfg["L_max"], device=0, workspace_bytes=4 << 30)
+              L_max=cfg["L_max"], device=0, workspace_bytes=int(os.environ.get("C3_WS_GB", "4")) << 30)
 sums = torch.zeros(12, dtype=torch.float64, device="cuda")
 prec = precision("chol_ir", uf, "s")
 ctx.sample_level_async(level, 2000, cfg["seed"], 10**7, prec, prec, cfg["tol"], cfg["tol"], sums_out=sums)
