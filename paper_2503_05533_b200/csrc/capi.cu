@@ -1,5 +1,6 @@
 // capi.cu -- the C-ABI of include/mlmc.h: plan, workspace, per-level sampling and Algorithm 2.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -449,6 +450,10 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
     int rc;
     CU(cudaMemsetAsync(sums_dev, 0, sizeof(double) * kSumsLen, st));
     if (xsums) CU(cudaMemsetAsync(xsums, 0, sizeof(unsigned long long) * kXLen, st));
+    struct NvtxRange {   // Nsight / NVTX range of the level's passes (a no-op without a tool attached)
+        explicit NvtxRange(int l) { char b[48]; std::snprintf(b, sizeof(b), "mlmc level %d", l); nvtxRangePushA(b); }
+        ~NvtxRange() { nvtxRangePop(); }
+    } nvtx_range(level);
     for (uint64_t done = 0; done < n;) {
         const uint64_t nb = std::min<uint64_t>(B, n - done);
         CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, st));

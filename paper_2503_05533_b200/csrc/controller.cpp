@@ -13,8 +13,12 @@
 // of a round in one mlmc_sample_levels_async call) or over a caller-supplied
 // host sampler (mlmc_adaptive_run_host: CPU tests of the controller and of the
 // multi-rank exchange).
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -171,6 +175,9 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
         cost = n > 0 ? sum(l, 4) / n : 0.0;
     };
 
+    // MLMC_ROUND_LOG=<path>: rank 0 appends one JSON line per round (round, L, N_l, level statistics, eps_l,
+    // the two tests) -- the run's trace, for long runs and post-mortems
+    const char* log_path = o.rank == 0 ? std::getenv("MLMC_ROUND_LOG") : nullptr;
     while (L <= L_max && rounds < max_rounds) {
         ++rounds;
         epsl.assign(L + 1, o.fixed_tol > 0 ? o.fixed_tol : 1e-10);
@@ -210,8 +217,10 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
             std::vector<double> s(lv.size() * MLMC_SUMS_LEN, 0.0);
             std::vector<u64> xs(exact ? lv.size() * kXLen : 0, 0);
             auto t0 = std::chrono::steady_clock::now();
+            nvtxRangePushA("mlmc adaptive round: sampling");
             local_rc = sampler((int)lv.size(), lv.data(), cnt.data(), first.data(), pf.data(), pc.data(), tf.data(),
                                tc.data(), s.data(), exact ? xs.data() : nullptr);
+            nvtxRangePop();
             solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             // a rank-local failure must not leave the other ranks waiting in the exchange: the error
             // travels in the round's all-reduce and every rank returns together
@@ -293,6 +302,19 @@ int adaptive_core(int h0_inv, int L_max, double eps, const mlmc_adaptive_opts& o
         double vsum = 0.0;
         for (int l = 0; l <= L; ++l) vsum += V[l] / (double)acc[l].drawn;                 // R25
         const bool var_ok = vsum <= TOL * TOL / 2.0;
+        if (log_path) {
+            if (FILE* f = std::fopen(log_path, "a")) {
+                std::fprintf(f, "{\"round\": %d, \"L\": %d, \"eps\": %.17g, \"bias_fail\": %s, \"var_ok\": %s, "
+                                "\"solve_seconds\": %.6g, \"levels\": [", rounds, L, TOL, bias_fail ? "true" : "false",
+                             var_ok ? "true" : "false", solve_s);
+                for (int l = 0; l <= L; ++l)
+                    std::fprintf(f, "%s{\"N\": %llu, \"mean\": %.17g, \"var\": %.17g, \"cost\": %.17g, "
+                                    "\"eps_l\": %.17g, \"target\": %.17g}", l ? ", " : "",
+                                 (unsigned long long)acc[l].drawn, mean[l], V[l], C[l], epsl[l], target[l]);
+                std::fprintf(f, "]}\n");
+                std::fclose(f);
+            }
+        }
         if (!bias_fail && var_ok) { code = MLMC_OK; break; }                                // steps 12-13
         if (bias_fail) {
             if (L == L_max) {

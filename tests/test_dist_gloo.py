@@ -266,3 +266,17 @@ def test_rank_local_sampler_failure_stops_every_rank():
     for p in procs:
         p.join(timeout=60)
     assert res[0] != "no error" and res[1] != "no error", res
+
+
+def test_round_log_json_lines(tmp_path, monkeypatch):
+    """MLMC_ROUND_LOG: one JSON line per adaptive round (the controller's trace), consistent with the result."""
+    import json
+    path = tmp_path / "rounds.jsonl"
+    monkeypatch.setenv("MLMC_ROUND_LOG", str(path))
+    r = _run_dyadic(None)
+    lines = [json.loads(x) for x in path.read_text().splitlines()]
+    assert len(lines) == r["rounds"] and [x["round"] for x in lines] == list(range(1, r["rounds"] + 1))
+    last = lines[-1]
+    assert last["L"] == r["L"] and [lv["N"] for lv in last["levels"]] == r["N"]
+    assert all(abs(lv["mean"] - m) <= 1e-15 * abs(m) for lv, m in zip(last["levels"], r["mean"]))
+    assert last["var_ok"] and not last["bias_fail"]
