@@ -91,20 +91,42 @@ def dd_solve(engine, group=None, check_every: int = 32, max_steps: int = 10 ** 7
     object with its interface: pass_, scalar, sums, row, exchange_offsets, result, rank, world)."""
     import torch.distributed as dist
     world, rank = engine.world, engine.rank
+    # NCCL moves the device rows and sums directly (NVLink); a CPU backend (gloo: tests, or several processes
+    # sharing one GPU) goes through host staging copies of the same rows
+    staged = world > 1 and dist.get_backend(group) != "nccl" and engine.sums.device.type == "cuda"
+    if staged:
+        import torch
+        h_sums = torch.empty(3, dtype=torch.float64)
+        h_rows = [torch.empty(engine.lay.pitch, dtype=torch.float64) for _ in range(4)]
     for step in range(max_steps):
         engine.pass_()
         if world > 1:
-            dist.all_reduce(engine.sums, group=group)
             o = engine.exchange_offsets(step)
+            if staged:
+                h_sums.copy_(engine.sums)
+                dist.all_reduce(h_sums, group=group)
+                engine.sums.copy_(h_sums)
+                send = {0: o[0], 2: o[2]}
+                for q, off in send.items():
+                    if off >= 0:
+                        h_rows[q].copy_(engine.row(off))
+                bufs = {q: h_rows[q] for q in range(4)}
+            else:
+                dist.all_reduce(engine.sums, group=group)
+                bufs = {q: engine.row(o[q]) if o[q] >= 0 else None for q in range(4)}
             ops = []
             if o[0] >= 0:
-                ops.append(dist.P2POp(dist.isend, engine.row(o[0]), rank - 1, group))
-                ops.append(dist.P2POp(dist.irecv, engine.row(o[1]), rank - 1, group))
+                ops.append(dist.P2POp(dist.isend, bufs[0], rank - 1, group))
+                ops.append(dist.P2POp(dist.irecv, bufs[1], rank - 1, group))
             if o[2] >= 0:
-                ops.append(dist.P2POp(dist.isend, engine.row(o[2]), rank + 1, group))
-                ops.append(dist.P2POp(dist.irecv, engine.row(o[3]), rank + 1, group))
+                ops.append(dist.P2POp(dist.isend, bufs[2], rank + 1, group))
+                ops.append(dist.P2POp(dist.irecv, bufs[3], rank + 1, group))
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
+            if staged:
+                for q in (1, 3):
+                    if o[q] >= 0:
+                        engine.row(o[q]).copy_(h_rows[q])
         engine.scalar()
         if (step + 1) % check_every == 0 and engine.done():
             break
