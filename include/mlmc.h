@@ -352,7 +352,7 @@ typedef struct {
     uint64_t bytes;          /* device workspace bytes (caller allocates, owns) */
     uint64_t plane_off[5];   /* Lanczos vectors P0, P1, P2 (rotating), cE, cN: rows x pitch doubles */
     uint64_t sums_off;       /* 3 doubles: partial sums of the last pass (SUM-all-reduce in place) */
-    uint64_t state_off, partials_off, counter_off, xi_off, a_off;   /* internal */
+    uint64_t state_off, partials_off, counter_off, rpart_off, xi_off, a_off;   /* internal */
 } mlmc_dd_layout;
 typedef struct mlmc_dd mlmc_dd;
 /* host only: the partition and workspace layout of rank/world on mesh N = 1/h (m KL terms) */
@@ -370,6 +370,19 @@ int  mlmc_dd_scalar(mlmc_dd* dd);   /* Givens step + stopping test on the reduce
  * 3 non-finite), done (0/1)} -- Q valid once done */
 int  mlmc_dd_result(mlmc_dd* dd, double out[5]);
 int  mlmc_dd_run_local(mlmc_dd* dd, double out[5]);   /* world = 1: the whole solve, then mlmc_dd_result */
+/* The exchange FUSED into the solve kernel over peer memory (world <= 8): the slab tiles store their boundary
+ * rows straight into the neighbours' ghost rows, each rank's leader CTA stores its rank partial into every
+ * rank's table and bumps every rank's arrival counter (system-scope atomics), and every rank adds the world
+ * partials in rank order -- one kernel for the whole solve, no host round trip per step.
+ *   mlmc_dd_run_peer: this rank's part; peer_ws[q] = rank q's dd workspace as mapped on THIS device (CUDA IPC /
+ *   symmetric memory over NVLink; peer_ws[rank] = its own).  Every rank must call it (the ranks wait on one
+ *   another inside the kernel) after every rank's mlmc_dd_begin has completed.  Synchronous.
+ *   mlmc_dd_run_emulated: all `world` ranks of one solve whose slab solvers live on this ctx's device
+ *   (dds[q] = rank q), in ONE cooperative launch -- the single-GPU test of the same kernel.  Synchronous.
+ * out as mlmc_dd_result (every rank holds the same result).  Errors: EINVAL, ECUDA (cooperative launch
+ * not possible).                                                                                          */
+int  mlmc_dd_run_peer(mlmc_dd* dd, void* const* peer_ws, double out[5]);
+int  mlmc_dd_run_emulated(mlmc_dd* const* dds, int world, double out[5]);
 void mlmc_dd_destroy(mlmc_dd* dd);
 
 /* ---- host-only helpers (no device needed; used by the controller) ---------- */

@@ -59,7 +59,7 @@ class DDLayout(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("N", "rank", "world", "j0", "j1", "rows", "pitch", "tiles")] + \
                [("bytes", C.c_uint64), ("plane_off", C.c_uint64 * 5), ("sums_off", C.c_uint64),
                 ("state_off", C.c_uint64), ("partials_off", C.c_uint64), ("counter_off", C.c_uint64),
-                ("xi_off", C.c_uint64), ("a_off", C.c_uint64)]
+                ("rpart_off", C.c_uint64), ("xi_off", C.c_uint64), ("a_off", C.c_uint64)]
 
 
 class KernelStat(C.Structure):
@@ -137,6 +137,8 @@ def lib():
     L.mlmc_dd_scalar.argtypes = [vp]
     L.mlmc_dd_result.argtypes = [vp, dp]
     L.mlmc_dd_run_local.argtypes = [vp, dp]
+    L.mlmc_dd_run_peer.argtypes = [vp, C.POINTER(vp), dp]
+    L.mlmc_dd_run_emulated.argtypes = [C.POINTER(vp), C.c_int, dp]
     L.mlmc_dd_destroy.argtypes = [vp]
     L.mlmc_dd_destroy.restype = None
     _lib = L

@@ -965,7 +965,7 @@ int mlmc_kl_modes(double sigma2, double corr_len, int m, int32_t* ik, int32_t* j
 
 // ---------------------------------------------------------------- K3d: one sample over row slabs (NEXT-3)
 int mlmc_dd_layout_get(int N, int m, int rank, int world, mlmc_dd_layout* out) {
-    if (!out || N < 4 || world < 1 || rank < 0 || rank >= world || m < 1) return MLMC_EINVAL;
+    if (!out || N < 4 || world < 1 || world > kDDMaxRanks || rank < 0 || rank >= world || m < 1) return MLMC_EINVAL;
     const int C = N - 1;
     const int j0 = 1 + (int)((int64_t)rank * C / world), j1 = 1 + (int)((int64_t)(rank + 1) * C / world);
     if (j1 - j0 < 2) return MLMC_EINVAL;                  // a slab sends its second row: >= 2 rows each
@@ -979,8 +979,11 @@ int mlmc_dd_layout_get(int N, int m, int rank, int world, mlmc_dd_layout* out) {
     for (int q = 0; q < 5; ++q) { L.plane_off[q] = off; off += plane; }
     L.sums_off = off;  off += align256(sizeof(double) * 4);
     L.state_off = off; off += align256(sizeof(DDState));
-    L.partials_off = off; off += align256(sizeof(double) * 6 * (size_t)L.tiles);   // x2: the persistent kernel
-    L.counter_off = off; off += align256(sizeof(unsigned) * 4);
+    // CTA partials, double-buffered ([2][CTAs][3]): a persistent grid has at most min(tiles, resident slots) CTAs
+    // per rank, the fused-exchange grid up to the largest rank's tile count (+1 row of tiles)
+    L.partials_off = off; off += align256(sizeof(double) * 6 * (size_t)(L.tiles + 64));
+    L.counter_off = off; off += align256(sizeof(unsigned) * 4);     // [0] CTA arrivals, [1] rank arrivals
+    L.rpart_off = off; off += align256(sizeof(double) * 2 * kDDMaxRanks * 3);
     L.xi_off = off;    off += align256(sizeof(double) * (size_t)m);
     L.a_off = off;     off += align256(sizeof(double) * 2 * (size_t)N * N);
     L.bytes = off;
@@ -1148,6 +1151,72 @@ int mlmc_dd_run_local(mlmc_dd* dd, double out[5]) {
         CU(cudaMemcpyAsync(&done, &st_dev->done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
     }
+    return mlmc_dd_result(dd, out);
+}
+
+namespace {
+// the fused-exchange launch description of ranks 0..world-1 whose workspaces are at ws[q] (device-accessible)
+DDPeerLaunch dd_peer_desc(int N, int m, int world, void* const* ws) {
+    DDPeerLaunch D{};
+    D.N = N;
+    D.world = world;
+    for (int q = 0; q < world; ++q) {
+        mlmc_dd_layout L{};
+        mlmc_dd_layout_get(N, m, q, world, &L);
+        unsigned char* b = static_cast<unsigned char*>(ws[q]);
+        D.j0[q] = L.j0; D.j1[q] = L.j1; D.rows[q] = L.rows;
+        D.planes[q] = reinterpret_cast<double*>(b + L.plane_off[0]);
+        D.plane_stride[q] = (L.plane_off[1] - L.plane_off[0]) / sizeof(double);
+        D.st[q] = reinterpret_cast<DDState*>(b + L.state_off);
+        D.partials[q] = reinterpret_cast<double*>(b + L.partials_off);
+        D.counter[q] = reinterpret_cast<unsigned*>(b + L.counter_off);
+        D.xcounter[q] = reinterpret_cast<unsigned*>(b + L.counter_off) + 1;
+        D.rpart[q] = reinterpret_cast<double*>(b + L.rpart_off);
+        D.sums[q] = reinterpret_cast<double*>(b + L.sums_off);
+    }
+    return D;
+}
+}  // namespace
+
+int mlmc_dd_run_emulated(mlmc_dd* const* dds, int world, double out[5]) {
+    if (!dds || world < 1 || world > kDDMaxRanks || !dds[0]) return MLMC_EINVAL;
+    int rc = dd_check(dds[0]);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dds[0]->ctx;
+    std::vector<void*> ws(world);
+    for (int q = 0; q < world; ++q) {
+        if (!dds[q] || dds[q]->ctx != ctx || dds[q]->L.rank != q || dds[q]->L.world != world ||
+            dds[q]->L.N != dds[0]->L.N)
+            return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_emulated: dds[q] must be rank q of `world` on one ctx / mesh");
+        ws[q] = dds[q]->ws;
+    }
+    DDPeerLaunch D = dd_peer_desc(dds[0]->L.N, ctx->pr.m, world, ws.data());
+    D.rank0 = 0;
+    D.nranks = world;
+    cudaStream_t s = ctx->stream;
+    for (int q = 0; q < world; ++q) CU(cudaMemsetAsync(D.counter[q], 0, sizeof(unsigned) * 2, s));
+    CU(counted(ctx, s, 2, D.N, [&] { return launch_dd_peer(D, s); }));
+    for (int q = 0; q < world; ++q) CU(cudaMemsetAsync(D.counter[q], 0, sizeof(unsigned) * 2, s));
+    return mlmc_dd_result(dds[0], out);
+}
+
+int mlmc_dd_run_peer(mlmc_dd* dd, void* const* peer_ws, double out[5]) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dd->ctx;
+    const int world = dd->L.world;
+    if (!peer_ws) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_peer: peer_ws is NULL");
+    for (int q = 0; q < world; ++q)
+        if (!peer_ws[q]) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_peer: a peer workspace is NULL");
+    DDPeerLaunch D = dd_peer_desc(dd->L.N, ctx->pr.m, world, peer_ws);
+    D.rank0 = dd->L.rank;
+    D.nranks = 1;
+    cudaStream_t s = ctx->stream;
+    // the counters were zeroed by mlmc_dd_begin on every rank (the caller synchronises the ranks between
+    // mlmc_dd_begin and this call, e.g. with a barrier)
+    CU(counted(ctx, s, 2, D.N, [&] { return launch_dd_peer(D, s); }));
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemsetAsync(D.counter[dd->L.rank], 0, sizeof(unsigned) * 2, s));
     return mlmc_dd_result(dd, out);
 }
 

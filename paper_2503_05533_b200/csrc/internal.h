@@ -192,6 +192,22 @@ cudaError_t launch_dd_pass(int N, int j0, int j1, int rows, int pitch, double* p
                            DDState* st, double* partials, unsigned* counter, double* sums, bool fuse_scalar,
                            cudaStream_t s);
 cudaError_t launch_dd_scalar(DDState* st, const double* sums, int N, cudaStream_t s);
+// World > 1 with the exchange fused into the kernel over peer memory (dd_peer_kernel); ranks rank0 ..
+// rank0 + nranks - 1 in this launch, every pointer of every rank device-accessible from the launching GPU.
+constexpr int kDDMaxRanks = 8;
+struct DDPeerLaunch {
+    int N, world, rank0, nranks;
+    int j0[kDDMaxRanks], j1[kDDMaxRanks], rows[kDDMaxRanks];
+    double* planes[kDDMaxRanks];
+    size_t plane_stride[kDDMaxRanks];
+    DDState* st[kDDMaxRanks];
+    double* partials[kDDMaxRanks];
+    unsigned* counter[kDDMaxRanks];
+    double* rpart[kDDMaxRanks];
+    unsigned* xcounter[kDDMaxRanks];
+    double* sums[kDDMaxRanks];
+};
+cudaError_t launch_dd_peer(const DDPeerLaunch& L, cudaStream_t s);
 // world = 1: the whole solve in one cooperative launch (partials needs 6 x tiles doubles)
 cudaError_t launch_dd_persistent(int N, int j0, int j1, int rows, int pitch, double* planes, size_t plane_stride,
                                  DDState* st, double* partials, unsigned* counter, double* sums, cudaStream_t s);

@@ -146,8 +146,12 @@ struct DDSmem {
     double box[4][DBH][DBW];       // p_j, p_{j-1}, cE, cN
     double PN[DPH][DPW];
 };
+// send_lo / send_hi (peer-memory exchange, dd_peer_kernel): the row in the lower / upper neighbour's p_{j+1}
+// plane that receives this slab's row j0 + 1 / j1 - 2 (its ghost row), or null -- the halo is pushed by the
+// tile that forms it, straight into the neighbour's memory (NVLink stores between GPUs)
 __device__ __forceinline__ double3 dd_tile(int tile, int N, int j0, int j1, int rows, int pitch, double* planes,
-                                           size_t plane_stride, int step, double ct, double c1, double c0, DDSmem& sm) {
+                                           size_t plane_stride, int step, double ct, double c1, double c0, DDSmem& sm,
+                                           double* send_lo = nullptr, double* send_hi = nullptr) {
     const int C = N - 1, tid = threadIdx.x, NT = blockDim.x;
     const int tiles_x = (C + DTW - 1) / DTW;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -218,6 +222,16 @@ __device__ __forceinline__ double3 dd_tile(int tile, int N, int j0, int j1, int 
         const int py = j1 - (y0 - 1);
         for (int x = tid; x < DTW; x += NT)
             if (x0 + x <= C) Pn[(size_t)(j1 - (j0 - 2)) * pitch + x0 + x + 1] = sm.PN[py][x + 1];
+    }
+    if (send_lo && y0 <= j0 + 1 && j0 + 1 < ylim) {          // row j0 + 1 -> rank - 1's ghost row
+        const int py = j0 + 1 - (y0 - 1);
+        for (int x = tid; x < DTW; x += NT)
+            if (x0 + x <= C) send_lo[x0 + x + 1] = sm.PN[py][x + 1];
+    }
+    if (send_hi && y0 <= j1 - 2 && j1 - 2 < ylim) {          // row j1 - 2 -> rank + 1's ghost row
+        const int py = j1 - 2 - (y0 - 1);
+        for (int x = tid; x < DTW; x += NT)
+            if (x0 + x <= C) send_hi[x0 + x + 1] = sm.PN[py][x + 1];
     }
     __syncthreads();                              // box / PN free for the next tile
     return make_double3(sa, sb, sc);
@@ -356,6 +370,115 @@ dd_persistent_kernel(int N, int j0, int j1, int rows, int pitch, double* __restr
         sums[0] = sums[1] = sums[2] = 0.0;
     }
 }
+// ---- World > 1 with the exchange fused into the kernel (peer memory).  Each rank runs
+// its slab as dd_persistent_kernel does, and the step's collective lives in the same kernel: the tiles that
+// form rows j0 + 1 / j1 - 2 store them straight into the neighbours' ghost rows (peer pointers: NVLink stores
+// between GPUs), each rank's leader CTA adds its CTAs' partials and stores the rank partial into EVERY rank's
+// rank-partial table, then increments every rank's arrival counter (system-scope atomics); every CTA waits
+// for its rank's counter to reach world x step and adds the world rank partials in rank order -- identical on
+// every rank -- before its own copy of the scalar step.  One launch covers ranks rank0 .. rank0 + gridDim.y - 1:
+// all of them for the one-GPU emulation (a cooperative launch: every CTA of every rank co-resident), one per
+// process on a multi-GPU node (each rank's grid cooperative on its GPU; the ranks wait on one another only
+// through the counters, and all ranks launch).
+struct DDPeerParams {
+    int N, world, rank0;
+    int j0[kDDMaxRanks], j1[kDDMaxRanks], rows[kDDMaxRanks], tiles[kDDMaxRanks];
+    double* planes[kDDMaxRanks];
+    size_t plane_stride[kDDMaxRanks];
+    DDState* st[kDDMaxRanks];
+    double* partials[kDDMaxRanks];     // this rank's CTA partials, [2][ctas][3]
+    unsigned* counter[kDDMaxRanks];    // this rank's CTA arrivals
+    double* rpart[kDDMaxRanks];        // rank partial table, [2][kDDMaxRanks][3] (written by every rank)
+    unsigned* xcounter[kDDMaxRanks];   // rank arrivals (incremented by every rank)
+    double* sums[kDDMaxRanks];
+};
+
+__global__ void __launch_bounds__(DT)
+dd_peer_kernel(const __grid_constant__ DDPeerParams P) {
+    __shared__ DDSmem sm;
+    __shared__ double red[3][32];
+    __shared__ DDState ls;
+    const int tid = threadIdx.x, r = P.rank0 + blockIdx.y, W = P.world, pitch = P.N + 2;
+    if (tid == 0) ls = *P.st[r];
+    __syncthreads();
+    for (unsigned gen = 1;; ++gen) {
+        if (ls.done) break;                          // identical in every CTA of every rank
+        const int pnext = (ls.step + 2) % 3;
+        double* send_lo = r > 0 ? P.planes[r - 1] + (size_t)pnext * P.plane_stride[r - 1] +
+                                      (size_t)(P.rows[r - 1] - 1) * pitch : nullptr;
+        double* send_hi = r + 1 < W ? P.planes[r + 1] + (size_t)pnext * P.plane_stride[r + 1] : nullptr;
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int t = blockIdx.x; t < P.tiles[r]; t += gridDim.x) {
+            const double3 q = dd_tile(t, P.N, P.j0[r], P.j1[r], P.rows[r], pitch, P.planes[r], P.plane_stride[r],
+                                      ls.step, ls.ct, ls.c1, ls.c0, sm, send_lo, send_hi);
+            a += q.x; b += q.y; c += q.z;
+        }
+        const double3 tsum = dd_block_sum(a, b, c, red);
+        if (tid < 32) {
+            double* pg = P.partials[r] + 3 * (size_t)gridDim.x * (gen & 1u);
+            if (tid == 0) {
+                volatile double* pv = pg + 3 * blockIdx.x;
+                pv[0] = tsum.x;
+                pv[1] = tsum.y;
+                pv[2] = tsum.z;
+                // the peer halo stores and the partial before the arrival (gpu scope: the leader's system-scope
+                // release below is ordered after this CTA's writes by the acquire of the counter -- causality
+                // carries them to the other GPUs' acquiring readers)
+                __threadfence();
+                atomicAdd(P.counter[r], 1u);
+            }
+            if (blockIdx.x == 0) {                   // the rank's leader: rank partial -> every rank's table
+                if (tid == 0) {
+                    unsigned seen;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(P.counter[r]) : "memory");
+                    } while (seen < gen * gridDim.x);
+                }
+                __syncwarp();
+                double A = 0.0, B = 0.0, Cc = 0.0;
+                for (unsigned k = tid; k < gridDim.x; k += 32) {
+                    A += __ldcg(pg + 3 * k);
+                    B += __ldcg(pg + 3 * k + 1);
+                    Cc += __ldcg(pg + 3 * k + 2);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    A += __shfl_xor_sync(0xffffffffu, A, o);
+                    B += __shfl_xor_sync(0xffffffffu, B, o);
+                    Cc += __shfl_xor_sync(0xffffffffu, Cc, o);
+                }
+                if (tid < W) {                       // lane q stores into rank q's table
+                    volatile double* t = P.rpart[tid] + 3 * ((size_t)(gen & 1u) * kDDMaxRanks + r);
+                    t[0] = A;
+                    t[1] = B;
+                    t[2] = Cc;
+                }
+                __syncwarp();
+                if (tid == 0) {
+                    __threadfence_system();
+                    for (int q = 0; q < W; ++q) atomicAdd_system(P.xcounter[q], 1u);
+                }
+            }
+            if (tid == 0) {                          // every CTA: all ranks' partials of this step are in
+                unsigned seen;
+                do {
+                    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(P.xcounter[r]) : "memory");
+                } while (seen < gen * (unsigned)W);
+                const volatile double* t = P.rpart[r] + 3 * (size_t)(gen & 1u) * kDDMaxRanks;
+                double S[3] = {0.0, 0.0, 0.0};
+                for (int q = 0; q < W; ++q) {        // rank order: identical on every rank
+                    S[0] += t[3 * q];
+                    S[1] += t[3 * q + 1];
+                    S[2] += t[3 * q + 2];
+                }
+                dd_scalar_step(&ls, S, P.N);
+            }
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid == 0) *P.st[r] = ls;
+}
+
 }  // namespace
 
 int dd_tiles(int N, int j0, int j1) {
@@ -398,6 +521,32 @@ cudaError_t launch_dd_persistent(int N, int j0, int j1, int rows, int pitch, dou
     e = cudaLaunchCooperativeKernel((const void*)dd_persistent_kernel, dim3(grid), dim3(DT), args, 0, s);
     if (e != cudaSuccess) return e;
     return cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+}
+
+// ranks rank0 .. rank0 + nranks - 1 in one cooperative launch (the caller zeroed the counters); every
+// pointer in P device-accessible from this GPU (peer-mapped for other GPUs' ranks)
+cudaError_t launch_dd_peer(const DDPeerLaunch& L, cudaStream_t s) {
+    DDPeerParams P{};
+    P.N = L.N;
+    P.world = L.world;
+    P.rank0 = L.rank0;
+    for (int q = 0; q < L.world; ++q) {
+        P.j0[q] = L.j0[q]; P.j1[q] = L.j1[q]; P.rows[q] = L.rows[q]; P.tiles[q] = dd_tiles(L.N, L.j0[q], L.j1[q]);
+        P.planes[q] = L.planes[q]; P.plane_stride[q] = L.plane_stride[q]; P.st[q] = L.st[q];
+        P.partials[q] = L.partials[q]; P.counter[q] = L.counter[q]; P.rpart[q] = L.rpart[q];
+        P.xcounter[q] = L.xcounter[q]; P.sums[q] = L.sums[q];
+    }
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dd_peer_kernel, DT, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1 || L.nranks < 1) return cudaErrorInvalidConfiguration;
+    int mt = 0;
+    for (int q = L.rank0; q < L.rank0 + L.nranks; ++q) mt = std::max(mt, P.tiles[q]);
+    const int ctas = std::max(1, std::min(mt, sms * per_sm / L.nranks));
+    void* args[] = {&P};
+    return cudaLaunchCooperativeKernel((const void*)dd_peer_kernel, dim3(ctas, L.nranks), dim3(DT), args, 0, s);
 }
 
 cudaError_t launch_dd_scalar(DDState* st, const double* sums, int N, cudaStream_t s) {

@@ -76,6 +76,14 @@ class SlabSolver:
         K.check(K.lib().mlmc_dd_run_local(self.dd, out), self.ctx.ctx)
         return {"Q": out[0], "iters": int(out[1]), "relres": out[2], "status": int(out[3]), "done": bool(out[4])}
 
+    def run_peer(self, peer_ptrs) -> dict:
+        """mlmc_dd_run_peer: this rank's part of the fused-exchange solve; peer_ptrs[q] = rank q's workspace as
+        mapped on this device (every rank calls it after every rank's begin())."""
+        arr = (C.c_void_p * len(peer_ptrs))(*[C.c_void_p(int(p)) for p in peer_ptrs])
+        out = (C.c_double * 5)()
+        K.check(K.lib().mlmc_dd_run_peer(self.dd, arr, out), self.ctx.ctx)
+        return {"Q": out[0], "iters": int(out[1]), "relres": out[2], "status": int(out[3]), "done": bool(out[4])}
+
     def close(self):
         if getattr(self, "dd", None):
             K.lib().mlmc_dd_destroy(self.dd)
@@ -131,6 +139,15 @@ def dd_solve(engine, group=None, check_every: int = 32, max_steps: int = 10 ** 7
         if (step + 1) % check_every == 0 and engine.done():
             break
     return engine.result()
+
+
+def dd_run_fused_emulated(engines: list) -> dict:
+    """All ranks of one solve (SlabSolvers of one ctx, engines[q] = rank q) in ONE cooperative launch of the
+    fused-exchange kernel (mlmc_dd_run_emulated): the peer-memory exchange of a multi-GPU run, on one GPU."""
+    arr = (C.c_void_p * len(engines))(*[e.dd for e in engines])
+    out = (C.c_double * 5)()
+    K.check(K.lib().mlmc_dd_run_emulated(arr, len(engines), out), engines[0].ctx.ctx)
+    return {"Q": out[0], "iters": int(out[1]), "relres": out[2], "status": int(out[3]), "done": bool(out[4])}
 
 
 def dd_solve_emulated(engines: list, check_every: int = 32, max_steps: int = 10 ** 7) -> dict:

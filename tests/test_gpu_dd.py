@@ -157,3 +157,34 @@ def test_dd_two_processes_on_one_gpu_gloo():
     assert r0 == r1 and r0["status"] == 0 and one["status"] == 0
     assert abs(r0["Q"] / one["Q"] - 1) < 1e-9
     assert abs(r0["iters"] - one["iters"]) <= max(2, 0.01 * one["iters"])
+
+
+@pytest.mark.parametrize("level,G,tol", [(5, 2, 1e-10), (5, 3, 1e-10), (6, 4, 1e-8), (6, 8, 1e-8)])
+def test_dd_fused_peer_exchange_emulated(level, G, tol):
+    """The fused-exchange kernel (mlmc_dd_run_emulated: the per-step halo rows pushed into the neighbours' ghost
+    rows and the rank partials into every rank's table from inside the solve kernel, all G ranks in one
+    cooperative launch): same result as the host-driven G-slab solve to rounding, within the residual bound
+    of the oracle's direct solve (h = 1/256) or of K3c (h = 1/512)."""
+    from paper_2503_05533_b200.dd import dd_run_fused_emulated
+    cfg, ctx = _ctx(ws=8 << 30)
+    seed, k = 43, 1
+    N = cfg["h0_inv"] << level
+    eng = [SlabSolver(ctx, level, g, G) for g in range(G)]
+    for e in eng:
+        e.begin(seed, level, k, tol)
+    r = dd_run_fused_emulated(eng)
+    per_rank = [e.result() for e in eng]
+    for e in eng:
+        e.close()
+    assert all(p == per_rank[0] for p in per_rank) and per_rank[0]["Q"] == r["Q"]
+    assert r["status"] == 0 and r["relres"] <= tol
+    host = _solve(ctx, level, G, seed, level, k, tol)[0]
+    assert abs(r["Q"] / host["Q"] - 1) < tol and abs(r["iters"] - host["iters"]) <= max(2, 0.01 * host["iters"])
+    if level == 5:
+        q, bn, xn = _exact(cfg, N, seed, level, k)
+        assert abs(r["Q"] - q) <= tol * bn * xn * (1 + 1e-6) + 1e-14 * q
+    else:
+        ref = ctx.sample_level(level, 1, seed=seed, first_index=k, prec_fine=precision("minres"), tol_fine=tol,
+                               tol_coarse=tol, per_sample=True).per_sample[0]
+        assert abs(r["Q"] - ref[0]) <= 2 * 1.5 * tol * abs(ref[0])
+    ctx.close()

@@ -13,7 +13,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workloads as W  # noqa: E402
 from paper_2503_05533_b200 import Context, precision  # noqa: E402
-from paper_2503_05533_b200.dd import SlabSolver, dd_solve_emulated  # noqa: E402
+from paper_2503_05533_b200.dd import SlabSolver, dd_run_fused_emulated, dd_solve_emulated  # noqa: E402
 
 
 def ev_time(fn):
@@ -55,6 +55,16 @@ def main():
             row[f"k3d_G{G}"] = {"ms_fine_solve": ms, "wall_ms": wall, "iters": it, "us_per_step": 1e3 * ms / max(it, 1),
                                 "Q": res[0]["Q"], "status": res[0]["status"],
                                 "note": "whole GPU, CUDA graphs" if G == 1 else "G slabs emulated on one GPU, host-driven"}
+            for e in eng:
+                e.close()
+        for G in (2, 4, 8):        # the fused peer-memory exchange, all ranks in one cooperative launch
+            eng = [SlabSolver(ctx, level, g, G) for g in range(G)]
+            for e in eng:
+                e.begin(seed, level, k, tol)
+            res, ms, wall = ev_time(lambda: dd_run_fused_emulated(eng))
+            row[f"k3d_fused_G{G}"] = {"ms_fine_solve": ms, "iters": res["iters"], "Q": res["Q"],
+                                      "us_per_step": 1e3 * ms / max(res["iters"], 1), "status": res["status"],
+                                      "note": "G slabs, exchange fused into the kernel, one cooperative launch"}
             for e in eng:
                 e.close()
         out[f"h=1/{N}"] = row
