@@ -965,7 +965,7 @@ int mlmc_kl_modes(double sigma2, double corr_len, int m, int32_t* ik, int32_t* j
 
 // ---------------------------------------------------------------- K3d: one sample over row slabs (NEXT-3)
 int mlmc_dd_layout_get(int N, int m, int rank, int world, mlmc_dd_layout* out) {
-    if (!out || N < 4 || world < 1 || world > kDDMaxRanks || rank < 0 || rank >= world || m < 1) return MLMC_EINVAL;
+    if (!out || N < 4 || world < 1 || rank < 0 || rank >= world || m < 1) return MLMC_EINVAL;
     const int C = N - 1;
     const int j0 = 1 + (int)((int64_t)rank * C / world), j1 = 1 + (int)((int64_t)(rank + 1) * C / world);
     if (j1 - j0 < 2) return MLMC_EINVAL;                  // a slab sends its second row: >= 2 rows each
@@ -1205,6 +1205,7 @@ int mlmc_dd_run_peer(mlmc_dd* dd, void* const* peer_ws, double out[5]) {
     if (rc) return rc;
     mlmc_ctx* ctx = dd->ctx;
     const int world = dd->L.world;
+    if (world > kDDMaxRanks) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_peer: at most 8 ranks (one NVLink node)");
     if (!peer_ws) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_peer: peer_ws is NULL");
     for (int q = 0; q < world; ++q)
         if (!peer_ws[q]) return fail(ctx, MLMC_EINVAL, "mlmc_dd_run_peer: a peer workspace is NULL");
