@@ -383,6 +383,13 @@ int  mlmc_dd_run_local(mlmc_dd* dd, double out[5]);   /* world = 1: the whole so
  * not possible).                                                                                          */
 int  mlmc_dd_run_peer(mlmc_dd* dd, void* const* peer_ws, double out[5]);
 int  mlmc_dd_run_emulated(mlmc_dd* const* dds, int world, double out[5]);
+/* Peer mapping for mlmc_dd_run_peer (one process per GPU): mlmc_dd_ipc_handle gives a 64-byte CUDA IPC handle
+ * of the allocation holding this rank's workspace and the workspace's byte offset in it; a peer process opens
+ * it with mlmc_dd_ipc_open (*ptr = the workspace as mapped on the peer's device, *base = the mapping to pass to
+ * mlmc_dd_ipc_close).  Errors: EINVAL, ECUDA.                                                              */
+int  mlmc_dd_ipc_handle(mlmc_dd* dd, void* handle64, uint64_t* offset);
+int  mlmc_dd_ipc_open(mlmc_ctx* ctx, const void* handle64, uint64_t offset, void** ptr, void** base);
+int  mlmc_dd_ipc_close(mlmc_ctx* ctx, void* base);
 void mlmc_dd_destroy(mlmc_dd* dd);
 
 /* ---- host-only helpers (no device needed; used by the controller) ---------- */

@@ -139,6 +139,9 @@ def lib():
     L.mlmc_dd_run_local.argtypes = [vp, dp]
     L.mlmc_dd_run_peer.argtypes = [vp, C.POINTER(vp), dp]
     L.mlmc_dd_run_emulated.argtypes = [C.POINTER(vp), C.c_int, dp]
+    L.mlmc_dd_ipc_handle.argtypes = [vp, C.c_char_p, C.POINTER(C.c_uint64)]
+    L.mlmc_dd_ipc_open.argtypes = [vp, C.c_char_p, C.c_uint64, C.POINTER(vp), C.POINTER(vp)]
+    L.mlmc_dd_ipc_close.argtypes = [vp, vp]
     L.mlmc_dd_destroy.argtypes = [vp]
     L.mlmc_dd_destroy.restype = None
     _lib = L

@@ -1,4 +1,5 @@
 // capi.cu -- the C-ABI of include/mlmc.h: plan, workspace, per-level sampling and Algorithm 2.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -9,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -1219,6 +1221,60 @@ int mlmc_dd_run_peer(mlmc_dd* dd, void* const* peer_ws, double out[5]) {
     CU(cudaStreamSynchronize(s));
     CU(cudaMemsetAsync(D.counter[dd->L.rank], 0, sizeof(unsigned) * 2, s));
     return mlmc_dd_result(dd, out);
+}
+
+// ---- peer mapping of the slab workspaces (CUDA IPC; one process per GPU on an NVLink node)
+namespace {
+using PFN_getAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_getAddressRange address_range_fn() {
+    static PFN_getAddressRange fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_getAddressRange>(p);
+    });
+    return fn;
+}
+}  // namespace
+
+int mlmc_dd_ipc_handle(mlmc_dd* dd, void* handle, uint64_t* offset) {
+    int rc = dd_check(dd);
+    if (rc) return rc;
+    mlmc_ctx* ctx = dd->ctx;
+    if (!handle || !offset) return fail(ctx, MLMC_EINVAL, "mlmc_dd_ipc_handle: NULL output");
+    auto range = address_range_fn();
+    if (!range) return fail(ctx, MLMC_ECUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dd->ws)) != CUDA_SUCCESS)
+        return fail(ctx, MLMC_ECUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));   // the allocation holding the workspace
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (uint64_t)(reinterpret_cast<CUdeviceptr>(dd->ws) - base);
+    return MLMC_OK;
+}
+
+int mlmc_dd_ipc_open(mlmc_ctx* ctx, const void* handle, uint64_t offset, void** ptr, void** base_out) {
+    if (!ctx || !handle || !ptr || !base_out) return MLMC_EINVAL;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    CU(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *base_out = base;
+    *ptr = static_cast<unsigned char*>(base) + offset;
+    return MLMC_OK;
+}
+
+int mlmc_dd_ipc_close(mlmc_ctx* ctx, void* base) {
+    if (!ctx || !base) return MLMC_EINVAL;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MLMC_ECUDA, "cudaSetDevice");
+    CU(cudaIpcCloseMemHandle(base));
+    return MLMC_OK;
 }
 
 void mlmc_dd_destroy(mlmc_dd* dd) {

@@ -84,6 +84,22 @@ class SlabSolver:
         K.check(K.lib().mlmc_dd_run_peer(self.dd, arr, out), self.ctx.ctx)
         return {"Q": out[0], "iters": int(out[1]), "relres": out[2], "status": int(out[3]), "done": bool(out[4])}
 
+    def ipc_handle(self):
+        """(64-byte CUDA IPC handle of this workspace's allocation, byte offset of the workspace in it)."""
+        h = C.create_string_buffer(64)
+        off = C.c_uint64()
+        K.check(K.lib().mlmc_dd_ipc_handle(self.dd, h, C.byref(off)), self.ctx.ctx)
+        return h.raw, off.value
+
+    def ipc_open(self, handle: bytes, offset: int):
+        """A peer's workspace mapped on this device: (pointer, mapping base for ipc_close)."""
+        ptr, base = C.c_void_p(), C.c_void_p()
+        K.check(K.lib().mlmc_dd_ipc_open(self.ctx.ctx, handle, offset, C.byref(ptr), C.byref(base)), self.ctx.ctx)
+        return ptr.value, base.value
+
+    def ipc_close(self, base: int):
+        K.check(K.lib().mlmc_dd_ipc_close(self.ctx.ctx, C.c_void_p(base)), self.ctx.ctx)
+
     def close(self):
         if getattr(self, "dd", None):
             K.lib().mlmc_dd_destroy(self.dd)
@@ -139,6 +155,35 @@ def dd_solve(engine, group=None, check_every: int = 32, max_steps: int = 10 ** 7
         if (step + 1) % check_every == 0 and engine.done():
             break
     return engine.result()
+
+
+def dd_solve_peer(engine, group=None) -> dict:
+    """One rank of the fused-exchange solve on a multi-GPU node (one process per GPU, every rank calls it after its
+    begin()): the workspaces are peer-mapped with CUDA IPC (handles exchanged over torch.distributed), then ONE
+    kernel per rank runs the whole solve, the ranks exchanging halo rows and partial sums through NVLink stores
+    and system-scope flags (mlmc_dd_run_peer).  Ranks must sit on distinct GPUs: they wait on one another inside
+    the kernel (on one GPU use dd_run_fused_emulated)."""
+    import torch.distributed as dist
+    world, rank = engine.world, engine.rank
+    mine = engine.ipc_handle()
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    ptrs, bases = [], []
+    for q in range(world):
+        if q == rank:
+            ptrs.append(engine.ws.data_ptr())
+        else:
+            p, b = engine.ipc_open(*allh[q])
+            ptrs.append(p)
+            bases.append(b)
+    engine.result()                            # this rank's begin() (planes, zeroed counters) is on the GPU ...
+    dist.barrier(group=group)                  # ... on every rank, before any rank's kernel stores into it
+    try:
+        return engine.run_peer(ptrs)
+    finally:
+        dist.barrier(group=group)              # nobody unmaps while a peer may still store into it
+        for b in bases:
+            engine.ipc_close(b)
 
 
 def dd_run_fused_emulated(engines: list) -> dict:

@@ -188,3 +188,64 @@ def test_dd_fused_peer_exchange_emulated(level, G, tol):
                                tol_coarse=tol, per_sample=True).per_sample[0]
         assert abs(r["Q"] - ref[0]) <= 2 * 1.5 * tol * abs(ref[0])
     ctx.close()
+
+
+def _ipc_worker(rank, world, port, q):
+    """Peer mapping of the slab workspaces (mlmc_dd_ipc_handle / _open / _close) between 2 processes on one GPU:
+    each rank reads the other's copy of the sample's triangle coefficients through the mapped pointer (no kernel
+    waits on another: only the mapping of dd_solve_peer is exercised, its kernel is tested emulated)."""
+    import os
+    import numpy as np
+    import torch.distributed as dist
+    import warnings
+    warnings.simplefilter("ignore", FutureWarning)
+    from cuda import cudart
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg, ctx = _ctx(ws=1 << 30)
+        eng = SlabSolver(ctx, 5, rank, world)
+        eng.begin(17, 5, 4, 1e-6)
+        eng.result()
+        allh = [None] * world
+        dist.all_gather_object(allh, eng.ipc_handle())
+        other = 1 - rank
+        ptr, base = eng.ipc_open(*allh[other])
+        lay = eng.lay
+        nbytes = 8 * 2 * lay.N * lay.N
+        mine = np.empty(2 * lay.N * lay.N, np.float64)
+        theirs = np.empty_like(mine)
+        err1, = cudart.cudaMemcpy(mine.ctypes.data, eng.ws.data_ptr() + lay.a_off, nbytes,
+                                  cudart.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+        from paper_2503_05533_b200.dd import layout as dd_layout
+        their_off = dd_layout(lay.N, cfg["m"], other, world).a_off       # the peer's own layout
+        err2, = cudart.cudaMemcpy(theirs.ctypes.data, ptr + their_off, nbytes,
+                                  cudart.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+        dist.barrier()
+        eng.ipc_close(base)
+        eng.close()
+        ctx.close()
+        q.put((rank, int(err1), int(err2), bool(np.array_equal(mine, theirs)), float(np.abs(mine).sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dd_peer_mapping_two_processes_one_gpu():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, e1, e2, same, tot in out:
+        assert e1 == 0 and e2 == 0 and same and tot > 0, (rank, e1, e2, same)
