@@ -528,8 +528,14 @@ def c3_leg(local, torch):
     import numpy as np
     from paper_2503_05533_b200 import Context, precision
     cfg = W.CONFIGS["C3"]
-    ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
-                  L_max=cfg["L_max"], device=local, workspace_bytes=48 << 30)   # one pass of 100k samples (180 GB HBM)
+    ctx, ws_gb = None, 0
+    for ws_gb in (48, 16, 4):          # one pass of 100k samples needs ~32 GB (fp32 factors); smaller: more passes
+        try:
+            ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                          h0_inv=cfg["h0_inv"], L_max=cfg["L_max"], device=local, workspace_bytes=ws_gb << 30)
+            break
+        except torch.cuda.OutOfMemoryError:
+            torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
     sums = torch.zeros(12, dtype=torch.float64, device=torch.device("cuda", local))
     out = {}
@@ -587,7 +593,8 @@ def c3_leg(local, torch):
                                                "pair + 10 n per residual, fine + coarse"},
                 "k4_algorithmic_bytes_per_sample": alg / n,
                 "k4_dram_bytes_per_sample_ncu": _ncu_traffic(key),
-                "k4_factor_stream_GBs": gbs, "k4_factor_stream_hbm_frac": gbs / HBM_PEAK_GBS}
+                "k4_factor_stream_GBs": gbs, "k4_factor_stream_hbm_frac": gbs / HBM_PEAK_GBS,
+                "workspace_GB": ws_gb}
     ctx.close()
     return out
 
