@@ -1,4 +1,4 @@
-# final round-2 evidence: GPU suite, smoke, bench (no profiler, clocks sampled), ncu launch list of the bench step
+# final round-2 evidence (rerun after the K3d peer kernel): GPU suite, smoke, bench (no profiler, clocks sampled), ncu launch list of the bench step
 # and a full capture of the top kernels (exported to CSV on the box)
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu.txt 2>&1
