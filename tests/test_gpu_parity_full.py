@@ -246,3 +246,31 @@ def test_ir_step_counts_match_oracle_per_sample(quad, tol, exact_frac):
         assert same >= exact_frac and np.max(np.abs(st - ps[:, 2])) <= (0 if exact_frac == 1.0 else 1), \
             (quad, tol, level, same, list(zip(st, ps[:, 2])))
     ctx.close()
+
+
+# ============================================================================ recorded policy-3 choices
+def test_auto_policy_with_recorded_choices_reproduces_fixed_policies():
+    """mlmc_auto_choice_set (policy 3 must be able to replay recorded decisions): with
+    MINRES recorded for every mesh and tolerance class, policy 3 takes no pilot and returns policy 0's run bit
+    for bit; with MG-PCG recorded for h <= 1/32 and MINRES above, policy 2's run bit for bit."""
+    cfg = W.CONFIGS["C4"]
+    meshes = [cfg["h0_inv"] << l for l in range(cfg["L_max"] + 1)]
+    ref0 = _ctx(cfg, ws=1 << 30)
+    r0 = ref0.adaptive_run(2e-4, k_p=0.05, seed=3, policy=0)
+    r2 = ref0.adaptive_run(2e-4, k_p=0.05, seed=3, policy=2)
+    ref0.close()
+    for fixed, rec in ((r0, lambda N: "minres"), (r2, lambda N: "mgcg" if N >= 32 else "minres")):
+        ctx = _ctx(cfg, ws=1 << 30)
+        for N in meshes:
+            for cls in (0, 1, 2):
+                ctx.auto_choice_set(N, cls, rec(N))
+        r3 = ctx.adaptive_run(2e-4, k_p=0.05, seed=3, policy=3)
+        assert r3["estimate"] == fixed["estimate"] and r3["N"] == fixed["N"] and r3["L"] == fixed["L"]
+        assert all(ctx.auto_choice(N)["ms_per_sample"] == -1.0 for N in meshes)   # recorded, never timed
+        ctx.close()
+    with pytest.raises(RuntimeError):
+        c = _ctx(cfg, ws=1 << 28)
+        try:
+            c.auto_choice_set(1024, 0, "minres")      # not a mesh of the plan
+        finally:
+            c.close()
