@@ -28,8 +28,8 @@ struct mlmc_ctx {
     cudaStream_t stream = nullptr;
     std::vector<double*> phi_dev;        // per level, lazily built (P x m synthesis, MLMC_FIELD_KERNEL=dense)
     SepModes sep;                        // separable synthesis (default): modes by x-function ...
-    int* sep_i = nullptr;                // ... on the device: aoff [K+1] | mk [m] | mb [m]
-    double* sep_c = nullptr;             //     c_k [m]
+    int* sep_i = nullptr;                // ... on the device: the K x K mode map (k of the pair (a, b), or -1)
+    double* sep_c = nullptr;             //     and its c_k (0 where no mode)
     std::vector<double*> tab_dev;        // per level: the four 1D tables [4][N][K], lazily built
     unsigned char* ws = nullptr;         // borrowed workspace
     size_t ws_bytes = 0;
@@ -199,16 +199,17 @@ struct LevelSched {
 };
 
 // Which synthesis a mesh uses (a function of N, m and K only, so results never depend on the batch):
-// the separable one (K1s) where it needs several times fewer flops than the P x m contraction -- 4 m N +
-// 4 K N^2 against 4 m N^2, weighted 5x for the CUDA-core kernel against the DMMA one (measured: at N = 8
-// the DMMA kernel wins even at m = 256) -- or where Phi would not be small (> 256 MB); the P x m one
-// (K1, DMMA) otherwise.  MLMC_FIELD_KERNEL=dense|ffma forces the P x m one, =sep the separable one.
+// the separable one (K1s) where the kernel supports the mesh and K, unless N = 8 and K > 16 (there the
+// per-sample K x K gather outweighs the 2N^2 x m contraction: measured on configs[4] level 0), or where
+// Phi would not be small (> 256 MB); the P x m one (K1) otherwise.  MLMC_FIELD_KERNEL=dense|ffma forces
+// the P x m one, =sep the separable one wherever it is supported.
 bool field_sep(const mlmc_ctx* ctx, int N) {
     if (field_use_dense()) return false;
+    const int K = ctx->sep.K;
+    if (!field_sep_supported(N, K)) return false;
     if (field_force_sep()) return true;
-    const double m = ctx->pr.m, K = ctx->sep.K > 0 ? ctx->sep.K : m;
-    const double phi_bytes = 8.0 * 2.0 * N * N * m;
-    return 5.0 * (m + K * N) < N * m || phi_bytes > 256.0 * (1 << 20);
+    const double phi_bytes = 8.0 * 2.0 * N * N * ctx->pr.m;
+    return N >= 16 || K <= 16 || phi_bytes > 256.0 * (1 << 20);
 }
 
 // Plan data of a level's field synthesis, built on first use: the separable tables (a few KB per level)
@@ -219,14 +220,20 @@ int ensure_phi(mlmc_ctx* ctx, int level) {
     if (field_sep(ctx, N)) {
         if (!ctx->sep_i) {
             const int m = ctx->pr.m, K = ctx->sep.K;
-            std::vector<int32_t> ints(ctx->sep.aoff);
-            ints.insert(ints.end(), ctx->sep.mk.begin(), ctx->sep.mk.end());
-            ints.insert(ints.end(), ctx->sep.mb.begin(), ctx->sep.mb.end());
-            CU(cudaMalloc(&ctx->sep_i, sizeof(int32_t) * ints.size()));
-            CU(cudaMemcpy(ctx->sep_i, ints.data(), sizeof(int32_t) * ints.size(), cudaMemcpyHostToDevice));
-            CU(cudaMalloc(&ctx->sep_c, sizeof(double) * m));
-            CU(cudaMemcpy(ctx->sep_c, ctx->sep.mc.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
-            (void)K;
+            std::vector<int32_t> kmap((size_t)K * K, -1);
+            std::vector<double> cmap((size_t)K * K, 0.0);
+            for (int a = 0; a < K; ++a)
+                for (int c = ctx->sep.aoff[a]; c < ctx->sep.aoff[a + 1]; ++c) {
+                    const size_t e = (size_t)a * K + ctx->sep.mb[c];
+                    if (kmap[e] >= 0) return fail(ctx, MLMC_EINVAL, "two KL modes share a pair of 1D functions");
+                    kmap[e] = ctx->sep.mk[c];
+                    cmap[e] = ctx->sep.mc[c];
+                }
+            (void)m;
+            CU(cudaMalloc(&ctx->sep_i, sizeof(int32_t) * kmap.size()));
+            CU(cudaMemcpy(ctx->sep_i, kmap.data(), sizeof(int32_t) * kmap.size(), cudaMemcpyHostToDevice));
+            CU(cudaMalloc(&ctx->sep_c, sizeof(double) * cmap.size()));
+            CU(cudaMemcpy(ctx->sep_c, cmap.data(), sizeof(double) * cmap.size(), cudaMemcpyHostToDevice));
         }
         if (ctx->tab_dev[level]) return MLMC_OK;
         std::vector<double> tab;
@@ -252,10 +259,7 @@ cudaError_t field(const mlmc_ctx* ctx, int mesh, const double* xi, double* a, ui
                   cudaStream_t st) {
     const int N = level_N(ctx, mesh), m = ctx->pr.m;
     if (!field_sep(ctx, N)) return launch_field(ctx->phi_dev[mesh], xi, a, 2 * N * N, m, nb, keys, st);
-    const int K = ctx->sep.K;
-    const int* aoff = ctx->sep_i;
-    return launch_field_sep(ctx->tab_dev[mesh], aoff, aoff + K + 1, aoff + K + 1 + m, ctx->sep_c, K, xi, a, N, m, nb,
-                            keys, st);
+    return launch_field_sep(ctx->tab_dev[mesh], ctx->sep_i, ctx->sep_c, ctx->sep.K, xi, a, N, m, nb, keys, st);
 }
 
 int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {

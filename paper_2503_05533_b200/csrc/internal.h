@@ -42,11 +42,12 @@ cudaError_t launch_rng(double* xi, int m, uint64_t nb, uint64_t seed, int level,
 // by the caller): keys[2b] = max_p a (bits), keys[2b+1] = ~min_p a (bits), the coefficient contrast.
 cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, int m, uint64_t nb,
                          unsigned long long* keys, cudaStream_t s);
-// K1s (default): the same a_T from the separable form, a = exp(f^T W) with W = sum_k c_k xi_k g (two small
-// contractions per sample instead of the P x m one); tab / aoff / mk / mb / mc as in SepModes (device).
-cudaError_t launch_field_sep(const double* tab, const int* aoff, const int* mk, const int* mb, const double* mc,
-                             int K, const double* xi, double* a, int N, int m, uint64_t nb, unsigned long long* keys,
-                             cudaStream_t s);
+// K1s: the same a_T from the separable form, a = exp(F W) with W = C_xi G^T (two small DMMA contractions
+// per sample instead of the P x m one).  tab: the four 1D tables [4][N][K] (build_sep_tables); kmap / cmap
+// (device, K x K): the mode k = (a, b) and its c_k, or -1 / 0 where no mode has that pair.
+cudaError_t launch_field_sep(const double* tab, const int* kmap, const double* cmap, int K, const double* xi,
+                             double* a, int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s);
+bool field_sep_supported(int N, int K);   // N = 8, 16 or a multiple of 32; K <= 32
 bool field_use_dense();   // MLMC_FIELD_KERNEL=dense|ffma selects the P x m synthesis (A/B)
 bool field_force_sep();   // MLMC_FIELD_KERNEL=sep selects the separable synthesis on every mesh (tests)
 // Longest-first order of nb <= kOrderMax systems by descending contrast max a / min a (a single-CTA

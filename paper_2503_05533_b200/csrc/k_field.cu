@@ -294,137 +294,226 @@ cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cud
 // Both fields are sums of products: g(x1, x2) = sum_k c_k xi_k f_{a_k}(x1) g_{b_k}(x2) (the 2D KL modes of
 // the separable covariance, R11; Eq. (20)'s sin x cos terms).  With f, g tabulated at the N centroid
 // abscissae (i + 1/3) h, (i + 2/3) h of each axis, a lower triangle (centroid ((i+2/3)h, (j+1/3)h)) gets
-//     g_L(i, j) = sum_a f23[i][a] W_L[a][j],   W_L[a][j] = sum_{k: a_k = a} c_k xi_k g13[j][b_k],
-// an upper one the same with f13 and g23.  Per sample: 2 m N + 4 K N^2 flops instead of 4 m N^2 (K = the
+//     g_L(i, j) = sum_a F23[i][a] W_L[a][j],   W_L[a][j] = sum_{k: a_k = a} c_k xi_k G13[j][b_k],
+// an upper one the same with F13 and G23.  Per sample 4 m N + 4 K N^2 flops instead of 4 m N^2 (K = the
 // number of 1D functions: 16 for configs[1], 30 for configs[4]); the same values as the P x m synthesis
-// up to the order of the binary64 sums.  A CTA takes SB samples x a TJ-row x TI-column tile of the mesh:
-// u = c xi (gathered in the CSR order), W_L / W_U for its rows, then the outputs (i fastest, so the
-// (lower, upper) pairs of a row are stored as contiguous double2), exp, and the contrast keys.
-__global__ void __launch_bounds__(256) field_sep_kernel(const double* __restrict__ tab, const int* __restrict__ aoff,
-                                                        const int* __restrict__ mk, const int* __restrict__ mb,
-                                                        const double* __restrict__ mc, int K,
+// up to the order of the binary64 sums.
+//
+// Per sample both stages are small matrix products on the FP64 tensor cores (DMMA m8n8k4):
+//     W_t = C_xi G_t^T     (Kp x Kp) (Kp x N):  C_xi[a][b] = c_k xi_k for the mode k = (a, b), else 0
+//     g_t = F_t W_t        (N x Kp) (Kp x N):   t = lower (F23, G13) / upper (F13, G23)
+// with K zero-padded to KP in {8, 16, 32}; C_xi is gathered through the K x K mode map (kmap, cmap:
+// every (a, b) pair belongs to at most one mode).  A CTA owns a TJ x TJ tile of the mesh (TJ = min(N,
+// 32)), stages its F and G tables and the mode map once, and loops over groups of SB samples
+// (SB (TJ/8)^2 >= 8 output blocks; see launch_sep_t): gather C_xi, W for its rows, then the 8 x 8 output blocks -- the
+// lower and upper triangles of a block in one warp, so that a thread holds (L, U) at two adjacent
+// cells and stores 2 x double2 = the 32 contiguous bytes a[2(jN+i) .. 2(jN+i)+3].  Warp w always takes
+// column block w mod (TJ/8), so its F fragments stay in registers; all trip counts are compile-time
+// (unrolled: the loads and DMMA chains of a thread's blocks are independent).  Every sum runs over b,
+// resp. a, in ascending order whatever the tiling.  Shared-memory pitches are 4 mod 16 doubles: the
+// fragment loads (row tq, column gq) are conflict-free.
+namespace {
+__host__ __device__ constexpr int sep_pitch(int w) { return ((w + 15) / 16) * 16 + 4; }
+template <int TJ, int KP, int SB>
+__host__ __device__ constexpr size_t sep_smem() {
+    return (size_t)8 * (2 * (size_t)KP * sep_pitch(SB * TJ)              // W_t[a][s TJ + jj]
+                        + 2 * (size_t)KP * sep_pitch(TJ)                  // F_t[a][ii]
+                        + 2 * (size_t)KP * sep_pitch(TJ)                  // G_t[b][jj]
+                        + (size_t)SB * KP * sep_pitch(KP)                 // C_xi[s][a][b]
+                        + (size_t)KP * KP) +                              // c of the mode map
+           4 * (size_t)KP * KP +                                          // k of the mode map
+           16 * (size_t)SB;                                               // contrast keys
+}
+}  // namespace
+
+template <int TJ, int KP, int SB>
+__global__ void __launch_bounds__(256, KP == 32 ? (TJ == 8 ? 2 : 3) : 4) field_sep_kernel(const double* __restrict__ tab, const int* __restrict__ kmap,
+                                                        const double* __restrict__ cmap, int K,
                                                         const double* __restrict__ xi, double* __restrict__ a, int N,
-                                                        int m, int nb, int SB, int TJ, int TI,
-                                                        unsigned long long* __restrict__ keys) {
+                                                        int m, int nb, unsigned long long* __restrict__ keys) {
+    constexpr int TI = TJ, SJ = SB * TJ;
+    constexpr int PW = sep_pitch(SJ), PF = sep_pitch(TI), PG = sep_pitch(TJ), PC = sep_pitch(KP);
+    constexpr int NT = 256, NW = 8, NBJ = TJ / 8, NBI = TI / 8, PER = NBJ * NBI, NK4 = KP / 4;
+    constexpr int NAB = KP / 8, WPER = 2 * NAB * NBJ;
+    static_assert(NW % NBI == 0 && (SB * PER) % NW == 0 && (SB * WPER) % NW == 0, "even warp split");
     extern __shared__ __align__(16) double fsm[];
-    double* u = fsm;                               // [SB][m] in CSR order
-    double* W0 = u + SB * m;                       // [SB][K][TJ]
-    double* W1 = W0 + SB * K * TJ;
-    double* F23 = W1 + SB * K * TJ;                // [K][TI]
-    double* F13 = F23 + K * TI;
-    double* G13 = F13 + K * TI;                    // [K][TJ]
-    double* G23 = G13 + K * TJ;
-    unsigned long long* kk = reinterpret_cast<unsigned long long*>(G23 + K * TJ);   // [SB][2]
-    const int tid = threadIdx.x;
-    const int b0 = blockIdx.x * SB, j0 = blockIdx.y * TJ, i0 = blockIdx.z * TI;
-    const int ns = min(SB, nb - b0), nj = min(TJ, N - j0), ni = min(TI, N - i0);
-    const size_t NK = (size_t)N * K;
-    for (int e = tid; e < SB * m; e += blockDim.x) {
-        const int sm = e / m, q = e % m;
-        u[e] = sm < ns ? __ldg(mc + q) * __ldg(xi + (size_t)(b0 + sm) * m + __ldg(mk + q)) : 0.0;
-    }
-    for (int e = tid; e < K * TI; e += blockDim.x) {
-        const int q = e / TI, ii = e % TI;
-        const bool in = ii < ni;
-        F13[e] = in ? __ldg(tab + (size_t)(i0 + ii) * K + q) : 0.0;
-        F23[e] = in ? __ldg(tab + NK + (size_t)(i0 + ii) * K + q) : 0.0;
-    }
-    for (int e = tid; e < K * TJ; e += blockDim.x) {
-        const int q = e / TJ, jj = e % TJ;
-        const bool in = jj < nj;
-        G13[e] = in ? __ldg(tab + 2 * NK + (size_t)(j0 + jj) * K + q) : 0.0;
-        G23[e] = in ? __ldg(tab + 3 * NK + (size_t)(j0 + jj) * K + q) : 0.0;
-    }
-    if (tid < 2 * SB) kk[tid] = 0ull;
-    __syncthreads();
-    for (int e = tid; e < SB * K * TJ; e += blockDim.x) {
-        const int sm = e / (K * TJ), r = e % (K * TJ), q = r / TJ, jj = r % TJ;
-        const double* us = u + sm * m;
-        double w0 = 0.0, w1 = 0.0;
-        const int e1 = __ldg(aoff + q + 1);
-        for (int c = __ldg(aoff + q); c < e1; ++c) {
-            const double uc = us[c];
-            const int bq = __ldg(mb + c);
-            w0 = fma(uc, G13[bq * TJ + jj], w0);
-            w1 = fma(uc, G23[bq * TJ + jj], w1);
+    double* W = fsm;                               // [2][KP][PW]
+    double* F = W + 2 * KP * PW;                   // [2][KP][PF]   t = 0: F23, t = 1: F13
+    double* G = F + 2 * KP * PF;                   // [2][KP][PG]   t = 0: G13, t = 1: G23
+    double* Cx = G + 2 * KP * PG;                  // [SB][KP][PC]
+    double* Cm = Cx + SB * KP * PC;                // [KP * KP]  c_k of the pair (a, b), 0 if none
+    int* Km = reinterpret_cast<int*>(Cm + KP * KP);                                // [KP * KP]  k, or -1
+    unsigned long long* kk = reinterpret_cast<unsigned long long*>(Km + KP * KP);  // [SB][2]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int nti = N / TI;
+    const int j0 = (blockIdx.y / nti) * TJ, i0 = (blockIdx.y % nti) * TI;
+    const size_t NK = (size_t)N * K, P = 2 * (size_t)N * N;
+    {   // the tile's 1D tables, [t][x][q] -> [t][q][x], zero-padded q >= K (q fastest: coalesced reads)
+        constexpr int R = (2 * TI * KP + NT - 1) / NT;
+        double fv[R], gv[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = tid + NT * r, t = e / (TI * KP), ii = (e / KP) % TI, q = e % KP;
+            const bool in = e < 2 * TI * KP && q < K;
+            fv[r] = in ? __ldg(tab + (t == 0 ? NK : 0) + (size_t)(i0 + ii) * K + q) : 0.0;
+            gv[r] = in ? __ldg(tab + (2 + t) * NK + (size_t)(j0 + ii) * K + q) : 0.0;
         }
-        W0[e] = w0;
-        W1[e] = w1;
-    }
-    __syncthreads();
-    const int P = 2 * N * N;
-    for (int e = tid; e < SB * TJ * TI; e += blockDim.x) {
-        const int sm = e / (TJ * TI), r = e % (TJ * TI), jj = r / TI, ii = r % TI;
-        const bool live = sm < ns && jj < nj && ii < ni;
-        double v0 = 0.0, v1 = 0.0;
-        if (live) {
-            const double* w0 = W0 + sm * K * TJ + jj;
-            const double* w1 = W1 + sm * K * TJ + jj;
-            double g0 = 0.0, g1 = 0.0;
-            for (int q = 0; q < K; ++q) {
-                g0 = fma(F23[q * TI + ii], w0[q * TJ], g0);
-                g1 = fma(F13[q * TI + ii], w1[q * TJ], g1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = tid + NT * r, t = e / (TI * KP), ii = (e / KP) % TI, q = e % KP;
+            if (e < 2 * TI * KP) {
+                F[(t * KP + q) * PF + ii] = fv[r];
+                G[(t * KP + q) * PG + ii] = gv[r];
             }
-            v0 = exp(g0);
-            v1 = exp(g1);
-            *reinterpret_cast<double2*>(a + (size_t)(b0 + sm) * P + 2 * ((size_t)(j0 + jj) * N + i0 + ii)) =
-                make_double2(v0, v1);
         }
-        if (keys) {
-            // contrast partials: a warp's outputs belong to one sample when TJ * TI is a multiple of 32
-            double mx = live ? fmax(v0, v1) : 0.0, mn = live ? fmin(v0, v1) : DBL_MAX;
-            const int s0 = __shfl_sync(0xffffffffu, sm, 0);
-            if (__all_sync(0xffffffffu, sm == s0)) {
+        for (int e = tid; e < KP * KP; e += NT) {
+            const int ra = e / KP, rb = e % KP;
+            const bool in = ra < K && rb < K;
+            const int k = in ? __ldg(kmap + ra * K + rb) : -1;
+            Km[e] = k;
+            Cm[e] = k >= 0 ? __ldg(cmap + ra * K + rb) : 0.0;
+        }
+    }
+    __syncthreads();
+    const int ib = warp % NBI;                     // this warp's column block (fixed)
+    double fL[NK4], fU[NK4];
+#pragma unroll
+    for (int k = 0; k < NK4; ++k) {
+        fL[k] = F[(4 * k + tq) * PF + 8 * ib + gq];
+        fU[k] = F[(KP + 4 * k + tq) * PF + 8 * ib + gq];
+    }
+    const int ngroups = (nb + SB - 1) / SB;
+    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int b0 = grp * SB, ns = min(SB, nb - b0);
+        {   // C_xi[s][a][b] = c xi_k (gathered)
+            constexpr int R = (SB * KP * KP + NT - 1) / NT;
+            double v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int e = tid + NT * r, sm = e / (KP * KP), me = e % (KP * KP);
+                const int k = e < SB * KP * KP ? Km[me] : -1;
+                v[r] = (k >= 0 && sm < ns) ? Cm[me] * __ldg(xi + (size_t)(b0 + sm) * m + k) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int e = tid + NT * r, sm = e / (KP * KP), me = e % (KP * KP);
+                if (e < SB * KP * KP) Cx[(sm * KP + me / KP) * PC + me % KP] = v[r];
+            }
+        }
+        if (keys && tid < 2 * SB) kk[tid] = tid & 1 ? ~0ull : 0ull;   // per sample: bits(max) up, bits(min) down
+        __syncthreads();
+        // W_t[a][s TJ + jj] = sum_b C_xi[s][a][b] G_t[b][jj]  (8 x 8 blocks, KP / 4 DMMA each)
+#pragma unroll
+        for (int n = 0; n < SB * WPER / NW; ++n) {
+            const int task = warp + NW * n;
+            const int sm = task / WPER, r = task % WPER, t = r / (NAB * NBJ), ab = (r / NBJ) % NAB, jb = r % NBJ;
+            double d0 = 0.0, d1 = 0.0;
+            const double* ca = Cx + (sm * KP + 8 * ab + gq) * PC + tq;          // A[row a][col b]
+            const double* gb = G + (t * KP + tq) * PG + 8 * jb + gq;            // B[row b][col jj]
+#pragma unroll
+            for (int k = 0; k < NK4; ++k) dmma(d0, d1, ca[4 * k], gb[4 * k * PG]);
+            *reinterpret_cast<double2*>(W + (t * KP + 8 * ab + gq) * PW + sm * TJ + 8 * jb + 2 * tq) =
+                make_double2(d0, d1);
+        }
+        __syncthreads();
+        // g_t[jj][ii] = sum_a W_t[a][jj] F_t[a][ii], exp, store; contrast keys per sample
+        constexpr int NB = SB * PER / NW;          // blocks per warp; a warp's blocks of one sample are adjacent
+        double mx = 0.0, mn = DBL_MAX;
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+            const int blk = warp + NW * n, sm = blk / PER, jb = (blk % PER) / NBI;
+            if (sm < ns) {
+                double dL0 = 0.0, dL1 = 0.0, dU0 = 0.0, dU1 = 0.0;
+                const double* wL = W + tq * PW + sm * TJ + 8 * jb + gq;         // A[row jj][col a]
+#pragma unroll
+                for (int k = 0; k < NK4; ++k) {
+                    dmma(dL0, dL1, wL[4 * k * PW], fL[k]);
+                    dmma(dU0, dU1, wL[(KP + 4 * k) * PW], fU[k]);
+                }
+                const int j = j0 + 8 * jb + gq, i = i0 + 8 * ib + 2 * tq;
+                const double l0 = exp(dL0), u0 = exp(dU0), l1 = exp(dL1), u1 = exp(dU1);
+                double* dst = a + (size_t)(b0 + sm) * P + 2 * ((size_t)j * N + i);
+                *reinterpret_cast<double2*>(dst) = make_double2(l0, u0);
+                *reinterpret_cast<double2*>(dst + 2) = make_double2(l1, u1);
+                mx = fmax(mx, fmax(fmax(l0, u0), fmax(l1, u1)));
+                mn = fmin(mn, fmin(fmin(l0, u0), fmin(l1, u1)));
+            }
+            const bool last = n + 1 == NB || (warp + NW * (n + 1)) / PER != sm;
+            if (keys && last) {                                   // warp-uniform
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                     mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
                 }
-                if ((tid & 31) == 0 && s0 < ns) {
-                    atomicMax(kk + 2 * s0, (unsigned long long)__double_as_longlong(mx));
-                    atomicMax(kk + 2 * s0 + 1, ~(unsigned long long)__double_as_longlong(mn));
+                if (lane == 0 && sm < ns) {
+                    atomicMax(kk + 2 * sm, (unsigned long long)__double_as_longlong(mx));
+                    atomicMin(kk + 2 * sm + 1, (unsigned long long)__double_as_longlong(mn));
                 }
-            } else if (live) {
-                atomicMax(kk + 2 * sm, (unsigned long long)__double_as_longlong(mx));
-                atomicMax(kk + 2 * sm + 1, ~(unsigned long long)__double_as_longlong(mn));
+                mx = 0.0;
+                mn = DBL_MAX;
             }
         }
-    }
-    if (keys) {
-        __syncthreads();
-        if (tid < ns) {
-            atomicMax(keys + 2 * (b0 + tid), kk[2 * tid]);
-            atomicMax(keys + 2 * (b0 + tid) + 1, kk[2 * tid + 1]);
+        if (keys) {
+            __syncthreads();
+            if (tid < ns) {                                       // the global keys hold ~bits(min): max of ~
+                atomicMax(keys + 2 * (b0 + tid), kk[2 * tid]);
+                atomicMax(keys + 2 * (b0 + tid) + 1, ~kk[2 * tid + 1]);
+            }
         }
+        __syncthreads();                                          // Cx, W and kk are rewritten next group
     }
 }
 
-cudaError_t launch_field_sep(const double* tab, const int* aoff, const int* mk, const int* mb, const double* mc,
-                             int K, const double* xi, double* a, int N, int m, uint64_t nb, unsigned long long* keys,
-                             cudaStream_t s) {
-    if (nb == 0) return cudaSuccess;
-    // tile: all of a small mesh per CTA with several samples, else 16 rows x 64 columns of one sample
-    int SB, TJ, TI;
-    if (N <= 8) { SB = 16; TJ = N; TI = N; }
-    else if (N <= 16) { SB = 4; TJ = N; TI = N; }
-    else if (N <= 32) { SB = 1; TJ = N; TI = N; }
-    else { SB = 1; TJ = 16; TI = 64; }
-    auto bytes = [&](int sb) {
-        return (size_t)8 * ((size_t)sb * m + 2 * (size_t)sb * K * TJ + 2 * (size_t)K * TI + 2 * (size_t)K * TJ) +
-               16 * (size_t)sb;
-    };
-    while (SB > 1 && bytes(SB) > 200 * 1024) SB /= 2;
-    const size_t smem = bytes(SB);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(field_sep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
-    const dim3 grid((unsigned)((nb + SB - 1) / SB), (unsigned)((N + TJ - 1) / TJ), (unsigned)((N + TI - 1) / TI));
-    field_sep_kernel<<<grid, 256, smem, s>>>(tab, aoff, mk, mb, mc, K, xi, a, N, m, (int)nb, SB, TJ, TI, keys);
+namespace {
+// SB samples per group: 8 at N = 8, 4 at N = 16 (8 output blocks per group), 1 at N >= 32 (two per group
+// measured 7% slower at configs[1] level 3: fewer CTAs to hide the latency of the phases).
+template <int TJ, int KP, int SB>
+cudaError_t launch_sep_t(const double* tab, const int* kmap, const double* cmap, int K, const double* xi, double* a,
+                         int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
+    constexpr size_t smem = sep_smem<TJ, KP, SB>();
+    static_assert(smem <= 227 * 1024, "separable synthesis tile exceeds shared memory");
+    static PerDevice<KernelOcc> cache;
+    const KernelOcc occ = occ_of(cache, field_sep_kernel<TJ, KP, SB>, 256, smem);
+    if (occ.err != cudaSuccess) return occ.err;
+    const uint64_t tiles = (uint64_t)(N / TJ) * (N / TJ);
+    if (tiles > 65535) return cudaErrorInvalidValue;
+    const uint64_t groups = (nb + SB - 1) / SB;
+    const uint64_t all = (uint64_t)occ.per_sm * occ.sms;
+    const uint64_t gx = std::min<uint64_t>(groups, std::max<uint64_t>(1, all / tiles));
+    field_sep_kernel<TJ, KP, SB><<<dim3((unsigned)gx, (unsigned)tiles), 256, smem, s>>>(tab, kmap, cmap, K, xi, a, N,
+                                                                                       m, (int)nb, keys);
     return cudaGetLastError();
+}
+template <int TJ, int KP>
+cudaError_t launch_sep_sb(const double* tab, const int* kmap, const double* cmap, int K, const double* xi, double* a,
+                          int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
+    if constexpr (TJ == 8) {
+        return launch_sep_t<TJ, KP, 8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    } else if constexpr (TJ == 16) {
+        return launch_sep_t<TJ, KP, 4>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    } else {
+        return launch_sep_t<TJ, KP, 1>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    }
+}
+template <int TJ>
+cudaError_t launch_sep_k(const double* tab, const int* kmap, const double* cmap, int K, const double* xi, double* a,
+                         int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
+    if (K <= 8) return launch_sep_sb<TJ, 8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    if (K <= 16) return launch_sep_sb<TJ, 16>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    return launch_sep_sb<TJ, 32>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+}
+}  // namespace
+
+bool field_sep_supported(int N, int K) { return N >= 8 && (N < 32 ? (N & (N - 1)) == 0 : N % 32 == 0) && K >= 1 && K <= 32; }
+
+cudaError_t launch_field_sep(const double* tab, const int* kmap, const double* cmap, int K, const double* xi,
+                             double* a, int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
+    if (nb == 0) return cudaSuccess;
+    if (!field_sep_supported(N, K) || nb > 0x7fffffffull) return cudaErrorInvalidValue;
+    if (N >= 32) return launch_sep_k<32>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    if (N == 16) return launch_sep_k<16>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    return launch_sep_k<8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
 }
 
 static bool field_use_ffma() {

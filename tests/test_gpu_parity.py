@@ -76,17 +76,18 @@ def test_rng_and_field_match_oracle(cfg_name):
 
 def test_field_synthesis_paths_match_oracle():
     """configs[4] (m = 256, K = 30 one-dimensional functions): h = 1/8 takes the P x m synthesis on the FP64
-    tensor cores, h = 1/16 .. 1/64 the separable one (K1s; ragged sample blocks and 16 x 64 tiles);
-    both reproduce the oracle's centroid-by-centroid KL sum to 1e-12."""
+    tensor cores (N = 8 with K > 16), h = 1/16 .. 1/512 the separable one (K1s: 8 samples x 8 x 8, 4 x 16 x 16
+    and 32 x 32 tiles, up to 256 tiles per sample at h = 1/512; ragged sample groups); both reproduce the
+    oracle's centroid-by-centroid KL sum to 1e-12."""
     cfg = W.CONFIGS["C5"]
-    ctx = _ctx(cfg, L_max=3)
+    ctx = _ctx(cfg, L_max=6)
     P = _oracle(cfg)
-    for level, mesh in ((0, 0), (1, 1), (3, 3), (3, 2)):
-        n = 37
+    for level, mesh, n, ks in ((0, 0, 37, (0, 17, 36)), (1, 1, 37, (0, 17, 36)), (3, 3, 37, (0, 17, 36)),
+                               (3, 2, 37, (0, 17, 36)), (4, 4, 5, (0, 4)), (6, 6, 3, (2,))):
         xi, a = ctx.debug_field(level, mesh, n, seed=12, first_index=77)
         xi, a = xi.cpu().numpy(), a.cpu().numpy()
         N = cfg["h0_inv"] << mesh
-        for k in (0, 17, 36):
+        for k in ks:
             ref_a = P.field_triangles(N, oc.normals(12, level, 77 + k, cfg["m"]))
             assert np.max(np.abs(a[k] / ref_a - 1)) < 1e-12, (level, mesh, k)
     ctx.close()
