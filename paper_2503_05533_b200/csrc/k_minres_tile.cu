@@ -580,6 +580,9 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             IF_TUNING(if (var == 1) return run_tile<16, 2, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 2) return run_tile<16, 2, 6, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             // (conductances in shared memory, 6 / 8 CTAs per SM: level-1 pass 0.60 / 0.61 ms vs 0.51 ms)
+            // v3 (8 rows per thread, 16 systems per 128-thread CTA: the scalar recurrences shared by half as
+            // many threads): 0.266 vs 0.206 ms per level-1 launch, C2 step 2.41 vs 2.36 ms (255 registers, spills)
+            IF_TUNING(if (var == 3) return run_tile<16, 8, 2, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             return run_tile<16, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 32:
             IF_TUNING(if (var == 1) return run_tile<32, 4, 4, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
@@ -589,17 +592,19 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             // on configs[1] level 2, bit-identical records
             IF_TUNING(if (var == 4) return run_tile<32, 4, 5, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 5) return run_tile<32, 4, 4, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            // v6 (8 rows per thread, 2 systems per CTA, 4 per SM): 0.524 vs 0.490 ms per level-2 launch, C2 step
+            // 2.344 vs 2.361 ms (within run-to-run noise)
+            IF_TUNING(if (var == 6) return run_tile<32, 8, 2, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             return run_tile<32, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 64:
             // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67, v4 2.97
+            // (v2 / v3, 512-thread systems, dropped: the one-warp cross-warp reduction holds <= 10 warps)
             // (v4: every conductance in shared memory, two systems per SM; bit-identical records, but the
             // ~60 shared loads per thread and step outweigh the second resident system); per launch
             // (tools/tune_minres.py): v0 1.671 ms, v5 (west conductances in shared memory, no in-loop
             // spills) 1.723, v6 (diagonal in shared memory) 1.722, v1 1.711 -- v0's few L1-resident
             // spill reloads cost less than the shared loads that remove them
             IF_TUNING(if (var == 1) return run_tile<64, 8, 1, 3, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
-            IF_TUNING(if (var == 2) return run_tile<64, 4, 1, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
-            IF_TUNING(if (var == 3) return run_tile<64, 4, 1, 3, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 4) return run_tile<64, 8, 2, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 5) return run_tile<64, 8, 1, 2, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 6) return run_tile<64, 8, 1, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)

@@ -42,6 +42,10 @@ def run(levels, n, steps=20, warm=3):
 
 out = {}
 out["all levels, N = (20000, 5000, 1200, 300)"] = run([0, 1, 2, 3], [20000, 5000, 1200, 300])
+if os.environ.get("STEP_PROBE_QUICK") == "1":          # the full step only (tuning A/B)
+    print(json.dumps(out))
+    ctx.close()
+    sys.exit(0)
 for n3 in (148, 200, 450, 600):
     out[f"all levels, level 3 N = {n3}"] = run([0, 1, 2, 3], [20000, 5000, 1200, n3])
 out["levels 0-2 only"] = run([0, 1, 2], [20000, 5000, 1200])
