@@ -83,7 +83,8 @@ def test_field_synthesis_paths_match_oracle():
     ctx = _ctx(cfg, L_max=6)
     P = _oracle(cfg)
     for level, mesh, n, ks in ((0, 0, 37, (0, 17, 36)), (1, 1, 37, (0, 17, 36)), (3, 3, 37, (0, 17, 36)),
-                               (3, 2, 37, (0, 17, 36)), (4, 4, 5, (0, 4)), (6, 6, 3, (2,))):
+                               (3, 2, 37, (0, 17, 36)), (4, 4, 5, (0, 4)), (6, 6, 3, (2,)), (1, 1, 1, (0,)),
+                               (2, 2, 1, (0,))):
         xi, a = ctx.debug_field(level, mesh, n, seed=12, first_index=77)
         xi, a = xi.cpu().numpy(), a.cpu().numpy()
         N = cfg["h0_inv"] << mesh
