@@ -198,6 +198,22 @@ struct LevelSched {
     cudaEvent_t fork = nullptr, join = nullptr, prep = nullptr, gate = nullptr;
 };
 
+// Scheduling knobs of the concurrent-levels step, for A/B runs of the tuning build only (MLMC_SCHED_GATE=0:
+// no gate behind the largest level's fields; MLMC_SCHED_FORK=0: coarse halves after the fine ones on one
+// stream; MLMC_SCHED_PRIO=0: every level stream at the same priority, =2: the largest level's coarse stream one
+// step below its fine one).  The production build uses the defaults, which measured fastest on configs[1]
+// (tools/gpu_call_r02ac.sh: 2.341 ms; no gate 2.472, no fork 2.376, flat priorities 2.379, coarse one step
+// lower 2.348).
+int sched_knob(const char* name) {
+#ifdef MLMC_TUNING
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : 1;
+#else
+    (void)name;
+    return 1;
+#endif
+}
+
 // Which synthesis a mesh uses (a function of N, m and K only, so results never depend on the batch):
 // the separable one (K1s) where the kernel supports the mesh and K, unless N = 8 and K > 16 (there the
 // per-sample K x K gather outweighs the 2N^2 x m contraction: measured on configs[4] level 0), or where
@@ -492,7 +508,7 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         double* xc = reinterpret_cast<double*>(ex.ws + L.xc);
         // (the fork is per pass: the join below orders the next pass's field writes after this coarse solve);
         // with per-kernel profiling on, the solves stay serialised so that every launch's event time is its own
-        const bool fork = sch && level > 0 && sch->st_c && Nf < kGmMinN && !c2f && !ctx->prof_on;
+        const bool fork = sch && level > 0 && sch->st_c && Nf < kGmMinN && !c2f && !ctx->prof_on && sched_knob("MLMC_SCHED_FORK");
         if (fork) {
             CU(cudaEventRecord(sch->fork, st));
             CU(cudaStreamWaitEvent(sch->st_c, sch->fork, 0));
@@ -782,11 +798,14 @@ int sample_levels_impl(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_
         cudaDeviceGetStreamPriorityRange(&least, &greatest);
         while ((int)ctx->aux.size() < nlev) {
             const int k = (int)ctx->aux.size();
-            const int prio = std::max(greatest, least - (least - greatest) * (MLMC_MAX_LEVELS - k) / MLMC_MAX_LEVELS);
+            const int prio = sched_knob("MLMC_SCHED_PRIO")
+                                 ? std::max(greatest, least - (least - greatest) * (MLMC_MAX_LEVELS - k) / MLMC_MAX_LEVELS)
+                                 : greatest;
             cudaStream_t s;
             CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, k == 0 ? greatest : prio));
             ctx->aux.push_back(s);
-            CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, k == 0 ? greatest : prio));
+            const int prio_c = k == 0 && sched_knob("MLMC_SCHED_PRIO") == 2 ? std::min(least, greatest + 1) : prio;
+            CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, k == 0 && prio_c == prio ? greatest : prio_c));
             ctx->aux_c.push_back(s);
             cudaEvent_t e;
             CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -810,8 +829,8 @@ int sample_levels_impl(mlmc_ctx* ctx, int nlev, const int* levels, const uint64_
         sch.st_c = ctx->aux_c[k];
         sch.fork = ctx->cfork_ev[k];
         sch.join = ctx->cjoin_ev[k];
-        sch.prep = k == 0 ? ctx->prep_ev[0] : nullptr;
-        sch.gate = k == 0 ? nullptr : ctx->prep_ev[0];
+        sch.prep = k == 0 && sched_knob("MLMC_SCHED_GATE") ? ctx->prep_ev[0] : nullptr;
+        sch.gate = k == 0 || !sched_knob("MLMC_SCHED_GATE") ? nullptr : ctx->prep_ev[0];
         const bool top_single =
             max_batch(ctx, levels[order[0]], slice[order[0]], &prec_fine[order[0]], &prec_coarse[order[0]]) >= n[order[0]];
         if (!top_single) sch.prep = sch.gate = nullptr;   // the largest level runs in passes: no gate
