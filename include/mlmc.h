@@ -145,9 +145,10 @@ typedef struct mlmc_ctx mlmc_ctx;   /* opaque */
  * mlmc_plan_levels: validate `problem`, compute the KL eigenpairs on the host
  * (1D transcendental equations, R11), and upload each level's synthesis data
  * to the device lazily on first use of the level: the matrix Phi_l[p][k]
- * (2 N_l^2 triangle centroids x m, binary64) on meshes where the direct
- * contraction is cheaper, else the separable form's four N_l x K tables of the
- * 1D functions (K = number of 1D modes in use).  Creates its own stream unless
+ * (2 N_l^2 triangle centroids x m, binary64) where the separable form does not
+ * apply (h = 1/8 with K > 16 one-dimensional modes, or K > 32), else the
+ * separable form's four N_l x K tables of the 1D functions and the K x K mode
+ * map (K = number of 1D modes in use).  Creates its own stream unless
  * one is bound later.  Errors: EINVAL (bad problem), ECUDA (no device).
  * The ctx owns its plan data; free with mlmc_destroy.                        */
 int  mlmc_plan_levels(const mlmc_problem* problem, mlmc_ctx** out);
