@@ -433,7 +433,7 @@ def run_ours(args):
         _dbg("c1 leg done")
         line["c3_cholesky_ir"] = c3_leg(local, torch)
         _dbg("c3 leg done")
-        line["k3c_fine_meshes"] = fine_leg(local, torch)
+        line["fine_meshes"] = fine_leg(local, torch)
         _dbg("fine leg done")
         if rank == 0:
             line["fine_single_system"] = dd_leg(local, torch)
@@ -676,11 +676,12 @@ def c2f_leg(local, torch):
 
 
 def fine_leg(local, torch):
-    """K3c, the streamed MINRES of the fine meshes (configs[4] field, h = 1/256 and 1/512): one batch of
-    148 systems (one per SM) per mesh, 300 MINRES steps each (max_iter; the finest levels of configs[4]
-    need thousands -- the rate per step is what the roofline measures).  K3c moves p_j, p_{j-1}, cE, cN
-    in and p_{j+1} out once per step: 40 algorithmic bytes per unknown and step (DESIGN.md section 6);
-    the kernel time is the library's per-launch CUDA-event time."""
+    """MINRES on the fine meshes of configs[4]: K3b (h = 1/128 on 4-CTA clusters, 1/256 on 16-CTA clusters, every
+    row on chip) and K3c (h = 1/512, streamed): one batch of 148 systems per mesh, 300 MINRES steps each
+    (max_iter; the finest levels need thousands -- the rate per step is what the roofline measures).  K3b is
+    FP64-ALU work on chip (28 flops per unknown and step); K3c moves p_j, p_{j-1}, cE, cN in and
+    p_{j+1} out once per step: 40 algorithmic bytes per unknown and step.  The kernel time
+    is the library's per-launch CUDA-event time."""
     from paper_2503_05533_b200 import Context, precision
     cfg = W.CONFIGS["C5"]
     ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=cfg["h0_inv"],
@@ -689,7 +690,7 @@ def fine_leg(local, torch):
     nb, steps = 148, 300
     prec = precision("minres", max_iter=steps)
     out = {}
-    for level in (5, 6):
+    for level in (4, 5, 6):
         N = cfg["h0_inv"] << level
         ctx.sample_level_async(level, 2, cfg["seed"], 10**6, prec, prec, 1e-14, 1e-14, sums_out=sums)
         ctx.profile_enable(True)
@@ -699,10 +700,17 @@ def fine_leg(local, torch):
         s = sums.cpu().numpy()
         k_ms = sum(r[3] for r in prof if r[0] == "minres" and r[1] == N)
         node_steps = s[7] * (N - 1) ** 2
-        gbs = 40.0 * node_steps / (k_ms / 1e3) / 1e9
-        out[f"h=1/{N}"] = {"systems": nb, "minres_steps_each": s[7] / nb, "kernel_ms": k_ms,
-                           "unknown_steps_per_s": node_steps / (k_ms / 1e3), "achieved_GBs_40B": gbs,
-                           "hbm_frac": gbs / HBM_PEAK_GBS, "bound": "hbm"}
+        row = {"systems": nb, "minres_steps_each": s[7] / nb, "kernel_ms": k_ms,
+               "unknown_steps_per_s": node_steps / (k_ms / 1e3)}
+        if N <= 256:                                                   # K3b: on chip, FP64 ALU
+            tf = FLOPS_PER_NODE_ITER * node_steps / (k_ms / 1e3) / 1e12
+            row.update({"kernel": "K3b minres cluster", "achieved_TFLOPs_28": tf, "fp64_frac": tf / FP64_PEAK_TFLOPS,
+                        "bound": "alu"})
+        else:                                                          # K3c: streamed, HBM
+            gbs = 40.0 * node_steps / (k_ms / 1e3) / 1e9
+            row.update({"kernel": "K3c minres stream", "achieved_GBs_40B": gbs, "hbm_frac": gbs / HBM_PEAK_GBS,
+                        "bound": "hbm"})
+        out[f"h=1/{N}"] = row
     # K3m-t, the temporally blocked MG-PCG on the same meshes (NEXT-4): a real solve to 1e-6, 148 systems.
     # Algorithmic bytes per fine unknown and CG step: 106 on the fine level (passes C 44, A 37, B 25) + 37
     # for the coarser levels' plain V-cycle passes = 143 B (ncu measured 147).

@@ -380,7 +380,11 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
         int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;   // finite-precision Lanczos at contrast ~1e7 (Eq. (20), sigma = 2) needs > n
         bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
         if (keys && order) CU(counted(ctx, ex.st, MLMC_K_ORDER, N, [&] { return launch_order(keys, (int)nb, order, ex.st); }));
-        if (N >= kGmMinN && minres_stream_supported(N) && !use_gm_kernel())
+        if (N >= kGmMinN && minres_cluster_supported(N) && !use_gm_kernel())
+            CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
+                return launch_minres_cluster(N, a, nb, tol, mi, rec, slot, ctr, keys ? order : nullptr, ex.st);
+            }));
+        else if (N >= kGmMinN && minres_stream_supported(N) && !use_gm_kernel())
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
                 return launch_minres_stream(N, a, nb, tol, mi, rec, slot, ctr, gm_scratch, gm_ctas, ex.st,
                                             keys ? order : nullptr);

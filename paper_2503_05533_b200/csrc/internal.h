@@ -77,6 +77,10 @@ cudaError_t launch_minres_gm(int N, const double* a, uint64_t nb, double tol, in
 // K3c for N = 128, 256, 512: one pass per MINRES step streamed through HBM with TMA-tiled planes
 // (k_minres_stream.cu); same scratch convention (nctas CTAs x minres_stream_scratch_per_cta(N) bytes).
 bool minres_stream_supported(int N);
+// K3b: MINRES of one system per thread-block cluster, every row resident on chip (h = 1/128: 4 CTAs, 1/256: 16)
+bool minres_cluster_supported(int N);
+cudaError_t launch_minres_cluster(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                                  unsigned* ctr, const int* order, cudaStream_t s);
 // Tiled TMA tensor map (cuTensorMapEncodeTiled via the runtime's driver entry point): `map` points to a
 // CUtensorMap, dims innermost first, strides in bytes for dims 1.., zero OOB fill.  false on failure.
 bool encode_tensor_map(void* map, bool f64, int rank, void* base, const uint64_t* dims, const uint64_t* strides,

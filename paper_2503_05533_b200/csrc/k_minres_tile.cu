@@ -23,7 +23,9 @@
 // Tile-local phantom nodes (column N when the last pair overhangs, row N when the
 // last strip does) keep exactly zero entries: their conductances are zero and
 // their y is scaled by a per-thread 0 instead of 1/beta.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
@@ -33,27 +35,34 @@
 
 namespace mlmc {
 namespace {
+namespace cg = cooperative_groups;
 
 // Conductance placement (template CM, bit flags): 1 = diagonal d from a shared grid,
 // 2 = west conductance of column 0 from a shared grid; everything else in registers.
-template <int N, int R, int MINB_, int CM_>
+template <int N, int R, int MINB_, int CM_, int CL_ = 1>
 struct TileCfg {
     static constexpr int CM = CM_;
     static constexpr bool DS = CM & 1, WS = CM & 2, CS = CM & 4;
     static_assert(!(CS && (DS || WS)), "CS keeps every conductance in shared memory");
     static constexpr int C = N - 1;                       // interior columns / rows
     static constexpr int PAIRS = N / 2;                   // pair p: columns 2p+1, 2p+2 (column N is a phantom)
-    static constexpr int S = (C + R - 1) / R;             // row strips
-    static constexpr int TPS = PAIRS * S;                 // threads per system
+    static constexpr int S = (C + R - 1) / R;             // row strips of the system
+    // CL > 1 (K3b): one system per cluster of CL CTAs, CTA rank c owning strips c SL .. c SL + SL - 1
+    static constexpr int CL = CL_;
+    static_assert(CL == 1 || (S % CL == 0 && CM == 0), "whole strips per CTA; conductances in registers");
+    static constexpr int SL = S / CL;                     // strips per CTA
+    static constexpr int TPS = PAIRS * SL;                // threads per system (per CTA when CL > 1)
     static_assert(TPS % 32 == 0 || TPS == 16, "a system fills whole warps or one half-warp");
     static_assert(S * R == C || S * R == C + 1, "strips end at row C or at the boundary row N");
     static constexpr int NW = TPS >= 32 ? TPS / 32 : 1;
     static constexpr int GROUPS = TPS >= 128 ? 1 : 128 / TPS;
+    static_assert(CL == 1 || GROUPS == 1, "a clustered system fills its CTA");
     static constexpr int BLOCK = TPS * GROUPS;
     static constexpr int MINB = MINB_;
     static constexpr int PW = PAIRS + 2;                  // plane pitch: halo pair on both sides
     static constexpr int RP = 2 * PW;                     // grid row pitch (two parity planes)
-    static constexpr int ROWS = S * R + 2;                // grid rows 0 .. S*R+1 (0 and S*R+1 stay zero)
+    static constexpr int ROWS = SL * R + 2;               // grid rows 0 .. SL*R+1 (halo rows: zero, or the
+                                                          // neighbouring CTAs' boundary rows when CL > 1)
     static constexpr int GRID = ROWS * RP;
     static constexpr int DGRID = DS ? S * R * 2 * PAIRS : 0;   // d at [(row-1) * 2 * PAIRS + parity * PAIRS + pair]
     static constexpr int WGRID = WS ? S * R * PAIRS : 0;       // -cW of column 0 at [(row-1) * PAIRS + pair]
@@ -63,7 +72,11 @@ struct TileCfg {
     static constexpr int CEG = CS ? S * R * 2 * PE : 0;
     static constexpr int CNG = CS ? (S * R + 1) * 2 * PE : 0;
     static constexpr int RED = 4 * NW;                         // reduction buffer: NW x (3 partials + pad)
-    static constexpr int SMEM_PER_GROUP = GRID + DGRID + WGRID + CEG + CNG + RED;
+    // CL > 1: every CTA's partials [2 parities][CL][4] (pushed to each CTA), the neighbours' boundary-row
+    // t = A p_j [2 parities][2 sides][N] (side 0: the row below this CTA's first row, 1: the row above its
+    // last), p_{j-1} of those halo rows [2][N], two mbarriers (one per parity)
+    static constexpr int CLX = CL > 1 ? 8 * CL + 4 * N + 2 * N + 2 : 0;
+    static constexpr int SMEM_PER_GROUP = GRID + DGRID + WGRID + CEG + CNG + RED + CLX;
     static constexpr size_t SMEM = sizeof(double) * SMEM_PER_GROUP * GROUPS + 16 * GROUPS;
 };
 
@@ -128,6 +141,33 @@ __device__ __forceinline__ double4 tsum3(double a, double b, double c, double* b
     }
 }
 
+// K3b cluster exchange: st.async stores into a peer CTA's shared memory that complete-tx on the peer's
+// mbarrier (no cluster-wide barrier and no fence in the step loop); as with TMA multicast, the receiver's
+// CTA-scope wait on its own mbarrier makes the tracked bytes visible (no L1 invalidation per step)
+__device__ __forceinline__ uint32_t sm32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ uint32_t mapa32(uint32_t a, int r) {
+    uint32_t o;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
+    return o;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
 // One MINRES step per stencil, one reduction per step (R27):
 //   step j:  t = A p_j;  reduce (p_j . t, p_j . p_j, 1 . p_j)           [the only reduction]
 //            beta_j = ||p_j||, alpha_j = p_j.t / p_j.p_j (= v_j^T A v_j), sigma_j = 1^T v_j
@@ -144,13 +184,14 @@ __device__ __forceinline__ double4 tsum3(double a, double b, double c, double* b
 // of the coarse solution xio[job][(N/2-1)^2] of the same sample (the coarse half of the coupled sample): MINRES
 // then runs on A e = r0 = b - A x0 with the SAME stopping rule ||b - A x_k|| <= tol ||b|| (phibar_k <= tol
 // ||b||, not tol ||r0||), and Q = h^2 (1^T x0 + 1^T e_k).
-template <int N, int R, int MINB, int CM, bool VERIFY, int XM = 0>
-__global__ void __launch_bounds__(TileCfg<N, R, MINB, CM>::BLOCK, MINB)
+template <int N, int R, int MINB, int CM, bool VERIFY, int XM = 0, int CL = 1>
+__global__ void __launch_bounds__(TileCfg<N, R, MINB, CM, CL>::BLOCK, MINB)
 minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max_iter, double* __restrict__ out,
                    int slot, unsigned* __restrict__ job_counter, const int* __restrict__ order,
                    double* __restrict__ xio) {
     static_assert(XM != 1 || VERIFY, "writing x needs the VERIFY instantiation (x carried)");
-    using K = TileCfg<N, R, MINB, CM>;
+    static_assert(CL == 1 || (!VERIFY && XM == 0), "K3b: plain MINRES from x0 = 0");
+    using K = TileCfg<N, R, MINB, CM, CL>;
     constexpr int PAIRS = K::PAIRS, PW = K::PW, RP = K::RP, TPS = K::TPS, GROUPS = K::GROUPS;
     constexpr bool DS = K::DS, WS = K::WS, CS = K::CS;
     constexpr int P = 2 * N * N, PE = K::PE;
@@ -162,26 +203,57 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
     double* CEg = Wg + K::WGRID;
     double* CNg = CEg + K::CEG;
     double* red = CNg + K::CNG;                           // NW x 4 doubles (3 partials + pad)
+    double* part = red + K::RED;                          // CL > 1: [2][CL][4] CTA partials by step parity
+    double* thb = part + 8 * CL;                          //         [2][2][N] neighbours' boundary t
+    double* hst = thb + 4 * N;                            //         [2][N] p_{j-1} of the two halo rows
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(hst + 2 * N);   //     [2] arrivals of the step's pushes
     int* jobslot = reinterpret_cast<int*>(smem + K::SMEM_PER_GROUP * GROUPS) + 4 * g;
+    const int rank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
 
     const int p = tg % PAIRS, s = tg / PAIRS;
-    const int i0 = 2 * p + 1, i1 = i0 + 1, j0 = s * R + 1;   // tile: columns i0, i1; rows j0 .. j0+R-1
+    const int jl0 = s * R + 1;                            // first row of the tile in this CTA's grid
+    const int i0 = 2 * p + 1, i1 = i0 + 1, j0 = rank * K::SL * R + jl0;   // tile: columns i0, i1; rows j0 .. j0+R-1
     const bool col1_live = i1 <= K::C;
     const bool top_live = j0 + R - 1 <= K::C;
     const double h = 1.0 / N, h2 = h * h;
-    double* const own = Sg + j0 * RP + p + 1;
-    const double* const westp = Sg + j0 * RP + PW + p;
-    const double* const eastp = Sg + j0 * RP + p + 2;
-    double* const dgp = Dg + (j0 - 1) * 2 * PAIRS + p;
-    double* const wgp = Wg + (j0 - 1) * PAIRS + p;
+    double* const own = Sg + jl0 * RP + p + 1;
+    const double* const westp = Sg + jl0 * RP + PW + p;
+    const double* const eastp = Sg + jl0 * RP + p + 2;
+    double* const dgp = Dg + (jl0 - 1) * 2 * PAIRS + p;
+    double* const wgp = Wg + (jl0 - 1) * PAIRS + p;
+    // CL > 1: the first strip keeps the halo row below the CTA (side 0), the last strip the one above (side 1)
+    const bool halo_lo = CL > 1 && s == 0 && rank > 0;
+    const bool halo_hi = CL > 1 && s == K::SL - 1 && rank < CL - 1;
 
     for (int e = tg; e < K::GRID; e += TPS) Sg[e] = 0.0;   // halo rows / pairs are never written again
+    // K3b: bytes each step's wait expects (every CTA's 3 partials, N t values from each neighbour); the step
+    // count gk runs on across jobs (identical in every CTA of the cluster) and picks buffer and phase
+    const uint32_t tx_bytes = CL > 1 ? (uint32_t)(24 * CL + (rank > 0 ? 8 * N : 0) + (rank < CL - 1 ? 8 * N : 0)) : 0u;
+    uint32_t gk = 0;
+    if constexpr (CL > 1) {
+        if (tg == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm32(mbar)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm32(mbar + 1)) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        cg::this_cluster().sync();                       // no push before every peer's barriers exist
+    }
 
     for (;;) {
-        if (tg == 0) *jobslot = (int)atomicAdd(job_counter, 1u);
-        tsync<TPS, GROUPS>(g);
-        const int job = *jobslot;
-        tsync<TPS, GROUPS>(g);
+        int job;
+        if constexpr (CL > 1) {          // rank 0 draws the job; the cluster barrier also ends the last job
+            auto cl = cg::this_cluster();
+            if (rank == 0 && tg == 0) jobslot[0] = (int)atomicAdd(job_counter, 1u);
+            cl.sync();
+            if (tg == 0) jobslot[1] = *cl.map_shared_rank(jobslot, 0);
+            __syncthreads();
+            job = jobslot[1];
+        } else {
+            if (tg == 0) *jobslot = (int)atomicAdd(job_counter, 1u);
+            tsync<TPS, GROUPS>(g);
+            job = *jobslot;
+            tsync<TPS, GROUPS>(g);
+        }
         if (job >= nb) break;
         const int sj = order ? __ldg(order + job) : job;     // longest-first order (order_kernel) if given
         const double* a = a_all + (size_t)sj * P;
@@ -360,6 +432,19 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 own[r * RP] = b0;
                 own[r * RP + PW] = b1;
             }
+            if constexpr (CL > 1) {   // halo rows (the neighbours' boundary rows, all live): p_1 = b, p_0 = 0
+                const double hb1 = col1_live ? h2 : 0.0;
+                if (halo_lo) {
+                    Sg[p + 1] = h2;
+                    Sg[PW + p + 1] = hb1;
+                    hst[2 * p] = hst[2 * p + 1] = 0.0;
+                }
+                if (halo_hi) {
+                    Sg[(K::SL * R + 1) * RP + p + 1] = h2;
+                    Sg[(K::SL * R + 1) * RP + PW + p + 1] = hb1;
+                    hst[N + 2 * p] = hst[N + 2 * p + 1] = 0.0;
+                }
+            }
         }
         tsync<TPS, GROUPS>(g);                               // the grid holds p_1 = b (XM = 2: r0)
         const double bnorm = h2 * (double)K::C;              // ||b||_2 = h^2 sqrt(n), n = C^2
@@ -387,7 +472,43 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 pc0 += YA[r];
                 pc1 += YB[r];
             }
-            const double4 S = tsum3<TPS, GROUPS>(pa0 + pa1, pb0 + pb1, pc0 + pc1, red, tg, g);
+            double4 S = tsum3<TPS, GROUPS>(pa0 + pa1, pb0 + pb1, pc0 + pc1, red, tg, g);
+            if constexpr (CL > 1) {
+                // K3b: the CTA sums are pushed into every CTA of the cluster and added there in rank order
+                // (the same association everywhere); the boundary rows' t = A p_j go to the neighbour that
+                // keeps them as a halo row.  One cluster barrier per step publishes both (buffers alternate
+                // by step parity); every read after it is local.
+                const int par = gk & 1;
+                const uint32_t bar = sm32(mbar + par);
+                double* tab = part + 4 * CL * par;            // [CL][4] of this parity
+                if (tg == 0) mbar_expect_tx(bar, tx_bytes);
+                if (tg < 3 * CL) {
+                    const int q = tg % 3, dst = tg / 3;
+                    st_async_f64(mapa32(sm32(tab + 4 * rank + q), dst), q == 0 ? S.x : (q == 1 ? S.y : S.z),
+                                 mapa32(bar, dst));
+                }
+                if (s == 0 && rank > 0) {                    // first row = the row above rank - 1's last one
+                    const uint32_t d = mapa32(sm32(thb + (2 * par + 1) * N + 2 * p), rank - 1);
+                    const uint32_t rb = mapa32(bar, rank - 1);
+                    st_async_f64(d, T0[0], rb);
+                    st_async_f64(d + 8, T1[0], rb);
+                }
+                if (s == K::SL - 1 && rank < CL - 1) {       // last row = the row below rank + 1's first one
+                    const uint32_t d = mapa32(sm32(thb + 2 * par * N + 2 * p), rank + 1);
+                    const uint32_t rb = mapa32(bar, rank + 1);
+                    st_async_f64(d, T0[R - 1], rb);
+                    st_async_f64(d + 8, T1[R - 1], rb);
+                }
+                mbar_wait_cluster(bar, (gk >> 1) & 1u);
+                double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+                for (int q = 0; q < CL; ++q) {
+                    sx += tab[4 * q];
+                    sy += tab[4 * q + 1];
+                    sz += tab[4 * q + 2];
+                }
+                S = make_double4(sx, sy, sz, 0.0);
+            }
             const double bb = S.y;
             const double invb = bb > 0.0 ? rsqrt(bb) : 0.0;
             const double beta = __dmul_rn(bb, invb);         // beta_j = ||p_j||
@@ -450,6 +571,37 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 own[r * RP] = q0;
                 own[r * RP + PW] = q1;
             }
+            if constexpr (CL > 1) {
+                // the halo rows' p_{j+1}, rebuilt from the neighbour's t with the same operations it applies to
+                // its own boundary row (a full row: coefficient ct, ct1 on the phantom column), so both copies
+                // agree bit for bit; the grid halo row holds p_j, hst p_{j-1}
+                const int par = gk & 1;
+                ++gk;
+                if (halo_lo) {
+                    double* gh = Sg + p + 1;
+                    const double* tb = thb + 2 * par * N + 2 * p;
+                    double* hs = hst + 2 * p;
+                    const double y0 = gh[0], y1 = gh[PW];
+                    const double q0 = fma(ct, tb[0], fma(c1, y0, c0 * hs[0]));
+                    const double q1 = fma(ct1, tb[1], fma(c1, y1, c0 * hs[1]));
+                    hs[0] = y0;
+                    hs[1] = y1;
+                    gh[0] = q0;
+                    gh[PW] = q1;
+                }
+                if (halo_hi) {
+                    double* gh = Sg + (K::SL * R + 1) * RP + p + 1;
+                    const double* tb = thb + (2 * par + 1) * N + 2 * p;
+                    double* hs = hst + N + 2 * p;
+                    const double y0 = gh[0], y1 = gh[PW];
+                    const double q0 = fma(ct, tb[0], fma(c1, y0, c0 * hs[0]));
+                    const double q1 = fma(ct1, tb[1], fma(c1, y1, c0 * hs[1]));
+                    hs[0] = y0;
+                    hs[1] = y1;
+                    gh[0] = q0;
+                    gh[PW] = q1;
+                }
+            }
             // stopping test of iteration k (uniform across the system); the p_{j+1} pass of the
             // last step is discarded
             if (k == 0) {
@@ -507,7 +659,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 }
             }
         }
-        if (tg == 0) {
+        if (tg == 0 && rank == 0) {
             double* o = out + (size_t)sj * kRecLen;
             o[0 + slot] = h2 * (XM == 2 ? sum_x0 + Xq : Xq);
             o[2 + slot] = (double)k;
@@ -516,6 +668,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
         }
         tsync<TPS, GROUPS>(g);      // grid reuse by the next job
     }
+    if constexpr (CL > 1) cg::this_cluster().sync();   // no CTA leaves while a peer may still read its memory
 }
 
 template <int N, int R, int MINB, int CM, bool VERIFY, int XM = 0>
@@ -539,7 +692,86 @@ cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, dou
     }
 }
 
+// K3b launch: persistent clusters of CL CTAs (one system each), as many as fit at once
+template <int N, int R, int CL>
+cudaError_t run_cluster(const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot, unsigned* ctr,
+                        const int* order, cudaStream_t s) {
+    using K = TileCfg<N, R, 1, 0, CL>;
+    auto kern = minres_tile_kernel<N, R, 1, 0, false, 0, CL>;
+    static PerDevice<int> mc_cache;                      // per device: smem / cluster attributes, cluster occupancy
+    cudaError_t de = cudaSuccess;
+    const int max_clusters = mc_cache.get([&]() -> int {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
+        if (e == cudaSuccess && CL > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return -(int)e;
+        cudaLaunchConfig_t qc = {};
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = CL;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.gridDim = dim3(CL * 16);
+        qc.blockDim = dim3(K::BLOCK);
+        qc.dynamicSmemBytes = K::SMEM;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int mcl = 0;
+        e = cudaOccupancyMaxActiveClusters(&mcl, kern, &qc);
+        if (e != cudaSuccess) return -(int)e;
+        return mcl < 1 ? -(int)cudaErrorInvalidConfiguration : mcl;
+    }, &de);
+    if (de != cudaSuccess) return de;
+    if (max_clusters < 0) return (cudaError_t)(-max_clusters);
+    const int clusters = (int)std::min<uint64_t>(nb, (uint64_t)max_clusters);
+    if (clusters <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(clusters * CL);
+    cfg.blockDim = dim3(K::BLOCK);
+    cfg.dynamicSmemBytes = K::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, (int)nb, tol, max_iter, out, slot, ctr, order, (double*)nullptr);
+}
+
 }  // namespace
+
+// K3b (SURVEY 2.C, 8(a) a6a "resident" layout): h = 1/128 on 4-CTA clusters (32 rows per CTA), h = 1/256 on
+// 16-CTA clusters (16 rows per CTA); each CTA holds its rows like the h = 1/64 tile (8 rows x 2 columns per
+// thread, conductances in registers).  MLMC_MINRES_K3B=0 hands those meshes back to K3c (A/B runs).
+bool minres_cluster_supported(int N) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("MLMC_MINRES_K3B");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return env == 1 && (N == 128 || N == 256);
+}
+
+cudaError_t launch_minres_cluster(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
+                                  unsigned* ctr, const int* order, cudaStream_t s) {
+    if (nb == 0) return cudaSuccess;
+#ifdef MLMC_TUNING
+    {   // MLMC_MINRES_CLUSTER_N128=8: 8-CTA clusters of 128-thread CTAs (two systems' slabs per SM): 21.8 vs
+        // 21.7 ms for 148 systems, 61.3 vs 60.3 ms for 441 (tools/gpu_call_r02ae.sh)
+        char name[64];
+        std::snprintf(name, sizeof(name), "MLMC_MINRES_CLUSTER_N%d", N);
+        const char* e = std::getenv(name);
+        const int v = e ? std::atoi(e) : 0;
+        if (N == 128 && v == 8) return run_cluster<128, 8, 8>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+    }
+#endif
+    switch (N) {
+        case 128: return run_cluster<128, 8, 4>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        case 256: return run_cluster<256, 8, 16>(a, nb, tol, max_iter, out, slot, ctr, order, s);
+        default: return cudaErrorNotSupported;
+    }
+}
 
 // Tile shape per mesh: MLMC_MINRES_TILE_N<N>=<index> selects an alternative for tuning runs;
 // -1 hands the mesh back to the column-strip kernel (k_minres.cu).
@@ -565,6 +797,15 @@ int minres_tile_variant(int N) {
 #else
 #define IF_TUNING(...)
 #endif
+// MLMC_MINRES_K3B_N64=1: h = 1/64 through the K3b cluster kernel (a cross-check of its exchange, not a default)
+static bool k3b_n64() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("MLMC_MINRES_K3B_N64");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
 // Variant table (index = MLMC_MINRES_TILE_N<N>): <N, R, MINB, CM>; measured with tools/tune_minres.py.
 template <bool V, int XM>
 static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, double tol, int max_iter, double* out,
@@ -608,6 +849,12 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             IF_TUNING(if (var == 4) return run_tile<64, 8, 2, 4, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 5) return run_tile<64, 8, 1, 2, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 6) return run_tile<64, 8, 1, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            // K3b layout at h = 1/64 (one system per 2-CTA cluster of 128-thread CTAs, two systems' slabs per SM):
+            // bit-identical records (the pairwise warp-total tree splits into the two CTAs' halves) but 2.03 vs
+            // 1.65 ms per level-3 launch, C2 step 2.70 vs 2.34 ms; kept as the cross-check of the cluster
+            // exchange (MLMC_MINRES_K3B_N64=1, tests/test_gpu_parity_full.py)
+            if constexpr (!V && XM == 0)
+                if (k3b_n64()) return run_cluster<64, 8, 2>(a, nb, tol, max_iter, out, slot, ctr, order, s);
             return run_tile<64, 8, 1, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         default: return cudaErrorNotSupported;
     }

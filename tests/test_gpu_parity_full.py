@@ -274,3 +274,100 @@ def test_auto_policy_with_recorded_choices_reproduces_fixed_policies():
             c.auto_choice_set(1024, 0, "minres")      # not a mesh of the plan
         finally:
             c.close()
+
+
+# ============================================================================ K3b: cluster-resident MINRES
+def _k3c_records(level, n, seed, tol, first_index=0):
+    """The same level solved with K3b switched off (MLMC_MINRES_K3B=0: h = 1/128, 1/256 on K3c), in a
+    subprocess (the switch is read once per process)."""
+    import json
+    import subprocess
+    import textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import json, sys
+        sys.path.insert(0, %r)
+        import workloads as W
+        from paper_2503_05533_b200 import Context, precision
+        cfg = W.CONFIGS["C5"]
+        ctx = Context(field=cfg["field"], m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"],
+                      h0_inv=cfg["h0_inv"], L_max=cfg["L_max"], device=0, workspace_bytes=8 << 30)
+        mr = precision("minres")
+        r = ctx.sample_level(%d, %d, seed=%d, first_index=%d, prec_fine=mr, prec_coarse=mr, tol_fine=%r,
+                             tol_coarse=%r, per_sample=True)
+        print(json.dumps(r.per_sample.tolist()))
+        ctx.close()
+    """) % (root, level, n, seed, first_index, tol, tol)
+    env = dict(os.environ, MLMC_MINRES_K3B="0")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+
+
+def test_cluster_resident_minres_h128_h256():
+    """K3b (one system per 4-CTA cluster at h = 1/128, per 16-CTA cluster at h = 1/256; every row on chip,
+    halo rows rebuilt from the neighbour's t): per sample within the residual bound of the oracle's direct
+    binary64 solve; against the streamed K3c on the same samples (different summation order) the same Q to
+    the tolerance both were solved to and step counts within max(2, 1%); more systems than resident clusters (the
+    job loop and the longest-first order); a single system equals the same sample inside a batch."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg)
+    P = _oracle(cfg)
+    mr = precision("minres")
+    for level, n, tol in ((5, 3, 1e-9), (4, 160, 1e-7)):
+        Nf = cfg["h0_inv"] << level
+        r = ctx.sample_level(level, n, seed=41, prec_fine=mr, prec_coarse=mr, tol_fine=tol, tol_coarse=tol,
+                             per_sample=True)
+        ps = r.per_sample
+        assert r.sums["n_fail"] == 0 and np.all(ps[:, 6:8] == 0), level
+        assert np.all(ps[:, 4] <= tol * 1.0001) and np.all(ps[:, 5] <= tol * 1.0001), level
+        ks = [0, n - 1]
+        exs = _pmap(lambda k: (_exact(P, Nf, oc.normals(41, level, k, cfg["m"])),
+                               _exact(P, Nf // 2, oc.normals(41, level, k, cfg["m"]))), ks)
+        for k, ex in zip(ks, exs):
+            _check_bound(ps, k, ex, tol, tol, ("k3b", level))
+        pc = _k3c_records(level, n, 41, tol)
+        assert np.all(pc[:, 6:8] == 0)
+        # both within tol ||b|| ||x|| <= 1.5 tol Q of the exact Q (DESIGN.md section 4)
+        assert np.all(np.abs(ps[:, :2] - pc[:, :2]) <= 2 * 1.5 * tol * np.abs(pc[:, :2]) + 1e-15), level
+        # step counts: the two kernels add the same products in different orders; over thousands of Lanczos
+        # steps (loss of orthogonality) that moves the stopping step by up to ~0.5% (measured: 40 of 10881)
+        assert np.all(np.abs(ps[:, 2:4] - pc[:, 2:4]) <= np.maximum(2, 0.01 * pc[:, 2:4])), level
+        one = ctx.sample_level(level, 1, seed=41, first_index=n - 1, prec_fine=mr, prec_coarse=mr, tol_fine=tol,
+                               tol_coarse=tol, per_sample=True).per_sample
+        assert np.array_equal(one[0], ps[n - 1]), level
+    ctx.close()
+
+
+def test_cluster_exchange_bit_identical_to_single_cta_tile():
+    """The K3b cluster machinery (CTA sums pushed by st.async into every CTA and added in rank order, the halo
+    rows' p_{j+1} rebuilt from the neighbour's t) run at h = 1/64 on 2-CTA clusters (MLMC_MINRES_K3B_N64=1):
+    the pairwise tree of the 8 warp totals splits exactly into the two CTAs' halves, so every record of
+    configs[1] level 3 (300 systems, more than resident clusters) equals the single-CTA tile kernel's bit for
+    bit -- any error in the exchange or the halo reconstruction would show."""
+    import json
+    import subprocess
+    import textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import json, sys
+        sys.path.insert(0, %r)
+        import workloads as W
+        from paper_2503_05533_b200 import Context, precision
+        cfg = W.CONFIGS["C2"]
+        ctx = Context(field="expcov", m=cfg["m"], sigma2=cfg["sigma2"], corr_len=cfg["corr_len"], h0_inv=8,
+                      L_max=3, device=0, workspace_bytes=2 << 30)
+        mr = precision("minres")
+        r = ctx.sample_level(3, 300, seed=7, prec_fine=mr, prec_coarse=mr, tol_fine=1e-8, tol_coarse=1e-6,
+                             per_sample=True)
+        print(json.dumps(r.per_sample.tolist()))
+        ctx.close()
+    """) % root
+    recs = []
+    for v in ("0", "1"):
+        env = dict(os.environ, MLMC_MINRES_K3B_N64=v)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        recs.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
+    assert np.all(recs[0][:, 6:8] == 0)
+    assert np.array_equal(recs[0], recs[1])
