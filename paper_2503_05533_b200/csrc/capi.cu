@@ -512,7 +512,14 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         double* xc = reinterpret_cast<double*>(ex.ws + L.xc);
         // (the fork is per pass: the join below orders the next pass's field writes after this coarse solve);
         // with per-kernel profiling on, the solves stay serialised so that every launch's event time is its own
-        const bool fork = sch && level > 0 && sch->st_c && Nf < kGmMinN && !c2f && !ctx->prof_on && sched_knob("MLMC_SCHED_FORK");
+        // (K3b keeps its system on chip, so a fine half on it may fork as well -- its coarse half then runs on the
+        // SMs its clusters leave free -- unless that coarse half uses the shared scratch: configs[4] level 4 pass
+        // 24.1 -> 21.4 ms, level 5 329 -> 308 ms for 148 samples, tools/fork_probe.py)
+        const auto on_chip = [&](int Nm, const mlmc_precision* pm) {
+            return Nm < kGmMinN || (pm->solver == MLMC_SOLVER_MINRES && minres_cluster_supported(Nm) && !use_gm_kernel());
+        };
+        const bool fork = sch && level > 0 && sch->st_c && on_chip(Nf, pf) && on_chip(Nc, pc) && !c2f && !ctx->prof_on &&
+                          sched_knob("MLMC_SCHED_FORK");
         if (fork) {
             CU(cudaEventRecord(sch->fork, st));
             CU(cudaStreamWaitEvent(sch->st_c, sch->fork, 0));
