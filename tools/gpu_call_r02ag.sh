@@ -6,4 +6,4 @@ timeout 900 ncu --set full --clock-control none --import-source on --kernel-name
    -k "regex:minres_tile_kernel<.int.128" -s 1 -c 1 -o /tmp/prof_k3b -f python tools/k3b_one.py > gpurun_out/ncu_k3b.log 2>&1
 echo "ncu rc=$?"
 ncu -i /tmp/prof_k3b.ncu-rep --page raw --csv > gpurun_out/prof_k3b.raw.csv
-ncu -i /tmp/prof_k3b.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_k3b.src.csv 2>/dev/null; echo "src rc=$?"
+ncu -i /tmp/prof_k3b.ncu-rep --page source --csv > gpurun_out/prof_k3b.src.csv 2> gpurun_out/prof_k3b.src.err; echo "src rc=$?"; head -c 600 gpurun_out/prof_k3b.src.csv
