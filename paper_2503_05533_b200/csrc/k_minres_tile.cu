@@ -685,7 +685,17 @@ cudaError_t run_tile(const double* a, uint64_t nb, double tol, int max_iter, dou
     const KernelOcc occ = occ_of(occ_cache, kern, K::BLOCK, K::SMEM);
     if (occ.err != cudaSuccess) return occ.err;
     const uint64_t need = (nb + K::GROUPS - 1) / K::GROUPS;
-    const uint64_t grid = std::min<uint64_t>(need, (uint64_t)occ.per_sm * occ.sms);
+    uint64_t grid = std::min<uint64_t>(need, (uint64_t)occ.per_sm * occ.sms);
+#ifdef MLMC_TUNING
+    {   // MLMC_TILE_CTAS_N<N>=c: at most c persistent CTAs (A/B of leaving SMs to the other levels of a step;
+        // configs[1] level 3 capped at 128 / 112 / 100 / 90 / 80 CTAs: C2 step 2.33 / 2.33 / 2.39 / 2.65 / 2.81 ms
+        // against 2.33 uncapped, tools/gpu_call_r02ai.sh)
+        char name[48];
+        std::snprintf(name, sizeof(name), "MLMC_TILE_CTAS_N%d", N);
+        const char* e = std::getenv(name);
+        if (e && std::atoi(e) > 0) grid = std::min<uint64_t>(grid, (uint64_t)std::atoi(e));
+    }
+#endif
     if (grid == 0) return cudaSuccess;
     kern<<<(unsigned)grid, K::BLOCK, K::SMEM, s>>>(a, (int)nb, tol, max_iter, out, slot, ctr, order, xio);
     return cudaGetLastError();
