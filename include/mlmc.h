@@ -96,7 +96,8 @@ typedef struct {
  * MINRES reports phibar_k/||b|| (the stopping quantity) as the residual and
  * computes Q from the scalar recurrence of 1^T x_k (R26); with
  * MLMC_FLAG_VERIFY it also carries x_k and reports ||b - A x_k||/||b||, with
- * bit-identical Q.                                                          */
+ * bit-identical Q (meshes h >= 1/64, the on-chip tile kernel; EINVAL on the
+ * finer meshes, whose kernels keep no x_k).                                 */
 typedef enum { MLMC_FMT_E4M3 = 0, MLMC_FMT_F16 = 1, MLMC_FMT_F32 = 2, MLMC_FMT_F64 = 3 } mlmc_fmt;
 typedef enum { MLMC_SOLVER_MINRES = 0, MLMC_SOLVER_CHOL_IR = 1, MLMC_SOLVER_MGCG = 2, MLMC_SOLVER_CG = 3 } mlmc_solver;
 

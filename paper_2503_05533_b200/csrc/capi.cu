@@ -283,6 +283,8 @@ int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
     if (!(tol > 0.0) || !std::isfinite(tol)) return fail(ctx, MLMC_EINVAL, "tolerance must be > 0");
     if (p->solver == MLMC_SOLVER_MINRES) {
         if (!minres_supported(N)) return fail(ctx, MLMC_EINVAL, "MINRES kernel not built for N=" + std::to_string(N));
+        if ((p->flags & MLMC_FLAG_VERIFY) && N >= kGmMinN)   // x_k is carried by the on-chip tile kernels only
+            return fail(ctx, MLMC_EINVAL, "MLMC_FLAG_VERIFY needs h >= 1/64 (N <= 64), got N=" + std::to_string(N));
         return MLMC_OK;
     }
     if (p->solver == MLMC_SOLVER_MGCG) {

@@ -346,8 +346,9 @@ def test_adaptive_C4_matches_oracle_controller():
 
 # ============================================================================ K3c: streamed fine meshes
 def test_streamed_minres_fine_mesh_parity():
-    """K3c (h = 1/128 fine, 1/64 coarse; configs[4] field): per-sample Q within the rigorous residual
-    bound of the oracle's direct banded Cholesky solve, at a tight and a loose tolerance."""
+    """h = 1/128 fine (K3b since round 2; K3c before), 1/64 coarse, configs[4] field: per-sample Q within the
+    rigorous residual bound of the oracle's direct banded Cholesky solve, at a tight and a loose tolerance;
+    MLMC_FLAG_VERIFY is refused on this mesh (EINVAL)."""
     cfg = W.CONFIGS["C5"]
     ctx = _ctx(cfg, ws=1 << 30)
     P = _oracle(cfg)
@@ -365,6 +366,9 @@ def test_streamed_minres_fine_mesh_parity():
             assert abs(ps[k, 1] - qc) <= tol * bc * xc * (1 + 1e-6) + 1e-14 * qc
         if tol < 1e-10:
             assert np.max(np.abs(ps[:, 0] / np.array([e[0][0] for e in exs]) - 1)) < 1e-9
+    # the true-residual instantiation exists on the on-chip tile meshes only: refused here, not ignored
+    with pytest.raises(RuntimeError, match="VERIFY"):
+        ctx.sample_level(4, 2, seed=11, prec_fine=precision("minres", verify=True), tol_fine=1e-6, tol_coarse=1e-6)
     ctx.close()
 
 
