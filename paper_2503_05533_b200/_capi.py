@@ -117,6 +117,7 @@ def lib():
     L.mlmc_kl_modes.argtypes = [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), dp, dp,
                                 C.c_int]
     L.mlmc_debug_field.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]
+    L.mlmc_debug_trace.argtypes = [vp, vp, C.c_uint32, C.POINTER(C.c_uint32)]
     L.mlmc_sample_level_xi.argtypes = [vp, C.c_int, C.c_uint64, vp, C.POINTER(Precision), C.POINTER(Precision),
                                        C.c_double, C.c_double, C.POINTER(LevelSums), vp]
     L.mlmc_sample_levels_xi.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.POINTER(vp),

@@ -79,6 +79,8 @@ cudaError_t launch_minres_gm(int N, const double* a, uint64_t nb, double tol, in
 bool minres_stream_supported(int N);
 // K3b: MINRES of one system per thread-block cluster, every row resident on chip (h = 1/128: 4 CTAs, 1/256: 16)
 bool minres_cluster_supported(int N);
+// job trace of the tile / K3b MINRES kernels (tuning build only; cudaErrorNotSupported otherwise)
+cudaError_t minres_trace(unsigned long long* buf, unsigned cap, unsigned* count);
 cudaError_t launch_minres_cluster(int N, const double* a, uint64_t nb, double tol, int max_iter, double* out, int slot,
                                   unsigned* ctr, const int* order, cudaStream_t s);
 // Tiled TMA tensor map (cuTensorMapEncodeTiled via the runtime's driver entry point): `map` points to a

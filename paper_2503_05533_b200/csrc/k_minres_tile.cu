@@ -37,6 +37,19 @@ namespace mlmc {
 namespace {
 namespace cg = cooperative_groups;
 
+#ifdef MLMC_TUNING
+// job trace of the tuning build (tools/step_trace.py): per system solve {start, end (%globaltimer ns), smid << 32 | N,
+// cluster rank << 32 | job}
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned int g_trace_cap = 0;
+__device__ unsigned int g_trace_n = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // Conductance placement (template CM, bit flags): 1 = diagonal d from a shared grid,
 // 2 = west conductance of column 0 from a shared grid; everything else in registers.
 template <int N, int R, int MINB_, int CM_, int CL_ = 1>
@@ -255,6 +268,9 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
             tsync<TPS, GROUPS>(g);
         }
         if (job >= nb) break;
+#ifdef MLMC_TUNING
+        const unsigned long long trace_t0 = (tg == 0 && g_trace) ? gtimer() : 0ull;
+#endif
         const int sj = order ? __ldg(order + job) : job;     // longest-first order (order_kernel) if given
         const double* a = a_all + (size_t)sj * P;
         auto aL = [&](int ii, int jj) { return __ldg(a + 2 * (jj * N + ii)); };
@@ -659,6 +675,19 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 }
             }
         }
+#ifdef MLMC_TUNING
+        if (tg == 0 && g_trace) {
+            const unsigned idx = atomicAdd(&g_trace_n, 1u);
+            if (idx < g_trace_cap) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                g_trace[4 * (size_t)idx] = trace_t0;
+                g_trace[4 * (size_t)idx + 1] = gtimer();
+                g_trace[4 * (size_t)idx + 2] = ((unsigned long long)smid << 32) | (unsigned)N;
+                g_trace[4 * (size_t)idx + 3] = ((unsigned long long)rank << 32) | (unsigned)job;
+            }
+        }
+#endif
         if (tg == 0 && rank == 0) {
             double* o = out + (size_t)sj * kRecLen;
             o[0 + slot] = h2 * (XM == 2 ? sum_x0 + Xq : Xq);
@@ -880,6 +909,27 @@ cudaError_t launch_minres_tile(int N, const double* a, uint64_t nb, double tol, 
                       : tile_dispatch<false, 2>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
     return verify ? tile_dispatch<true, 0>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, nullptr, s)
                   : tile_dispatch<false, 0>(N, var, a, nb, tol, max_iter, out, slot, ctr, order, nullptr, s);
+}
+
+// Job trace (tuning build): buf != nullptr arms it (cap records of 4 u64 on the device, count reset); buf ==
+// nullptr disarms it and returns the number of records written (may exceed cap).  Production: NotSupported.
+cudaError_t minres_trace(unsigned long long* buf, unsigned cap, unsigned* count) {
+#ifdef MLMC_TUNING
+    cudaError_t e;
+    if (buf) {
+        const unsigned zero = 0;
+        if ((e = cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof cap)) != cudaSuccess) return e;
+        if ((e = cudaMemcpyToSymbol(g_trace_n, &zero, sizeof zero)) != cudaSuccess) return e;
+        return cudaMemcpyToSymbol(g_trace, &buf, sizeof buf);
+    }
+    unsigned long long* none = nullptr;
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+    if (count && (e = cudaMemcpyFromSymbol(count, g_trace_n, sizeof *count)) != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_trace, &none, sizeof none);
+#else
+    (void)buf; (void)cap; (void)count;
+    return cudaErrorNotSupported;
+#endif
 }
 
 }  // namespace mlmc
