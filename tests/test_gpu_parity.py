@@ -372,6 +372,21 @@ def test_streamed_minres_fine_mesh_parity():
     ctx.close()
 
 
+def test_job_trace_is_refused_by_the_production_build():
+    """mlmc_debug_trace (schedule analysis, tools/step_trace.py) records only in the MLMC_TUNING build; the
+    production library answers EINVAL with a message instead of silently recording nothing."""
+    import ctypes as C
+    from paper_2503_05533_b200 import _capi as K
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg)
+    buf = torch.zeros(64, dtype=torch.int64, device="cuda")
+    cnt = C.c_uint32()
+    rc = K.lib().mlmc_debug_trace(ctx.ctx, C.c_void_p(buf.data_ptr()), 16, C.byref(cnt))
+    assert rc == 2, rc                                    # MLMC_EINVAL
+    assert b"MLMC_TUNING" in K.lib().mlmc_last_error(ctx.ctx)
+    ctx.close()
+
+
 # ============================================================================ the paper's experiment
 def test_paper_experiment_mpml_cost_gain_without_accuracy_loss():
     """Section 5.1: adaptive MPML vs standard adaptive MLMC (fixed MINRES tol 1e-6) on the
