@@ -65,7 +65,7 @@ struct TileCfg {
     static_assert(CL == 1 || (S % CL == 0 && CM == 0), "whole strips per CTA; conductances in registers");
     static constexpr int SL = S / CL;                     // strips per CTA
     static constexpr int TPS = PAIRS * SL;                // threads per system (per CTA when CL > 1)
-    static_assert(TPS % 32 == 0 || TPS == 16, "a system fills whole warps or one half-warp");
+    static_assert(TPS % 32 == 0 || TPS == 16 || TPS == 8, "a system fills whole warps or a half / quarter warp");
     static_assert(S * R == C || S * R == C + 1, "strips end at row C or at the boundary row N");
     static constexpr int NW = TPS >= 32 ? TPS / 32 : 1;
     static constexpr int GROUPS = TPS >= 128 ? 1 : 128 / TPS;
@@ -98,7 +98,8 @@ struct TileCfg {
 template <int TPS>
 __device__ __forceinline__ unsigned lane_mask() {
     if constexpr (TPS >= 32) return 0xffffffffu;
-    else return 0xffffu << (threadIdx.x & 16);
+    else if constexpr (TPS == 16) return 0xffffu << (threadIdx.x & 16);
+    else return 0xffu << (threadIdx.x & 24);
 }
 template <int TPS, int GROUPS>
 __device__ __forceinline__ void tsync(int g) {
@@ -119,7 +120,7 @@ __device__ __forceinline__ void tsync(int g) {
 template <int TPS, int GROUPS>
 __device__ __forceinline__ double4 tsum3(double a, double b, double c, double* buf, int tg, int g) {
     constexpr int W = TPS >= 32 ? 32 : TPS;
-    static_assert(W == 16 || W == 32, "reduce-scatter needs 16 or 32 lanes");
+    static_assert(W == 8 || W == 16 || W == 32, "reduce-scatter needs 8, 16 or 32 lanes");
     const unsigned msk = lane_mask<TPS>();
     const int lane = threadIdx.x & (W - 1);
     constexpr int O1 = W / 2, O2 = W / 4;
@@ -851,11 +852,14 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
                                  int slot, unsigned* ctr, const int* order, double* xio, cudaStream_t s) {
     (void)var;
     switch (N) {
-        case 8:   // two systems per warp (16 threads each)
-            IF_TUNING(if (var == 1) return run_tile<8, 2, 5, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+        case 8:   // four systems per warp (8 threads each, 4 rows x 2 columns per thread), 16 per CTA
+            // (round 2: half as many threads share each system's scalar recurrences as in the former two systems
+            // per warp <8, 2, 4>, now v1: C2 step 2.355 / 2.360 vs 2.380 / 2.379 ms, alternating runs)
+            IF_TUNING(if (var == 1) return run_tile<8, 2, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            IF_TUNING(if (var == 2) return run_tile<8, 2, 5, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             // (conductances in shared memory with 8 / 6 systems-pairs per SM: 0.133 / 0.127 ms vs 0.109 ms on
             // configs[1] level 0; 16 systems per warp-pair cannot hide the extra shared loads)
-            return run_tile<8, 2, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
+            return run_tile<8, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 16:
             IF_TUNING(if (var == 1) return run_tile<16, 2, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             IF_TUNING(if (var == 2) return run_tile<16, 2, 6, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
