@@ -414,7 +414,7 @@ int mlmc_debug_field(mlmc_ctx* ctx, int level, int mesh_level, uint64_t n, uint6
 
 /* Job trace of the on-chip MINRES kernels (h >= 1/256), for schedule analysis (tools/step_trace.py): with
  * dev_buf != NULL every system solve started afterwards appends {start, end (globaltimer ns), smid << 32 | N,
- * cluster rank << 32 | job} as 4 uint64 to dev_buf (device, cap records); with dev_buf == NULL the trace is
+ * (cluster rank * 2 + half: 0 fine, 1 coarse) << 32 | job} as 4 uint64 to dev_buf (device, cap records); with dev_buf == NULL the trace is
  * stopped (after a device synchronisation) and *count = records written (may exceed cap).  Only the
  * MLMC_TUNING build records; the production build returns EINVAL.                                   */
 int mlmc_debug_trace(mlmc_ctx* ctx, void* dev_buf, uint32_t cap, uint32_t* count);

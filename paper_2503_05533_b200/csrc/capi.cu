@@ -137,7 +137,7 @@ WsLayout ws_layout(const mlmc_ctx* c, int level, uint64_t batch, const mlmc_prec
     L.a_c = off;    off += align256(sizeof(double) * batch * 2 * (size_t)Nc * Nc);
     L.rec = off;    off += align256(sizeof(double) * batch * kRecLen);
     L.chunks = off; off += align256(sizeof(double) * (kSumsLen + kXLen) * ((batch + kChunk - 1) / kChunk + 1));
-    L.ctr = off;    off += align256(sizeof(unsigned) * 16);
+    L.ctr = off;    off += align256(sizeof(unsigned) * 32);   // job counters (0 / 4 fine / coarse, 8 / 12 escalation), 16 / 17 order
     // contrast keys and longest-first orders of the fine / coarse MINRES solves (order_kernel)
     L.keys_f = off; off += align256(sizeof(unsigned long long) * 2 * batch);
     L.keys_c = off; off += align256(sizeof(unsigned long long) * 2 * batch);
@@ -271,11 +271,13 @@ int ensure_phi(mlmc_ctx* ctx, int level) {
 }
 
 // K1 + K2 of mesh level `mesh` for nb samples (xi -> a), on stream st
+// (order / done: see launch_field_sep -- only on the separable path; the caller orders the P x m one itself)
 cudaError_t field(const mlmc_ctx* ctx, int mesh, const double* xi, double* a, uint64_t nb, unsigned long long* keys,
-                  cudaStream_t st) {
+                  cudaStream_t st, int* order = nullptr, unsigned* done = nullptr) {
     const int N = level_N(ctx, mesh), m = ctx->pr.m;
     if (!field_sep(ctx, N)) return launch_field(ctx->phi_dev[mesh], xi, a, 2 * N * N, m, nb, keys, st);
-    return launch_field_sep(ctx->tab_dev[mesh], ctx->sep_i, ctx->sep_c, ctx->sep.K, xi, a, N, m, nb, keys, st);
+    return launch_field_sep(ctx->tab_dev[mesh], ctx->sep_i, ctx->sep_c, ctx->sep.K, xi, a, N, m, nb, keys, st, order,
+                            done);
 }
 
 int check_prec(mlmc_ctx* ctx, const mlmc_precision* p, int N, double tol) {
@@ -381,7 +383,7 @@ int solve_mesh(mlmc_ctx* ctx, const Exec& ex, int N, const mlmc_precision* p, do
     if (p->solver == MLMC_SOLVER_MINRES) {
         int mi = p->max_iter > 0 ? p->max_iter : 16 * n + 1000;   // finite-precision Lanczos at contrast ~1e7 (Eq. (20), sigma = 2) needs > n
         bool verify = (p->flags & MLMC_FLAG_VERIFY) != 0;
-        if (keys && order) CU(counted(ctx, ex.st, MLMC_K_ORDER, N, [&] { return launch_order(keys, (int)nb, order, ex.st); }));
+        // (the longest-first order, `order`, is formed by run_level right after the fields)
         if (N >= kGmMinN && minres_cluster_supported(N) && !use_gm_kernel())
             CU(counted(ctx, ex.st, MLMC_K_MINRES, N, [&] {
                 return launch_minres_cluster(N, a, nb, tol, mi, rec, slot, ctr, keys ? order : nullptr, ex.st);
@@ -484,7 +486,7 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
     } nvtx_range(level);
     for (uint64_t done = 0; done < n;) {
         const uint64_t nb = std::min<uint64_t>(B, n - done);
-        CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, st));
+        CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 32, st));
         if (xi_in) {
             CU(cudaMemcpyAsync(xi, xi_in + done * m, sizeof(double) * m * nb,
                                xi_in_is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -497,13 +499,22 @@ int run_level(mlmc_ctx* ctx, const Exec& ex, int level, uint64_t n, uint64_t see
         unsigned long long* kc = ord_c ? reinterpret_cast<unsigned long long*>(ex.ws + L.keys_c) : nullptr;
         if (kf) CU(cudaMemsetAsync(kf, 0, sizeof(unsigned long long) * 2 * nb, st));
         if (kc) CU(cudaMemsetAsync(kc, 0, sizeof(unsigned long long) * 2 * nb, st));
-        CU(counted(ctx, st, MLMC_K_FIELD, Nf,
-                   [&] { return field(ctx, level, xi, af, nb, kf, st); }));
-        if (level > 0)
-            CU(counted(ctx, st, MLMC_K_FIELD, Nc,
-                       [&] { return field(ctx, level - 1, xi, ac, nb, kc, st); }));
         int* of = reinterpret_cast<int*>(ex.ws + L.ord_f);
         int* oc = reinterpret_cast<int*>(ex.ws + L.ord_c);
+        // longest-first orders with the fields: on the separable path the field kernel's last CTA forms the order
+        // (ctr[16], ctr[17] count the CTAs done); otherwise one order kernel right after the field, before the
+        // gate.  A separate one-CTA kernel that waits for a whole free SM sat behind the other levels' solves
+        // (the job trace showed level 2's fine solves starting only at 1.86 ms of a 2.4 ms step).
+        const bool fuse_f = kf && field_sep(ctx, Nf), fuse_c = kc && field_sep(ctx, Nc);
+        CU(counted(ctx, st, MLMC_K_FIELD, Nf, [&] {
+            return field(ctx, level, xi, af, nb, kf, st, fuse_f ? of : nullptr, fuse_f ? ctr + 16 : nullptr);
+        }));
+        if (level > 0)
+            CU(counted(ctx, st, MLMC_K_FIELD, Nc, [&] {
+                return field(ctx, level - 1, xi, ac, nb, kc, st, fuse_c ? oc : nullptr, fuse_c ? ctr + 17 : nullptr);
+            }));
+        if (kf && !fuse_f) CU(counted(ctx, st, MLMC_K_ORDER, Nf, [&] { return launch_order(kf, (int)nb, of, st); }));
+        if (kc && !fuse_c) CU(counted(ctx, st, MLMC_K_ORDER, Nc, [&] { return launch_order(kc, (int)nb, oc, st); }));
         if (level == 0) CU(cudaMemsetAsync(rec, 0, sizeof(double) * kRecLen * nb, st));
         const bool sched = sch && nb == n;               // single pass only
         if (sched && sch->prep) CU(cudaEventRecord(sch->prep, st));

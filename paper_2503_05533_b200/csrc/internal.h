@@ -45,8 +45,11 @@ cudaError_t launch_field(const double* phi, const double* xi, double* a, int P, 
 // K1s: the same a_T from the separable form, a = exp(F W) with W = C_xi G^T (two small DMMA contractions
 // per sample instead of the P x m one).  tab: the four 1D tables [4][N][K] (build_sep_tables); kmap / cmap
 // (device, K x K): the mode k = (a, b) and its c_k, or -1 / 0 where no mode has that pair.
+// order / done (optional, with keys; nb <= kOrderMax): the last CTA also writes the longest-first order of the
+// batch (as launch_order would); done is a zeroed device counter.
 cudaError_t launch_field_sep(const double* tab, const int* kmap, const double* cmap, int K, const double* xi,
-                             double* a, int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s);
+                             double* a, int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s,
+                             int* order = nullptr, unsigned* done = nullptr);
 bool field_sep_supported(int N, int K);   // N = 8, 16 or a multiple of 32; K <= 32
 bool field_use_dense();   // MLMC_FIELD_KERNEL=dense|ffma selects the P x m synthesis (A/B)
 bool field_force_sep();   // MLMC_FIELD_KERNEL=sep selects the separable synthesis on every mesh (tests)
@@ -55,6 +58,7 @@ bool field_force_sep();   // MLMC_FIELD_KERNEL=sep selects the separable synthes
 // iteration count (correlation 0.83 on configs[1] level 3), so the job counter hands out the long
 // solves first (LPT scheduling of the persistent CTAs).
 constexpr int kOrderMax = 4096;
+constexpr size_t kOrderScratch = 4 * kOrderMax + 4 * 512 + 4 * 64;   // bytes of shared memory the order needs
 cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cudaStream_t s);
 // K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].  order (optional,
 // device, nb ints): the sequence in which the systems are taken (order_kernel: longest first).

@@ -228,59 +228,69 @@ __global__ void __launch_bounds__(256) field_dmma_kernel(const double* __restric
     }
 }
 
-// Longest-first order: one CTA of 1024 threads buckets the nb <= kOrderMax systems by log contrast
-// (256 buckets between the batch's extremes, highest contrast first) -- a counting sort, four barriers,
-// instead of a comparison sort: the schedule only needs the long solves early, and the order within
-// a bucket (atomic placement) does not change any result (every system is solved independently).
-__global__ void __launch_bounds__(1024) order_kernel(const unsigned long long* __restrict__ keys, int nb,
-                                                     int* __restrict__ order) {
+// Longest-first order: one CTA buckets the nb <= kOrderMax systems by log contrast (256 buckets between the
+// batch's extremes, highest contrast first) -- a counting sort, four barriers, instead of a comparison sort:
+// the schedule only needs the long solves early, and the order within a bucket (atomic placement) does not
+// change any result (every system is solved independently).  Run by order_kernel (1024 threads) or by the
+// last CTA of the separable field kernel (256 threads) over `scratch` (kOrderScratch bytes of shared memory).
+__device__ void lpt_order_block(const unsigned long long* __restrict__ keys, int nb, int* __restrict__ order,
+                                unsigned char* scratch) {
     constexpr int NBK = 256;
-    __shared__ float lk[kOrderMax];
-    __shared__ int cnt[NBK], pos[NBK];
-    __shared__ float red_lo[32], red_hi[32];
+    float* lk = reinterpret_cast<float*>(scratch);            // [kOrderMax]
+    int* cnt = reinterpret_cast<int*>(lk + kOrderMax);       // [NBK]
+    int* pos = cnt + NBK;                                     // [NBK]
+    float* red_lo = reinterpret_cast<float*>(pos + NBK);      // [32]
+    float* red_hi = red_lo + 32;                              // [32]
+    const int tid = threadIdx.x, nt = blockDim.x;
     float lo = FLT_MAX, hi = -FLT_MAX;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-        const double mx = __longlong_as_double((long long)keys[2 * i]);
-        const double mn = __longlong_as_double((long long)~keys[2 * i + 1]);
+    for (int i = tid; i < nb; i += nt) {
+        const double mx = __longlong_as_double((long long)__ldcg(keys + 2 * i));
+        const double mn = __longlong_as_double((long long)~__ldcg(keys + 2 * i + 1));
         const float v = (mn > 0.0 && mx >= mn) ? (float)log(mx / mn) : 1e30f;
         lk[i] = v;
         lo = fminf(lo, v);
         hi = fmaxf(hi, v);
     }
-    if (threadIdx.x < NBK) cnt[threadIdx.x] = 0;
+    for (int i = tid; i < NBK; i += nt) cnt[i] = 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    if ((threadIdx.x & 31) == 0) { red_lo[threadIdx.x >> 5] = lo; red_hi[threadIdx.x >> 5] = hi; }
+    if ((tid & 31) == 0) { red_lo[tid >> 5] = lo; red_hi[tid >> 5] = hi; }
     __syncthreads();
     lo = red_lo[0];
     hi = red_hi[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fminf(lo, red_lo[w]); hi = fmaxf(hi, red_hi[w]); }
+    for (int w = 1; w < (nt >> 5); ++w) { lo = fminf(lo, red_lo[w]); hi = fmaxf(hi, red_hi[w]); }
     const float scale = hi > lo ? (NBK - 1) / (hi - lo) : 0.0f;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    for (int i = tid; i < nb; i += nt) {
         const int bk = (NBK - 1) - min(NBK - 1, max(0, (int)((lk[i] - lo) * scale)));   // 0 = highest contrast
         lk[i] = __int_as_float(bk);
         atomicAdd(&cnt[bk], 1);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {                            // exclusive prefix sum of the 256 counts (one warp)
+    if (tid < 32) {                                   // exclusive prefix sum of the 256 counts (one warp)
         int v[NBK / 32], run = 0;
 #pragma unroll
-        for (int j = 0; j < NBK / 32; ++j) { v[j] = cnt[threadIdx.x * (NBK / 32) + j]; run += v[j]; }
+        for (int j = 0; j < NBK / 32; ++j) { v[j] = cnt[tid * (NBK / 32) + j]; run += v[j]; }
         int incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((int)threadIdx.x >= o) incl += t;
+            if (tid >= o) incl += t;
         }
         int base = incl - run;
 #pragma unroll
-        for (int j = 0; j < NBK / 32; ++j) { pos[threadIdx.x * (NBK / 32) + j] = base; base += v[j]; }
+        for (int j = 0; j < NBK / 32; ++j) { pos[tid * (NBK / 32) + j] = base; base += v[j]; }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) order[atomicAdd(&pos[__float_as_int(lk[i])], 1)] = i;
+    for (int i = tid; i < nb; i += nt) order[atomicAdd(&pos[__float_as_int(lk[i])], 1)] = i;
+}
+
+__global__ void __launch_bounds__(1024) order_kernel(const unsigned long long* __restrict__ keys, int nb,
+                                                     int* __restrict__ order) {
+    __shared__ __align__(16) unsigned char scratch[kOrderScratch];
+    lpt_order_block(keys, nb, order, scratch);
 }
 
 cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cudaStream_t s) {
@@ -330,7 +340,8 @@ template <int TJ, int KP, int SB>
 __global__ void __launch_bounds__(256, KP == 32 ? (TJ == 8 ? 2 : 3) : 4) field_sep_kernel(const double* __restrict__ tab, const int* __restrict__ kmap,
                                                         const double* __restrict__ cmap, int K,
                                                         const double* __restrict__ xi, double* __restrict__ a, int N,
-                                                        int m, int nb, unsigned long long* __restrict__ keys) {
+                                                        int m, int nb, unsigned long long* __restrict__ keys,
+                                                        int* __restrict__ order, unsigned* __restrict__ done) {
     constexpr int TI = TJ, SJ = SB * TJ;
     constexpr int PW = sep_pitch(SJ), PF = sep_pitch(TI), PG = sep_pitch(TJ), PC = sep_pitch(KP);
     constexpr int NT = 256, NW = 8, NBJ = TJ / 8, NBI = TI / 8, PER = NBJ * NBI, NK4 = KP / 4;
@@ -463,6 +474,18 @@ __global__ void __launch_bounds__(256, KP == 32 ? (TJ == 8 ? 2 : 3) : 4) field_s
         }
         __syncthreads();                                          // Cx, W and kk are rewritten next group
     }
+    if (order) {   // the last CTA to finish forms the longest-first order from the completed contrast keys
+        __shared__ int last;
+        if (tid == 0) {
+            __threadfence();
+            last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            lpt_order_block(keys, nb, order, reinterpret_cast<unsigned char*>(fsm));
+        }
+    }
 }
 
 namespace {
@@ -470,8 +493,10 @@ namespace {
 // measured 7% slower at configs[1] level 3: fewer CTAs to hide the latency of the phases).
 template <int TJ, int KP, int SB>
 cudaError_t launch_sep_t(const double* tab, const int* kmap, const double* cmap, int K, const double* xi, double* a,
-                         int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
-    constexpr size_t smem = sep_smem<TJ, KP, SB>();
+                         int N, int m, uint64_t nb, unsigned long long* keys, int* order, unsigned* done,
+                         cudaStream_t s) {
+    // (the tile's shared memory doubles as the order's scratch in the last CTA)
+    constexpr size_t smem = sep_smem<TJ, KP, SB>() > kOrderScratch ? sep_smem<TJ, KP, SB>() : kOrderScratch;
     static_assert(smem <= 227 * 1024, "separable synthesis tile exceeds shared memory");
     static PerDevice<KernelOcc> cache;
     const KernelOcc occ = occ_of(cache, field_sep_kernel<TJ, KP, SB>, 256, smem);
@@ -481,39 +506,43 @@ cudaError_t launch_sep_t(const double* tab, const int* kmap, const double* cmap,
     const uint64_t groups = (nb + SB - 1) / SB;
     const uint64_t all = (uint64_t)occ.per_sm * occ.sms;
     const uint64_t gx = std::min<uint64_t>(groups, std::max<uint64_t>(1, all / tiles));
+    if (order && (!keys || !done || nb > (uint64_t)kOrderMax)) return cudaErrorInvalidValue;
     field_sep_kernel<TJ, KP, SB><<<dim3((unsigned)gx, (unsigned)tiles), 256, smem, s>>>(tab, kmap, cmap, K, xi, a, N,
-                                                                                       m, (int)nb, keys);
+                                                                                       m, (int)nb, keys, order, done);
     return cudaGetLastError();
 }
 template <int TJ, int KP>
 cudaError_t launch_sep_sb(const double* tab, const int* kmap, const double* cmap, int K, const double* xi, double* a,
-                          int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
+                          int N, int m, uint64_t nb, unsigned long long* keys, int* order, unsigned* done,
+                          cudaStream_t s) {
     if constexpr (TJ == 8) {
-        return launch_sep_t<TJ, KP, 8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+        return launch_sep_t<TJ, KP, 8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
     } else if constexpr (TJ == 16) {
-        return launch_sep_t<TJ, KP, 4>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+        return launch_sep_t<TJ, KP, 4>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
     } else {
-        return launch_sep_t<TJ, KP, 1>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+        return launch_sep_t<TJ, KP, 1>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
     }
 }
 template <int TJ>
 cudaError_t launch_sep_k(const double* tab, const int* kmap, const double* cmap, int K, const double* xi, double* a,
-                         int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
-    if (K <= 8) return launch_sep_sb<TJ, 8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
-    if (K <= 16) return launch_sep_sb<TJ, 16>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
-    return launch_sep_sb<TJ, 32>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+                         int N, int m, uint64_t nb, unsigned long long* keys, int* order, unsigned* done,
+                         cudaStream_t s) {
+    if (K <= 8) return launch_sep_sb<TJ, 8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
+    if (K <= 16) return launch_sep_sb<TJ, 16>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
+    return launch_sep_sb<TJ, 32>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
 }
 }  // namespace
 
 bool field_sep_supported(int N, int K) { return N >= 8 && (N < 32 ? (N & (N - 1)) == 0 : N % 32 == 0) && K >= 1 && K <= 32; }
 
 cudaError_t launch_field_sep(const double* tab, const int* kmap, const double* cmap, int K, const double* xi,
-                             double* a, int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s) {
+                             double* a, int N, int m, uint64_t nb, unsigned long long* keys, cudaStream_t s,
+                             int* order, unsigned* done) {
     if (nb == 0) return cudaSuccess;
     if (!field_sep_supported(N, K) || nb > 0x7fffffffull) return cudaErrorInvalidValue;
-    if (N >= 32) return launch_sep_k<32>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
-    if (N == 16) return launch_sep_k<16>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
-    return launch_sep_k<8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, s);
+    if (N >= 32) return launch_sep_k<32>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
+    if (N == 16) return launch_sep_k<16>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
+    return launch_sep_k<8>(tab, kmap, cmap, K, xi, a, N, m, nb, keys, order, done, s);
 }
 
 static bool field_use_ffma() {

@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 
 #ifdef MLMC_TUNING
 // job trace of the tuning build (tools/step_trace.py): per system solve {start, end (%globaltimer ns), smid << 32 | N,
-// cluster rank << 32 | job}
+// (cluster rank * 2 + record slot: 0 fine, 1 coarse) << 32 | job}
 __device__ unsigned long long* g_trace = nullptr;
 __device__ unsigned int g_trace_cap = 0;
 __device__ unsigned int g_trace_n = 0;
@@ -685,7 +685,7 @@ minres_tile_kernel(const double* __restrict__ a_all, int nb, double tol, int max
                 g_trace[4 * (size_t)idx] = trace_t0;
                 g_trace[4 * (size_t)idx + 1] = gtimer();
                 g_trace[4 * (size_t)idx + 2] = ((unsigned long long)smid << 32) | (unsigned)N;
-                g_trace[4 * (size_t)idx + 3] = ((unsigned long long)rank << 32) | (unsigned)job;
+                g_trace[4 * (size_t)idx + 3] = ((unsigned long long)(rank * 2 + slot) << 32) | (unsigned)job;
             }
         }
 #endif

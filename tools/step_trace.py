@@ -48,11 +48,13 @@ t = buf[: 4 * n].view(n, 4).cpu().numpy().astype(np.uint64)
 t0 = t[:, 0].min()
 start, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3            # microseconds
 sm, mesh = (t[:, 2] >> np.uint64(32)).astype(int), (t[:, 2] & np.uint64(0xffffffff)).astype(int)
+half = ((t[:, 3] >> np.uint64(32)) & np.uint64(1)).astype(int)          # 0 fine, 1 coarse
+mesh = mesh * 10 + half                                                  # key: N * 10 + half
 out = {"step_ms_events": e0.elapsed_time(e1), "records": int(n), "span_us": float(end.max()), "meshes": {}}
 for N in sorted(set(mesh.tolist())):
     k = mesh == N
     d = end[k] - start[k]
-    out["meshes"][str(N)] = {"solves": int(k.sum()), "first_start_us": float(start[k].min()),
+    out["meshes"][f"N={N // 10} {'coarse' if N % 10 else 'fine'}"] = {"solves": int(k.sum()), "first_start_us": float(start[k].min()),
                              "last_start_us": float(start[k].max()), "last_end_us": float(end[k].max()),
                              "mean_us": float(d.mean()), "max_us": float(d.max()), "sum_ms": float(d.sum() / 1e3)}
 # busy SMs over time (a solve occupies its SM from start to end; several groups of one CTA overlap)
