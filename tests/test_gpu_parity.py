@@ -484,7 +484,8 @@ def test_paper_direct_solver_experiment_same_samples():
 
 
 def test_streamed_minres_edge_cases_and_order_invariance():
-    """K3c with fewer systems than SMs, one system, and a batch just over one wave; the longest-first
+    """h = 1/128 (K3b since round 2: 4-CTA clusters; K3c before) with no system, one, fewer than the resident
+    clusters, and more than one wave; the longest-first
     job order (C2 level 3, the tile kernel) changes no per-sample result: the same samples drawn one
     at a time (no ordering: a single system) and in a batch agree bit for bit."""
     cfg = W.CONFIGS["C5"]
