@@ -1076,7 +1076,7 @@ struct mlmc_dd {
     int mesh_level = 0;
     mlmc_dd_layout L{};
     unsigned char* ws = nullptr;
-    cudaGraphExec_t chunk = nullptr;      // mlmc_dd_run_local: kChunk steps (pass + scalar) as one graph
+    cudaGraphExec_t chunk = nullptr;      // mlmc_dd_run_local: kDDChunk steps (pass + scalar) as one graph
 };
 
 namespace {
