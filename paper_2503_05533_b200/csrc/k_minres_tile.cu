@@ -867,6 +867,8 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             // v3 (8 rows per thread, 16 systems per 128-thread CTA: the scalar recurrences shared by half as
             // many threads): 0.266 vs 0.206 ms per level-1 launch, C2 step 2.41 vs 2.36 ms (255 registers, spills)
             IF_TUNING(if (var == 3) return run_tile<16, 8, 2, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            // v4 (capped at 128 registers for 4 CTAs per SM; 168 B spilled): C2 step 2.364 vs 2.342 ms
+            IF_TUNING(if (var == 4) return run_tile<16, 4, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             return run_tile<16, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 32:
             IF_TUNING(if (var == 1) return run_tile<32, 4, 4, 1, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
@@ -879,6 +881,8 @@ static cudaError_t tile_dispatch(int N, int var, const double* a, uint64_t nb, d
             // v6 (8 rows per thread, 2 systems per CTA, 4 per SM): 0.524 vs 0.490 ms per level-2 launch, C2 step
             // 2.344 vs 2.361 ms (within run-to-run noise)
             IF_TUNING(if (var == 6) return run_tile<32, 8, 2, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
+            // v7 (128 registers, 4 CTAs per SM; 124 B spilled): 0.537 vs 0.496 ms per launch, C2 step 2.397 vs 2.342 ms
+            IF_TUNING(if (var == 7) return run_tile<32, 4, 4, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);)
             return run_tile<32, 4, 3, 0, V, XM>(a, nb, tol, max_iter, out, slot, ctr, order, xio, s);
         case 64:
             // measured (configs[1] level 3, 300 systems): v0 2.04 ms, v1 2.23, v2 3.74, v3 3.67, v4 2.97
