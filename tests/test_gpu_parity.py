@@ -671,6 +671,20 @@ def test_c_quickstart(tmp_path):
     assert "level 3:" in r.stdout and "adaptive MPML" in r.stdout
 
 
+def test_python_quickstart():
+    """examples/quickstart.py (the Python binding end to end: per-level batches, the concurrent step into a device
+    tensor, Algorithm 2 with policies 0 and 3) runs and its estimates lie in the survey's sanity range."""
+    import re
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "examples", "quickstart.py")], capture_output=True,
+                       text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "failures 0" in r.stdout and "adaptive (policy 3)" in r.stdout
+    ests = [float(x) for x in re.findall(r"estimate (?:from one concurrent step: )?([0-9.]+)", r.stdout)]
+    assert len(ests) == 3 and all(0.028 < e < 0.042 for e in ests), r.stdout   # seeded: fixed values ~0.037
+
+
 def test_separable_synthesis_on_every_mesh_subprocess():
     """MLMC_FIELD_KERNEL=sep (read once per process, hence a subprocess): the separable synthesis on every
     mesh, for the BASELINE field (configs[1]) and the paper's Eq. (20) field, against the oracle."""
