@@ -367,9 +367,9 @@ struct AutoChooser {
     static mlmc_precision q(int solver, int uf, int us, int u, int max_iter = 0) {
         return mlmc_precision{solver, uf, us, u, u, max_iter, 0};
     }
+    // (MINRES last: its pilot is screened against the best time of the others, see choose)
     std::vector<mlmc_precision> candidates(int N, double tol) const {
         std::vector<mlmc_precision> c;
-        c.push_back(q(MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64));
         c.push_back(q(MLMC_SOLVER_MGCG, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64));
         if (N <= 32) {   // the banded factors (K4)
             if (tol >= 1e-3) c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F16, MLMC_FMT_F32));
@@ -381,7 +381,18 @@ struct AutoChooser {
             c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F16, MLMC_FMT_F32, MLMC_FMT_F64));
             c.push_back(q(MLMC_SOLVER_CHOL_IR, MLMC_FMT_F32, MLMC_FMT_F64, MLMC_FMT_F64));
         }
+        c.push_back(q(MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64));
         return c;
+    }
+    // device ms of the pilot's solves on mesh N (the library's per-launch events)
+    double pilot_ms(int N) const {
+        mlmc_kernel_stat st[64];
+        int cnt = 0;
+        mlmc_profile_read(ctx, st, 64, &cnt);
+        double t = 0.0;
+        for (int i = 0; i < std::min(cnt, 64); ++i)
+            if (st[i].N == N && (st[i].kind == MLMC_K_MINRES || st[i].kind == MLMC_K_CHOL_IR)) t += st[i].ms;
+        return t;
     }
     int choose(int level, int N, double tol, mlmc_precision* out) {
         // the admissible candidates change at tol = 1e-3 and 1e-5: one choice per (mesh, tolerance class),
@@ -394,13 +405,45 @@ struct AutoChooser {
         std::vector<double> ms(cand.size(), 0.0);
         // the coarse half of a pilot sample is a loose MINRES solve (it only has to converge, not to be timed)
         const mlmc_precision cheap = q(MLMC_SOLVER_MINRES, MLMC_FMT_F64, MLMC_FMT_F64, MLMC_FMT_F64, 4 * n_unk + 400);
+        const uint64_t pseed = seed ^ 0x9e3779b97f4a7c15ull;
         for (size_t c = 0; c < cand.size(); ++c) {
             mlmc_precision p = cand[c];
             p.max_iter = p.solver == MLMC_SOLVER_CHOL_IR ? 50 : 4 * n_unk + 400;   // the pilot's budget
+            double best = -1.0;
+            for (size_t b = 0; b < c; ++b)
+                if (ms[b] >= 0 && (best < 0 || ms[b] < best)) best = ms[b];
+            if (p.solver == MLMC_SOLVER_MINRES && best > 0.0) {
+                // screening: kScreen MINRES steps on the same pilot batch; if they already cost more than the best
+                // candidate's whole solve, or the residual decay they show extrapolates (log-linearly) to a
+                // solve slower than it, MINRES is dominated and its full pilot (thousands of steps on the fine
+                // meshes: ~2.5 s of the first configs[4] run at eps = 1e-5) is skipped
+                constexpr int kScreen = 200;
+                mlmc_precision ps = p;
+                ps.max_iter = kScreen;
+                std::vector<double> rec((size_t)npilot * MLMC_SAMPLE_LEN, 0.0);
+                mlmc_level_sums ss;
+                int rs = mlmc_profile_enable(ctx, 1);
+                if (!rs) rs = mlmc_sample_level(ctx, level, npilot, pseed, 0, &ps, &cheap, tol, 0.5, &ss, rec.data());
+                const double t_screen = rs ? -1.0 : pilot_ms(N);
+                mlmc_profile_enable(ctx, 0);
+                if (!rs && ss.n_fail > 0) {                   // not converged within kScreen steps
+                    double worst = 0.0;                       // steps the slowest sample would need
+                    for (uint64_t k = 0; k < npilot; ++k) {
+                        const double rr = rec[k * MLMC_SAMPLE_LEN + 4];
+                        const double need = (rr > 0.0 && rr < 1.0) ? kScreen * std::log(tol) / std::log(rr)
+                                                                   : 1e300;
+                        worst = std::max(worst, need);
+                    }
+                    const double est = t_screen * worst / kScreen;
+                    if (t_screen >= best || est >= 1.5 * best) { ms[c] = -1.0; continue; }
+                } else if (!rs) {                             // converged within the screen: that is its pilot
+                    ms[c] = t_screen;
+                    continue;
+                }
+            }
             mlmc_level_sums sums;
             int rc = mlmc_profile_enable(ctx, 1);
-            if (!rc) rc = mlmc_sample_level(ctx, level, npilot, seed ^ 0x9e3779b97f4a7c15ull, 0, &p, &cheap, tol, 0.5,
-                                            &sums, nullptr);
+            if (!rc) rc = mlmc_sample_level(ctx, level, npilot, pseed, 0, &p, &cheap, tol, 0.5, &sums, nullptr);
             if (rc == MLMC_EINVAL) { mlmc_profile_enable(ctx, 0); ms[c] = -1.0; continue; }   // not built here
             if (rc) {                            // agree on the failure before leaving
                 mlmc_profile_enable(ctx, 0);
@@ -411,13 +454,8 @@ struct AutoChooser {
                 }
                 return rc;
             }
-            mlmc_kernel_stat st[64];
-            int cnt = 0;
-            mlmc_profile_read(ctx, st, 64, &cnt);
+            const double t = pilot_ms(N);
             mlmc_profile_enable(ctx, 0);
-            double t = 0.0;
-            for (int i = 0; i < std::min(cnt, 64); ++i)
-                if (st[i].N == N && (st[i].kind == MLMC_K_MINRES || st[i].kind == MLMC_K_CHOL_IR)) t += st[i].ms;
             ms[c] = sums.n_fail > 0 ? -1.0 : t;     // a failed pilot solve: inadmissible
         }
         if (world > 1 && allreduce) {   // one SUM all-reduce: pilot times, failure counts, error flag

@@ -788,6 +788,22 @@ def test_adaptive_auto_policy():
     ctx.close()
 
 
+def test_auto_policy_screens_minres_on_fine_meshes():
+    """Policy 3 on configs[4] down to h = 1/128: MINRES's pilot is screened against the best candidate so far
+    (200 steps and a log-linear extrapolation of their residual decay) instead of being run to thousands of
+    steps; on h >= 1/64 MG-PCG is the choice by a wide margin (37x at h = 1/128), the run converges."""
+    cfg = W.CONFIGS["C5"]
+    ctx = _ctx(cfg, L_max=4, ws=4 << 30)
+    r = ctx.adaptive_run(6e-5, k_p=0.05, seed=4, policy=3, on_fail=1)
+    assert r["code"] in (0, 4) and r["n_fail"] == 0 and 0.030 < r["estimate"] < 0.038, r
+    assert r["L"] >= 3, r
+    for N in (64, 128):
+        if (cfg["h0_inv"] << r["L"]) >= N:
+            ch = ctx.auto_choice(N)
+            assert ch is not None and ch["solver"] == "mgcg", (N, ch)
+    ctx.close()
+
+
 def test_escalation_repairs_failed_minres_solves():
     """on_fail = 2 / MLMC_FLAG_ESCALATE: MINRES capped far below what the tolerance needs fails
     on every sample; escalation solves each again with MG-PCG, so every record ends with status 4, the
