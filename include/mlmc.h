@@ -301,10 +301,11 @@ int mlmc_adaptive_run(mlmc_ctx* ctx, double eps, const mlmc_adaptive_opts* opts,
                       mlmc_allreduce_fn allreduce, void* user, mlmc_result* out);
 
 /* Policy 3 (auto) of mlmc_adaptive_run: on first use of a mesh the controller times every candidate --
- * MINRES, MG-PCG and, on h >= 1/32, the Cholesky-IR quads the level tolerance admits (q/h/s factors with
- * binary16/32 vectors, h/s factors with binary64 vectors) -- on a pilot batch of its own (seed ^ a
+ * MG-PCG, on h >= 1/32 the Cholesky-IR quads the level tolerance admits (q/h/s factors with binary16/32
+ * vectors, h/s factors with binary64 vectors), and MINRES last -- on a pilot batch of its own (seed ^ a
  * constant, never part of the estimate; 8..512 samples by mesh size; kernel device time) and keeps the
- * fastest whose pilot solves all converged; pilot times are summed across ranks so all ranks agree.  A
+ * fastest whose pilot solves all converged; MINRES first runs 200 steps and is dropped when they already
+ * cost more than the best candidate's solve or their residual decay extrapolates to a slower one; pilot times are summed across ranks so all ranks agree.  A
  * choice is kept in the context per (mesh, tolerance class: >= 1e-3, >= 1e-5, below) for later runs.
  * mlmc_auto_choice returns the latest precision chosen for mesh N (= 1/h) and its pilot cost in device
  * ms per sample.  Errors: EINVAL (no choice made for N).                                                */
