@@ -372,6 +372,45 @@ def test_streamed_minres_fine_mesh_parity():
     ctx.close()
 
 
+def test_async_profile_workspace_and_level_info_entry_points():
+    """The C-ABI calls the other tests reach only indirectly: mlmc_sample_level_async (device sums and device
+    per-sample records, no synchronisation) equals mlmc_sample_level bit for bit; mlmc_profile_enable / _read
+    count the launches of every kernel class of the pass (the longest-first order is formed inside the field
+    launch on this mesh, so no separate order launch); mlmc_workspace_bytes[_prec] grow with the batch and
+    the Cholesky-IR scratch; mlmc_level_info_get returns the mesh geometry (level table)."""
+    cfg = W.CONFIGS["C2"]
+    ctx = _ctx(cfg)
+    mr = precision("minres")
+    ref = ctx.sample_level(3, 50, seed=4, first_index=9, prec_fine=mr, prec_coarse=mr, tol_fine=1e-8, tol_coarse=1e-6,
+                           per_sample=True)
+    sums = torch.zeros(12, dtype=torch.float64, device="cuda")
+    ps = torch.zeros((50, 8), dtype=torch.float64, device="cuda")
+    ctx.profile_enable(True)
+    ctx.sample_level_async(3, 50, seed=4, first_index=9, prec_fine=mr, prec_coarse=mr, tol_fine=1e-8, tol_coarse=1e-6,
+                           sums_out=sums, per_sample_out=ps)
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    torch.cuda.synchronize()
+    assert np.array_equal(ps.cpu().numpy(), ref.per_sample)
+    got = sums.cpu().numpy()
+    want = np.array([ref.sums[f] for f in ("sum_y", "sum_y2", "sum_qf", "sum_qc", "sum_cost", "n", "n_fail",
+                                             "iters_f", "iters_c", "iters_f_max", "iters_c_max", "n_escalated")])
+    assert np.array_equal(got, want)
+    kinds = {(k, N): c for k, N, c, ms in prof}
+    assert kinds.get(("minres", 64)) == 1 and kinds.get(("minres", 32)) == 1, prof
+    assert kinds.get(("field", 64)) == 1 and kinds.get(("field", 32)) == 1 and ("order", 64) not in kinds, prof
+    assert all(ms > 0 for k, N, c, ms in prof if k in ("minres", "field")), prof
+    w1, w2 = ctx.workspace_bytes(2, 100), ctx.workspace_bytes(2, 1000)
+    assert 0 < w1 < w2
+    ir = precision("chol_ir", "h", "s")
+    assert ctx.workspace_bytes_prec(2, 1000, ir, ir) > ctx.workspace_bytes_prec(2, 1000, mr, mr) > 0
+    for l in range(4):
+        info = ctx.level_info(l)
+        N = cfg["h0_inv"] << l
+        assert info == {"N": N, "n": (N - 1) ** 2, "P": 2 * N * N, "bw": N - 1, "h": 1.0 / N}, info
+    ctx.close()
+
+
 def test_job_trace_is_refused_by_the_production_build():
     """mlmc_debug_trace (schedule analysis, tools/step_trace.py) records only in the MLMC_TUNING build; the
     production library answers EINVAL with a message instead of silently recording nothing."""
