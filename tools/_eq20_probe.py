@@ -1,5 +1,9 @@
-import sys, math
-sys.path.insert(0,'/root/repo')
+"""MINRES on the paper's Eq. (20) field (sigma = 2, contrast up to ~1e7): failures and iteration counts per level
+and tolerance, 200 samples each -- the probe behind the default iteration cap 16 n + 1000.
+python tools/_eq20_probe.py"""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workloads as W
 from paper_2503_05533_b200 import Context, precision
 cfg = W.CONFIGS["EQ20"]

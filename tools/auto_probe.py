@@ -1,5 +1,9 @@
-import os, sys, time, json
-sys.path.insert(0, os.getcwd())
+"""Policy 3 on configs[4] at eps = 1e-5: wall time of the first adaptive run (pilots included), the choice per
+mesh (mlmc_auto_choice), and a second run with the choices cached.  python tools/auto_probe.py"""
+import os
+import sys
+import time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workloads as W
 from paper_2503_05533_b200 import Context
 cfg = W.CONFIGS["C5"]
