@@ -476,6 +476,8 @@ __global__ void __launch_bounds__(256, KP == 32 ? (TJ == 8 ? 2 : 3) : 4) field_s
     }
     if (order) {   // the last CTA to finish forms the longest-first order from the completed contrast keys
         __shared__ int last;
+        __threadfence();                                      // every thread's key atomics before the count
+        __syncthreads();
         if (tid == 0) {
             __threadfence();
             last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
