@@ -246,7 +246,9 @@ int mlmc_sample_level_xi(mlmc_ctx* ctx, int level, uint64_t n, const double* xi,
  * table; mlmc_profile_read synchronises the stream and copies at most `max`
  * entries (count = entries available).                                       */
 enum { MLMC_K_RNG = 0, MLMC_K_FIELD = 1, MLMC_K_MINRES = 2, MLMC_K_CHOL_IR = 3, MLMC_K_SUMS = 4,
-       MLMC_K_ORDER = 5 /* longest-first job order of a MINRES launch */ };
+       MLMC_K_ORDER = 5 /* longest-first job order of a MINRES launch: a kernel of its own only after the
+                           P x m field synthesis; the separable field kernel forms it in its last CTA
+                           (counted as MLMC_K_FIELD) */ };
 typedef struct { int32_t kind; int32_t N; uint64_t launches; double ms; } mlmc_kernel_stat;
 int mlmc_profile_enable(mlmc_ctx* ctx, int on);
 int mlmc_profile_read(mlmc_ctx* ctx, mlmc_kernel_stat* stats, int max, int* count);
