@@ -361,15 +361,25 @@ bool use_gm_kernel() {
 }
 
 // Longest-first job order for a MINRES solve (LPT scheduling of the persistent CTAs): worth it where
-// a launch is a few waves of long solves (h >= 1/32: the tile and streamed kernels, nb <= kOrderMax).  MLMC_ORDER=0
-// switches it off (A/B runs).
+// a launch is a few waves of long solves (h >= 1/16: the tile and streamed kernels, nb <= kOrderMax).  MLMC_ORDER=0
+// switches it off (A/B runs).  (h = 1/16 since round 2, kOrderMax 8192 for configs[1] level 1's 5000 systems: C2 step
+// 2.339 / 2.342 / 2.341 vs 2.343 / 2.346 / 2.346 ms from h = 1/32 on, alternating runs; identical sums)
 bool use_order(const mlmc_precision* p, int N, uint64_t nb) {
     static int env = -1;
     if (env < 0) {
         const char* e = std::getenv("MLMC_ORDER");
         env = (e && e[0] == '0') ? 0 : 1;
     }
-    if (!env || p->solver != MLMC_SOLVER_MINRES || N < 32 || nb < 2 || nb > (uint64_t)kOrderMax) return false;
+    int min_n = kOrderMinN;
+#ifdef MLMC_TUNING
+    static int env_n = -1;
+    if (env_n < 0) {
+        const char* e = std::getenv("MLMC_ORDER_MIN_N");
+        env_n = e ? std::atoi(e) : kOrderMinN;
+    }
+    min_n = env_n;
+#endif
+    if (!env || p->solver != MLMC_SOLVER_MINRES || N < min_n || nb < 2 || nb > (uint64_t)kOrderMax) return false;
     if (N >= kGmMinN) return minres_stream_supported(N) && !use_gm_kernel();   // streamed kernel (K3c)
     return minres_tile_variant(N) >= 0;
 }

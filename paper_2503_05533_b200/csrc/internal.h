@@ -57,7 +57,8 @@ bool field_force_sep();   // MLMC_FIELD_KERNEL=sep selects the separable synthes
 // bitonic sort of the field keys): order[i] = system index.  The contrast predicts the MINRES
 // iteration count (correlation 0.83 on configs[1] level 3), so the job counter hands out the long
 // solves first (LPT scheduling of the persistent CTAs).
-constexpr int kOrderMax = 4096;
+constexpr int kOrderMax = 8192;
+constexpr int kOrderMinN = 16;   // (tuning build: MLMC_ORDER_MIN_N overrides in use_order)
 constexpr size_t kOrderScratch = 4 * kOrderMax + 4 * 512 + 4 * 64;   // bytes of shared memory the order needs
 cudaError_t launch_order(const unsigned long long* keys, int nb, int* order, cudaStream_t s);
 // K3: MINRES for nb systems on the N x N mesh; writes out[b*8 + {0,2,4,6} + slot].  order (optional,
